@@ -1,0 +1,265 @@
+/*
+ * vismmoe.h -- C-ABI of the B200-native VisMMOE per-layer hot path.
+ *
+ * One shared library (paper_2605_05899_b200/libvismmoe.so, sm_100a) exports
+ * every entry point below.  Conventions:
+ *   - plain pointers + sizes, no torch types; device pointers are marked `d_`,
+ *     host pointers `h_`;
+ *   - all device entry points are asynchronous on the caller's `stream`
+ *     (a cudaStream_t passed as void*); ownership of buffers stays with the
+ *     caller (torch tensors passed by data_ptr);
+ *   - every function returns an int status (0 = OK); on failure the message is
+ *     available from vmm_last_error() (thread-local).  Codes map 1:1 onto the
+ *     reference's exception classes (pkg/src/moesim/errors.py:4-29):
+ *       1 ValidationError  2 ContractError  3 SimulationError  4 TraceError
+ *       5 PlanningError    6 device/CUDA error
+ *   - handles (engine, stack) are single-owner and not reentrant, matching the
+ *     reference's single-owner cache (pkg/src/moesim/cache.py:79).
+ *
+ * Reference interface each group replaces is cited per function.
+ */
+#ifndef VISMMOE_H
+#define VISMMOE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VMM_OK 0
+#define VMM_EVALIDATION 1
+#define VMM_ECONTRACT 2
+#define VMM_ESIMULATION 3
+#define VMM_ETRACE 4
+#define VMM_EPLANNING 5
+#define VMM_ECUDA 6
+
+#define VMM_MAX_EXPERTS 256 /* expert ids are bit-packed in 4 x u64 words */
+
+const char *vmm_last_error(void);
+int vmm_abi_version(void);
+/* 0 if device `dev` is sm_100 and the kernels of this library can run there */
+int vmm_device_check(int dev);
+
+/* ------------------------------------------------------------------------
+ * Token compression (prune), batched over R requests, one CTA per request.
+ * Replaces compress() pkg/src/moesim/compress.py:142-185 (normalize_saliency
+ * :104-114, salient core :156-157, active_experts :125-132,
+ * marginal_expansion :135-139, extras order :174) and
+ * CompressionPlan.retained_ids :63-65.
+ *   d_saliency [T] f64, d_modality [T] u8 (0 visual, 1 text, 2 decode),
+ *   d_routes [P][T][k] i32: routes of the prefix layers for all T tokens,
+ *   d_req_off [R+1] i32 token offsets, d_k_core/d_k_keep [R] i32 budgets
+ *   (host: floor(alpha*n_visual), floor(beta*n_visual), exactly as :151-152).
+ * Outputs (token-indexed, per request segment): s_norm/delta/score f64 (NaN
+ * where undefined), flags u8 (bit0 core, bit1 keep, bit2 retained),
+ * d_retained i32 (request-local ids, ascending, packed at d_req_off[r]),
+ * d_n_retained [R] i32, d_target [R][4] u64 expert bitmask, d_status [R] i32
+ * (0 ok, 1 invalid saliency, 2 too many visual tokens).
+ * ------------------------------------------------------------------------ */
+int vmm_prune(const double *d_saliency, const uint8_t *d_modality, const int32_t *d_routes,
+              const int32_t *d_req_off, const int32_t *d_k_core, const int32_t *d_k_keep,
+              int R, int T, int P, int k, int experts, double lam,
+              double *d_s_norm, double *d_delta, double *d_score, uint8_t *d_flags,
+              int32_t *d_retained, int32_t *d_n_retained, uint64_t *d_target, int32_t *d_status,
+              void *stream);
+
+/* Row gather (stream compaction of hidden states): dst[i] = src[idx[i]], bf16 rows of H. */
+int vmm_gather_rows(const void *d_src, const int32_t *d_idx, int n, int H, void *d_dst, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Router: logits = X[N,H] . W_g[E,H]^T (bf16 in, fp32 accumulate), per-token
+ * top-k by (logit desc, id asc) and softmax over the k selected logits, so
+ * gates are > 0 and sum to 1 (the RoutingTrace contract, trace.py:80-81,
+ * :375-382).  Optional per-expert pick counts (u32 [E], accumulated) give the
+ * layer's demand set (trace.active_union, trace.py:102-107).
+ * No reference implementation exists (router absent in the reference).
+ * ------------------------------------------------------------------------ */
+int vmm_route_topk(const void *d_x, const void *d_wg, int N, int H, int E, int k,
+                   int32_t *d_ids, float *d_gates, float *d_logits /* nullable [N,E] */,
+                   uint32_t *d_counts /* nullable [E] */, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Demand / predictor kernels (pkg/src/moesim/predictor.py)
+ * ------------------------------------------------------------------------ */
+/* counts[l][e] = #picks of expert e at layer `layers[l]` over token ids (trace.active_union,
+ * predictor.demand_set :115-117).  d_routes is the full [L][T][k] table. */
+int vmm_demand_counts(const int32_t *d_routes, int L, int T, int k, int E,
+                      const int32_t *d_layers, int n_layers, const int32_t *d_ids, int n_ids,
+                      uint32_t *d_counts, void *stream);
+/* Oracle targets y[c][e] = max_{d<=W, ctx+d<=L-1} decay[d-1]*[count[ctx+d][e]>0]
+ * (build_targets :120-148).  d_counts is [L][E] over all layers. */
+int vmm_oracle_targets(const uint32_t *d_counts, int L, int E, const int32_t *d_ctx, int n_ctx,
+                       int window, const double *d_decay, double *d_y, void *stream);
+/* History histogram (routing_histogram :63-75), bit-exact: per expert, the
+ * weight pow[ctx-past] is added count times in ascending past order, then the
+ * vector is divided by numpy's pairwise sum.  d_counts [L][E]. */
+int vmm_history(const uint32_t *d_counts, int L, int E, const int32_t *d_ctx, int n_ctx,
+                const double *d_pow, double *d_y, void *stream);
+/* MLP predictor (build_features :86-112 + MLPModel.forward :196-202 + sigmoid :547):
+ * x = [hist(ctx) ; mean_i(emb[ids_i] + drift[ctx]) ; h_v]; y = sigmoid(Wo relu(W2 relu(W1 x+b1)+b2)+bo).
+ * fp64 throughout; weights row-major as the reference stores them. */
+int vmm_mlp_predict(const double *d_hist /* [n_ctx][E] */, const double *d_emb, int D,
+                    const double *d_drift /* [L][D] */, const int32_t *d_ids, int n_ids,
+                    const double *d_hv /* [D] */, const int32_t *d_ctx, int n_ctx, int E,
+                    const double *d_w1, const double *d_b1, int d_hidden,
+                    const double *d_w2, const double *d_b2, int d_bottleneck,
+                    const double *d_wo, const double *d_bo,
+                    double *d_feat /* nullable [n_ctx][E+2D] */, double *d_y, void *stream);
+/* Gate-reuse lookahead: counts of experts in the top-k of W_next applied to
+ * layer-l hidden states, normalised by N*k -> y f64 [E]. */
+int vmm_gate_lookahead(const void *d_x, const void *d_wnext, int N, int H, int E, int k,
+                       uint32_t *d_scratch_counts /* [E] */, double *d_y, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Expert permutation and combine (no reference numerics; pipeline.py:573 order)
+ * plan: stable counting sort of the N*k (token, slot) picks by expert.
+ *   d_offsets [E+1] i32, d_src_row [N*k] i32 (token of each permuted row),
+ *   d_pos [N*k] i32 (permuted row of pick (t, j)).
+ * ------------------------------------------------------------------------ */
+int vmm_permute_plan(const int32_t *d_ids, int N, int k, int E, int32_t *d_offsets,
+                     int32_t *d_src_row, int32_t *d_pos, void *stream);
+/* Xp[p] = X[src_row[p]] for the n_rows permuted rows (bf16 rows of H) */
+int vmm_permute_rows(const void *d_x, const int32_t *d_src_row, int n_rows, int H, void *d_xp, void *stream);
+/* out[t] = resid[t] + sum_j gates[t,j] * Y[pos[t,j]]  (bf16 rows, fp32 accumulate, j ascending) */
+int vmm_combine(const void *d_y, const int32_t *d_pos, const float *d_gates, const void *d_resid,
+                int N, int k, int H, void *d_out, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Grouped bf16 SwiGLU expert FFN on tcgen05/TMEM with TMA operands.
+ * Expert weights live in slots of one HBM arena; slot s holds
+ *   W13[s] : [2I][H] bf16, rows interleaved per 64-row block (64 gate rows, then
+ *            the 64 matching up rows), K-major;
+ *   W2[s]  : [H][I]  bf16, K-major.
+ * d_slot_of_expert [E] i32 maps expert -> arena slot for this layer.
+ * Xp: permuted token rows [M_total][H]; d_offsets [E+1] from vmm_permute_plan.
+ * H1 scratch [M_total][I] bf16; Y out [M_total][H] bf16.
+ * ------------------------------------------------------------------------ */
+int vmm_grouped_swiglu(const void *d_xp, const int32_t *d_offsets, int E, int M_total,
+                       int H, int I, const void *d_w13_arena, const void *d_w2_arena, long long n_slots,
+                       const int32_t *d_slot_of_expert, void *d_h1, void *d_y, void *stream);
+/* Reference (CUDA-core, fp32) version of the same contraction for cross-checks. */
+int vmm_grouped_swiglu_simt(const void *d_xp, const int32_t *d_offsets, int E, int M_total,
+                            int H, int I, const void *d_w13_arena, const void *d_w2_arena,
+                            const int32_t *d_slot_of_expert, void *d_h1, void *d_y, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Cache policy + logical-clock engine (C++ mirror of ExpertCache,
+ * pkg/src/moesim/cache.py:78-278, and _Engine, pipeline.py:382-760).
+ * ------------------------------------------------------------------------ */
+typedef struct vmm_engine vmm_engine;
+
+typedef struct {
+  int layers, experts, num_slabs;
+  int victim_fifo;         /* victim_policy == "fifo" */
+  int speculative_grace;
+  int budget, window;      /* predictor.budget / window */
+  int l_pinned, shared;
+  int prefetching;         /* predictor attached and budget > 0 */
+  int reactive;            /* simulate_reactive */
+  int event_log;
+  double transfer_ms, gpu_ms;
+  double boot_ms;          /* compress latency (if compressed) + bootstrap (if prefetching) */
+  const double *decay;     /* [window] gamma**(d-1), host-computed */
+} vmm_engine_config;
+
+/* one transfer / eviction decision, in decision order */
+typedef struct {
+  double t;        /* logical time */
+  int32_t kind;    /* 0 issue, 1 complete, 2 evict */
+  int32_t layer, expert, slab;
+} vmm_engine_event;
+
+typedef struct {
+  double makespan, total_compute, total_transfer, exposed_transfer, prefill_ms;
+  long long hits, misses, stalls, rejected_loads, on_demand_transfers, inflight_waits, evictions;
+  int decode_steps;
+} vmm_engine_report;
+
+int vmm_engine_create(const vmm_engine_config *cfg, vmm_engine **out);
+void vmm_engine_destroy(vmm_engine *e);
+/* boot interval + first emission (pipeline.py:697-707); y may be NULL if !prefetching */
+int vmm_engine_begin(vmm_engine *e, const double *h_y_boot);
+/* run one layer (pipeline.py:709-721 / 723-740).  demand: expert ids ascending.
+ * phase 0 prefill / 1 decode; step = decode step or -1.  If the engine is
+ * prefetching and the layer is emitting, h_y is the predictor output for
+ * context `layer` (else NULL). */
+int vmm_engine_layer(vmm_engine *e, int layer, const int32_t *h_demand, int n_demand,
+                     int phase, int step, const double *h_y);
+/* close a decode step (records decode_ms_per_step) */
+int vmm_engine_end_step(vmm_engine *e);
+int vmm_engine_finish(vmm_engine *e, vmm_engine_report *rep);
+/* which layers emit after running (prefill: layer >= l_pinned && layer < L-1;
+ * decode: additionally layer == l_pinned-1) -> 1/0 */
+int vmm_engine_emits(const vmm_engine *e, int layer, int phase);
+/* drain the parity event log (issue/complete/evict exactly as the reference's
+ * event_log, pipeline.py:446-478, 617-618) since the last call; returns count */
+int vmm_engine_events(vmm_engine *e, vmm_engine_event *h_out, int cap);
+int vmm_engine_pending_events(const vmm_engine *e);
+/* drain transfer commands (layer, expert, slab) triples in issue order; these
+ * drive the copy stream (also emitted in reactive mode) */
+int vmm_engine_copies(vmm_engine *e, int32_t *h_out, int cap);
+/* decode_ms_per_step values; returns the count */
+int vmm_engine_decode_ms(const vmm_engine *e, double *h_out, int cap);
+/* per-layer stats rows: (phase, step, layer, start, end, stall, transfers, hits) */
+int vmm_engine_layer_stats(vmm_engine *e, double *h_out /* [n][8] */, int cap);
+/* slab currently holding (layer, expert) or -1 */
+int vmm_engine_slab_of(const vmm_engine *e, int layer, int expert);
+/* snapshot of one slab: key (-1 if free), state 0 free/1 loading/2 resident,
+ * class 0 expired/1 speculative/2 required, priority, ready_time (NaN if none) */
+int vmm_engine_slab(const vmm_engine *e, int slab, int *layer, int *expert, int *state, int *cls,
+                    double *priority, double *ready);
+
+/* Standalone cache (ExpertCache drop-in; same transitions as the engine's) */
+typedef struct vmm_cache vmm_cache;
+int vmm_cache_create(int num_slabs, int victim_fifo, vmm_cache **out);
+void vmm_cache_destroy(vmm_cache *c);
+/* returns 0 miss / 1 hit / 2 in-flight; ready NaN if none */
+int vmm_cache_lookup(const vmm_cache *c, int layer, int expert, double *ready);
+/* status out: 0 already resident / 1 enqueued / 2 rejected; slab -1 if none;
+ * evicted (-1,-1) if none.  cls 1 speculative, 2 required */
+int vmm_cache_request(vmm_cache *c, int layer, int expert, double priority, int cls, int *status,
+                      int *slab, int *ev_layer, int *ev_expert);
+int vmm_cache_set_ready(vmm_cache *c, int layer, int expert, double t);
+int vmm_cache_complete(vmm_cache *c, int layer, int expert, double t);
+int vmm_cache_cancel(vmm_cache *c, int layer, int expert);
+int vmm_cache_executed(vmm_cache *c, int layer, int expert);
+/* window: n keys (layer,expert) pairs; prio: n_p (layer, expert, value) triples as doubles */
+int vmm_cache_reclassify(vmm_cache *c, const int32_t *h_window, int n, int grace,
+                         const int32_t *h_prio_keys, const double *h_prio_vals, int n_p);
+int vmm_cache_select_victim(vmm_cache *c);
+int vmm_cache_info(const vmm_cache *c, long long *evictions, int *occupancy, int *step);
+int vmm_cache_slab(const vmm_cache *c, int slab, int *layer, int *expert, int *state, int *cls,
+                   double *priority, double *ready, int *last_window_step, int *executed, int *seq);
+
+/* ------------------------------------------------------------------------
+ * Expert transfer runtime: pinned host pool -> HBM slab arena on a dedicated
+ * copy stream with one event per slab fill; slab reuse waits on the compute
+ * event of the layer that last read the slab (pipeline.py:440-494 made real).
+ * ------------------------------------------------------------------------ */
+typedef struct vmm_xfer vmm_xfer;
+int vmm_xfer_create(int num_slabs, size_t slab_bytes, int max_layers, vmm_xfer **out);
+void vmm_xfer_destroy(vmm_xfer *x);
+/* enqueue host->slab copy of `bytes` from h_src (pinned) into d_dst on the copy
+ * stream; it first waits for the compute event of the last layer that was
+ * fenced on this slab (so a slab is never overwritten while being read).
+ * `reserved` must be 0. */
+int vmm_xfer_copy(vmm_xfer *x, int slab, const void *h_src, void *d_dst, size_t bytes, int reserved);
+/* make `compute_stream` wait for the newest fill among the given slabs
+ * (FIFO copy stream => covers all older fills) and register them as read by
+ * the next layer */
+int vmm_xfer_fence(vmm_xfer *x, const int32_t *h_slabs, int n, void *compute_stream);
+/* record the compute event closing the reads registered since the last call */
+int vmm_xfer_layer_done(vmm_xfer *x, int layer, void *compute_stream);
+int vmm_xfer_reset_stats(vmm_xfer *x);
+int vmm_xfer_sync(vmm_xfer *x);
+/* copy-stream accounting: bytes issued and wall ms between first and last copy (events) */
+int vmm_xfer_stats(vmm_xfer *x, double *bytes, double *busy_ms, long long *copies);
+void *vmm_xfer_stream(vmm_xfer *x);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VISMMOE_H */

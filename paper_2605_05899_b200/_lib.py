@@ -1,0 +1,161 @@
+"""ctypes binding of libvismmoe.so (the C-ABI declared in include/vismmoe.h).
+
+The library is built in-tree by `paper_2605_05899_b200.build` for sm_100a.
+There is deliberately no fallback: if the library is missing, or no sm_100
+device is present when a device entry point is used, this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from .errors import DeviceError, raise_status
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libvismmoe.so")
+
+P = C.c_void_p
+I32 = C.c_int
+I64 = C.c_longlong
+F64 = C.c_double
+SZ = C.c_size_t
+PI32 = C.POINTER(C.c_int32)
+PF64 = C.POINTER(C.c_double)
+
+
+class EngineConfig(C.Structure):
+    _fields_ = [
+        ("layers", I32), ("experts", I32), ("num_slabs", I32), ("victim_fifo", I32),
+        ("speculative_grace", I32), ("budget", I32), ("window", I32), ("l_pinned", I32),
+        ("shared", I32), ("prefetching", I32), ("reactive", I32), ("event_log", I32),
+        ("transfer_ms", F64), ("gpu_ms", F64), ("boot_ms", F64), ("decay", PF64),
+    ]
+
+
+class EngineEvent(C.Structure):
+    _fields_ = [("t", F64), ("kind", C.c_int32), ("layer", C.c_int32), ("expert", C.c_int32), ("slab", C.c_int32)]
+
+
+class EngineReport(C.Structure):
+    _fields_ = [
+        ("makespan", F64), ("total_compute", F64), ("total_transfer", F64), ("exposed_transfer", F64),
+        ("prefill_ms", F64), ("hits", I64), ("misses", I64), ("stalls", I64), ("rejected_loads", I64),
+        ("on_demand_transfers", I64), ("inflight_waits", I64), ("evictions", I64), ("decode_steps", I32),
+    ]
+
+
+_SIGS = {
+    "vmm_last_error": (C.c_char_p, []),
+    "vmm_abi_version": (I32, []),
+    "vmm_device_check": (I32, [I32]),
+    "vmm_prune": (I32, [P, P, P, P, P, P, I32, I32, I32, I32, I32, F64, P, P, P, P, P, P, P, P, P]),
+    "vmm_gather_rows": (I32, [P, P, I32, I32, P, P]),
+    "vmm_route_topk": (I32, [P, P, I32, I32, I32, I32, P, P, P, P, P]),
+    "vmm_demand_counts": (I32, [P, I32, I32, I32, I32, P, I32, P, I32, P, P]),
+    "vmm_oracle_targets": (I32, [P, I32, I32, P, I32, I32, P, P, P]),
+    "vmm_history": (I32, [P, I32, I32, P, I32, P, P, P]),
+    "vmm_mlp_predict": (I32, [P, P, I32, P, P, I32, P, P, I32, I32, P, P, I32, P, P, I32, P, P, P, P, P]),
+    "vmm_gate_lookahead": (I32, [P, P, I32, I32, I32, I32, P, P, P]),
+    "vmm_permute_plan": (I32, [P, I32, I32, I32, P, P, P, P]),
+    "vmm_permute_rows": (I32, [P, P, I32, I32, P, P]),
+    "vmm_combine": (I32, [P, P, P, P, I32, I32, I32, P, P]),
+    "vmm_grouped_swiglu": (I32, [P, P, I32, I32, I32, I32, P, P, I64, P, P, P, P]),
+    "vmm_grouped_swiglu_simt": (I32, [P, P, I32, I32, I32, I32, P, P, P, P, P, P]),
+    "vmm_engine_create": (I32, [C.POINTER(EngineConfig), C.POINTER(P)]),
+    "vmm_engine_destroy": (None, [P]),
+    "vmm_engine_begin": (I32, [P, P]),
+    "vmm_engine_layer": (I32, [P, I32, P, I32, I32, I32, P]),
+    "vmm_engine_end_step": (I32, [P]),
+    "vmm_engine_finish": (I32, [P, C.POINTER(EngineReport)]),
+    "vmm_engine_emits": (I32, [P, I32, I32]),
+    "vmm_engine_events": (I32, [P, P, I32]),
+    "vmm_engine_pending_events": (I32, [P]),
+    "vmm_engine_copies": (I32, [P, P, I32]),
+    "vmm_engine_decode_ms": (I32, [P, P, I32]),
+    "vmm_engine_layer_stats": (I32, [P, P, I32]),
+    "vmm_engine_slab_of": (I32, [P, I32, I32]),
+    "vmm_engine_slab": (I32, [P, I32, PI32, PI32, PI32, PI32, PF64, PF64]),
+    "vmm_cache_create": (I32, [I32, I32, C.POINTER(P)]),
+    "vmm_cache_destroy": (None, [P]),
+    "vmm_cache_lookup": (I32, [P, I32, I32, PF64]),
+    "vmm_cache_request": (I32, [P, I32, I32, F64, I32, PI32, PI32, PI32, PI32]),
+    "vmm_cache_set_ready": (I32, [P, I32, I32, F64]),
+    "vmm_cache_complete": (I32, [P, I32, I32, F64]),
+    "vmm_cache_cancel": (I32, [P, I32, I32]),
+    "vmm_cache_executed": (I32, [P, I32, I32]),
+    "vmm_cache_reclassify": (I32, [P, P, I32, I32, P, P, I32]),
+    "vmm_cache_select_victim": (I32, [P]),
+    "vmm_cache_info": (I32, [P, C.POINTER(I64), PI32, PI32]),
+    "vmm_cache_slab": (I32, [P, I32, PI32, PI32, PI32, PI32, PF64, PF64, PI32, PI32, PI32]),
+    "vmm_xfer_create": (I32, [I32, SZ, I32, C.POINTER(P)]),
+    "vmm_xfer_destroy": (None, [P]),
+    "vmm_xfer_copy": (I32, [P, I32, P, P, SZ, I32]),
+    "vmm_xfer_fence": (I32, [P, P, I32, P]),
+    "vmm_xfer_layer_done": (I32, [P, I32, P]),
+    "vmm_xfer_sync": (I32, [P]),
+    "vmm_xfer_stats": (I32, [P, PF64, PF64, C.POINTER(I64)]),
+    "vmm_xfer_reset_stats": (I32, [P]),
+    "vmm_xfer_stream": (P, [P]),
+}
+
+_lock = threading.Lock()
+_lib = None
+_device_ok = None
+
+
+def exported_symbols() -> list[str]:
+    return sorted(_SIGS)
+
+
+def load():
+    """Load the shared library (no device needed)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise DeviceError(
+                    f"{LIB_PATH} is missing: build it with `python -m paper_2605_05899_b200.build` "
+                    "(there is no CPU fallback)"
+                )
+            lib = C.CDLL(LIB_PATH)
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def check(status: int) -> None:
+    if status:
+        msg = load().vmm_last_error().decode(errors="replace")
+        raise_status(status, msg)
+
+
+def lib():
+    """Library handle for device entry points: requires an sm_100 GPU."""
+    global _device_ok
+    L = load()
+    if _device_ok is None:
+        import torch
+
+        if not torch.cuda.is_available():
+            _device_ok = False
+        else:
+            _device_ok = L.vmm_device_check(torch.cuda.current_device()) == 0
+    if not _device_ok:
+        raise DeviceError("the VisMMOE hot path needs an sm_100 (B200) device; no CPU fallback exists")
+    return L
+
+
+def ptr(t) -> int | None:
+    """data_ptr of a torch tensor (None passes NULL)."""
+    return None if t is None else t.data_ptr()
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream

@@ -1,0 +1,418 @@
+// Grouped bf16 SwiGLU expert FFN on 5th-gen tensor cores (sm_100a).
+//
+//   H1[m, :] = SiLU(Xp[m] . Wg^T) * (Xp[m] . Wu^T)      (GEMM1, fused epilogue)
+//   Y [m, :] = H1[m] . Wd^T                              (GEMM2)
+// for the rows m of each expert (contiguous after vmm_permute_plan), with the
+// expert's weights read from an HBM arena slot chosen by the expert cache
+// (slot table).  No reference numerics exist (the reference models expert
+// compute as a constant, pkg/src/moesim/pipeline.py:546-552).
+//
+// Kernel anatomy (one 128x128 output tile per CTA, 6 warps):
+//   warp 0      : TMA producer  -- A tile [128 x 64] of Xp/H1 and B tile
+//                 [128 x 64] of the weight slot, SWIZZLE_128B, mbarrier tx
+//   warp 1      : TMEM allocator + single-thread tcgen05.mma issuer
+//                 (M=128, N=128, K=16 per instruction, fp32 accumulate in TMEM)
+//   warps 2..5  : epilogue -- tcgen05.ld 32x32b, SwiGLU / bf16 pack, stores
+// A kStages-deep smem ring (full/empty mbarriers) overlaps TMA with MMA.
+#include <cuda.h>
+#include <math.h>
+
+#include <mutex>
+#include <unordered_map>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 64;
+constexpr int kStages = 4;
+constexpr int kThreads = 192;
+constexpr uint32_t kTileBytes = BM * BK * 2;  // 16 KB (A) == BN*BK*2 (B)
+constexpr uint32_t kStageBytes = 2 * kTileBytes;
+constexpr size_t kSmemBytes = (size_t)kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+
+// ---- PTX helpers -----------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap *map, uint64_t *bar, void *dst, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap *map, uint64_t *bar, void *dst, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+// K-major, SWIZZLE_128B smem matrix descriptor (rows of 128 B, 8-row groups 1024 B apart)
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);  // start address
+  d |= (uint64_t)1 << 16;                 // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;       // SBO: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                 // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
+  return d;
+}
+// kind::f16 instruction descriptor: BF16 x BF16 -> F32, K-major A and B, M=128, N=128
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+// 32 lanes x 32 consecutive fp32 columns -> 32 registers per thread
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t *>(&h);
+}
+
+__device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
+
+// ---- the grouped GEMM ---------------------------------------------------
+// kSwiGLU: epilogue fuses SiLU(gate) * up over the interleaved 64|64 column
+// halves and writes 64 bf16 per row; otherwise writes 128 bf16 per row.
+template <bool kSwiGLU>
+__global__ void __launch_bounds__(kThreads, 1)
+grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                    const int32_t *__restrict__ offsets, const int32_t *__restrict__ slot_of, int E, int K,
+                    __nv_bfloat16 *__restrict__ out, int ld_out) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * kStageBytes);
+  uint64_t *empty = full + kStages;
+  uint64_t *tmem_full = empty + kStages;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
+  __shared__ int s_expert, s_row0, s_row_end, s_slot;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_tile = blockIdx.x;
+  const int m_tile = blockIdx.y;
+
+  // locate (expert, first row) of this m-tile: tiles are ceil(M_e / BM) per expert
+  if (threadIdx.x == 0) {
+    int acc = 0, found = -1, r0 = 0, r1 = 0;
+    for (int e = 0; e < E; ++e) {
+      int lo = offsets[e], hi = offsets[e + 1];
+      int nt = (hi - lo + BM - 1) / BM;
+      if (m_tile < acc + nt) {
+        found = e;
+        r0 = lo + (m_tile - acc) * BM;
+        r1 = hi;
+        break;
+      }
+      acc += nt;
+    }
+    s_expert = found;
+    s_row0 = r0;
+    s_row_end = r1;
+    s_slot = found >= 0 ? slot_of[found] : 0;
+  }
+  __syncthreads();
+  if (s_expert < 0) return;  // uniform: surplus tile slot
+  const int row0 = s_row0, row_end = s_row_end, slot = s_slot;
+  const int nk = K / BK;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&map_a);
+    prefetch_tmap(&map_b);
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % kStages;
+        if (kb >= kStages) mbar_wait(&empty[s], ((kb / kStages) - 1) & 1);
+        unsigned char *a_dst = smem + s * kStageBytes;
+        unsigned char *b_dst = a_dst + kTileBytes;
+        mbar_expect_tx(&full[s], kStageBytes);
+        tma_load_2d(&map_a, &full[s], a_dst, kb * BK, row0);
+        tma_load_3d(&map_b, &full[s], b_dst, kb * BK, n_tile * BN, slot);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % kStages;
+        mbar_wait(&full[s], (kb / kStages) & 1);
+        tc_fence_after();
+        const uint32_t a_addr = smem_u32(smem + s * kStageBytes);
+        const uint32_t b_addr = a_addr + kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk) {
+          // advance 16 bf16 = 32 B along K inside the 128 B swizzle atom
+          umma_bf16(tmem, sw128_desc(a_addr + kk * 32), sw128_desc(b_addr + kk * 32), (kb | kk) != 0);
+        }
+        umma_commit(&empty[s]);
+      }
+      umma_commit(tmem_full);
+    }
+    __syncwarp();
+  } else {
+    // epilogue: warp w reads TMEM lanes [32*(w%4), +32)
+    const int q = warp & 3;
+    const int row = row0 + q * 32 + lane;
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    const uint32_t t_base = tmem + ((uint32_t)(q * 32) << 16);
+    if constexpr (kSwiGLU) {
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        float g[32], u[32];
+        tmem_ld32(t_base + half * 32, g);
+        tmem_ld32(t_base + 64 + half * 32, u);
+        if (row < row_end) {
+          uint4 *dst = reinterpret_cast<uint4 *>(out + (long long)row * ld_out + n_tile * (BN / 2) + half * 32);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            uint4 o;
+            o.x = pack_bf16(silu(g[8 * v + 0]) * u[8 * v + 0], silu(g[8 * v + 1]) * u[8 * v + 1]);
+            o.y = pack_bf16(silu(g[8 * v + 2]) * u[8 * v + 2], silu(g[8 * v + 3]) * u[8 * v + 3]);
+            o.z = pack_bf16(silu(g[8 * v + 4]) * u[8 * v + 4], silu(g[8 * v + 5]) * u[8 * v + 5]);
+            o.w = pack_bf16(silu(g[8 * v + 6]) * u[8 * v + 6], silu(g[8 * v + 7]) * u[8 * v + 7]);
+            dst[v] = o;
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) {
+        float a[32];
+        tmem_ld32(t_base + c * 32, a);
+        if (row < row_end) {
+          uint4 *dst = reinterpret_cast<uint4 *>(out + (long long)row * ld_out + n_tile * BN + c * 32);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            uint4 o;
+            o.x = pack_bf16(a[8 * v + 0], a[8 * v + 1]);
+            o.y = pack_bf16(a[8 * v + 2], a[8 * v + 3]);
+            o.z = pack_bf16(a[8 * v + 4], a[8 * v + 5]);
+            o.w = pack_bf16(a[8 * v + 6], a[8 * v + 7]);
+            dst[v] = o;
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+  }
+}
+
+// ---- CUDA-core cross-check path -------------------------------------------
+__device__ __forceinline__ int expert_of_row(const int32_t *offsets, int E, int row) {
+  int lo = 0, hi = E - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (offsets[mid] <= row) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void simt_gemm1_kernel(const __nv_bfloat16 *__restrict__ xp, const int32_t *__restrict__ offsets, int E,
+                                  int M, int H, int I, const __nv_bfloat16 *__restrict__ w13,
+                                  const int32_t *__restrict__ slot_of, __nv_bfloat16 *__restrict__ h1) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)M * I) return;
+  int m = (int)(idx / I), f = (int)(idx % I);
+  int e = expert_of_row(offsets, E, m);
+  const __nv_bfloat16 *w = w13 + (long long)slot_of[e] * 2 * I * H;
+  int gr = (f / 64) * 128 + (f % 64), ur = gr + 64;
+  float g = 0.f, u = 0.f;
+  for (int kk = 0; kk < H; ++kk) {
+    float x = __bfloat162float(xp[(long long)m * H + kk]);
+    g = fmaf(x, __bfloat162float(w[(long long)gr * H + kk]), g);
+    u = fmaf(x, __bfloat162float(w[(long long)ur * H + kk]), u);
+  }
+  h1[(long long)m * I + f] = __float2bfloat16(silu(g) * u);
+}
+
+__global__ void simt_gemm2_kernel(const __nv_bfloat16 *__restrict__ h1, const int32_t *__restrict__ offsets, int E,
+                                  int M, int H, int I, const __nv_bfloat16 *__restrict__ w2,
+                                  const int32_t *__restrict__ slot_of, __nv_bfloat16 *__restrict__ y) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)M * H) return;
+  int m = (int)(idx / H), n = (int)(idx % H);
+  int e = expert_of_row(offsets, E, m);
+  const __nv_bfloat16 *w = w2 + (long long)slot_of[e] * H * I;
+  float a = 0.f;
+  for (int kk = 0; kk < I; ++kk) a = fmaf(__bfloat162float(h1[(long long)m * I + kk]),
+                                          __bfloat162float(w[(long long)n * I + kk]), a);
+  y[(long long)m * H + n] = __float2bfloat16(a);
+}
+
+// ---- host side: tensor maps via the driver entry point ---------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+int make_map(CUtensorMap *m, const void *base, int rank, const uint64_t *dims, const uint64_t *strides_bytes,
+             const uint32_t *box) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return vmm::fail(VMM_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t d[3], s[2];
+  cuuint32_t b[3], es[3] = {1, 1, 1};
+  for (int i = 0; i < rank; ++i) { d[i] = dims[i]; b[i] = box[i]; }
+  for (int i = 0; i < rank - 1; ++i) s[i] = strides_bytes[i];
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void *>(base), d, s, b, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return vmm::fail(VMM_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return VMM_OK;
+}
+
+}  // namespace
+
+extern "C" int vmm_grouped_swiglu(const void *d_xp, const int32_t *d_offsets, int E, int M_total, int H, int I,
+                                  const void *d_w13_arena, const void *d_w2_arena, long long n_slots,
+                                  const int32_t *d_slot_of_expert, void *d_h1, void *d_y, void *stream) {
+  if (M_total <= 0) return VMM_OK;
+  if (H % BN || H % BK || I % 64 || I % BK || (2 * I) % BN)
+    return vmm::fail(VMM_EVALIDATION, "grouped_swiglu: hidden must be a multiple of 128, inter of 64");
+  if (E < 1 || E > VMM_MAX_EXPERTS) return vmm::fail(VMM_EVALIDATION, "experts must lie in [1, 256]");
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e1 = cudaFuncSetAttribute(grouped_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)kSmemBytes);
+    cudaError_t e2 = cudaFuncSetAttribute(grouped_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)kSmemBytes);
+    if (e1 != cudaSuccess) return vmm::cuda_status(e1, "ffn attr");
+    if (e2 != cudaSuccess) return vmm::cuda_status(e2, "ffn attr");
+    attr = true;
+  }
+  CUtensorMap ma1, mb1, ma2, mb2;
+  int st;
+  {
+    uint64_t dims[2] = {(uint64_t)H, (uint64_t)M_total};
+    uint64_t str[1] = {(uint64_t)H * 2};
+    uint32_t box[2] = {BK, BM};
+    if ((st = make_map(&ma1, d_xp, 2, dims, str, box))) return st;
+  }
+  {
+    uint64_t dims[3] = {(uint64_t)H, (uint64_t)2 * I, (uint64_t)n_slots};
+    uint64_t str[2] = {(uint64_t)H * 2, (uint64_t)2 * I * H * 2};
+    uint32_t box[3] = {BK, BN, 1};
+    if ((st = make_map(&mb1, d_w13_arena, 3, dims, str, box))) return st;
+  }
+  {
+    uint64_t dims[2] = {(uint64_t)I, (uint64_t)M_total};
+    uint64_t str[1] = {(uint64_t)I * 2};
+    uint32_t box[2] = {BK, BM};
+    if ((st = make_map(&ma2, d_h1, 2, dims, str, box))) return st;
+  }
+  {
+    uint64_t dims[3] = {(uint64_t)I, (uint64_t)H, (uint64_t)n_slots};
+    uint64_t str[2] = {(uint64_t)I * 2, (uint64_t)H * I * 2};
+    uint32_t box[3] = {BK, BN, 1};
+    if ((st = make_map(&mb2, d_w2_arena, 3, dims, str, box))) return st;
+  }
+  const int m_tiles = (M_total + BM - 1) / BM + E;
+  cudaStream_t s = (cudaStream_t)stream;
+  dim3 g1((2 * I) / BN, m_tiles), g2(H / BN, m_tiles);
+  grouped_gemm_kernel<true><<<g1, kThreads, kSmemBytes, s>>>(ma1, mb1, d_offsets, d_slot_of_expert, E, H,
+                                                             (__nv_bfloat16 *)d_h1, I);
+  VMM_LAUNCH_CHECK("grouped_gemm_kernel<swiglu>");
+  grouped_gemm_kernel<false><<<g2, kThreads, kSmemBytes, s>>>(ma2, mb2, d_offsets, d_slot_of_expert, E, I,
+                                                              (__nv_bfloat16 *)d_y, H);
+  VMM_LAUNCH_CHECK("grouped_gemm_kernel<down>");
+  return VMM_OK;
+}
+
+extern "C" int vmm_grouped_swiglu_simt(const void *d_xp, const int32_t *d_offsets, int E, int M_total, int H, int I,
+                                       const void *d_w13_arena, const void *d_w2_arena,
+                                       const int32_t *d_slot_of_expert, void *d_h1, void *d_y, void *stream) {
+  if (M_total <= 0) return VMM_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  long long n1 = (long long)M_total * I, n2 = (long long)M_total * H;
+  simt_gemm1_kernel<<<(unsigned)((n1 + 255) / 256), 256, 0, s>>>((const __nv_bfloat16 *)d_xp, d_offsets, E, M_total,
+                                                                  H, I, (const __nv_bfloat16 *)d_w13_arena,
+                                                                  d_slot_of_expert, (__nv_bfloat16 *)d_h1);
+  VMM_LAUNCH_CHECK("simt_gemm1_kernel");
+  simt_gemm2_kernel<<<(unsigned)((n2 + 255) / 256), 256, 0, s>>>((const __nv_bfloat16 *)d_h1, d_offsets, E, M_total,
+                                                                  H, I, (const __nv_bfloat16 *)d_w2_arena,
+                                                                  d_slot_of_expert, (__nv_bfloat16 *)d_y);
+  VMM_LAUNCH_CHECK("simt_gemm2_kernel");
+  return VMM_OK;
+}

@@ -1,0 +1,166 @@
+// Token permutation by expert and the gate-weighted combine.
+//
+// The reference executes each layer's demanded experts in ascending id order
+// (pkg/src/moesim/pipeline.py:573) and has no numerics; here the N*k picks of
+// a layer are stably counting-sorted by expert (ties by (token, slot)) so each
+// expert's rows are contiguous for the grouped FFN, and the combine reduces
+// the k expert outputs per token in slot order (deterministic, no atomics).
+#include "common.cuh"
+
+namespace {
+
+constexpr int kThreads = 1024;
+constexpr int kWarps = kThreads / 32;
+
+__global__ void __launch_bounds__(kThreads, 1)
+permute_plan_kernel(const int32_t *__restrict__ ids, int n_picks, int k, int E, int32_t *__restrict__ offsets,
+                    int32_t *__restrict__ src_row, int32_t *__restrict__ pos) {
+  extern __shared__ int32_t cnt[];  // [kWarps][E] then [E] totals
+  int32_t *tot = cnt + kWarps * E;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < kWarps * E + E; i += kThreads) cnt[i] = 0;
+  __syncthreads();
+  const int seg = (n_picks + kWarps - 1) / kWarps;
+  const int lo = warp * seg;
+  const int hi = min(n_picks, lo + seg);
+  // pass 1: per-warp counts (segment order is the pick order)
+  for (int c0 = lo; c0 < hi; c0 += 32) {
+    int i = c0 + lane;
+    int e = (i < hi) ? ids[i] : -1;
+    unsigned peers = __match_any_sync(0xffffffffu, e);
+    int leader = __ffs(peers) - 1;
+    if (e >= 0 && lane == leader) cnt[warp * E + e] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // expert totals, exclusive scan over experts, then per-warp bases
+  for (int e = threadIdx.x; e < E; e += kThreads) {
+    int s = 0;
+    for (int w = 0; w < kWarps; ++w) s += cnt[w * E + e];
+    tot[e] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int e = 0; e < E; ++e) {
+      offsets[e] = run;
+      int t = tot[e];
+      tot[e] = run;
+      run += t;
+    }
+    offsets[E] = run;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += kThreads) {
+    int run = tot[e];
+    for (int w = 0; w < kWarps; ++w) {
+      int c = cnt[w * E + e];
+      cnt[w * E + e] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  // pass 2: stable positions
+  for (int c0 = lo; c0 < hi; c0 += 32) {
+    int i = c0 + lane;
+    int e = (i < hi) ? ids[i] : -1;
+    unsigned peers = __match_any_sync(0xffffffffu, e);
+    int leader = __ffs(peers) - 1;
+    int rank = __popc(peers & ((1u << lane) - 1u));
+    int basep = (e >= 0) ? cnt[warp * E + e] : 0;
+    if (e >= 0) {
+      int p = basep + rank;
+      pos[i] = p;
+      src_row[p] = i / k;
+    }
+    __syncwarp();
+    if (e >= 0 && lane == leader) cnt[warp * E + e] = basep + __popc(peers);
+    __syncwarp();
+  }
+}
+
+// Xp[p] = X[src_row[p]] (bf16 rows, 16-byte vectors, one warp per row)
+__global__ void permute_rows_kernel(const uint4 *__restrict__ x, const int32_t *__restrict__ src_row, int n,
+                                    int row_vec, uint4 *__restrict__ xp) {
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int r = warp; r < n; r += nw) {
+    const uint4 *s = x + (long long)src_row[r] * row_vec;
+    uint4 *d = xp + (long long)r * row_vec;
+    for (int c = lane; c < row_vec; c += 32) d[c] = __ldg(s + c);
+  }
+}
+
+// out[t] = resid[t] + sum_j gates[t,j] * Y[pos[t,j]]; each thread owns 8 columns
+__global__ void combine_kernel(const uint4 *__restrict__ y, const int32_t *__restrict__ pos,
+                               const float *__restrict__ gates, const uint4 *__restrict__ resid, int N, int k,
+                               int row_vec, uint4 *__restrict__ out) {
+  long long total = (long long)N * row_vec;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    int t = (int)(i / row_vec);
+    int c = (int)(i % row_vec);
+    float acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+    for (int j = 0; j < k; ++j) {
+      float g = gates[(long long)t * k + j];
+      uint4 v = __ldg(y + (long long)pos[(long long)t * k + j] * row_vec + c);
+      const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&v);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = fmaf(g, __bfloat162float(h[q]), acc[q]);
+    }
+    uint4 rv = resid ? __ldg(resid + i) : make_uint4(0, 0, 0, 0);
+    const __nv_bfloat16 *rh = reinterpret_cast<const __nv_bfloat16 *>(&rv);
+    uint4 o;
+    __nv_bfloat16 *oh = reinterpret_cast<__nv_bfloat16 *>(&o);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) oh[q] = __float2bfloat16(__bfloat162float(rh[q]) + acc[q]);
+    out[i] = o;
+  }
+}
+
+}  // namespace
+
+extern "C" int vmm_permute_plan(const int32_t *d_ids, int N, int k, int E, int32_t *d_offsets, int32_t *d_src_row,
+                                int32_t *d_pos, void *stream) {
+  if (E < 1 || E > VMM_MAX_EXPERTS) return vmm::fail(VMM_EVALIDATION, "experts must lie in [1, 256]");
+  size_t smem = sizeof(int32_t) * ((size_t)kWarps * E + E);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(permute_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(sizeof(int32_t) * (kWarps * VMM_MAX_EXPERTS + VMM_MAX_EXPERTS)));
+    if (e != cudaSuccess) return vmm::cuda_status(e, "permute attr");
+    attr = true;
+  }
+  permute_plan_kernel<<<1, kThreads, smem, (cudaStream_t)stream>>>(d_ids, N * k, k, E, d_offsets, d_src_row, d_pos);
+  VMM_LAUNCH_CHECK("permute_plan_kernel");
+  return VMM_OK;
+}
+
+extern "C" int vmm_permute_rows(const void *d_x, const int32_t *d_src_row, int n_rows, int H, void *d_xp,
+                                void *stream) {
+  if (n_rows <= 0) return VMM_OK;
+  if ((H * 2) % 16) return vmm::fail(VMM_EVALIDATION, "hidden size must be a multiple of 8");
+  int row_vec = H * 2 / 16;
+  int blocks = 148 * 8;
+  permute_rows_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((const uint4 *)d_x, d_src_row, n_rows, row_vec,
+                                                                (uint4 *)d_xp);
+  VMM_LAUNCH_CHECK("permute_rows_kernel");
+  return VMM_OK;
+}
+
+extern "C" int vmm_combine(const void *d_y, const int32_t *d_pos, const float *d_gates, const void *d_resid, int N,
+                           int k, int H, void *d_out, void *stream) {
+  if (N <= 0) return VMM_OK;
+  if ((H * 2) % 16) return vmm::fail(VMM_EVALIDATION, "hidden size must be a multiple of 8");
+  int row_vec = H * 2 / 16;
+  long long total = (long long)N * row_vec;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  combine_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((const uint4 *)d_y, d_pos, d_gates,
+                                                           (const uint4 *)d_resid, N, k, row_vec, (uint4 *)d_out);
+  VMM_LAUNCH_CHECK("combine_kernel");
+  return VMM_OK;
+}

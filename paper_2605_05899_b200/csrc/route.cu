@@ -1,0 +1,141 @@
+// Router: gate projection + per-token top-k + softmax over the selected logits.
+//
+// The reference has no router; its output contract is the RoutingTrace
+// layout (pkg/src/moesim/trace.py:80-81; gates > 0 summing to 1, :375-382).
+// Tie-break on equal logits: lower expert id first (as predictor.py:439).
+// Also used for the gate-reuse lookahead predictor (layer l+1's gate on h_l).
+//
+// v1 contraction: shared-memory tiled fp32 FMA, one fixed accumulation order
+// per (token, expert) so integer-valued inputs give exact logits.
+#include <math.h>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int kTok = 16;    // tokens per CTA
+constexpr int kKc = 64;     // K chunk
+constexpr int kThreads = 256;
+constexpr int kMaxE = 256;
+constexpr int kMaxK = 16;
+
+__global__ void __launch_bounds__(kThreads)
+route_kernel(const __nv_bfloat16 *__restrict__ x, const __nv_bfloat16 *__restrict__ wg, int N, int H, int E,
+             int k, int32_t *__restrict__ ids, float *__restrict__ gates, float *__restrict__ logits_out,
+             uint32_t *__restrict__ counts) {
+  extern __shared__ __align__(16) float sm[];
+  float *xs = sm;                      // [kTok][kKc+1]
+  float *ws = xs + kTok * (kKc + 1);   // [E][kKc+1]
+  float *lg = ws + E * (kKc + 1);      // [kTok][E]
+  const int t0 = blockIdx.x * kTok;
+  const int tx = threadIdx.x & 31;     // expert lane
+  const int ty = threadIdx.x >> 5;     // token group (8 groups x 2 tokens)
+  const int ej = (E + 31) / 32;
+  float acc[2][kMaxE / 32];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int j = 0; j < kMaxE / 32; ++j) acc[a][j] = 0.f;
+
+  for (int k0 = 0; k0 < H; k0 += kKc) {
+    for (int i = threadIdx.x; i < kTok * kKc; i += kThreads) {
+      int r = i / kKc, c = i % kKc;
+      int t = t0 + r;
+      xs[r * (kKc + 1) + c] = (t < N && k0 + c < H) ? __bfloat162float(x[(long long)t * H + k0 + c]) : 0.f;
+    }
+    for (int i = threadIdx.x; i < E * kKc; i += kThreads) {
+      int r = i / kKc, c = i % kKc;
+      ws[r * (kKc + 1) + c] = (k0 + c < H) ? __bfloat162float(wg[(long long)r * H + k0 + c]) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int c = 0; c < kKc; ++c) {
+      float xa = xs[(2 * ty) * (kKc + 1) + c];
+      float xb = xs[(2 * ty + 1) * (kKc + 1) + c];
+#pragma unroll
+      for (int j = 0; j < kMaxE / 32; ++j) {
+        if (j < ej) {
+          int e = tx + 32 * j;
+          float w = (e < E) ? ws[e * (kKc + 1) + c] : 0.f;
+          acc[0][j] = fmaf(xa, w, acc[0][j]);
+          acc[1][j] = fmaf(xb, w, acc[1][j]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int j = 0; j < kMaxE / 32; ++j) {
+      int e = tx + 32 * j;
+      if (j < ej && e < E) lg[(2 * ty + a) * E + e] = acc[a][j];
+    }
+  __syncthreads();
+
+  // top-k per token: one warp per token
+  for (int r = ty; r < kTok; r += kThreads / 32) {
+    int t = t0 + r;
+    if (t >= N) break;
+    const float *row = lg + r * E;
+    if (logits_out)
+      for (int e = tx; e < E; e += 32) logits_out[(long long)t * E + e] = row[e];
+    unsigned taken[kMaxE / 32];
+#pragma unroll
+    for (int j = 0; j < kMaxE / 32; ++j) taken[j] = 0;
+    float vals[kMaxK];
+    int sel[kMaxK];
+    for (int s = 0; s < k; ++s) {
+      float best = -INFINITY;
+      int bi = 0x7fffffff;
+      for (int j = 0; j < ej; ++j) {
+        int e = tx + 32 * j;
+        if (e < E && !((taken[j] >> tx) & 1u)) {
+          float v = row[e];
+          if (v > best || (v == best && e < bi) || bi == 0x7fffffff) { best = v; bi = e; }
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        float ov = __shfl_xor_sync(0xffffffffu, best, o);
+        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (oi != 0x7fffffff && (bi == 0x7fffffff || ov > best || (ov == best && oi < bi))) { best = ov; bi = oi; }
+      }
+      vals[s] = best;
+      sel[s] = bi;
+      if ((bi & 31) == tx) taken[bi >> 5] |= 1u << tx;
+    }
+    if (tx == 0) {
+      float m = vals[0];
+      float ex[kMaxK];
+      float sum = 0.f;
+      for (int s = 0; s < k; ++s) { ex[s] = expf(vals[s] - m); sum += ex[s]; }
+      for (int s = 0; s < k; ++s) {
+        if (ids) ids[(long long)t * k + s] = sel[s];
+        if (gates) gates[(long long)t * k + s] = ex[s] / sum;
+        if (counts) atomicAdd(&counts[sel[s]], 1u);
+      }
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" int vmm_route_topk(const void *d_x, const void *d_wg, int N, int H, int E, int k, int32_t *d_ids,
+                              float *d_gates, float *d_logits, uint32_t *d_counts, void *stream) {
+  if (N <= 0) return VMM_OK;
+  if (E < 1 || E > kMaxE) return vmm::fail(VMM_EVALIDATION, "router: experts must lie in [1, 256]");
+  if (k < 1 || k > kMaxK || k > E) return vmm::fail(VMM_EVALIDATION, "router: k must lie in [1, min(16, E)]");
+  size_t smem = sizeof(float) * ((size_t)kTok * (kKc + 1) + (size_t)E * (kKc + 1) + (size_t)kTok * E);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return vmm::cuda_status(e, "route attr");
+    attr = true;
+  }
+  int grid = (N + kTok - 1) / kTok;
+  route_kernel<<<grid, kThreads, smem, (cudaStream_t)stream>>>((const __nv_bfloat16 *)d_x,
+                                                              (const __nv_bfloat16 *)d_wg, N, H, E, k, d_ids,
+                                                              d_gates, d_logits, d_counts);
+  VMM_LAUNCH_CHECK("route_kernel");
+  return VMM_OK;
+}

@@ -1,0 +1,159 @@
+// Expert transfer runtime: pinned host pool -> HBM slab arena.
+//
+// Makes the reference's logical transfer channel (pkg/src/moesim/pipeline.py:
+// 440-494: one serial channel, issue order decided by the policy) real: every
+// decided issue becomes a cudaMemcpyAsync on ONE dedicated copy stream (FIFO,
+// so the physical order equals the decided order) followed by an event.
+//   * compute never reads a slab before its fill lands: vmm_xfer_fence makes
+//     the compute stream wait for the newest fill among the slabs a layer
+//     reads (FIFO => one wait covers all older fills);
+//   * a slab is never overwritten while a layer may still read it: the copy
+//     into slab s first waits for the compute event of the last layer fenced
+//     on s (again one wait per newer reader, FIFO on the compute stream).
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/vismmoe.h"
+
+namespace vmm {
+int fail(int code, const std::string &msg);
+}  // namespace vmm
+
+namespace {
+int cuda_status(cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return VMM_OK;
+  return vmm::fail(VMM_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+}  // namespace
+
+namespace {
+constexpr int kRing = 8192;
+}
+
+struct vmm_xfer {
+  cudaStream_t stream = nullptr;
+  std::vector<cudaEvent_t> fill_ev, read_ev;
+  std::vector<long long> slab_fill_seq, slab_read_seq;
+  long long fill_seq = 0, read_seq = 0, copy_waited_read = 0;
+  std::vector<int> pending_readers;
+  double bytes = 0.0;
+  long long copies = 0;
+  cudaEvent_t t_first = nullptr, t_last = nullptr;
+  bool timing_started = false;
+};
+
+extern "C" {
+
+int vmm_xfer_create(int num_slabs, size_t slab_bytes, int max_layers, vmm_xfer **out) {
+  (void)slab_bytes;
+  (void)max_layers;
+  auto *x = new vmm_xfer();
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  cudaError_t e = cudaStreamCreateWithPriority(&x->stream, cudaStreamNonBlocking, prio_hi);
+  if (e != cudaSuccess) { delete x; return cuda_status(e, "copy stream"); }
+  x->fill_ev.resize(kRing);
+  x->read_ev.resize(kRing);
+  for (int i = 0; i < kRing; ++i) {
+    if ((e = cudaEventCreateWithFlags(&x->fill_ev[i], cudaEventDisableTiming)) != cudaSuccess) break;
+    if ((e = cudaEventCreateWithFlags(&x->read_ev[i], cudaEventDisableTiming)) != cudaSuccess) break;
+  }
+  if (e == cudaSuccess) e = cudaEventCreate(&x->t_first);
+  if (e == cudaSuccess) e = cudaEventCreate(&x->t_last);
+  if (e != cudaSuccess) { vmm_xfer_destroy(x); return cuda_status(e, "copy events"); }
+  x->slab_fill_seq.assign(num_slabs, 0);
+  x->slab_read_seq.assign(num_slabs, 0);
+  *out = x;
+  return VMM_OK;
+}
+
+void vmm_xfer_destroy(vmm_xfer *x) {
+  if (!x) return;
+  if (x->stream) cudaStreamSynchronize(x->stream);
+  for (auto ev : x->fill_ev) if (ev) cudaEventDestroy(ev);
+  for (auto ev : x->read_ev) if (ev) cudaEventDestroy(ev);
+  if (x->t_first) cudaEventDestroy(x->t_first);
+  if (x->t_last) cudaEventDestroy(x->t_last);
+  if (x->stream) cudaStreamDestroy(x->stream);
+  delete x;
+}
+
+int vmm_xfer_copy(vmm_xfer *x, int slab, const void *h_src, void *d_dst, size_t bytes, int wait_layer) {
+  (void)wait_layer;
+  if (slab < 0 || slab >= (int)x->slab_fill_seq.size()) return vmm::fail(VMM_ECONTRACT, "slab out of range");
+  cudaError_t e;
+  long long r = x->slab_read_seq[slab];
+  if (r > x->copy_waited_read) {
+    if ((e = cudaStreamWaitEvent(x->stream, x->read_ev[(r - 1) % kRing], 0)) != cudaSuccess)
+      return cuda_status(e, "copy wait reader");
+    x->copy_waited_read = r;
+  }
+  if (!x->timing_started) {
+    cudaEventRecord(x->t_first, x->stream);
+    x->timing_started = true;
+  }
+  if ((e = cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyHostToDevice, x->stream)) != cudaSuccess)
+    return cuda_status(e, "expert copy");
+  x->fill_seq++;
+  if ((e = cudaEventRecord(x->fill_ev[(x->fill_seq - 1) % kRing], x->stream)) != cudaSuccess)
+    return cuda_status(e, "fill event");
+  x->slab_fill_seq[slab] = x->fill_seq;
+  x->bytes += (double)bytes;
+  x->copies++;
+  return VMM_OK;
+}
+
+int vmm_xfer_fence(vmm_xfer *x, const int32_t *slabs, int n, void *compute_stream) {
+  long long need = 0;
+  for (int i = 0; i < n; ++i) {
+    int s = slabs[i];
+    if (s < 0 || s >= (int)x->slab_fill_seq.size()) continue;
+    if (x->slab_fill_seq[s] > need) need = x->slab_fill_seq[s];
+    x->pending_readers.push_back(s);
+  }
+  if (need > 0) {
+    cudaError_t e = cudaStreamWaitEvent((cudaStream_t)compute_stream, x->fill_ev[(need - 1) % kRing], 0);
+    if (e != cudaSuccess) return cuda_status(e, "fence wait");
+  }
+  return VMM_OK;
+}
+
+int vmm_xfer_layer_done(vmm_xfer *x, int layer, void *compute_stream) {
+  (void)layer;
+  if (x->pending_readers.empty()) return VMM_OK;
+  x->read_seq++;
+  cudaError_t e = cudaEventRecord(x->read_ev[(x->read_seq - 1) % kRing], (cudaStream_t)compute_stream);
+  if (e != cudaSuccess) return cuda_status(e, "reader event");
+  for (int s : x->pending_readers) x->slab_read_seq[s] = x->read_seq;
+  x->pending_readers.clear();
+  return VMM_OK;
+}
+
+int vmm_xfer_sync(vmm_xfer *x) { return cuda_status(cudaStreamSynchronize(x->stream), "copy sync"); }
+
+int vmm_xfer_stats(vmm_xfer *x, double *bytes, double *busy_ms, long long *copies) {
+  *bytes = x->bytes;
+  *copies = x->copies;
+  *busy_ms = 0.0;
+  if (x->timing_started) {
+    cudaEventRecord(x->t_last, x->stream);
+    cudaEventSynchronize(x->t_last);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, x->t_first, x->t_last);
+    *busy_ms = ms;
+  }
+  return VMM_OK;
+}
+
+int vmm_xfer_reset_stats(vmm_xfer *x) {
+  x->bytes = 0.0;
+  x->copies = 0;
+  x->timing_started = false;
+  return VMM_OK;
+}
+
+void *vmm_xfer_stream(vmm_xfer *x) { return (void *)x->stream; }
+
+}  // extern "C"

@@ -1,0 +1,189 @@
+"""Torch-facing wrappers of the device entry points of libvismmoe.
+
+Each function takes device tensors, launches on the current (or given) CUDA
+stream and returns device tensors; nothing here copies to the host unless the
+name says so.  Every call goes through the C-ABI (`_lib`), which refuses to
+run without an sm_100 device.
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _lib
+from ._lib import check, ptr, stream_ptr
+
+_i32 = torch.int32
+
+
+def _dev():
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+# ---------------------------------------------------------------------------
+# prune
+# ---------------------------------------------------------------------------
+def prune(saliency, modality, prefix_routes, req_off, k_core, k_keep, experts: int, lam: float, stream=None):
+    """Batched compression.  Shapes: saliency f64 [T], modality u8 [T],
+    prefix_routes i32 [P, T, k], req_off i32 [R+1], k_core/k_keep i32 [R].
+    Returns dict of device tensors (see include/vismmoe.h vmm_prune)."""
+    L = _lib.lib()
+    T = int(saliency.shape[0])
+    P, _, k = (int(x) for x in prefix_routes.shape)
+    R = int(req_off.shape[0]) - 1
+    dev = saliency.device
+    out = dict(
+        s_norm=torch.empty(T, dtype=torch.float64, device=dev),
+        delta=torch.empty(T, dtype=torch.float64, device=dev),
+        score=torch.empty(T, dtype=torch.float64, device=dev),
+        flags=torch.empty(T, dtype=torch.uint8, device=dev),
+        retained=torch.empty(max(T, 1), dtype=_i32, device=dev),
+        n_retained=torch.empty(R, dtype=_i32, device=dev),
+        target=torch.zeros(R, 4, dtype=torch.int64, device=dev),
+        status=torch.full((R,), -1, dtype=_i32, device=dev),
+    )
+    check(L.vmm_prune(ptr(saliency), ptr(modality), ptr(prefix_routes), ptr(req_off), ptr(k_core), ptr(k_keep),
+                      R, T, P, k, experts, float(lam), ptr(out["s_norm"]), ptr(out["delta"]), ptr(out["score"]),
+                      ptr(out["flags"]), ptr(out["retained"]), ptr(out["n_retained"]), ptr(out["target"]),
+                      ptr(out["status"]), stream_ptr(stream)))
+    return out
+
+
+def gather_rows(src, idx, stream=None, out=None):
+    n = int(idx.shape[0])
+    H = int(src.shape[1])
+    out = torch.empty(n, H, dtype=src.dtype, device=src.device) if out is None else out
+    check(_lib.lib().vmm_gather_rows(ptr(src), ptr(idx), n, H, ptr(out), stream_ptr(stream)))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# router / predictors
+# ---------------------------------------------------------------------------
+def route_topk(x, w_gate, k: int, counts=None, want_logits=False, stream=None, ids=None, gates=None):
+    """x bf16 [N, H], w_gate bf16 [E, H] -> (ids i32 [N,k], gates f32 [N,k], logits|None)."""
+    N, H = (int(s) for s in x.shape)
+    E = int(w_gate.shape[0])
+    ids = torch.empty(N, k, dtype=_i32, device=x.device) if ids is None else ids
+    gates = torch.empty(N, k, dtype=torch.float32, device=x.device) if gates is None else gates
+    logits = torch.empty(N, E, dtype=torch.float32, device=x.device) if want_logits else None
+    check(_lib.lib().vmm_route_topk(ptr(x), ptr(w_gate), N, H, E, k, ptr(ids), ptr(gates), ptr(logits),
+                                    ptr(counts), stream_ptr(stream)))
+    return ids, gates, logits
+
+
+def demand_counts(routes, layers, ids, experts: int, stream=None, out=None):
+    """routes i32 [L, T, k]; layers i32 [n]; ids i32 [m] -> u32-as-i32 counts [n, E]."""
+    L_, T, k = (int(s) for s in routes.shape)
+    n = int(layers.shape[0])
+    out = torch.empty(n, experts, dtype=_i32, device=routes.device) if out is None else out
+    check(_lib.lib().vmm_demand_counts(ptr(routes), L_, T, k, experts, ptr(layers), n, ptr(ids), int(ids.shape[0]),
+                                       ptr(out), stream_ptr(stream)))
+    return out
+
+
+def oracle_targets(counts_all, ctx, window: int, decay, stream=None):
+    L_, E = (int(s) for s in counts_all.shape)
+    y = torch.empty(int(ctx.shape[0]), E, dtype=torch.float64, device=counts_all.device)
+    check(_lib.lib().vmm_oracle_targets(ptr(counts_all), L_, E, ptr(ctx), int(ctx.shape[0]), window, ptr(decay),
+                                        ptr(y), stream_ptr(stream)))
+    return y
+
+
+def history(counts_all, ctx, pow_table, stream=None):
+    L_, E = (int(s) for s in counts_all.shape)
+    y = torch.empty(int(ctx.shape[0]), E, dtype=torch.float64, device=counts_all.device)
+    check(_lib.lib().vmm_history(ptr(counts_all), L_, E, ptr(ctx), int(ctx.shape[0]), ptr(pow_table), ptr(y),
+                                 stream_ptr(stream)))
+    return y
+
+
+def mlp_predict(hist, emb, drift, ids, h_v, ctx, model: dict, want_features=False, stream=None):
+    n_ctx, E = (int(s) for s in hist.shape)
+    D = int(emb.shape[1])
+    dh = int(model["w1"].shape[0])
+    db = int(model["w2"].shape[0])
+    y = torch.empty(n_ctx, E, dtype=torch.float64, device=hist.device)
+    feat = torch.empty(n_ctx, E + 2 * D, dtype=torch.float64, device=hist.device) if want_features else None
+    check(_lib.lib().vmm_mlp_predict(ptr(hist), ptr(emb), D, ptr(drift), ptr(ids), int(ids.shape[0]), ptr(h_v),
+                                     ptr(ctx), n_ctx, E, ptr(model["w1"]), ptr(model["b1"]), dh, ptr(model["w2"]),
+                                     ptr(model["b2"]), db, ptr(model["wo"]), ptr(model["bo"]), ptr(feat), ptr(y),
+                                     stream_ptr(stream)))
+    return y, feat
+
+
+def gate_lookahead(x, w_next, k: int, stream=None, scratch=None, out=None):
+    N, H = (int(s) for s in x.shape)
+    E = int(w_next.shape[0])
+    scratch = torch.empty(E, dtype=_i32, device=x.device) if scratch is None else scratch
+    out = torch.empty(E, dtype=torch.float64, device=x.device) if out is None else out
+    check(_lib.lib().vmm_gate_lookahead(ptr(x), ptr(w_next), N, H, E, k, ptr(scratch), ptr(out),
+                                        stream_ptr(stream)))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# permutation / expert FFN / combine
+# ---------------------------------------------------------------------------
+def permute_plan(ids, experts: int, stream=None, bufs=None):
+    N, k = (int(s) for s in ids.shape)
+    if bufs is None:
+        bufs = (torch.empty(experts + 1, dtype=_i32, device=ids.device),
+                torch.empty(max(N * k, 1), dtype=_i32, device=ids.device),
+                torch.empty(max(N * k, 1), dtype=_i32, device=ids.device))
+    offsets, src_row, pos = bufs
+    check(_lib.lib().vmm_permute_plan(ptr(ids), N, k, experts, ptr(offsets), ptr(src_row), ptr(pos),
+                                      stream_ptr(stream)))
+    return offsets, src_row, pos
+
+
+def permute_rows(x, src_row, n_rows: int, stream=None, out=None):
+    H = int(x.shape[1])
+    out = torch.empty(n_rows, H, dtype=x.dtype, device=x.device) if out is None else out
+    check(_lib.lib().vmm_permute_rows(ptr(x), ptr(src_row), n_rows, H, ptr(out), stream_ptr(stream)))
+    return out
+
+
+def grouped_swiglu(xp, offsets, w13_arena, w2_arena, slot_of, inter: int, stream=None, h1=None, y=None,
+                   simt: bool = False):
+    """Grouped SwiGLU over expert-contiguous rows of xp (tcgen05 path unless simt)."""
+    M, H = (int(s) for s in xp.shape)
+    E = int(offsets.shape[0]) - 1
+    h1 = torch.empty(M, inter, dtype=torch.bfloat16, device=xp.device) if h1 is None else h1
+    y = torch.empty(M, H, dtype=torch.bfloat16, device=xp.device) if y is None else y
+    L = _lib.lib()
+    if simt:
+        check(L.vmm_grouped_swiglu_simt(ptr(xp), ptr(offsets), E, M, H, inter, ptr(w13_arena), ptr(w2_arena),
+                                        ptr(slot_of), ptr(h1), ptr(y), stream_ptr(stream)))
+    else:
+        n_slots = int(w13_arena.shape[0])
+        check(L.vmm_grouped_swiglu(ptr(xp), ptr(offsets), E, M, H, inter, ptr(w13_arena), ptr(w2_arena), n_slots,
+                                   ptr(slot_of), ptr(h1), ptr(y), stream_ptr(stream)))
+    return h1, y
+
+
+def combine(y, pos, gates, resid, stream=None, out=None):
+    N, k = (int(s) for s in gates.shape)
+    H = int(y.shape[1])
+    out = torch.empty(N, H, dtype=torch.bfloat16, device=y.device) if out is None else out
+    check(_lib.lib().vmm_combine(ptr(y), ptr(pos), ptr(gates), ptr(resid), N, k, H, ptr(out), stream_ptr(stream)))
+    return out
+
+
+def interleave_w13(w_gate, w_up):
+    """[I,H] gate and up projections -> the arena's [2I,H] layout (64-row blocks
+    of gate rows followed by the matching 64 up rows)."""
+    I, H = (int(s) for s in w_gate.shape)
+    if I % 64:
+        raise ValueError("inter size must be a multiple of 64")
+    g = w_gate.reshape(I // 64, 64, H)
+    u = w_up.reshape(I // 64, 64, H)
+    return torch.stack([g, u], dim=1).reshape(2 * I, H).contiguous()
+
+
+def ceil_div(a, b):
+    return -(-a // b)
+
+
+__all__ = [n for n in dir() if not n.startswith("_") and n not in ("math", "torch")]

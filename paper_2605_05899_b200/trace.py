@@ -182,6 +182,8 @@ class RoutingTrace:
             list(ref.phase_marks), int(getattr(ref, "shared_experts", 0)),
         )
 
+    __hash__ = object.__hash__  # identity hash: device copies are cached per object
+
     def __eq__(self, other):
         if not isinstance(other, RoutingTrace):
             return NotImplemented

@@ -1,0 +1,97 @@
+"""Router, permutation, grouped SwiGLU (tcgen05) and combine vs the torch oracle.
+
+Tolerances (stated): routed ids exact on exact-arithmetic inputs;
+gates |d| <= 1e-6; FFN bf16 outputs assert_close(rtol=2e-2, atol=2e-2) plus
+relative Frobenius error <= 5e-3 against the fp32 restatement.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import moe_ref
+from paper_2605_05899_b200 import kernels
+
+pytestmark = pytest.mark.gpu
+
+
+def test_router_exact_ids_on_integer_inputs_with_ties():
+    g = torch.Generator().manual_seed(1)
+    for N, H, E, k in ((2368, 2048, 128, 8), (333, 256, 8, 2), (100, 2560, 4, 2), (64, 2048, 64, 6)):
+        x = torch.randint(-4, 5, (N, H), generator=g).to(torch.bfloat16)
+        w = torch.randint(-1, 2, (E, H), generator=g).to(torch.bfloat16)
+        counts = torch.zeros(E, dtype=torch.int32, device="cuda")
+        ids, gates, logits = kernels.route_topk(x.cuda(), w.cuda(), k, counts=counts, want_logits=True)
+        rid, rg, rl = moe_ref.route(x, w, k)
+        assert torch.equal(logits.cpu().double(), rl)
+        assert torch.equal(ids.cpu(), rid)
+        assert (gates.cpu() - rg).abs().max().item() <= 1e-6
+        assert torch.equal(counts.cpu().long(), torch.bincount(rid.reshape(-1).long(), minlength=E))
+
+
+def test_router_realistic_inputs_margin_aware():
+    g = torch.Generator().manual_seed(2)
+    x = torch.randn(1216, 2048, generator=g).to(torch.bfloat16)
+    w = (torch.randn(128, 2048, generator=g) / 45).to(torch.bfloat16)
+    ids, gates, _ = kernels.route_topk(x.cuda(), w.cuda(), 8)
+    rid, rg, rl = moe_ref.route(x, w, 8)
+    srt = torch.sort(rl, dim=1, descending=True).values
+    safe = (srt[:, 7] - srt[:, 8]) > 1e-3  # margin-safe tokens must agree exactly
+    assert torch.equal(ids.cpu()[safe], rid[safe])
+    assert safe.float().mean() > 0.9
+    torch.testing.assert_close(gates.cpu()[safe], rg[safe], rtol=1e-4, atol=1e-5)
+
+
+def test_permute_plan_is_stable_counting_sort():
+    g = torch.Generator().manual_seed(3)
+    ids = torch.stack([torch.randperm(128, generator=g)[:8] for _ in range(1216)]).int()
+    off, src, pos = kernels.permute_plan(ids.cuda(), 128)
+    roff, rsrc, rpos = moe_ref.permute(ids, 128)
+    assert torch.equal(off.cpu().long(), roff)
+    assert torch.equal(src.cpu().long(), rsrc)
+    assert torch.equal(pos.cpu().long().reshape(1216, 8), rpos)
+
+
+def _expert_setup(N, H, I, E, k, n_slots, seed):
+    g = torch.Generator().manual_seed(seed)
+    x = (torch.randn(N, H, generator=g)).to(torch.bfloat16)
+    wg = (torch.randn(n_slots, I, H, generator=g) / H ** 0.5).to(torch.bfloat16)
+    wu = (torch.randn(n_slots, I, H, generator=g) / H ** 0.5).to(torch.bfloat16)
+    wd = (torch.randn(n_slots, H, I, generator=g) / I ** 0.5).to(torch.bfloat16)
+    w13 = torch.stack([kernels.interleave_w13(wg[s], wu[s]) for s in range(n_slots)])
+    # skewed routing: some experts empty, some with > 128 rows
+    logits = torch.randn(N, E, generator=g) + torch.linspace(3, -3, E)
+    ids = torch.topk(logits, k, dim=1).indices.int()
+    slot_of = torch.randperm(n_slots, generator=g)[:E].int()
+    return x, wg, wu, wd, w13, ids, slot_of
+
+
+@pytest.mark.parametrize("simt", [False, True])
+@pytest.mark.parametrize("shape", [(1216, 2048, 768, 128, 8), (300, 256, 512, 8, 2), (640, 2048, 1408, 64, 6)])
+def test_grouped_swiglu_matches_fp32_restatement(shape, simt):
+    N, H, I, E, k = shape
+    n_slots = E + 3
+    x, wg, wu, wd, w13, ids, slot_of = _expert_setup(N, H, I, E, k, n_slots, seed=N + E)
+    off, src, pos = kernels.permute_plan(ids.cuda(), E)
+    M = N * k
+    xp = kernels.permute_rows(x.cuda(), src, M)
+    h1, y = kernels.grouped_swiglu(xp, off, w13.cuda(), wd.cuda(), slot_of.cuda(), I, simt=simt)
+    torch.cuda.synchronize()
+    roff, rsrc, rpos = moe_ref.permute(ids, E)
+    xr = x[rsrc]
+    assert torch.equal(xp.cpu(), xr)
+    h_exp = torch.empty(M, I, dtype=torch.bfloat16)
+    y_exp = torch.empty(M, H, dtype=torch.bfloat16)
+    for e in range(E):
+        a, b = int(roff[e]), int(roff[e + 1])
+        if b > a:
+            s = int(slot_of[e])
+            h_exp[a:b], y_exp[a:b] = moe_ref.expert_ffn(xr[a:b], wg[s], wu[s], wd[s])
+    torch.testing.assert_close(h1.cpu().float(), h_exp.float(), rtol=2e-2, atol=2e-2)
+    torch.testing.assert_close(y.cpu().float(), y_exp.float(), rtol=2e-2, atol=2e-2)
+    rel = (y.cpu().float() - y_exp.float()).norm() / y_exp.float().norm()
+    assert rel.item() <= 5e-3
+    # combine back to token order with residual
+    gates = torch.softmax(torch.randn(N, k), dim=1)
+    out = kernels.combine(y, pos, gates.cuda(), x.cuda())
+    ref = moe_ref.combine(y.cpu(), rpos, gates, x)
+    torch.testing.assert_close(out.cpu().float(), ref.float(), rtol=2e-2, atol=2e-2)
