@@ -1,0 +1,351 @@
+#!/usr/bin/env python3
+"""Benchmark: prefill tokens/s through the VL-MoE layer stack on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3_qwen3vl]
+    python bench.py --impl reference ...     # the reference CPU path (oracle port)
+
+One step = one request (BASELINE.json configs[2], Qwen3-VL-30B-A3B shape:
+2304 visual + 64 text tokens, 48 MoE layers, 128 experts top-8, expert
+intermediate 768, 8 pinned layers, 826-slab expert cache) through the whole
+stack: live router -> prune -> lookahead predictor -> expert cache with real
+H2D expert transfers -> permute -> grouped SwiGLU (tcgen05) -> combine.
+Synthetic bf16 hidden states and random-init weights of that shape.
+
+Multi-GPU (torchrun): requests are data-parallel, one engine + cache per GPU,
+no data-path collective ("scaling": "weak"); time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--workload", default="c3_qwen3vl")
+    p.add_argument("--routing", default="live", choices=["live", "trace"])
+    p.add_argument("--predictor", default=None)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--out", default=None)
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference's CPU path (oracle port: compress + simulate)
+# ---------------------------------------------------------------------------
+def _ref_worker_init(gen_kw, seed):
+    global _REF_TRACE
+    from paper_2605_05899_b200.trace import TraceGenConfig, generate_trace
+
+    kw = dict(gen_kw)
+    kw["seed"] = seed
+    _REF_TRACE = generate_trace(TraceGenConfig(**kw))
+
+
+def _ref_request(args):
+    sim, comp = args
+    from oracle import harness
+
+    t0 = time.perf_counter()
+    harness.simulate(_REF_TRACE, sim, comp, False)
+    return time.perf_counter() - t0
+
+
+def ref_sim_dict(w):
+    return dict(bandwidth_mb_per_ms=1.0, expert_size_mb=0.17, gpu_ms_per_expert=0.002, num_slabs=w.num_slabs,
+                victim_policy="priority", speculative_grace=w.grace, l_pinned=w.l_pinned, shared_experts=0,
+                compress_latency_ms=0.0, predictor_bootstrap_ms=0.0,
+                predictor=dict(kind="oracle", budget=w.budget, window=w.window, gamma=w.gamma,
+                               history_decay=w.history_decay))
+
+
+def run_reference(a, w):
+    import multiprocessing as mp
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    gen = {k: v for k, v in w.trace_config(seed=0).__dict__.items() if k != "seed"}
+    comp = dict(alpha=w.alpha, beta=w.beta, lam=w.lam, prefix=list(w.prefix_layers))
+    sim = ref_sim_dict(w)
+    cores = os.cpu_count() or 1
+    ctx = mp.get_context("fork")
+    pools = []
+    # one worker per core, each with its own synthetic request trace
+    pool = ctx.Pool(cores, initializer=_ref_worker_init, initargs=(gen, 0))
+    pools.append(pool)
+    times = []
+    for i in range(a.warmup + a.steps):
+        t0 = time.perf_counter()
+        pool.map(_ref_request, [(sim, comp)] * cores)
+        dt = time.perf_counter() - t0
+        if i >= a.warmup:
+            times.append(dt)
+    pool.close()
+    step = float(np.mean(times))
+    val = cores * w.n_tokens / step
+    line = {
+        "impl": "reference", "metric": "prefill tokens/s per VL-MoE layer stack", "value": val, "unit": "tokens/s",
+        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": step * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference trace generator, seed 0)",
+        "config": {"workload": w.name, "requests_per_step": cores, "predictor": "oracle B=%d W=%d" % (w.budget, w.window),
+                   "path": "compress + simulate (decision path; the reference has no router/FFN numerics)"},
+        "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "port",
+                         "sample": f"{cores} C3 requests per step, one per process (oracle port of moesim)"},
+        "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    def __init__(self, path):
+        self.path = path
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+            self.f.close()
+
+    def summary(self, dev_index=0):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9 or f[0] != str(dev_index):
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measure_h2d_peak(torch, dev):
+    n = 1 << 30
+    src = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    dst = torch.empty(n, dtype=torch.uint8, device=dev)
+    best = 0.0
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dst.copy_(src, non_blocking=True)
+        b.record()
+        b.synchronize()
+        best = max(best, n / (a.elapsed_time(b) * 1e-3) / 1e9)
+    del src, dst
+    return best
+
+
+def main():
+    a = parse()
+    from paper_2605_05899_b200.configs import WORKLOADS
+
+    w = WORKLOADS[a.workload]
+    if a.impl == "reference":
+        return run_reference(a, w)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2605_05899_b200 import kernels
+    from paper_2605_05899_b200.moe import MoEStack, StackConfig
+    from paper_2605_05899_b200.trace import generate_trace
+
+    predictor = a.predictor or ("gate" if a.routing == "live" else "oracle")
+    cfg = StackConfig.from_workload(w, routing=a.routing, predictor=predictor, host_layers=8)
+    stack = MoEStack(cfg, seed=1000 + rank)
+    tr = generate_trace(w.trace_config(seed=rank))
+    T = tr.num_tokens
+    g = torch.Generator(device=dev).manual_seed(rank)
+    x = torch.randn((T, w.hidden), generator=g, device=dev).to(torch.bfloat16)
+    sal = torch.from_numpy(tr.saliency).to(dev)
+    mod = torch.from_numpy(tr.device_modality()).to(dev)
+    dtr = None
+    if a.routing == "trace":
+        dtr = dict(routes=torch.from_numpy(tr.route_experts.astype(np.int32)).to(dev),
+                   gates=torch.from_numpy(tr.route_gates.astype(np.float32)).to(dev))
+    # host copies for the end-to-end leg
+    x_h = x.cpu().pin_memory()
+    sal_h = sal.cpu().pin_memory()
+    mod_h = mod.cpu().pin_memory()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > L2 (126 MB)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def step(e2e=False):
+        if e2e:
+            xd = x_h.to(dev, non_blocking=True)
+            sd = sal_h.to(dev, non_blocking=True)
+            md = mod_h.to(dev, non_blocking=True)
+        else:
+            xd, sd, md = x, sal, mod
+        res = stack.forward(xd, sd, md, trace=dtr)
+        if e2e:
+            out = torch.empty(res.hidden.shape, dtype=res.hidden.dtype, pin_memory=True)
+            out.copy_(res.hidden, non_blocking=True)
+            return res, out
+        return res, None
+
+    def timed(n, e2e=False, prof=False):
+        times, results = [], []
+        for _ in range(n):
+            flush.zero_()
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if prof:
+                stack.profile = []
+            e0.record()
+            res, out = step(e2e)
+            e1.record()
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+            results.append((res, list(stack.profile) if prof else None, out))
+            stack.profile = None
+        return times, results
+
+    # warm-up
+    timed(a.warmup)
+    barrier()
+    launches0 = kernels.LAUNCHES[0]
+    with ClockSampler(os.path.join(ROOT, "gpurun_out", f"clocks_rank{rank}.csv")
+                      if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else "/tmp/clocks.csv") as clk:
+        times, results = timed(a.steps, prof=True)
+    launches = (kernels.LAUNCHES[0] - launches0) // max(a.steps, 1)
+    e2e_times, e2e_results = timed(a.steps, e2e=True)
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ms = max_over_ranks(float(np.mean(times)))
+    ms_e2e = max_over_ranks(float(np.mean(e2e_times)))
+    value = world * T / (ms * 1e-3)
+    e2e_value = world * T / (ms_e2e * 1e-3)
+
+    # roofline: grouped SwiGLU (dominant kernel pair), live CUDA events in the timed region
+    prof = [p for _, pl, _ in results for p in pl]
+    durs = [p[0].elapsed_time(p[1]) for p in prof]
+    nbytes = [p[2] for p in prof]
+    ach = float(np.mean([b / (d * 1e-3) / 1e9 for b, d in zip(nbytes, durs)]))
+    peaks = {}
+    pk_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pk_path):
+        peaks = json.load(open(pk_path))
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    res0 = results[-1][0]
+    h2d_peak = measure_h2d_peak(torch, dev)
+    h2d_bytes = res0.h2d_bytes
+    rep = res0.report
+    h2d_gbs = h2d_bytes / (ms * 1e-3) / 1e9
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        try:
+            sys.path.insert(0, ROOT)
+            from oracle import harness
+
+            comp = dict(alpha=w.alpha, beta=w.beta, lam=w.lam, prefix=list(w.prefix_layers))
+            t0 = time.perf_counter()
+            n_req = 0
+            while time.perf_counter() - t0 < 10.0 or n_req == 0:
+                harness.simulate(tr, ref_sim_dict(w), comp, False)
+                n_req += 1
+            dt = (time.perf_counter() - t0) / n_req
+            cpu = {"value": T / dt, "unit": "tokens/s", "cores": 1, "kind": "port",
+                   "sample": f"{n_req} x one {w.name} request (compress + simulate, oracle predictor), single thread"}
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"value": None, "unit": "tokens/s", "cores": 1, "kind": "port", "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": "prefill tokens/s per VL-MoE layer stack", "value": value, "unit": "tokens/s",
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init weights, N(0,1) hidden states, reference trace generator saliency)",
+            "config": {"workload": w.name, "tokens": T, "layers": w.layers, "hidden": w.hidden, "experts": w.experts,
+                       "top_k": w.k, "moe_inter": w.inter, "l_pinned": w.l_pinned, "num_slabs": w.num_slabs,
+                       "routing": a.routing, "predictor": f"{predictor} B={w.budget} W={w.window}",
+                       "parallelism": f"dp{world} (requests)", "requests_per_gpu_step": 1,
+                       "l2": "flushed (256 MB write) between timed steps"},
+            "hit_rate": rep.hit_rate, "hits": rep.hits, "misses": rep.misses, "evictions": rep.evictions,
+            "retained_tokens": int(res0.hidden.shape[0]),
+            "h2d": {"gbs": h2d_gbs, "bytes_per_step": h2d_bytes, "copies_per_step": res0.copies,
+                    "peak_gbs": h2d_peak, "frac": h2d_gbs / h2d_peak if h2d_peak else None,
+                    "peak_source": "measured pinned 1 GiB H2D in this run"},
+            "roofline": {"bound": "hbm", "kernel": "grouped_swiglu (tcgen05 GEMM1+GEMM2)", "achieved": ach,
+                         "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+                         "traffic": None, "launch_ms": float(np.mean(durs)),
+                         "bytes_per_launch": float(np.mean(nbytes)),
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
+            "clocks": clk.summary(local),
+            "gpu_launches": int(launches),
+            "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": int(T * w.hidden * 2 + T * 9),
+                    "d2h_bytes_per_step": int(res0.hidden.numel() * 2), "ms_per_step": ms_e2e},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+        if a.out:
+            with open(a.out, "w") as f:
+                json.dump(line, f, indent=1)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -129,20 +129,22 @@ int vmm_combine(const void *d_y, const int32_t *d_pos, const float *d_gates, con
 
 /* ------------------------------------------------------------------------
  * Grouped bf16 SwiGLU expert FFN on tcgen05/TMEM with TMA operands.
- * Expert weights live in slots of one HBM arena; slot s holds
- *   W13[s] : [2I][H] bf16, rows interleaved per 64-row block (64 gate rows, then
- *            the 64 matching up rows), K-major;
- *   W2[s]  : [H][I]  bf16, K-major.
+ * Expert weights live in slots of one HBM arena, `slot_stride` bf16 elements
+ * apart (normally 3*I*H: one contiguous 9.44 MB block per Qwen3-VL expert, so
+ * a cache fill is ONE host->device copy):
+ *   W13 at d_w13_arena + s*stride : [2I][H] bf16, rows interleaved per 64-row
+ *            block (64 gate rows, then the 64 matching up rows), K-major;
+ *   W2  at d_w2_arena  + s*stride : [H][I]  bf16, K-major.
  * d_slot_of_expert [E] i32 maps expert -> arena slot for this layer.
  * Xp: permuted token rows [M_total][H]; d_offsets [E+1] from vmm_permute_plan.
  * H1 scratch [M_total][I] bf16; Y out [M_total][H] bf16.
  * ------------------------------------------------------------------------ */
 int vmm_grouped_swiglu(const void *d_xp, const int32_t *d_offsets, int E, int M_total,
-                       int H, int I, const void *d_w13_arena, const void *d_w2_arena, long long n_slots,
-                       const int32_t *d_slot_of_expert, void *d_h1, void *d_y, void *stream);
+                       int H, int I, const void *d_w13_arena, const void *d_w2_arena, long long slot_stride,
+                       long long n_slots, const int32_t *d_slot_of_expert, void *d_h1, void *d_y, void *stream);
 /* Reference (CUDA-core, fp32) version of the same contraction for cross-checks. */
 int vmm_grouped_swiglu_simt(const void *d_xp, const int32_t *d_offsets, int E, int M_total,
-                            int H, int I, const void *d_w13_arena, const void *d_w2_arena,
+                            int H, int I, const void *d_w13_arena, const void *d_w2_arena, long long slot_stride,
                             const int32_t *d_slot_of_expert, void *d_h1, void *d_y, void *stream);
 
 /* ------------------------------------------------------------------------
@@ -188,6 +190,12 @@ int vmm_engine_begin(vmm_engine *e, const double *h_y_boot);
  * context `layer` (else NULL). */
 int vmm_engine_layer(vmm_engine *e, int layer, const int32_t *h_demand, int n_demand,
                      int phase, int step, const double *h_y);
+/* With h_y == NULL an emitting layer defers its emission: the caller launches
+ * the layer's compute first, then calls vmm_engine_emit (so copies decided by
+ * the emission can wait for that compute). */
+int vmm_engine_emit(vmm_engine *e, int layer, const double *h_y);
+/* slabs holding (layer, demand[i]) after the layer ran (all must be resident) */
+int vmm_engine_slots(const vmm_engine *e, int layer, const int32_t *h_demand, int n, int32_t *h_slabs);
 /* close a decode step (records decode_ms_per_step) */
 int vmm_engine_end_step(vmm_engine *e);
 int vmm_engine_finish(vmm_engine *e, vmm_engine_report *rep);
@@ -254,7 +262,14 @@ int vmm_xfer_fence(vmm_xfer *x, const int32_t *h_slabs, int n, void *compute_str
 /* record the compute event closing the reads registered since the last call */
 int vmm_xfer_layer_done(vmm_xfer *x, int layer, void *compute_stream);
 int vmm_xfer_reset_stats(vmm_xfer *x);
+/* drain the engine's transfer commands and enqueue each as one copy of
+ * slot_bytes from the pinned host pool slot ((layer % host_layers)*experts +
+ * expert) into arena slot (slab_offset + slab) */
+int vmm_xfer_issue_engine(vmm_xfer *x, vmm_engine *e, const void *h_pool, int host_layers, int experts,
+                          void *d_arena, long long slab_offset, size_t slot_bytes, int *n_issued);
 int vmm_xfer_sync(vmm_xfer *x);
+/* make compute_stream wait for every copy issued so far */
+int vmm_xfer_join(vmm_xfer *x, void *compute_stream);
 /* copy-stream accounting: bytes issued and wall ms between first and last copy (events) */
 int vmm_xfer_stats(vmm_xfer *x, double *bytes, double *busy_ms, long long *copies);
 void *vmm_xfer_stream(vmm_xfer *x);

@@ -60,13 +60,15 @@ _SIGS = {
     "vmm_permute_plan": (I32, [P, I32, I32, I32, P, P, P, P]),
     "vmm_permute_rows": (I32, [P, P, I32, I32, P, P]),
     "vmm_combine": (I32, [P, P, P, P, I32, I32, I32, P, P]),
-    "vmm_grouped_swiglu": (I32, [P, P, I32, I32, I32, I32, P, P, I64, P, P, P, P]),
-    "vmm_grouped_swiglu_simt": (I32, [P, P, I32, I32, I32, I32, P, P, P, P, P, P]),
+    "vmm_grouped_swiglu": (I32, [P, P, I32, I32, I32, I32, P, P, I64, I64, P, P, P, P]),
+    "vmm_grouped_swiglu_simt": (I32, [P, P, I32, I32, I32, I32, P, P, I64, P, P, P, P]),
     "vmm_engine_create": (I32, [C.POINTER(EngineConfig), C.POINTER(P)]),
     "vmm_engine_destroy": (None, [P]),
     "vmm_engine_begin": (I32, [P, P]),
     "vmm_engine_layer": (I32, [P, I32, P, I32, I32, I32, P]),
     "vmm_engine_end_step": (I32, [P]),
+    "vmm_engine_emit": (I32, [P, I32, P]),
+    "vmm_engine_slots": (I32, [P, I32, P, I32, P]),
     "vmm_engine_finish": (I32, [P, C.POINTER(EngineReport)]),
     "vmm_engine_emits": (I32, [P, I32, I32]),
     "vmm_engine_events": (I32, [P, P, I32]),
@@ -94,9 +96,11 @@ _SIGS = {
     "vmm_xfer_fence": (I32, [P, P, I32, P]),
     "vmm_xfer_layer_done": (I32, [P, I32, P]),
     "vmm_xfer_sync": (I32, [P]),
+    "vmm_xfer_join": (I32, [P, P]),
     "vmm_xfer_stats": (I32, [P, PF64, PF64, C.POINTER(I64)]),
     "vmm_xfer_reset_stats": (I32, [P]),
     "vmm_xfer_stream": (P, [P]),
+    "vmm_xfer_issue_engine": (I32, [P, P, P, I32, I32, P, I64, SZ, PI32]),
 }
 
 _lock = threading.Lock()

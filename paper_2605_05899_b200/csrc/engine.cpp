@@ -554,9 +554,24 @@ int vmm_engine_layer(vmm_engine *e, int layer, const int32_t *dem, int n, int ph
   else if (e->c.reactive) st = e->reactive_layer(layer, dem, n, phase, step);
   else st = e->cached_layer(layer, dem, n, phase, step);
   if (st) return st;
-  if (vmm_engine_emits(e, layer, phase)) {
-    if (!y) return vmm::fail(VMM_ECONTRACT, "emission needs predictor scores");
-    e->emit(layer, e->cursor, y);
+  // with y == NULL an emitting layer defers its emission to vmm_engine_emit
+  if (y && vmm_engine_emits(e, layer, phase)) e->emit(layer, e->cursor, y);
+  return VMM_OK;
+}
+
+int vmm_engine_emit(vmm_engine *e, int layer, const double *y) {
+  if (!y) return vmm::fail(VMM_ECONTRACT, "emission needs predictor scores");
+  e->emit(layer, e->cursor, y);
+  return VMM_OK;
+}
+
+int vmm_engine_slots(const vmm_engine *e, int layer, const int32_t *demand, int n, int32_t *out) {
+  for (int i = 0; i < n; ++i) {
+    int s = e->cache.find(e->key(layer, demand[i]));
+    if (s < 0 || e->cache.slabs[s].state != RESIDENT)
+      return vmm::fail(VMM_ECONTRACT, "expert (" + std::to_string(layer) + ", " + std::to_string(demand[i]) +
+                                          ") is not resident after its layer ran");
+    out[i] = s;
   }
   return VMM_OK;
 }

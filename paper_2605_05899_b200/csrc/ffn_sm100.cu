@@ -279,13 +279,13 @@ __device__ __forceinline__ int expert_of_row(const int32_t *offsets, int E, int 
 }
 
 __global__ void simt_gemm1_kernel(const __nv_bfloat16 *__restrict__ xp, const int32_t *__restrict__ offsets, int E,
-                                  int M, int H, int I, const __nv_bfloat16 *__restrict__ w13,
+                                  int M, int H, int I, const __nv_bfloat16 *__restrict__ w13, long long stride,
                                   const int32_t *__restrict__ slot_of, __nv_bfloat16 *__restrict__ h1) {
   long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)M * I) return;
   int m = (int)(idx / I), f = (int)(idx % I);
   int e = expert_of_row(offsets, E, m);
-  const __nv_bfloat16 *w = w13 + (long long)slot_of[e] * 2 * I * H;
+  const __nv_bfloat16 *w = w13 + (long long)slot_of[e] * stride;
   int gr = (f / 64) * 128 + (f % 64), ur = gr + 64;
   float g = 0.f, u = 0.f;
   for (int kk = 0; kk < H; ++kk) {
@@ -297,13 +297,13 @@ __global__ void simt_gemm1_kernel(const __nv_bfloat16 *__restrict__ xp, const in
 }
 
 __global__ void simt_gemm2_kernel(const __nv_bfloat16 *__restrict__ h1, const int32_t *__restrict__ offsets, int E,
-                                  int M, int H, int I, const __nv_bfloat16 *__restrict__ w2,
+                                  int M, int H, int I, const __nv_bfloat16 *__restrict__ w2, long long stride,
                                   const int32_t *__restrict__ slot_of, __nv_bfloat16 *__restrict__ y) {
   long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)M * H) return;
   int m = (int)(idx / H), n = (int)(idx % H);
   int e = expert_of_row(offsets, E, m);
-  const __nv_bfloat16 *w = w2 + (long long)slot_of[e] * H * I;
+  const __nv_bfloat16 *w = w2 + (long long)slot_of[e] * stride;
   float a = 0.f;
   for (int kk = 0; kk < I; ++kk) a = fmaf(__bfloat162float(h1[(long long)m * I + kk]),
                                           __bfloat162float(w[(long long)n * I + kk]), a);
@@ -346,12 +346,14 @@ int make_map(CUtensorMap *m, const void *base, int rank, const uint64_t *dims, c
 }  // namespace
 
 extern "C" int vmm_grouped_swiglu(const void *d_xp, const int32_t *d_offsets, int E, int M_total, int H, int I,
-                                  const void *d_w13_arena, const void *d_w2_arena, long long n_slots,
-                                  const int32_t *d_slot_of_expert, void *d_h1, void *d_y, void *stream) {
+                                  const void *d_w13_arena, const void *d_w2_arena, long long slot_stride,
+                                  long long n_slots, const int32_t *d_slot_of_expert, void *d_h1, void *d_y,
+                                  void *stream) {
   if (M_total <= 0) return VMM_OK;
   if (H % BN || H % BK || I % 64 || I % BK || (2 * I) % BN)
     return vmm::fail(VMM_EVALIDATION, "grouped_swiglu: hidden must be a multiple of 128, inter of 64");
   if (E < 1 || E > VMM_MAX_EXPERTS) return vmm::fail(VMM_EVALIDATION, "experts must lie in [1, 256]");
+  if (slot_stride % 8) return vmm::fail(VMM_EVALIDATION, "slot stride must be a multiple of 8 elements");
   static bool attr = false;
   if (!attr) {
     cudaError_t e1 = cudaFuncSetAttribute(grouped_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -372,7 +374,7 @@ extern "C" int vmm_grouped_swiglu(const void *d_xp, const int32_t *d_offsets, in
   }
   {
     uint64_t dims[3] = {(uint64_t)H, (uint64_t)2 * I, (uint64_t)n_slots};
-    uint64_t str[2] = {(uint64_t)H * 2, (uint64_t)2 * I * H * 2};
+    uint64_t str[2] = {(uint64_t)H * 2, (uint64_t)slot_stride * 2};
     uint32_t box[3] = {BK, BN, 1};
     if ((st = make_map(&mb1, d_w13_arena, 3, dims, str, box))) return st;
   }
@@ -384,7 +386,7 @@ extern "C" int vmm_grouped_swiglu(const void *d_xp, const int32_t *d_offsets, in
   }
   {
     uint64_t dims[3] = {(uint64_t)I, (uint64_t)H, (uint64_t)n_slots};
-    uint64_t str[2] = {(uint64_t)I * 2, (uint64_t)H * I * 2};
+    uint64_t str[2] = {(uint64_t)I * 2, (uint64_t)slot_stride * 2};
     uint32_t box[3] = {BK, BN, 1};
     if ((st = make_map(&mb2, d_w2_arena, 3, dims, str, box))) return st;
   }
@@ -401,18 +403,18 @@ extern "C" int vmm_grouped_swiglu(const void *d_xp, const int32_t *d_offsets, in
 }
 
 extern "C" int vmm_grouped_swiglu_simt(const void *d_xp, const int32_t *d_offsets, int E, int M_total, int H, int I,
-                                       const void *d_w13_arena, const void *d_w2_arena,
+                                       const void *d_w13_arena, const void *d_w2_arena, long long slot_stride,
                                        const int32_t *d_slot_of_expert, void *d_h1, void *d_y, void *stream) {
   if (M_total <= 0) return VMM_OK;
   cudaStream_t s = (cudaStream_t)stream;
   long long n1 = (long long)M_total * I, n2 = (long long)M_total * H;
   simt_gemm1_kernel<<<(unsigned)((n1 + 255) / 256), 256, 0, s>>>((const __nv_bfloat16 *)d_xp, d_offsets, E, M_total,
                                                                   H, I, (const __nv_bfloat16 *)d_w13_arena,
-                                                                  d_slot_of_expert, (__nv_bfloat16 *)d_h1);
+                                                                  slot_stride, d_slot_of_expert, (__nv_bfloat16 *)d_h1);
   VMM_LAUNCH_CHECK("simt_gemm1_kernel");
   simt_gemm2_kernel<<<(unsigned)((n2 + 255) / 256), 256, 0, s>>>((const __nv_bfloat16 *)d_h1, d_offsets, E, M_total,
                                                                   H, I, (const __nv_bfloat16 *)d_w2_arena,
-                                                                  d_slot_of_expert, (__nv_bfloat16 *)d_y);
+                                                                  slot_stride, d_slot_of_expert, (__nv_bfloat16 *)d_y);
   VMM_LAUNCH_CHECK("simt_gemm2_kernel");
   return VMM_OK;
 }

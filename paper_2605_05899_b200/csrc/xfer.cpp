@@ -131,6 +131,13 @@ int vmm_xfer_layer_done(vmm_xfer *x, int layer, void *compute_stream) {
   return VMM_OK;
 }
 
+int vmm_xfer_join(vmm_xfer *x, void *compute_stream) {
+  cudaEvent_t ev = x->fill_ev[(x->fill_seq % kRing + kRing - 1) % kRing];
+  if (x->fill_seq == 0) return VMM_OK;
+  cudaError_t e = cudaStreamWaitEvent((cudaStream_t)compute_stream, ev, 0);
+  return cuda_status(e, "join copy stream");
+}
+
 int vmm_xfer_sync(vmm_xfer *x) { return cuda_status(cudaStreamSynchronize(x->stream), "copy sync"); }
 
 int vmm_xfer_stats(vmm_xfer *x, double *bytes, double *busy_ms, long long *copies) {
@@ -155,5 +162,27 @@ int vmm_xfer_reset_stats(vmm_xfer *x) {
 }
 
 void *vmm_xfer_stream(vmm_xfer *x) { return (void *)x->stream; }
+
+int vmm_engine_copies(vmm_engine *e, int32_t *out, int cap);
+
+int vmm_xfer_issue_engine(vmm_xfer *x, vmm_engine *e, const void *h_pool, int host_layers, int experts,
+                          void *d_arena, long long slab_offset, size_t slot_bytes, int *n_issued) {
+  int32_t buf[3 * 256];
+  int total = 0;
+  for (;;) {
+    int n = vmm_engine_copies(e, buf, 256);
+    if (n <= 0) break;
+    for (int i = 0; i < n; ++i) {
+      int layer = buf[3 * i], expert = buf[3 * i + 1], slab = buf[3 * i + 2];
+      const char *src = (const char *)h_pool + ((size_t)(layer % host_layers) * experts + expert) * slot_bytes;
+      char *dst = (char *)d_arena + (size_t)(slab_offset + slab) * slot_bytes;
+      int st = vmm_xfer_copy(x, slab, src, dst, slot_bytes, 0);
+      if (st) return st;
+    }
+    total += n;
+  }
+  if (n_issued) *n_issued = total;
+  return VMM_OK;
+}
 
 }  // extern "C"

@@ -16,6 +16,13 @@ from ._lib import check, ptr, stream_ptr
 
 _i32 = torch.int32
 
+# number of libvismmoe kernels launched through these wrappers (bench evidence)
+LAUNCHES = [0]
+
+
+def _n(k: int) -> None:
+    LAUNCHES[0] += k
+
 
 def _dev():
     return torch.device("cuda", torch.cuda.current_device())
@@ -43,6 +50,7 @@ def prune(saliency, modality, prefix_routes, req_off, k_core, k_keep, experts: i
         target=torch.zeros(R, 4, dtype=torch.int64, device=dev),
         status=torch.full((R,), -1, dtype=_i32, device=dev),
     )
+    _n(1)
     check(L.vmm_prune(ptr(saliency), ptr(modality), ptr(prefix_routes), ptr(req_off), ptr(k_core), ptr(k_keep),
                       R, T, P, k, experts, float(lam), ptr(out["s_norm"]), ptr(out["delta"]), ptr(out["score"]),
                       ptr(out["flags"]), ptr(out["retained"]), ptr(out["n_retained"]), ptr(out["target"]),
@@ -54,6 +62,7 @@ def gather_rows(src, idx, stream=None, out=None):
     n = int(idx.shape[0])
     H = int(src.shape[1])
     out = torch.empty(n, H, dtype=src.dtype, device=src.device) if out is None else out
+    _n(1)
     check(_lib.lib().vmm_gather_rows(ptr(src), ptr(idx), n, H, ptr(out), stream_ptr(stream)))
     return out
 
@@ -68,6 +77,7 @@ def route_topk(x, w_gate, k: int, counts=None, want_logits=False, stream=None, i
     ids = torch.empty(N, k, dtype=_i32, device=x.device) if ids is None else ids
     gates = torch.empty(N, k, dtype=torch.float32, device=x.device) if gates is None else gates
     logits = torch.empty(N, E, dtype=torch.float32, device=x.device) if want_logits else None
+    _n(1)
     check(_lib.lib().vmm_route_topk(ptr(x), ptr(w_gate), N, H, E, k, ptr(ids), ptr(gates), ptr(logits),
                                     ptr(counts), stream_ptr(stream)))
     return ids, gates, logits
@@ -78,6 +88,7 @@ def demand_counts(routes, layers, ids, experts: int, stream=None, out=None):
     L_, T, k = (int(s) for s in routes.shape)
     n = int(layers.shape[0])
     out = torch.empty(n, experts, dtype=_i32, device=routes.device) if out is None else out
+    _n(1)
     check(_lib.lib().vmm_demand_counts(ptr(routes), L_, T, k, experts, ptr(layers), n, ptr(ids), int(ids.shape[0]),
                                        ptr(out), stream_ptr(stream)))
     return out
@@ -86,6 +97,7 @@ def demand_counts(routes, layers, ids, experts: int, stream=None, out=None):
 def oracle_targets(counts_all, ctx, window: int, decay, stream=None):
     L_, E = (int(s) for s in counts_all.shape)
     y = torch.empty(int(ctx.shape[0]), E, dtype=torch.float64, device=counts_all.device)
+    _n(1)
     check(_lib.lib().vmm_oracle_targets(ptr(counts_all), L_, E, ptr(ctx), int(ctx.shape[0]), window, ptr(decay),
                                         ptr(y), stream_ptr(stream)))
     return y
@@ -94,6 +106,7 @@ def oracle_targets(counts_all, ctx, window: int, decay, stream=None):
 def history(counts_all, ctx, pow_table, stream=None):
     L_, E = (int(s) for s in counts_all.shape)
     y = torch.empty(int(ctx.shape[0]), E, dtype=torch.float64, device=counts_all.device)
+    _n(1)
     check(_lib.lib().vmm_history(ptr(counts_all), L_, E, ptr(ctx), int(ctx.shape[0]), ptr(pow_table), ptr(y),
                                  stream_ptr(stream)))
     return y
@@ -106,6 +119,7 @@ def mlp_predict(hist, emb, drift, ids, h_v, ctx, model: dict, want_features=Fals
     db = int(model["w2"].shape[0])
     y = torch.empty(n_ctx, E, dtype=torch.float64, device=hist.device)
     feat = torch.empty(n_ctx, E + 2 * D, dtype=torch.float64, device=hist.device) if want_features else None
+    _n(1)
     check(_lib.lib().vmm_mlp_predict(ptr(hist), ptr(emb), D, ptr(drift), ptr(ids), int(ids.shape[0]), ptr(h_v),
                                      ptr(ctx), n_ctx, E, ptr(model["w1"]), ptr(model["b1"]), dh, ptr(model["w2"]),
                                      ptr(model["b2"]), db, ptr(model["wo"]), ptr(model["bo"]), ptr(feat), ptr(y),
@@ -118,6 +132,7 @@ def gate_lookahead(x, w_next, k: int, stream=None, scratch=None, out=None):
     E = int(w_next.shape[0])
     scratch = torch.empty(E, dtype=_i32, device=x.device) if scratch is None else scratch
     out = torch.empty(E, dtype=torch.float64, device=x.device) if out is None else out
+    _n(2)
     check(_lib.lib().vmm_gate_lookahead(ptr(x), ptr(w_next), N, H, E, k, ptr(scratch), ptr(out),
                                         stream_ptr(stream)))
     return out
@@ -133,6 +148,7 @@ def permute_plan(ids, experts: int, stream=None, bufs=None):
                 torch.empty(max(N * k, 1), dtype=_i32, device=ids.device),
                 torch.empty(max(N * k, 1), dtype=_i32, device=ids.device))
     offsets, src_row, pos = bufs
+    _n(1)
     check(_lib.lib().vmm_permute_plan(ptr(ids), N, k, experts, ptr(offsets), ptr(src_row), ptr(pos),
                                       stream_ptr(stream)))
     return offsets, src_row, pos
@@ -141,32 +157,45 @@ def permute_plan(ids, experts: int, stream=None, bufs=None):
 def permute_rows(x, src_row, n_rows: int, stream=None, out=None):
     H = int(x.shape[1])
     out = torch.empty(n_rows, H, dtype=x.dtype, device=x.device) if out is None else out
+    _n(1)
     check(_lib.lib().vmm_permute_rows(ptr(x), ptr(src_row), n_rows, H, ptr(out), stream_ptr(stream)))
     return out
 
 
-def grouped_swiglu(xp, offsets, w13_arena, w2_arena, slot_of, inter: int, stream=None, h1=None, y=None,
-                   simt: bool = False):
-    """Grouped SwiGLU over expert-contiguous rows of xp (tcgen05 path unless simt)."""
+def grouped_swiglu(xp, offsets, arena, slot_of, inter: int, stream=None, h1=None, y=None, simt: bool = False):
+    """Grouped SwiGLU over expert-contiguous rows of xp (tcgen05 path unless simt).
+
+    arena: bf16 [n_slots, 3*I*H] -- per slot W13 ([2I,H], interleaved) then W2 ([H,I])."""
     M, H = (int(s) for s in xp.shape)
     E = int(offsets.shape[0]) - 1
+    n_slots, stride = (int(s) for s in arena.shape[:2])
+    if stride != 3 * inter * H:
+        raise ValueError("arena slot must hold W13 and W2 (3*I*H elements)")
+    w2_base = arena.data_ptr() + 2 * inter * H * 2
     h1 = torch.empty(M, inter, dtype=torch.bfloat16, device=xp.device) if h1 is None else h1
     y = torch.empty(M, H, dtype=torch.bfloat16, device=xp.device) if y is None else y
     L = _lib.lib()
     if simt:
-        check(L.vmm_grouped_swiglu_simt(ptr(xp), ptr(offsets), E, M, H, inter, ptr(w13_arena), ptr(w2_arena),
+        _n(2)
+        check(L.vmm_grouped_swiglu_simt(ptr(xp), ptr(offsets), E, M, H, inter, ptr(arena), w2_base, stride,
                                         ptr(slot_of), ptr(h1), ptr(y), stream_ptr(stream)))
     else:
-        n_slots = int(w13_arena.shape[0])
-        check(L.vmm_grouped_swiglu(ptr(xp), ptr(offsets), E, M, H, inter, ptr(w13_arena), ptr(w2_arena), n_slots,
+        _n(2)
+        check(L.vmm_grouped_swiglu(ptr(xp), ptr(offsets), E, M, H, inter, ptr(arena), w2_base, stride, n_slots,
                                    ptr(slot_of), ptr(h1), ptr(y), stream_ptr(stream)))
     return h1, y
+
+
+def pack_expert(w_gate, w_up, w_down):
+    """One arena/host-pool slot: [interleaved W13 (2I*H) | W2 (H*I)] bf16, flat."""
+    return torch.cat([interleave_w13(w_gate, w_up).reshape(-1), w_down.reshape(-1)])
 
 
 def combine(y, pos, gates, resid, stream=None, out=None):
     N, k = (int(s) for s in gates.shape)
     H = int(y.shape[1])
     out = torch.empty(N, H, dtype=torch.bfloat16, device=y.device) if out is None else out
+    _n(1)
     check(_lib.lib().vmm_combine(ptr(y), ptr(pos), ptr(gates), ptr(resid), N, k, H, ptr(out), stream_ptr(stream)))
     return out
 

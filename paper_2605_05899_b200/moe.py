@@ -1,0 +1,403 @@
+"""The live VL-MoE layer stack on one B200: router -> prune -> lookahead
+predictor -> expert cache (+ real H2D prefetch) -> permute -> grouped SwiGLU
+(tcgen05) -> combine, layer by layer.
+
+This is the device realisation of the reference's per-layer engine
+(`pkg/src/moesim/pipeline.py:695-760`).  Decisions are made by the native
+logical-clock engine exactly as the reference makes them (so the cache
+hit/miss/eviction/issue sequence of a run can be replayed bit-exactly by the
+reference's `simulate` on the routes the run produced); execution follows the
+decided schedule on real streams:
+
+  compute stream : route / predictor / permute / FFN / combine kernels
+  copy stream    : one cudaMemcpyAsync per decided expert transfer (pinned
+                   host pool -> HBM slab), FIFO in decision order, fenced by
+                   events both ways (vmm_xfer_*).
+
+HBM layout (SURVEY §8(d), C3 numbers):
+  arena   bf16 [l_pinned*E + num_slabs, 3*I*H]  -- slot = [W13 (2I x H,
+          64-row gate/up interleave) | W2 (H x I)], 9.44 MB per slot; the
+          first l_pinned*E slots hold the pinned prefix layers permanently,
+          the rest are the cache slabs (826 x 9.44 MB = 7.8 GB at C3)
+  router  bf16 [L, E, H]   (always resident, 0.5 MB per layer)
+  tokens  bf16 [T, H] -> retained [N_r, H] after prune; permuted [N_r*k, H]
+Host: pinned pool bf16 [host_layers*E, 3*I*H] (layer l is served from pool
+layer l % host_layers so pinned RAM stays bounded; bytes moved are real).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+import torch
+
+from . import _lib, kernels
+from ._lib import check
+from .compress import CompressionConfig
+from .configs import Workload
+from .errors import ContractError, ValidationError
+from .pipeline import Engine, PredictorSpec, SimConfig, SimReport
+from .predictor import decay_table, pow_table
+
+
+@dataclass
+class StackConfig:
+    layers: int
+    hidden: int
+    experts: int
+    k: int
+    inter: int
+    l_pinned: int
+    num_slabs: int
+    alpha: float = 0.1
+    beta: float = 0.5
+    lam: float = 2.0
+    predictor: str = "history"  # history | gate | oracle | none
+    budget: int = 20
+    window: int = 5
+    gamma: float = 0.8
+    history_decay: float = 0.5
+    speculative_grace: int = 1
+    victim_policy: str = "priority"
+    routing: str = "live"  # live | trace
+    host_layers: int = 8
+    transfer_ms: float = 0.17  # logical clock: 9.44 MB at ~55 GB/s (measured pinned H2D)
+    gpu_ms: float = 0.002      # logical clock: per-expert FFN time
+    compress_ms: float = 0.0
+    bootstrap_ms: float = 0.0
+    shared_experts: int = 0
+
+    @classmethod
+    def from_workload(cls, w: Workload, **kw) -> "StackConfig":
+        base = dict(layers=w.layers, hidden=w.hidden, experts=w.experts, k=w.k, inter=w.inter,
+                    l_pinned=w.l_pinned, num_slabs=w.num_slabs, alpha=w.alpha, beta=w.beta, lam=w.lam,
+                    predictor=w.predictor, budget=w.budget, window=w.window, gamma=w.gamma,
+                    history_decay=w.history_decay, speculative_grace=w.grace,
+                    shared_experts=w.shared_experts)
+        base.update(kw)
+        return cls(**base)
+
+    @property
+    def slot_elems(self) -> int:
+        return 3 * self.inter * self.hidden
+
+    @property
+    def slot_bytes(self) -> int:
+        return 2 * self.slot_elems
+
+    def sim_config(self) -> SimConfig:
+        """The reference SimConfig whose simulate() replays this stack's decisions."""
+        bw = 1.0
+        return SimConfig(
+            bandwidth_mb_per_ms=bw, expert_size_mb=self.transfer_ms * bw, gpu_ms_per_expert=self.gpu_ms,
+            l_pinned=self.l_pinned, num_slabs=self.num_slabs,
+            predictor=PredictorSpec(kind=self.predictor if self.predictor != "gate" else "oracle",
+                                    budget=self.budget, window=self.window, gamma=self.gamma,
+                                    history_decay=self.history_decay),
+            speculative_grace=self.speculative_grace, victim_policy=self.victim_policy,
+            compress_latency_ms=self.compress_ms, predictor_bootstrap_ms=self.bootstrap_ms,
+            shared_experts=self.shared_experts,
+        )
+
+
+class ExpertStore:
+    """Expert weights: pinned host pool + HBM slot arena + router weights."""
+
+    def __init__(self, cfg: StackConfig, seed: int = 0, device=None):
+        self.cfg = cfg
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        E, H, I, L = cfg.experts, cfg.hidden, cfg.inter, cfg.layers
+        self.host_layers = max(1, min(cfg.host_layers, L))
+        n_host = self.host_layers * E
+        g = torch.Generator(device=dev).manual_seed(seed)
+        self.pool = torch.empty((n_host, cfg.slot_elems), dtype=torch.bfloat16, pin_memory=True)
+        chunk = max(1, (512 << 20) // (cfg.slot_bytes))
+        for s0 in range(0, n_host, chunk):
+            s1 = min(n_host, s0 + chunk)
+            w = torch.randn((s1 - s0, cfg.slot_elems), generator=g, device=dev, dtype=torch.float32)
+            w[:, : 2 * I * H] *= 1.0 / math.sqrt(H)
+            w[:, 2 * I * H:] *= 1.0 / math.sqrt(I)
+            self.pool[s0:s1].copy_(w.to(torch.bfloat16))
+        self.n_pinned_slots = cfg.l_pinned * E
+        self.arena = torch.empty((self.n_pinned_slots + cfg.num_slabs, cfg.slot_elems), dtype=torch.bfloat16,
+                                 device=dev)
+        for l in range(cfg.l_pinned):
+            h = l % self.host_layers
+            self.arena[l * E:(l + 1) * E].copy_(self.pool[h * E:(h + 1) * E], non_blocking=True)
+        self.router = (torch.randn((L, E, H), generator=g, device=dev) / math.sqrt(H)).to(torch.bfloat16)
+        self.pinned_slot_of = (torch.arange(self.n_pinned_slots, dtype=torch.int32, device=dev).reshape(cfg.l_pinned, E)
+                               if cfg.l_pinned else None)
+        torch.cuda.synchronize(dev)
+
+    def expert(self, layer: int, expert: int):
+        """(w_gate [I,H], w_up [I,H], w_down [H,I]) of (layer, expert) from the host pool (for checks)."""
+        c = self.cfg
+        I, H = c.inter, c.hidden
+        slot = self.pool[(layer % self.host_layers) * c.experts + expert]
+        w13 = slot[: 2 * I * H].reshape(I // 64, 2, 64, H)
+        return w13[:, 0].reshape(I, H), w13[:, 1].reshape(I, H), slot[2 * I * H:].reshape(H, I)
+
+
+def route(x, w_gate, k: int, counts=None, stream=None):
+    """Router entry point (no reference equivalent): (ids i32 [N,k], gates f32 [N,k])."""
+    ids, gates, _ = kernels.route_topk(x, w_gate, k, counts=counts, stream=stream)
+    return ids, gates
+
+
+def moe_layer_forward(x, ids, gates, arena, slot_of, inter: int, experts: int, resid=True, stream=None,
+                      bufs: dict | None = None):
+    """One MoE layer on resident experts: permute -> grouped SwiGLU -> combine (+ residual)."""
+    N = int(x.shape[0])
+    k = int(ids.shape[1])
+    off, src, pos = kernels.permute_plan(ids, experts, stream=stream,
+                                         bufs=None if bufs is None else (bufs["off"], bufs["src"], bufs["pos"]))
+    xp = kernels.permute_rows(x, src, N * k, stream=stream, out=None if bufs is None else bufs["xp"][: N * k])
+    h1, y = kernels.grouped_swiglu(xp, off, arena, slot_of, inter, stream=stream,
+                                   h1=None if bufs is None else bufs["h1"][: N * k],
+                                   y=None if bufs is None else bufs["y"][: N * k])
+    out = kernels.combine(y, pos, gates, x if resid else None, stream=stream,
+                          out=None if bufs is None else bufs["out"][:N])
+    return out
+
+
+@dataclass
+class StackResult:
+    hidden: torch.Tensor            # [N_r, H] bf16 output of the last layer (retained tokens)
+    retained: np.ndarray            # retained token ids (ascending)
+    report: SimReport               # decisions / logical-clock report
+    prefix_routes: torch.Tensor     # [l_pinned, T, k] routes of the pinned prefix
+    routes: list                    # per post-prefix layer: ids [N_r, k] (device)
+    scores: dict                    # context layer -> predictor y (np.float64[E])
+    copies: int                     # expert transfers issued
+    h2d_bytes: float
+
+
+class MoEStack:
+    """One-request-at-a-time VL-MoE layer stack with the offloaded expert cache."""
+
+    def __init__(self, cfg: StackConfig, store: ExpertStore | None = None, seed: int = 0):
+        if cfg.predictor == "oracle" and cfg.routing != "trace":
+            raise ValidationError("the oracle predictor needs trace routing (future routes)")
+        if cfg.shared_experts:
+            raise ValidationError("shared experts are not supported by the live stack yet")
+        self.cfg = cfg
+        self.store = store or ExpertStore(cfg, seed)
+        self.device = self.store.device
+        self._L = _lib.lib()
+        h = C.c_void_p()
+        check(self._L.vmm_xfer_create(cfg.num_slabs, cfg.slot_bytes, cfg.layers, C.byref(h)))
+        self._x = h
+        E, L = cfg.experts, cfg.layers
+        self.slot_host = torch.zeros((L, E), dtype=torch.int32, pin_memory=True)
+        self.slot_dev = torch.zeros((L, E), dtype=torch.int32, device=self.device)
+        self.counts_host = torch.zeros((L, E), dtype=torch.int32, pin_memory=True)
+        self.y_host = torch.zeros((L + 1, E), dtype=torch.float64, pin_memory=True)
+        self.pow = torch.tensor(pow_table(cfg.history_decay, L), dtype=torch.float64, device=self.device)
+        self._bufs = {}
+        self.profile = None  # list -> (start_ev, end_ev, bytes, flops) per grouped SwiGLU launch pair
+
+    def __del__(self):
+        h = getattr(self, "_x", None)
+        if h:
+            self._L.vmm_xfer_destroy(h)
+            self._x = None
+
+    @property
+    def copy_stream_handle(self) -> int:
+        return self._L.vmm_xfer_stream(self._x)
+
+    def _buffers(self, n_tok: int):
+        c = self.cfg
+        if self._bufs.get("n", 0) < n_tok:
+            dev = self.device
+            M = n_tok * c.k
+            self._bufs = dict(
+                n=n_tok,
+                off=torch.empty(c.experts + 1, dtype=torch.int32, device=dev),
+                src=torch.empty(M, dtype=torch.int32, device=dev),
+                pos=torch.empty(M, dtype=torch.int32, device=dev),
+                xp=torch.empty(M, c.hidden, dtype=torch.bfloat16, device=dev),
+                h1=torch.empty(M, c.inter, dtype=torch.bfloat16, device=dev),
+                y=torch.empty(M, c.hidden, dtype=torch.bfloat16, device=dev),
+                out=torch.empty(n_tok, c.hidden, dtype=torch.bfloat16, device=dev),
+                out2=torch.empty(n_tok, c.hidden, dtype=torch.bfloat16, device=dev),
+                ids=torch.empty(n_tok, c.k, dtype=torch.int32, device=dev),
+                gates=torch.empty(n_tok, c.k, dtype=torch.float32, device=dev),
+                y_dev=torch.empty(c.experts, dtype=torch.float64, device=dev),
+                scratch=torch.empty(c.experts, dtype=torch.int32, device=dev),
+            )
+        return self._bufs
+
+    def _layer_compute(self, x, ids, gates, slot_of, bufs, out, n_experts=None):
+        c = self.cfg
+        N = int(x.shape[0])
+        off, src, pos = kernels.permute_plan(ids, c.experts, bufs=(bufs["off"], bufs["src"], bufs["pos"]))
+        xp = kernels.permute_rows(x, src, N * c.k, out=bufs["xp"][: N * c.k])
+        if self.profile is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+        _, y = kernels.grouped_swiglu(xp, off, self.store.arena, slot_of, c.inter, h1=bufs["h1"][: N * c.k],
+                                      y=bufs["y"][: N * c.k])
+        if self.profile is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record()
+            M = N * c.k
+            ne = c.experts if n_experts is None else n_experts
+            # algorithmic bytes: weights of the active experts once + Xp read + H1 write/read + Y write
+            nbytes = ne * c.slot_bytes + M * c.hidden * 2 * 2 + M * c.inter * 2 * 2
+            flops = 6.0 * M * c.hidden * c.inter
+            self.profile.append((e0, e1, nbytes, flops))
+        return kernels.combine(y, pos, gates, x, out=out[:N])
+
+    def forward(self, x, saliency, modality, trace=None, record: bool = False) -> StackResult:
+        """Prefill one request.  x bf16 [T, H] (device), saliency f64 [T],
+        modality u8 [T] (0 visual, 1 text; all prefill).  `trace` (routing
+        contract arrays on the device: routes i32 [L,T,k], gates f32 [L,T,k])
+        is required for routing="trace"."""
+        c = self.cfg
+        L, E, k, lp = c.layers, c.experts, c.k, c.l_pinned
+        dev = self.device
+        T = int(x.shape[0])
+        stream = torch.cuda.current_stream()
+        sp = stream.cuda_stream
+        bufs = self._buffers(T)
+        if c.routing == "trace" and trace is None:
+            raise ContractError("routing='trace' needs the trace's device routes")
+        check(self._L.vmm_xfer_reset_stats(self._x))
+
+        # --- pinned prefix: all prefill tokens, resident experts, no cache decisions
+        prefix = torch.empty((max(lp, 1), T, k), dtype=torch.int32, device=dev)
+        counts_pre = torch.zeros((max(lp, 1), E), dtype=torch.int32, device=dev)
+        x_ctx = None
+        cur = x
+        outs = (bufs["out"], bufs["out2"])
+        for l in range(lp):
+            if c.routing == "live":
+                ids, gates, _ = kernels.route_topk(cur, self.store.router[l], k, counts=counts_pre[l], ids=prefix[l],
+                                                   gates=bufs["gates"][:T])
+            else:
+                prefix[l].copy_(trace["routes"][l])
+                ids, gates = prefix[l], trace["gates"][l]
+                kernels.demand_counts(trace["routes"], torch.tensor([l], dtype=torch.int32, device=dev),
+                                      torch.arange(T, dtype=torch.int32, device=dev), E, out=counts_pre[l:l + 1])
+            if l == lp - 1:
+                x_ctx = cur  # input of layer lp-1: context of the boot emission (gate predictor)
+            cur = self._layer_compute(cur, ids, gates, self.store.pinned_slot_of[l], bufs, outs[l % 2])  # noqa
+
+        # --- prune (token compression) on the prefix routes
+        vis = int((modality == 0).sum().item()) if isinstance(modality, torch.Tensor) else int((np.asarray(modality) == 0).sum())
+        ccfg = CompressionConfig(c.alpha, c.beta, c.lam, tuple(range(lp)) if lp else (0,))
+        k_core, k_keep = ccfg.budgets(vis)
+        pr = kernels.prune(saliency, modality, prefix[:max(lp, 1)],
+                           torch.tensor([0, T], dtype=torch.int32, device=dev),
+                           torch.tensor([k_core], dtype=torch.int32, device=dev),
+                           torch.tensor([k_keep], dtype=torch.int32, device=dev), E, c.lam)
+        n_r = int(pr["n_retained"].item())
+        if int(pr["status"].item()) != 0:
+            raise ValidationError("saliency entries must be finite and >= 0")
+        ret = pr["retained"][:n_r]
+        xr = kernels.gather_rows(cur, ret, out=bufs["xp"][:n_r])  # scratch until permute of layer lp
+        xr = xr.clone()
+
+        # --- per-layer demand counts over the retained tokens
+        counts_ret = torch.zeros((L, E), dtype=torch.int32, device=dev)
+        if lp:
+            kernels.demand_counts(prefix[:lp], torch.arange(lp, dtype=torch.int32, device=dev), ret, E,
+                                  out=counts_ret[:lp])
+        oracle_table = None
+        if c.predictor == "oracle":
+            rl = trace["routes"]
+            kernels.demand_counts(rl, torch.arange(L, dtype=torch.int32, device=dev), ret, E, out=counts_ret)
+            ctx = torch.arange(max(lp - 1, 0), L, dtype=torch.int32, device=dev)
+            dec = torch.tensor(decay_table(c.gamma, c.window), dtype=torch.float64, device=dev)
+            oracle_table = kernels.oracle_targets(counts_ret, ctx, c.window, dec)
+
+        cfg = c.sim_config()
+        prefetching = c.predictor != "none" and c.budget > 0
+        eng = Engine(L, E, cfg, c.num_slabs, lp, 0, prefetching, False, c.compress_ms + (c.bootstrap_ms if prefetching else 0.0))
+        scores = {}
+
+        def predict(ctx: int, x_in):
+            """device y for context layer ctx (x_in: retained hidden states entering layer ctx)."""
+            if c.predictor == "history":
+                yt = kernels.history(counts_ret, torch.tensor([ctx], dtype=torch.int32, device=dev), self.pow)[0]
+            elif c.predictor == "gate":
+                yt = kernels.gate_lookahead(x_in, self.store.router[ctx + 1], k, scratch=bufs["scratch"],
+                                            out=bufs["y_dev"])
+            else:
+                yt = oracle_table[ctx - max(lp - 1, 0)]
+            self.y_host[ctx].copy_(yt, non_blocking=True)
+            return self.y_host[ctx]
+
+        # boot emission at context lp-1 over the retained tokens
+        if prefetching and lp > 0:
+            x_boot = kernels.gather_rows(x_ctx, ret) if c.predictor == "gate" else None
+            yb = predict(lp - 1, x_boot)
+            stream.synchronize()
+            scores[lp - 1] = yb.numpy().copy()
+            eng.begin(scores[lp - 1])
+        else:
+            eng.begin(None)
+        self._issue(eng)
+        cp = counts_pre[:lp].cpu().numpy() if lp else None
+        for l in range(lp):
+            eng.layer(l, np.flatnonzero(cp[l]).astype(np.int32), 0, -1, None)
+
+        # --- cached layers on the retained tokens
+        routes = []
+        cur = xr
+        n_copies = 0
+        ping = 0
+        for l in range(lp, L):
+            if c.routing == "live":
+                ids, gates, _ = kernels.route_topk(cur, self.store.router[l], k, counts=counts_ret[l],
+                                                   ids=bufs["ids"][:n_r], gates=bufs["gates"][:n_r])
+            else:
+                ids = trace["routes"][l].index_select(0, ret.long())
+                gates = trace["gates"][l].index_select(0, ret.long())
+                if c.predictor != "oracle":
+                    kernels.demand_counts(trace["routes"], torch.tensor([l], dtype=torch.int32, device=dev), ret, E,
+                                          out=counts_ret[l:l + 1])
+            if record:
+                routes.append(ids.clone())
+            emits = eng.emits(l, 0)
+            y_row = predict(l, cur) if emits else None
+            self.counts_host[l].copy_(counts_ret[l], non_blocking=True)
+            stream.synchronize()
+            demand = np.flatnonzero(self.counts_host[l].numpy()).astype(np.int32)
+            eng.layer(l, demand, 0, -1, None)
+            n_copies += self._issue(eng)
+            slabs = np.empty(len(demand), dtype=np.int32)
+            check(self._L.vmm_engine_slots(eng._h, l, demand.ctypes.data, len(demand), slabs.ctypes.data))
+            row = self.slot_host[l].numpy()
+            row[:] = 0
+            row[demand] = slabs + self.store.n_pinned_slots
+            self.slot_dev[l].copy_(self.slot_host[l], non_blocking=True)
+            check(self._L.vmm_xfer_fence(self._x, slabs.ctypes.data, len(slabs), sp))
+            cur = self._layer_compute(cur, ids, gates, self.slot_dev[l], bufs, outs[ping], n_experts=len(demand))
+            ping ^= 1
+            check(self._L.vmm_xfer_layer_done(self._x, l, sp))
+            if emits:
+                scores[l] = y_row.numpy().copy()
+                check(self._L.vmm_engine_emit(eng._h, l, scores[l].ctypes.data))
+                n_copies += self._issue(eng)
+        check(self._L.vmm_xfer_join(self._x, sp))  # the step ends when its last transfer has landed
+        report = eng.finish(with_events=False)
+        b, ms, cnt = C.c_double(), C.c_double(), C.c_longlong()
+        check(self._L.vmm_xfer_stats(self._x, C.byref(b), C.byref(ms), C.byref(cnt)))
+        return StackResult(hidden=cur, retained=ret.cpu().numpy(), report=report, prefix_routes=prefix[:lp],
+                           routes=routes, scores=scores, copies=n_copies, h2d_bytes=b.value)
+
+    def _issue(self, eng: Engine) -> int:
+        n = C.c_int()
+        check(self._L.vmm_xfer_issue_engine(self._x, eng._h, self.store.pool.data_ptr(), self.store.host_layers,
+                                            self.cfg.experts, self.store.arena.data_ptr(),
+                                            self.store.n_pinned_slots, self.cfg.slot_bytes, C.byref(n)))
+        return n.value
+
+    def sync(self):
+        check(self._L.vmm_xfer_sync(self._x))
+        torch.cuda.synchronize()

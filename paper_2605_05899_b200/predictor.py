@@ -218,7 +218,9 @@ def _rowwise_mean(emb: torch.Tensor, rows) -> torch.Tensor:
     acc = torch.zeros(emb.shape[1], dtype=torch.float64, device=emb.device)
     for r in range(sel.shape[0]):
         acc = acc + sel[r]
-    return acc / sel.shape[0]
+    # divide by a device tensor: torch turns division by a CPU scalar into a
+    # reciprocal multiply, which is not the correctly rounded quotient numpy computes
+    return acc / torch.full_like(acc, float(sel.shape[0]))
 
 
 def build_targets(trace, layer: int, window: int = DEFAULT_WINDOW, gamma: float = DEFAULT_GAMMA, token_ids=None):

@@ -57,12 +57,12 @@ def _expert_setup(N, H, I, E, k, n_slots, seed):
     wg = (torch.randn(n_slots, I, H, generator=g) / H ** 0.5).to(torch.bfloat16)
     wu = (torch.randn(n_slots, I, H, generator=g) / H ** 0.5).to(torch.bfloat16)
     wd = (torch.randn(n_slots, H, I, generator=g) / I ** 0.5).to(torch.bfloat16)
-    w13 = torch.stack([kernels.interleave_w13(wg[s], wu[s]) for s in range(n_slots)])
+    arena = torch.stack([kernels.pack_expert(wg[s], wu[s], wd[s]) for s in range(n_slots)])
     # skewed routing: some experts empty, some with > 128 rows
     logits = torch.randn(N, E, generator=g) + torch.linspace(3, -3, E)
     ids = torch.topk(logits, k, dim=1).indices.int()
     slot_of = torch.randperm(n_slots, generator=g)[:E].int()
-    return x, wg, wu, wd, w13, ids, slot_of
+    return x, wg, wu, wd, arena, ids, slot_of
 
 
 @pytest.mark.parametrize("simt", [False, True])
@@ -70,11 +70,11 @@ def _expert_setup(N, H, I, E, k, n_slots, seed):
 def test_grouped_swiglu_matches_fp32_restatement(shape, simt):
     N, H, I, E, k = shape
     n_slots = E + 3
-    x, wg, wu, wd, w13, ids, slot_of = _expert_setup(N, H, I, E, k, n_slots, seed=N + E)
+    x, wg, wu, wd, arena, ids, slot_of = _expert_setup(N, H, I, E, k, n_slots, seed=N + E)
     off, src, pos = kernels.permute_plan(ids.cuda(), E)
     M = N * k
     xp = kernels.permute_rows(x.cuda(), src, M)
-    h1, y = kernels.grouped_swiglu(xp, off, w13.cuda(), wd.cuda(), slot_of.cuda(), I, simt=simt)
+    h1, y = kernels.grouped_swiglu(xp, off, arena.cuda(), slot_of.cuda(), I, simt=simt)
     torch.cuda.synchronize()
     roff, rsrc, rpos = moe_ref.permute(ids, E)
     xr = x[rsrc]
