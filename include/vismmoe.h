@@ -123,6 +123,10 @@ int vmm_permute_plan(const int32_t *d_ids, int N, int k, int E, int32_t *d_offse
                      int32_t *d_src_row, int32_t *d_pos, void *stream);
 /* Xp[p] = X[src_row[p]] for the n_rows permuted rows (bf16 rows of H) */
 int vmm_permute_rows(const void *d_x, const int32_t *d_src_row, int n_rows, int H, void *d_xp, void *stream);
+/* Pre-MoE RMSNorm of the token rows (the layer's router and experts see the
+ * normalised rows, the residual is the raw row): y = x * rsqrt(mean(x^2)+eps) * w
+ * (w nullable = ones). */
+int vmm_rmsnorm(const void *d_x, const void *d_w, int n, int H, float eps, void *d_y, void *stream);
 /* out[t] = resid[t] + sum_j gates[t,j] * Y[pos[t,j]]  (bf16 rows, fp32 accumulate, j ascending) */
 int vmm_combine(const void *d_y, const int32_t *d_pos, const float *d_gates, const void *d_resid,
                 int N, int k, int H, void *d_out, void *stream);

@@ -121,7 +121,54 @@ __global__ void combine_kernel(const uint4 *__restrict__ y, const int32_t *__res
   }
 }
 
+// y[r] = x[r] * rsqrt(mean(x[r]^2) + eps) (* w), one warp per row, fp32 statistics
+__global__ void rmsnorm_kernel(const uint4 *__restrict__ x, const __nv_bfloat16 *__restrict__ w, int n, int row_vec,
+                               float eps, uint4 *__restrict__ y) {
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int r = warp; r < n; r += nw) {
+    const uint4 *s = x + (long long)r * row_vec;
+    float ss = 0.f;
+    for (int c = lane; c < row_vec; c += 32) {
+      uint4 v = __ldg(s + c);
+      const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&v);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) { float f = __bfloat162float(h[q]); ss = fmaf(f, f, ss); }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const float inv = rsqrtf(ss / (float)(row_vec * 8) + eps);
+    uint4 *d = y + (long long)r * row_vec;
+    for (int c = lane; c < row_vec; c += 32) {
+      uint4 v = __ldg(s + c);
+      const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&v);
+      uint4 o;
+      __nv_bfloat16 *oh = reinterpret_cast<__nv_bfloat16 *>(&o);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float f = __bfloat162float(h[q]) * inv;
+        if (w) f *= __bfloat162float(w[c * 8 + q]);
+        oh[q] = __float2bfloat16(f);
+      }
+      d[c] = o;
+    }
+  }
+}
+
 }  // namespace
+
+extern "C" int vmm_rmsnorm(const void *d_x, const void *d_w, int n, int H, float eps, void *d_y, void *stream) {
+  if (n <= 0) return VMM_OK;
+  if ((H * 2) % 16) return vmm::fail(VMM_EVALIDATION, "hidden size must be a multiple of 8");
+  int row_vec = H * 2 / 16;
+  int warps = n < 148 * 32 ? n : 148 * 32;
+  int blocks = (warps * 32 + 255) / 256;
+  rmsnorm_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((const uint4 *)d_x, (const __nv_bfloat16 *)d_w, n, row_vec,
+                                                           eps, (uint4 *)d_y);
+  VMM_LAUNCH_CHECK("rmsnorm_kernel");
+  return VMM_OK;
+}
 
 extern "C" int vmm_permute_plan(const int32_t *d_ids, int N, int k, int E, int32_t *d_offsets, int32_t *d_src_row,
                                 int32_t *d_pos, void *stream) {

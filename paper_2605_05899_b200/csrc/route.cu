@@ -92,6 +92,7 @@ route_kernel(const __nv_bfloat16 *__restrict__ x, const __nv_bfloat16 *__restric
         int e = tx + 32 * j;
         if (e < E && !((taken[j] >> tx) & 1u)) {
           float v = row[e];
+          if (v != v) v = -INFINITY;  // NaN ranks below every number
           if (v > best || (v == best && e < bi) || bi == 0x7fffffff) { best = v; bi = e; }
         }
       }
@@ -100,6 +101,7 @@ route_kernel(const __nv_bfloat16 *__restrict__ x, const __nv_bfloat16 *__restric
         int oi = __shfl_xor_sync(0xffffffffu, bi, o);
         if (oi != 0x7fffffff && (bi == 0x7fffffff || ov > best || (ov == best && oi < bi))) { best = ov; bi = oi; }
       }
+      if (bi == 0x7fffffff) bi = 0;  // unreachable for k <= E; keeps indices in range
       vals[s] = best;
       sel[s] = bi;
       if ((bi & 31) == tx) taken[bi >> 5] |= 1u << tx;

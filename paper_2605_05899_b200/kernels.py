@@ -191,6 +191,14 @@ def pack_expert(w_gate, w_up, w_down):
     return torch.cat([interleave_w13(w_gate, w_up).reshape(-1), w_down.reshape(-1)])
 
 
+def rmsnorm(x, weight=None, eps: float = 1e-6, stream=None, out=None):
+    n, H = (int(s) for s in x.shape)
+    out = torch.empty_like(x) if out is None else out
+    _n(1)
+    check(_lib.lib().vmm_rmsnorm(ptr(x), ptr(weight), n, H, float(eps), ptr(out), stream_ptr(stream)))
+    return out
+
+
 def combine(y, pos, gates, resid, stream=None, out=None):
     N, k = (int(s) for s in gates.shape)
     H = int(y.shape[1])

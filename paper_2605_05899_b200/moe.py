@@ -148,13 +148,16 @@ def route(x, w_gate, k: int, counts=None, stream=None):
 
 
 def moe_layer_forward(x, ids, gates, arena, slot_of, inter: int, experts: int, resid=True, stream=None,
-                      bufs: dict | None = None):
-    """One MoE layer on resident experts: permute -> grouped SwiGLU -> combine (+ residual)."""
+                      bufs: dict | None = None, xn=None):
+    """One MoE layer on resident experts: permute -> grouped SwiGLU -> combine (+ residual).
+
+    x: residual rows; xn: the normalised rows the router/experts see (default x)."""
     N = int(x.shape[0])
     k = int(ids.shape[1])
+    xn = x if xn is None else xn
     off, src, pos = kernels.permute_plan(ids, experts, stream=stream,
                                          bufs=None if bufs is None else (bufs["off"], bufs["src"], bufs["pos"]))
-    xp = kernels.permute_rows(x, src, N * k, stream=stream, out=None if bufs is None else bufs["xp"][: N * k])
+    xp = kernels.permute_rows(xn, src, N * k, stream=stream, out=None if bufs is None else bufs["xp"][: N * k])
     h1, y = kernels.grouped_swiglu(xp, off, arena, slot_of, inter, stream=stream,
                                    h1=None if bufs is None else bufs["h1"][: N * k],
                                    y=None if bufs is None else bufs["y"][: N * k])
@@ -224,6 +227,7 @@ class MoEStack:
                 y=torch.empty(M, c.hidden, dtype=torch.bfloat16, device=dev),
                 out=torch.empty(n_tok, c.hidden, dtype=torch.bfloat16, device=dev),
                 out2=torch.empty(n_tok, c.hidden, dtype=torch.bfloat16, device=dev),
+                xn=torch.empty(n_tok, c.hidden, dtype=torch.bfloat16, device=dev),
                 ids=torch.empty(n_tok, c.k, dtype=torch.int32, device=dev),
                 gates=torch.empty(n_tok, c.k, dtype=torch.float32, device=dev),
                 y_dev=torch.empty(c.experts, dtype=torch.float64, device=dev),
@@ -231,11 +235,11 @@ class MoEStack:
             )
         return self._bufs
 
-    def _layer_compute(self, x, ids, gates, slot_of, bufs, out, n_experts=None):
+    def _layer_compute(self, x, xn, ids, gates, slot_of, bufs, out, n_experts=None):
         c = self.cfg
         N = int(x.shape[0])
         off, src, pos = kernels.permute_plan(ids, c.experts, bufs=(bufs["off"], bufs["src"], bufs["pos"]))
-        xp = kernels.permute_rows(x, src, N * c.k, out=bufs["xp"][: N * c.k])
+        xp = kernels.permute_rows(xn, src, N * c.k, out=bufs["xp"][: N * c.k])
         if self.profile is not None:
             e0 = torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -275,8 +279,9 @@ class MoEStack:
         cur = x
         outs = (bufs["out"], bufs["out2"])
         for l in range(lp):
+            xn = kernels.rmsnorm(cur, out=bufs["xn"][:T])
             if c.routing == "live":
-                ids, gates, _ = kernels.route_topk(cur, self.store.router[l], k, counts=counts_pre[l], ids=prefix[l],
+                ids, gates, _ = kernels.route_topk(xn, self.store.router[l], k, counts=counts_pre[l], ids=prefix[l],
                                                    gates=bufs["gates"][:T])
             else:
                 prefix[l].copy_(trace["routes"][l])
@@ -284,8 +289,8 @@ class MoEStack:
                 kernels.demand_counts(trace["routes"], torch.tensor([l], dtype=torch.int32, device=dev),
                                       torch.arange(T, dtype=torch.int32, device=dev), E, out=counts_pre[l:l + 1])
             if l == lp - 1:
-                x_ctx = cur  # input of layer lp-1: context of the boot emission (gate predictor)
-            cur = self._layer_compute(cur, ids, gates, self.store.pinned_slot_of[l], bufs, outs[l % 2])  # noqa
+                x_ctx = xn  # normalised input of layer lp-1: context of the boot emission (gate predictor)
+            cur = self._layer_compute(cur, xn, ids, gates, self.store.pinned_slot_of[l], bufs, outs[l % 2])
 
         # --- prune (token compression) on the prefix routes
         vis = int((modality == 0).sum().item()) if isinstance(modality, torch.Tensor) else int((np.asarray(modality) == 0).sum())
@@ -341,7 +346,7 @@ class MoEStack:
             eng.begin(scores[lp - 1])
         else:
             eng.begin(None)
-        self._issue(eng)
+        n_copies = self._issue(eng)
         cp = counts_pre[:lp].cpu().numpy() if lp else None
         for l in range(lp):
             eng.layer(l, np.flatnonzero(cp[l]).astype(np.int32), 0, -1, None)
@@ -349,11 +354,11 @@ class MoEStack:
         # --- cached layers on the retained tokens
         routes = []
         cur = xr
-        n_copies = 0
         ping = 0
         for l in range(lp, L):
+            xn = kernels.rmsnorm(cur, out=bufs["xn"][:n_r])
             if c.routing == "live":
-                ids, gates, _ = kernels.route_topk(cur, self.store.router[l], k, counts=counts_ret[l],
+                ids, gates, _ = kernels.route_topk(xn, self.store.router[l], k, counts=counts_ret[l],
                                                    ids=bufs["ids"][:n_r], gates=bufs["gates"][:n_r])
             else:
                 ids = trace["routes"][l].index_select(0, ret.long())
@@ -364,7 +369,7 @@ class MoEStack:
             if record:
                 routes.append(ids.clone())
             emits = eng.emits(l, 0)
-            y_row = predict(l, cur) if emits else None
+            y_row = predict(l, xn) if emits else None
             self.counts_host[l].copy_(counts_ret[l], non_blocking=True)
             stream.synchronize()
             demand = np.flatnonzero(self.counts_host[l].numpy()).astype(np.int32)
@@ -377,7 +382,7 @@ class MoEStack:
             row[demand] = slabs + self.store.n_pinned_slots
             self.slot_dev[l].copy_(self.slot_host[l], non_blocking=True)
             check(self._L.vmm_xfer_fence(self._x, slabs.ctypes.data, len(slabs), sp))
-            cur = self._layer_compute(cur, ids, gates, self.slot_dev[l], bufs, outs[ping], n_experts=len(demand))
+            cur = self._layer_compute(cur, xn, ids, gates, self.slot_dev[l], bufs, outs[ping], n_experts=len(demand))
             ping ^= 1
             check(self._L.vmm_xfer_layer_done(self._x, l, sp))
             if emits:

@@ -130,25 +130,30 @@ def test_cached_run_bit_identical_to_all_resident_run():
     from paper_2605_05899_b200 import kernels
     cur = x
     for l in range(cfg.l_pinned):
-        ids, gates, _ = kernels.route_topk(cur, store.router[l], cfg.k)
+        xn = kernels.rmsnorm(cur)
+        ids, gates, _ = kernels.route_topk(xn, store.router[l], cfg.k)
         cur = moe_layer_forward(cur, ids, gates, arena, torch.arange(l * E, (l + 1) * E, dtype=torch.int32,
-                                                                      device="cuda"), cfg.inter, E)
+                                                                      device="cuda"), cfg.inter, E, xn=xn)
     ret = torch.from_numpy(res.retained.astype(np.int32)).cuda()
     cur = kernels.gather_rows(cur, ret)
     x_in = []
     for l in range(cfg.l_pinned, cfg.layers):
-        x_in.append(cur)
-        ids, gates, _ = kernels.route_topk(cur, store.router[l], cfg.k)
+        xn = kernels.rmsnorm(cur)
+        x_in.append((cur, xn))
+        ids, gates, _ = kernels.route_topk(xn, store.router[l], cfg.k)
         cur = moe_layer_forward(cur, ids, gates, arena, torch.arange(l * E, (l + 1) * E, dtype=torch.int32,
-                                                                      device="cuda"), cfg.inter, E)
+                                                                      device="cuda"), cfg.inter, E, xn=xn)
     torch.cuda.synchronize()
     assert res.copies > 0
     assert torch.equal(res.hidden, cur)
     # and close to a torch fp32 restatement of the last layer
     l = cfg.layers - 1
-    xl = x_in[-1].cpu()
+    xr, xl = (t.cpu() for t in x_in[-1])
+    # rmsnorm restated in fp32 (bf16 rounded like the device) vs the device rows
+    xnf = (xr.float() * torch.rsqrt(xr.float().pow(2).mean(1, keepdim=True) + 1e-6)).to(torch.bfloat16)
+    torch.testing.assert_close(xnf.float(), xl.float(), rtol=1e-2, atol=1e-2)
     ids, gates, _ = moe_ref.route(xl, store.router[l].cpu(), cfg.k)
-    acc = xl.float().clone()
+    acc = xr.float().clone()
     for t in range(0, xl.shape[0], 97):
         for j in range(cfg.k):
             e = int(ids[t, j])
