@@ -81,6 +81,13 @@ int vmm_route_topk(const void *d_x, const void *d_wg, int N, int H, int E, int k
                    int32_t *d_ids, float *d_gates, float *d_logits /* nullable [N,E] */,
                    uint32_t *d_counts /* nullable [E] */, void *stream);
 
+/* Fused router + gate-reuse lookahead for layer `layer` of a stacked router
+ * [L][E][H]: one tcgen05 GEMM against the adjacent gates of layers l and l+1;
+ * writes layer l's ids/gates/counts and the pick counts of layer l+1's gate on
+ * the same rows (the lookahead predictor's input).  E in {16,32,64,128}. */
+int vmm_route_lookahead(const void *d_x, const void *d_router, int layer, int L, int N, int H, int E, int k,
+                        int32_t *d_ids, float *d_gates, uint32_t *d_counts, uint32_t *d_la_counts, void *stream);
+
 /* ------------------------------------------------------------------------
  * Demand / predictor kernels (pkg/src/moesim/predictor.py)
  * ------------------------------------------------------------------------ */
@@ -110,6 +117,7 @@ int vmm_mlp_predict(const double *d_hist /* [n_ctx][E] */, const double *d_emb, 
                     double *d_feat /* nullable [n_ctx][E+2D] */, double *d_y, void *stream);
 /* Gate-reuse lookahead: counts of experts in the top-k of W_next applied to
  * layer-l hidden states, normalised by N*k -> y f64 [E]. */
+int vmm_normalize_counts(const uint32_t *d_counts, int E, double denom, double *d_y, void *stream);
 int vmm_gate_lookahead(const void *d_x, const void *d_wnext, int N, int H, int E, int k,
                        uint32_t *d_scratch_counts /* [E] */, double *d_y, void *stream);
 

@@ -52,6 +52,8 @@ _SIGS = {
     "vmm_prune": (I32, [P, P, P, P, P, P, I32, I32, I32, I32, I32, F64, P, P, P, P, P, P, P, P, P]),
     "vmm_gather_rows": (I32, [P, P, I32, I32, P, P]),
     "vmm_route_topk": (I32, [P, P, I32, I32, I32, I32, P, P, P, P, P]),
+    "vmm_route_lookahead": (I32, [P, P, I32, I32, I32, I32, I32, I32, P, P, P, P, P]),
+    "vmm_normalize_counts": (I32, [P, I32, F64, P, P]),
     "vmm_demand_counts": (I32, [P, I32, I32, I32, I32, P, I32, P, I32, P, P]),
     "vmm_oracle_targets": (I32, [P, I32, I32, P, I32, I32, P, P, P]),
     "vmm_history": (I32, [P, I32, I32, P, I32, P, P, P]),

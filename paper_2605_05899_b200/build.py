@@ -25,6 +25,8 @@ CU = {
     "prune.cu": ["-fmad=false"],
     "predict.cu": ["-fmad=false"],
     "route.cu": [],
+    "route_sm100.cu": [],
+    "sm100.cu": [],
     "permute.cu": [],
     "ffn_sm100.cu": [],
 }
@@ -46,7 +48,8 @@ def _run(cmd):
 
 
 def _stale(obj, src):
-    deps = [src, os.path.join(CSRC, "common.cuh"), os.path.join(HERE, "..", "include", "vismmoe.h")]
+    deps = [src, os.path.join(CSRC, "common.cuh"), os.path.join(CSRC, "sm100.cuh"),
+            os.path.join(HERE, "..", "include", "vismmoe.h")]
     return not os.path.exists(obj) or any(os.path.getmtime(d) > os.path.getmtime(obj) for d in deps if os.path.exists(d))
 
 

@@ -211,6 +211,12 @@ extern "C" int vmm_mlp_predict(const double *d_hist, const double *d_emb, int D,
   return VMM_OK;
 }
 
+extern "C" int vmm_normalize_counts(const uint32_t *d_counts, int E, double denom, double *d_y, void *stream) {
+  normalize_counts_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(d_counts, E, denom, d_y);
+  VMM_LAUNCH_CHECK("normalize_counts_kernel");
+  return VMM_OK;
+}
+
 extern "C" int vmm_gate_lookahead(const void *d_x, const void *d_wnext, int N, int H, int E, int k,
                                   uint32_t *d_scratch_counts, double *d_y, void *stream) {
   cudaStream_t s = (cudaStream_t)stream;

@@ -122,11 +122,32 @@ route_kernel(const __nv_bfloat16 *__restrict__ x, const __nv_bfloat16 *__restric
 
 }  // namespace
 
+namespace vmm {
+int route_sm100(const void *x, const void *wg_base, int w_row0, long long w_rows, int N, int H, int E, int k,
+                int32_t *ids, float *gates, float *logits, uint32_t *counts, uint32_t *la_counts, bool fused,
+                cudaStream_t s);
+}
+
+extern "C" int vmm_route_lookahead(const void *d_x, const void *d_router, int layer, int L, int N, int H, int E, int k,
+                                   int32_t *d_ids, float *d_gates, uint32_t *d_counts, uint32_t *d_la_counts,
+                                   void *stream) {
+  if (N <= 0) return VMM_OK;
+  if (layer < 0 || layer + 1 >= L) return vmm::fail(VMM_ECONTRACT, "lookahead needs a next layer");
+  int st = vmm::route_sm100(d_x, d_router, layer * E, (long long)L * E, N, H, E, k, d_ids, d_gates, nullptr,
+                            d_counts, d_la_counts, true, (cudaStream_t)stream);
+  if (st == -1) return vmm::fail(VMM_EVALIDATION, "fused route+lookahead needs E in {16,32,64,128}, H % 64 == 0");
+  return st;
+}
+
 extern "C" int vmm_route_topk(const void *d_x, const void *d_wg, int N, int H, int E, int k, int32_t *d_ids,
                               float *d_gates, float *d_logits, uint32_t *d_counts, void *stream) {
   if (N <= 0) return VMM_OK;
   if (E < 1 || E > kMaxE) return vmm::fail(VMM_EVALIDATION, "router: experts must lie in [1, 256]");
   if (k < 1 || k > kMaxK || k > E) return vmm::fail(VMM_EVALIDATION, "router: k must lie in [1, min(16, E)]");
+  int st = vmm::route_sm100(d_x, d_wg, 0, E, N, H, E, k, d_ids, d_gates, d_logits, d_counts, nullptr, false,
+                            (cudaStream_t)stream);
+  if (st != -1) return st;
+  // shapes the tcgen05 tile does not cover (E > 128 or H % 64): CUDA-core kernel
   size_t smem = sizeof(float) * ((size_t)kTok * (kKc + 1) + (size_t)E * (kKc + 1) + (size_t)kTok * E);
   static bool attr = false;
   if (!attr) {

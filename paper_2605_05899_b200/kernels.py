@@ -83,6 +83,26 @@ def route_topk(x, w_gate, k: int, counts=None, want_logits=False, stream=None, i
     return ids, gates, logits
 
 
+def route_lookahead(x, router, layer: int, k: int, counts, la_counts, stream=None, ids=None, gates=None):
+    """Fused router (layer) + gate lookahead (layer+1) on the same rows; router bf16 [L, E, H]."""
+    N, H = (int(s) for s in x.shape)
+    L_, E = int(router.shape[0]), int(router.shape[1])
+    ids = torch.empty(N, k, dtype=_i32, device=x.device) if ids is None else ids
+    gates = torch.empty(N, k, dtype=torch.float32, device=x.device) if gates is None else gates
+    _n(1)
+    check(_lib.lib().vmm_route_lookahead(ptr(x), ptr(router), layer, L_, N, H, E, k, ptr(ids), ptr(gates),
+                                         ptr(counts), ptr(la_counts), stream_ptr(stream)))
+    return ids, gates
+
+
+def normalize_counts(counts, denom: float, stream=None, out=None):
+    E = int(counts.shape[0])
+    out = torch.empty(E, dtype=torch.float64, device=counts.device) if out is None else out
+    _n(1)
+    check(_lib.lib().vmm_normalize_counts(ptr(counts), E, float(denom), ptr(out), stream_ptr(stream)))
+    return out
+
+
 def demand_counts(routes, layers, ids, experts: int, stream=None, out=None):
     """routes i32 [L, T, k]; layers i32 [n]; ids i32 [m] -> u32-as-i32 counts [n, E]."""
     L_, T, k = (int(s) for s in routes.shape)

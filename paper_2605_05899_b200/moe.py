@@ -357,7 +357,14 @@ class MoEStack:
         ping = 0
         for l in range(lp, L):
             xn = kernels.rmsnorm(cur, out=bufs["xn"][:n_r])
-            if c.routing == "live":
+            fused_la = (c.routing == "live" and c.predictor == "gate" and E % 16 == 0 and E <= 128
+                        and eng.emits(l, 0))
+            if fused_la:
+                # one tcgen05 GEMM against the adjacent gates of layers l and l+1
+                bufs["scratch"].zero_()
+                ids, gates = kernels.route_lookahead(xn, self.store.router, l, k, counts_ret[l], bufs["scratch"],
+                                                     ids=bufs["ids"][:n_r], gates=bufs["gates"][:n_r])
+            elif c.routing == "live":
                 ids, gates, _ = kernels.route_topk(xn, self.store.router[l], k, counts=counts_ret[l],
                                                    ids=bufs["ids"][:n_r], gates=bufs["gates"][:n_r])
             else:
@@ -369,7 +376,12 @@ class MoEStack:
             if record:
                 routes.append(ids.clone())
             emits = eng.emits(l, 0)
-            y_row = predict(l, xn) if emits else None
+            if emits and fused_la:
+                yt = kernels.normalize_counts(bufs["scratch"], float(n_r * k), out=bufs["y_dev"])
+                self.y_host[l].copy_(yt, non_blocking=True)
+                y_row = self.y_host[l]
+            else:
+                y_row = predict(l, xn) if emits else None
             self.counts_host[l].copy_(counts_ret[l], non_blocking=True)
             stream.synchronize()
             demand = np.flatnonzero(self.counts_host[l].numpy()).astype(np.int32)

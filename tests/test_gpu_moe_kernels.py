@@ -95,3 +95,20 @@ def test_grouped_swiglu_matches_fp32_restatement(shape, simt):
     out = kernels.combine(y, pos, gates.cuda(), x.cuda())
     ref = moe_ref.combine(y.cpu(), rpos, gates, x)
     torch.testing.assert_close(out.cpu().float(), ref.float(), rtol=2e-2, atol=2e-2)
+
+
+def test_fused_route_and_lookahead_exact_on_integer_inputs():
+    g = torch.Generator().manual_seed(9)
+    L, N, H, E, k = 4, 1216, 2048, 128, 8
+    x = torch.randint(-4, 5, (N, H), generator=g).to(torch.bfloat16)
+    router = torch.randint(-1, 2, (L, E, H), generator=g).to(torch.bfloat16)
+    for layer in (0, 2):
+        counts = torch.zeros(E, dtype=torch.int32, device="cuda")
+        la = torch.zeros(E, dtype=torch.int32, device="cuda")
+        ids, gates = kernels.route_lookahead(x.cuda(), router.cuda(), layer, k, counts, la)
+        rid, rg, _ = moe_ref.route(x, router[layer], k)
+        assert torch.equal(ids.cpu(), rid)
+        assert (gates.cpu() - rg).abs().max().item() <= 1e-6
+        nid, _, _ = moe_ref.route(x, router[layer + 1], k)
+        assert torch.equal(la.cpu().long(), torch.bincount(nid.reshape(-1).long(), minlength=E))
+        assert torch.equal(counts.cpu().long(), torch.bincount(rid.reshape(-1).long(), minlength=E))
