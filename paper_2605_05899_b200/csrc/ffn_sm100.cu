@@ -25,145 +25,182 @@ namespace {
 using namespace sm100;
 
 constexpr int BM = 128, BN = 128, BK = 64;
-constexpr int kStages = 4;
+constexpr int kStages = 6;
 constexpr int kThreads = 192;
 constexpr uint32_t kTileBytes = BM * BK * 2;  // 16 KB (A) == BN*BK*2 (B)
 constexpr uint32_t kStageBytes = 2 * kTileBytes;
 constexpr size_t kSmemBytes = (size_t)kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+int g_num_sms = 0;
 
-// ---- the grouped GEMM ---------------------------------------------------
-// kSwiGLU: epilogue fuses SiLU(gate) * up over the interleaved 64|64 column
-// halves and writes 64 bf16 per row; otherwise writes 128 bf16 per row.
+// ---- the grouped GEMM (persistent, warp-specialised) ----------------------
+// Tiles: (m_tile, n_tile) with n fastest; m_tiles are ceil(M_e / BM) per expert.
+// Roles: warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer, warps 2..5
+// epilogue.  The smem ring runs continuously across tiles and the accumulator
+// is double-buffered in TMEM (2 x BN columns), so the epilogue of tile i
+// overlaps the TMA/MMA of tile i+1 and HBM streaming never drains between tiles.
+struct TileInfo {
+  int expert, row0, row_end, slot, n_tile;
+};
+
+__device__ __forceinline__ TileInfo tile_info(int t, int n_tiles, const int *tile_base, const int *offs,
+                                              const int *slots, int E) {
+  TileInfo ti;
+  const int m_tile = t / n_tiles;
+  ti.n_tile = t - m_tile * n_tiles;
+  int lo = 0, hi = E - 1;  // last expert with tile_base[e] <= m_tile
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (tile_base[mid] <= m_tile) lo = mid; else hi = mid - 1;
+  }
+  // skip experts with zero tiles (tile_base[e] == tile_base[e+1])
+  while (lo + 1 < E && tile_base[lo + 1] <= m_tile) ++lo;
+  ti.expert = lo;
+  ti.row0 = offs[lo] + (m_tile - tile_base[lo]) * BM;
+  ti.row_end = offs[lo + 1];
+  ti.slot = slots[lo];
+  return ti;
+}
+
 template <bool kSwiGLU>
 __global__ void __launch_bounds__(kThreads, 1)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                     const int32_t *__restrict__ offsets, const int32_t *__restrict__ slot_of, int E, int K,
-                    __nv_bfloat16 *__restrict__ out, int ld_out) {
+                    int n_tiles, __nv_bfloat16 *__restrict__ out, int ld_out) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * kStageBytes);
   uint64_t *empty = full + kStages;
-  uint64_t *tmem_full = empty + kStages;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
-  __shared__ int s_expert, s_row0, s_row_end, s_slot;
+  uint64_t *tmem_full = empty + kStages;   // [2]
+  uint64_t *tmem_empty = tmem_full + 2;    // [2]
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 2);
+  __shared__ int s_offs[VMM_MAX_EXPERTS + 1], s_tile_base[VMM_MAX_EXPERTS + 1], s_slots[VMM_MAX_EXPERTS];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_tile = blockIdx.x;
-  const int m_tile = blockIdx.y;
-
-  // locate (expert, first row) of this m-tile: tiles are ceil(M_e / BM) per expert
-  if (threadIdx.x == 0) {
-    int acc = 0, found = -1, r0 = 0, r1 = 0;
-    for (int e = 0; e < E; ++e) {
-      int lo = offsets[e], hi = offsets[e + 1];
-      int nt = (hi - lo + BM - 1) / BM;
-      if (m_tile < acc + nt) {
-        found = e;
-        r0 = lo + (m_tile - acc) * BM;
-        r1 = hi;
-        break;
-      }
-      acc += nt;
-    }
-    s_expert = found;
-    s_row0 = r0;
-    s_row_end = r1;
-    s_slot = found >= 0 ? slot_of[found] : 0;
-  }
+  for (int e = threadIdx.x; e <= E; e += blockDim.x) s_offs[e] = offsets[e];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) s_slots[e] = slot_of[e];
   __syncthreads();
-  if (s_expert < 0) return;  // uniform: surplus tile slot
-  const int row0 = s_row0, row_end = s_row_end, slot = s_slot;
-  const int nk = K / BK;
-
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int e = 0; e < E; ++e) {
+      s_tile_base[e] = acc;
+      acc += (s_offs[e + 1] - s_offs[e] + BM - 1) / BM;
+    }
+    s_tile_base[E] = acc;
+  }
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&map_a);
     prefetch_tmap(&map_b);
     for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    mbar_init(tmem_full, 1);
+    for (int b = 0; b < 2; ++b) { mbar_init(&tmem_full[b], 1); mbar_init(&tmem_empty[b], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(BN));
+                 "r"(2 * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int total = s_tile_base[E] * n_tiles;
+  const int nk = K / BK;
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kStages;
-        if (kb >= kStages) mbar_wait(&empty[s], ((kb / kStages) - 1) & 1);
-        unsigned char *a_dst = smem + s * kStageBytes;
-        unsigned char *b_dst = a_dst + kTileBytes;
-        mbar_expect_tx(&full[s], kStageBytes);
-        tma_load_2d(&map_a, &full[s], a_dst, kb * BK, row0);
-        tma_load_3d(&map_b, &full[s], b_dst, kb * BK, n_tile * BN, slot);
+      int it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const TileInfo ti = tile_info(t, n_tiles, s_tile_base, s_offs, s_slots, E);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % kStages;
+          if (it >= kStages) mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
+          unsigned char *a_dst = smem + s * kStageBytes;
+          mbar_expect_tx(&full[s], kStageBytes);
+          tma_load_2d(&map_a, &full[s], a_dst, kb * BK, ti.row0);
+          tma_load_3d(&map_b, &full[s], a_dst + kTileBytes, kb * BK, ti.n_tile * BN, ti.slot);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kStages;
-        mbar_wait(&full[s], (kb / kStages) & 1);
+      int it = 0, local = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+        const int b = local & 1, use = local >> 1;
+        if (use > 0) mbar_wait(&tmem_empty[b], (use - 1) & 1);
         tc_fence_after();
-        const uint32_t a_addr = smem_u32(smem + s * kStageBytes);
-        const uint32_t b_addr = a_addr + kTileBytes;
+        const uint32_t acc = tmem + b * BN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % kStages;
+          mbar_wait(&full[s], (it / kStages) & 1);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + s * kStageBytes);
+          const uint32_t b_addr = a_addr + kTileBytes;
 #pragma unroll
-        for (int kk = 0; kk < BK / 16; ++kk) {
-          // advance 16 bf16 = 32 B along K inside the 128 B swizzle atom
-          umma_bf16(tmem, sw128_desc(a_addr + kk * 32), sw128_desc(b_addr + kk * 32), idesc_bf16(BM, BN),
-                    (kb | kk) != 0);
+          for (int kk = 0; kk < BK / 16; ++kk)  // 16 bf16 = 32 B steps inside the 128 B swizzle atom
+            umma_bf16(acc, sw128_desc(a_addr + kk * 32), sw128_desc(b_addr + kk * 32), idesc_bf16(BM, BN),
+                      (kb | kk) != 0);
+          umma_commit(&empty[s]);
         }
-        umma_commit(&empty[s]);
+        umma_commit(&tmem_full[b]);
       }
-      umma_commit(tmem_full);
     }
     __syncwarp();
   } else {
     // epilogue: warp w reads TMEM lanes [32*(w%4), +32)
     const int q = warp & 3;
-    const int row = row0 + q * 32 + lane;
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
-    const uint32_t t_base = tmem + ((uint32_t)(q * 32) << 16);
-    if constexpr (kSwiGLU) {
+    int local = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+      const TileInfo ti = tile_info(t, n_tiles, s_tile_base, s_offs, s_slots, E);
+      const int b = local & 1, use = local >> 1;
+      const int row = ti.row0 + q * 32 + lane;
+      mbar_wait(&tmem_full[b], use & 1);
+      tc_fence_after();
+      const uint32_t t_base = tmem + b * BN + ((uint32_t)(q * 32) << 16);
+      if constexpr (kSwiGLU) {
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        float g[32], u[32];
-        tmem_ld32(t_base + half * 32, g);
-        tmem_ld32(t_base + 64 + half * 32, u);
-        if (row < row_end) {
-          uint4 *dst = reinterpret_cast<uint4 *>(out + (long long)row * ld_out + n_tile * (BN / 2) + half * 32);
+        for (int half = 0; half < 2; ++half) {
+          float g[32], u[32];
+          tmem_ld32(t_base + half * 32, g);
+          tmem_ld32(t_base + 64 + half * 32, u);
+          if (half == 1) {  // accumulator fully read: hand the buffer back to the MMA warp
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tmem_empty[b]);
+          }
+          if (row < ti.row_end) {
+            uint4 *dst = reinterpret_cast<uint4 *>(out + (long long)row * ld_out + ti.n_tile * (BN / 2) + half * 32);
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            uint4 o;
-            o.x = pack_bf16(silu(g[8 * v + 0]) * u[8 * v + 0], silu(g[8 * v + 1]) * u[8 * v + 1]);
-            o.y = pack_bf16(silu(g[8 * v + 2]) * u[8 * v + 2], silu(g[8 * v + 3]) * u[8 * v + 3]);
-            o.z = pack_bf16(silu(g[8 * v + 4]) * u[8 * v + 4], silu(g[8 * v + 5]) * u[8 * v + 5]);
-            o.w = pack_bf16(silu(g[8 * v + 6]) * u[8 * v + 6], silu(g[8 * v + 7]) * u[8 * v + 7]);
-            dst[v] = o;
+            for (int v = 0; v < 4; ++v) {
+              uint4 o;
+              o.x = pack_bf16(silu(g[8 * v + 0]) * u[8 * v + 0], silu(g[8 * v + 1]) * u[8 * v + 1]);
+              o.y = pack_bf16(silu(g[8 * v + 2]) * u[8 * v + 2], silu(g[8 * v + 3]) * u[8 * v + 3]);
+              o.z = pack_bf16(silu(g[8 * v + 4]) * u[8 * v + 4], silu(g[8 * v + 5]) * u[8 * v + 5]);
+              o.w = pack_bf16(silu(g[8 * v + 6]) * u[8 * v + 6], silu(g[8 * v + 7]) * u[8 * v + 7]);
+              dst[v] = o;
+            }
           }
         }
-      }
-    } else {
+      } else {
 #pragma unroll
-      for (int c = 0; c < BN / 32; ++c) {
-        float a[32];
-        tmem_ld32(t_base + c * 32, a);
-        if (row < row_end) {
-          uint4 *dst = reinterpret_cast<uint4 *>(out + (long long)row * ld_out + n_tile * BN + c * 32);
+        for (int c = 0; c < BN / 32; ++c) {
+          float a[32];
+          tmem_ld32(t_base + c * 32, a);
+          if (c == BN / 32 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tmem_empty[b]);
+          }
+          if (row < ti.row_end) {
+            uint4 *dst = reinterpret_cast<uint4 *>(out + (long long)row * ld_out + ti.n_tile * BN + c * 32);
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            uint4 o;
-            o.x = pack_bf16(a[8 * v + 0], a[8 * v + 1]);
-            o.y = pack_bf16(a[8 * v + 2], a[8 * v + 3]);
-            o.z = pack_bf16(a[8 * v + 4], a[8 * v + 5]);
-            o.w = pack_bf16(a[8 * v + 6], a[8 * v + 7]);
-            dst[v] = o;
+            for (int v = 0; v < 4; ++v) {
+              uint4 o;
+              o.x = pack_bf16(a[8 * v + 0], a[8 * v + 1]);
+              o.y = pack_bf16(a[8 * v + 2], a[8 * v + 3]);
+              o.z = pack_bf16(a[8 * v + 4], a[8 * v + 5]);
+              o.w = pack_bf16(a[8 * v + 6], a[8 * v + 7]);
+              dst[v] = o;
+            }
           }
         }
       }
@@ -173,7 +210,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_cons
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
   }
 }
 
@@ -266,13 +303,21 @@ extern "C" int vmm_grouped_swiglu(const void *d_xp, const int32_t *d_offsets, in
     uint32_t box[3] = {BK, BN, 1};
     if ((st = make_map(&mb2, d_w2_arena, 3, dims, str, box))) return st;
   }
-  const int m_tiles = (M_total + BM - 1) / BM + E;
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  // persistent: one CTA per SM (bounded by the largest possible tile count)
+  const int max_m_tiles = (M_total + BM - 1) / BM + E;
+  const int n1 = (2 * I) / BN, n2 = H / BN;
   cudaStream_t s = (cudaStream_t)stream;
-  dim3 g1((2 * I) / BN, m_tiles), g2(H / BN, m_tiles);
-  grouped_gemm_kernel<true><<<g1, kThreads, kSmemBytes, s>>>(ma1, mb1, d_offsets, d_slot_of_expert, E, H,
+  int g1 = g_num_sms < max_m_tiles * n1 ? g_num_sms : max_m_tiles * n1;
+  int g2 = g_num_sms < max_m_tiles * n2 ? g_num_sms : max_m_tiles * n2;
+  grouped_gemm_kernel<true><<<g1, kThreads, kSmemBytes, s>>>(ma1, mb1, d_offsets, d_slot_of_expert, E, H, n1,
                                                              (__nv_bfloat16 *)d_h1, I);
   VMM_LAUNCH_CHECK("grouped_gemm_kernel<swiglu>");
-  grouped_gemm_kernel<false><<<g2, kThreads, kSmemBytes, s>>>(ma2, mb2, d_offsets, d_slot_of_expert, E, I,
+  grouped_gemm_kernel<false><<<g2, kThreads, kSmemBytes, s>>>(ma2, mb2, d_offsets, d_slot_of_expert, E, I, n2,
                                                               (__nv_bfloat16 *)d_y, H);
   VMM_LAUNCH_CHECK("grouped_gemm_kernel<down>");
   return VMM_OK;
