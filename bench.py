@@ -39,6 +39,7 @@ def parse():
     p.add_argument("--workload", default="c3_qwen3vl")
     p.add_argument("--routing", default="live", choices=["live", "trace"])
     p.add_argument("--predictor", default=None)
+    p.add_argument("--requests", type=int, default=1, help="requests per GPU per step (C5 batch sweep)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--out", default=None)
     return p.parse_args()
@@ -202,14 +203,23 @@ def main():
     predictor = a.predictor or ("gate" if a.routing == "live" else "oracle")
     cfg = StackConfig.from_workload(w, routing=a.routing, predictor=predictor, host_layers=8)
     stack = MoEStack(cfg, seed=1000 + rank)
-    tr = generate_trace(w.trace_config(seed=rank))
-    T = tr.num_tokens
+    R = a.requests
+    tr = generate_trace(w.trace_config(seed=rank * R))
+    T1 = tr.num_tokens
+    T = T1 * R
     g = torch.Generator(device=dev).manual_seed(rank)
     x = torch.randn((T, w.hidden), generator=g, device=dev).to(torch.bfloat16)
-    sal = torch.from_numpy(tr.saliency).to(dev)
-    mod = torch.from_numpy(tr.device_modality()).to(dev)
+    # requests beyond the first: same shape, saliency drawn like the generator's Gamma(2, 1)
+    rng = np.random.default_rng(1000 + rank)
+    sal_np = np.concatenate([tr.saliency] + [rng.gamma(2.0, 1.0, size=T1) for _ in range(R - 1)])
+    mod_np = np.concatenate([tr.device_modality()] * R)
+    sal = torch.from_numpy(sal_np).to(dev)
+    mod = torch.from_numpy(mod_np).to(dev)
+    req_off = [r * T1 for r in range(R + 1)]
     dtr = None
     if a.routing == "trace":
+        if R != 1:
+            raise SystemExit("--routing trace supports --requests 1")
         dtr = dict(routes=torch.from_numpy(tr.route_experts.astype(np.int32)).to(dev),
                    gates=torch.from_numpy(tr.route_gates.astype(np.float32)).to(dev))
     # host copies for the end-to-end leg
@@ -230,7 +240,7 @@ def main():
             md = mod_h.to(dev, non_blocking=True)
         else:
             xd, sd, md = x, sal, mod
-        res = stack.forward(xd, sd, md, trace=dtr)
+        res = stack.forward(xd, sd, md, trace=dtr, req_off=req_off)
         if e2e:
             out = torch.empty(res.hidden.shape, dtype=res.hidden.dtype, pin_memory=True)
             out.copy_(res.hidden, non_blocking=True)
@@ -319,7 +329,7 @@ def main():
             "config": {"workload": w.name, "tokens": T, "layers": w.layers, "hidden": w.hidden, "experts": w.experts,
                        "top_k": w.k, "moe_inter": w.inter, "l_pinned": w.l_pinned, "num_slabs": w.num_slabs,
                        "routing": a.routing, "predictor": f"{predictor} B={w.budget} W={w.window}",
-                       "parallelism": f"dp{world} (requests)", "requests_per_gpu_step": 1,
+                       "parallelism": f"dp{world} (requests)", "requests_per_gpu_step": R,
                        "l2": "flushed (256 MB write) between timed steps"},
             "hit_rate": rep.hit_rate, "hits": rep.hits, "misses": rep.misses, "evictions": rep.evictions,
             "retained_tokens": int(res0.hidden.shape[0]),

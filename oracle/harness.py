@@ -61,8 +61,15 @@ def plan_and_scores(trace, sim: dict, compression: dict | None, y_override=None)
     return retained, comp, scores
 
 
-def simulate(trace, sim: dict, compression: dict | None, reactive: bool, y_override=None):
-    retained, comp, scores = plan_and_scores(trace, sim, compression, y_override)
+def simulate(trace, sim: dict, compression: dict | None, reactive: bool, y_override=None, retained=None):
+    """`retained` overrides the compressed token set (a batch of requests each
+    compressed on its own, merged into one trace: ExecutionPlan with a prebuilt
+    compression, pipeline.py:153-170)."""
+    ret0, comp, scores = plan_and_scores(trace, sim, compression if retained is None else None, y_override)
+    if retained is not None:
+        ret0 = np.asarray(retained, dtype=np.int64)
+        comp = {"retained": ret0} if compression is not None else None
+    retained = ret0
     p = sim["predictor"]
     prefetching = (scores is not None) and int(p["budget"]) > 0 and not reactive
     l_pinned = int(sim["l_pinned"]) if sim.get("l_pinned") is not None else int(sim.get("l_semantic", 1))

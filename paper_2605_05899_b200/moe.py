@@ -176,6 +176,7 @@ class StackResult:
     scores: dict                    # context layer -> predictor y (np.float64[E])
     copies: int                     # expert transfers issued
     h2d_bytes: float
+    retained_offsets: np.ndarray = None  # [R+1] rows of each request in `hidden`
 
 
 class MoEStack:
@@ -256,11 +257,16 @@ class MoEStack:
             self.profile.append((e0, e1, nbytes, flops))
         return kernels.combine(y, pos, gates, x, out=out[:N])
 
-    def forward(self, x, saliency, modality, trace=None, record: bool = False) -> StackResult:
-        """Prefill one request.  x bf16 [T, H] (device), saliency f64 [T],
-        modality u8 [T] (0 visual, 1 text; all prefill).  `trace` (routing
-        contract arrays on the device: routes i32 [L,T,k], gates f32 [L,T,k])
-        is required for routing="trace"."""
+    def forward(self, x, saliency, modality, trace=None, record: bool = False, req_off=None) -> StackResult:
+        """Prefill a batch of requests through the whole stack.
+
+        x bf16 [T, H] (device), saliency f64 [T], modality u8 [T] (0 visual,
+        1 text; all prefill).  `req_off` (host ints, R+1) splits the rows into
+        R requests (default: one request); each request is compressed on its
+        own (one prune CTA per request) and the layers then run on the union of
+        the retained rows, so expert transfers are shared by the batch.
+        `trace` (device routes i32 [L,T,k], gates f32 [L,T,k]) is required for
+        routing="trace"."""
         c = self.cfg
         L, E, k, lp = c.layers, c.experts, c.k, c.l_pinned
         dev = self.device
@@ -292,18 +298,25 @@ class MoEStack:
                 x_ctx = xn  # normalised input of layer lp-1: context of the boot emission (gate predictor)
             cur = self._layer_compute(cur, xn, ids, gates, self.store.pinned_slot_of[l], bufs, outs[l % 2])
 
-        # --- prune (token compression) on the prefix routes
-        vis = int((modality == 0).sum().item()) if isinstance(modality, torch.Tensor) else int((np.asarray(modality) == 0).sum())
+        # --- prune (token compression) on the prefix routes, one CTA per request
+        offs = [0, T] if req_off is None else [int(v) for v in req_off]
+        R = len(offs) - 1
+        mod_h = modality.cpu().numpy() if isinstance(modality, torch.Tensor) else np.asarray(modality)
         ccfg = CompressionConfig(c.alpha, c.beta, c.lam, tuple(range(lp)) if lp else (0,))
-        k_core, k_keep = ccfg.budgets(vis)
+        budgets = [ccfg.budgets(int((mod_h[offs[r]:offs[r + 1]] == 0).sum())) for r in range(R)]
         pr = kernels.prune(saliency, modality, prefix[:max(lp, 1)],
-                           torch.tensor([0, T], dtype=torch.int32, device=dev),
-                           torch.tensor([k_core], dtype=torch.int32, device=dev),
-                           torch.tensor([k_keep], dtype=torch.int32, device=dev), E, c.lam)
-        n_r = int(pr["n_retained"].item())
-        if int(pr["status"].item()) != 0:
+                           torch.tensor(offs, dtype=torch.int32, device=dev),
+                           torch.tensor([b[0] for b in budgets], dtype=torch.int32, device=dev),
+                           torch.tensor([b[1] for b in budgets], dtype=torch.int32, device=dev), E, c.lam)
+        n_ret = pr["n_retained"].cpu().numpy()
+        if (pr["status"].cpu().numpy() != 0).any():
             raise ValidationError("saliency entries must be finite and >= 0")
-        ret = pr["retained"][:n_r]
+        if R == 1:
+            ret = pr["retained"][: int(n_ret[0])]
+        else:  # request-local ids -> global row ids, requests in order
+            ret = torch.cat([pr["retained"][offs[r]: offs[r] + int(n_ret[r])] + offs[r] for r in range(R)])
+        n_r = int(ret.shape[0])
+        ret_off = np.concatenate([[0], np.cumsum(n_ret)]).astype(np.int64)
         xr = kernels.gather_rows(cur, ret, out=bufs["xp"][:n_r])  # scratch until permute of layer lp
         xr = xr.clone()
 
@@ -406,7 +419,8 @@ class MoEStack:
         b, ms, cnt = C.c_double(), C.c_double(), C.c_longlong()
         check(self._L.vmm_xfer_stats(self._x, C.byref(b), C.byref(ms), C.byref(cnt)))
         return StackResult(hidden=cur, retained=ret.cpu().numpy(), report=report, prefix_routes=prefix[:lp],
-                           routes=routes, scores=scores, copies=n_copies, h2d_bytes=b.value)
+                           routes=routes, scores=scores, copies=n_copies, h2d_bytes=b.value,
+                           retained_offsets=ret_off)
 
     def _issue(self, eng: Engine) -> int:
         n = C.c_int()

@@ -162,3 +162,46 @@ def test_cached_run_bit_identical_to_all_resident_run():
             acc[t] += gates[t, j] * y[0].float()
     rows = list(range(0, xl.shape[0], 97))
     torch.testing.assert_close(res.hidden.cpu()[rows].float(), acc[rows], rtol=3e-2, atol=3e-2)
+
+
+def test_batched_requests_share_transfers_and_replay_exactly():
+    """R requests in one pass: each request is compressed on its own (prune CTA
+    per request, identical to the oracle's per-request compress) and the
+    layers run on the union of retained rows; the batch's decisions replay
+    exactly through the oracle engine on the merged routes."""
+    from oracle import compress_ref
+    cfg = tiny_cfg(routing="live", predictor="gate")
+    trs = [small_trace(cfg, seed=s) for s in (11, 12, 13)]
+    stack = MoEStack(cfg)
+    xs, sals, mods = [], [], []
+    for i, tr in enumerate(trs):
+        x, sal, mod, _ = request(tr, cfg.hidden, seed=20 + i)
+        xs.append(x), sals.append(sal), mods.append(mod)
+    offs = np.cumsum([0] + [t.num_tokens for t in trs]).tolist()
+    res = stack.forward(torch.cat(xs), torch.cat(sals), torch.cat(mods), record=True, req_off=offs)
+    T = offs[-1]
+    re = np.zeros((cfg.layers, T, cfg.k), dtype=np.int64)
+    re[:] = np.arange(cfg.k)
+    re[: cfg.l_pinned] = res.prefix_routes.cpu().numpy()
+    for i, l in enumerate(range(cfg.l_pinned, cfg.layers)):
+        re[l, res.retained] = res.routes[i].cpu().numpy()
+    # per-request compression of the live prefix routes == the batch's retained rows
+    exp_ret = []
+    for r, tr in enumerate(trs):
+        o = compress_ref.compress(tr.saliency, tr.modality, [], re[:, offs[r]:offs[r + 1]], cfg.experts,
+                                  cfg.alpha, cfg.beta, cfg.lam, list(range(cfg.l_pinned)))
+        exp_ret.append(o["retained"] + offs[r])
+    exp_ret = np.concatenate(exp_ret)
+    assert res.retained.tolist() == exp_ret.tolist()
+    assert res.retained_offsets[-1] == len(exp_ret)
+    merged = RoutingTrace(cfg.layers, cfg.experts, cfg.k, re, np.full(re.shape, 1.0 / cfg.k),
+                          np.concatenate([t.saliency for t in trs]), np.concatenate([t.modality for t in trs]),
+                          np.concatenate([t.embedding for t in trs]))
+    sd = _sim_dict(cfg)
+    sd["predictor"]["kind"] = "history"
+    comp = dict(alpha=cfg.alpha, beta=cfg.beta, lam=cfg.lam, prefix=list(range(cfg.l_pinned)))
+    exp = harness.simulate(merged, sd, comp, False, y_override=lambda ctx, ids: res.scores[ctx], retained=exp_ret)
+    got = res.report.to_dict()
+    for key in _F:
+        assert got[key] == exp[key], key
+    assert got["per_layer"] == exp["per_layer"]
