@@ -287,15 +287,31 @@ def main():
     e2e_value = world * T / (ms_e2e * 1e-3)
 
     # roofline: grouped SwiGLU (dominant kernel pair), live CUDA events in the timed region
-    prof = [p for _, pl, _ in results for p in pl]
+    # (post-prefix layers only: the steady-state loop; the pinned prefix runs on all T rows)
+    prof = [p for _, pl, _ in results for p in pl[w.l_pinned:]]
     durs = [p[0].elapsed_time(p[1]) for p in prof]
     nbytes = [p[2] for p in prof]
-    ach = float(np.mean([b / (d * 1e-3) / 1e9 for b, d in zip(nbytes, durs)]))
+    nflops = [p[3] for p in prof]
     peaks = {}
     pk_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(pk_path):
         peaks = json.load(open(pk_path))
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    tc_peak = float(peaks.get("bf16_tflops_sustained", 1400.0))
+    t_mem = sum(nbytes) / (hbm_peak * 1e9)
+    t_tc = sum(nflops) / (tc_peak * 1e12)
+    t_act = sum(durs) * 1e-3
+    if t_tc > t_mem:
+        bound, ach, peak, unit = "tensor", sum(nflops) / t_act / 1e12, tc_peak, "TFLOP/s"
+        peak_src = "MEASURED_PEAKS.json bf16_tflops_sustained" if "bf16_tflops_sustained" in peaks else "fallback"
+    else:
+        bound, ach, peak, unit = "hbm", sum(nbytes) / t_act / 1e9, hbm_peak, "GB/s"
+        peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        tj = json.load(open(tpath)).get(f"{w.name}/R{a.requests}")
+        traffic = tj["dram_bytes_per_launch"] if tj else None
     res0 = results[-1][0]
     h2d_peak = measure_h2d_peak(torch, dev)
     h2d_bytes = res0.h2d_bytes
@@ -336,11 +352,13 @@ def main():
             "h2d": {"gbs": h2d_gbs, "bytes_per_step": h2d_bytes, "copies_per_step": res0.copies,
                     "peak_gbs": h2d_peak, "frac": h2d_gbs / h2d_peak if h2d_peak else None,
                     "peak_source": "measured pinned 1 GiB H2D in this run"},
-            "roofline": {"bound": "hbm", "kernel": "grouped_swiglu (tcgen05 GEMM1+GEMM2)", "achieved": ach,
-                         "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
-                         "traffic": None, "launch_ms": float(np.mean(durs)),
-                         "bytes_per_launch": float(np.mean(nbytes)),
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
+            "roofline": {"bound": bound, "kernel": "grouped_swiglu (tcgen05 GEMM1+GEMM2 per post-prefix layer)",
+                         "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
+                         "traffic": traffic, "launch_ms": float(np.mean(durs)),
+                         "bytes_per_launch": float(np.mean(nbytes)), "flops_per_launch": float(np.mean(nflops)),
+                         "hbm_frac": (sum(nbytes) / t_act / 1e9) / hbm_peak,
+                         "tensor_frac": (sum(nflops) / t_act / 1e12) / tc_peak,
+                         "peak_source": peak_src},
             "clocks": clk.summary(local),
             "gpu_launches": int(launches),
             "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": int(T * w.hidden * 2 + T * 9),
