@@ -188,13 +188,12 @@ def main():
     import torch
     import torch.distributed as dist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2605_05899_b200 import dist as vdist
+
+    rank, world, local = vdist.env_rank_world()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    vdist.init("nccl", dev)
 
     from paper_2605_05899_b200 import kernels
     from paper_2605_05899_b200.moe import MoEStack, StackConfig
@@ -275,11 +274,7 @@ def main():
     e2e_times, e2e_results = timed(a.steps, e2e=True)
 
     def max_over_ranks(v):
-        if world == 1:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return vdist.max_over_ranks(v, dev)
 
     ms = max_over_ranks(float(np.mean(times)))
     ms_e2e = max_over_ranks(float(np.mean(e2e_times)))
