@@ -179,6 +179,15 @@ class StackResult:
     retained_offsets: np.ndarray = None  # [R+1] rows of each request in `hidden`
 
 
+@dataclass
+class DecodeResult:
+    hidden: torch.Tensor            # [1, H] output of the last layer
+    copies: int                     # expert transfers issued during the step
+    h2d_bytes: float
+    routes: list                    # per layer ids [1, k] (device) when recorded
+    scores: dict = None             # context layer -> predictor y of this step's emissions
+
+
 class MoEStack:
     """One-request-at-a-time VL-MoE layer stack with the offloaded expert cache."""
 
@@ -257,7 +266,8 @@ class MoEStack:
             self.profile.append((e0, e1, nbytes, flops))
         return kernels.combine(y, pos, gates, x, out=out[:N])
 
-    def forward(self, x, saliency, modality, trace=None, record: bool = False, req_off=None) -> StackResult:
+    def forward(self, x, saliency, modality, trace=None, record: bool = False, req_off=None,
+                keep_session: bool = False) -> StackResult:
         """Prefill a batch of requests through the whole stack.
 
         x bf16 [T, H] (device), saliency f64 [T], modality u8 [T] (0 visual,
@@ -418,9 +428,107 @@ class MoEStack:
         report = eng.finish(with_events=False)
         b, ms, cnt = C.c_double(), C.c_double(), C.c_longlong()
         check(self._L.vmm_xfer_stats(self._x, C.byref(b), C.byref(ms), C.byref(cnt)))
+        self._sess = dict(eng=eng, step=0, trace=trace) if keep_session else None
         return StackResult(hidden=cur, retained=ret.cpu().numpy(), report=report, prefix_routes=prefix[:lp],
                            routes=routes, scores=scores, copies=n_copies, h2d_bytes=b.value,
                            retained_offsets=ret_off)
+
+    # ------------------------------------------------------------------
+    # decode phase (pipeline.py:723-740): one token per step, the prefill's
+    # cache persists, emissions after the last pinned layer and every cached
+    # layer < L-1 over the single token
+    # ------------------------------------------------------------------
+    def decode_step(self, x_tok, tok: int | None = None, record: bool = False) -> "DecodeResult":
+        """x_tok bf16 [1, H]: the decode token's hidden state entering layer 0.
+        With routing="trace", `tok` is the token's row in the session trace."""
+        sess = getattr(self, "_sess", None)
+        if sess is None:
+            raise ContractError("decode_step needs forward(..., keep_session=True) first")
+        c = self.cfg
+        L, E, k, lp = c.layers, c.experts, c.k, c.l_pinned
+        dev = self.device
+        eng, s = sess["eng"], sess["step"]
+        stream = torch.cuda.current_stream()
+        sp = stream.cuda_stream
+        bufs = self._buffers(1)
+        trace = sess["trace"]
+        if c.routing == "trace" and tok is None:
+            raise ContractError("routing='trace' decode needs the token's trace row")
+        check(self._L.vmm_xfer_reset_stats(self._x))
+        counts = torch.zeros((L, E), dtype=torch.int32, device=dev)
+        ids_tok = None
+        if c.routing == "trace":
+            ids_tok = trace["routes"][:, tok:tok + 1].contiguous()  # [L, 1, k]
+            one = torch.zeros(1, dtype=torch.int32, device=dev)
+            kernels.demand_counts(ids_tok, torch.arange(L, dtype=torch.int32, device=dev), one, E, out=counts)
+            if c.predictor == "oracle":
+                dec = torch.tensor(decay_table(c.gamma, c.window), dtype=torch.float64, device=dev)
+                otab = kernels.oracle_targets(counts, torch.arange(L, dtype=torch.int32, device=dev), c.window, dec)
+        outs = (bufs["out"], bufs["out2"])
+        cur, n_copies, routes, scores = x_tok, 0, [], {}
+        for l in range(L):
+            xn = kernels.rmsnorm(cur, out=bufs["xn"][:1])
+            emits = eng.emits(l, 1)
+            la = emits and c.routing == "live" and c.predictor == "gate" and E % 16 == 0 and E <= 128
+            if c.routing == "live":
+                if la:
+                    bufs["scratch"].zero_()
+                    ids, gates = kernels.route_lookahead(xn, self.store.router, l, k, counts[l], bufs["scratch"],
+                                                         ids=bufs["ids"][:1], gates=bufs["gates"][:1])
+                else:
+                    ids, gates, _ = kernels.route_topk(xn, self.store.router[l], k, counts=counts[l],
+                                                       ids=bufs["ids"][:1], gates=bufs["gates"][:1])
+            else:
+                ids, gates = ids_tok[l], trace["gates"][l, tok:tok + 1]
+            if record:
+                routes.append(ids.clone())
+            if emits:
+                if la:
+                    yt = kernels.normalize_counts(bufs["scratch"], float(k), out=bufs["y_dev"])
+                elif c.predictor == "history":
+                    yt = kernels.history(counts, torch.tensor([l], dtype=torch.int32, device=dev), self.pow)[0]
+                elif c.predictor == "oracle":
+                    yt = otab[l]
+                else:
+                    yt = kernels.gate_lookahead(xn, self.store.router[l + 1], k, scratch=bufs["scratch"],
+                                                out=bufs["y_dev"])
+                self.y_host[l].copy_(yt, non_blocking=True)
+            self.counts_host[l].copy_(counts[l], non_blocking=True)
+            stream.synchronize()
+            demand = np.flatnonzero(self.counts_host[l].numpy()).astype(np.int32)
+            eng.layer(l, demand, 1, s, None)
+            n_copies += self._issue(eng)
+            if l < lp:
+                cur = self._layer_compute(cur, xn, ids, gates, self.store.pinned_slot_of[l], bufs, outs[l % 2])
+            else:
+                slabs = np.empty(len(demand), dtype=np.int32)
+                check(self._L.vmm_engine_slots(eng._h, l, demand.ctypes.data, len(demand), slabs.ctypes.data))
+                row = self.slot_host[l].numpy()
+                row[:] = 0
+                row[demand] = slabs + self.store.n_pinned_slots
+                self.slot_dev[l].copy_(self.slot_host[l], non_blocking=True)
+                check(self._L.vmm_xfer_fence(self._x, slabs.ctypes.data, len(slabs), sp))
+                cur = self._layer_compute(cur, xn, ids, gates, self.slot_dev[l], bufs, outs[l % 2],
+                                          n_experts=len(demand))
+                check(self._L.vmm_xfer_layer_done(self._x, l, sp))
+            if emits:
+                y = self.y_host[l].numpy().copy()
+                scores[l] = y
+                check(self._L.vmm_engine_emit(eng._h, l, y.ctypes.data))
+                n_copies += self._issue(eng)
+        eng.end_step()
+        sess["step"] = s + 1
+        check(self._L.vmm_xfer_join(self._x, sp))
+        b, ms, cnt = C.c_double(), C.c_double(), C.c_longlong()
+        check(self._L.vmm_xfer_stats(self._x, C.byref(b), C.byref(ms), C.byref(cnt)))
+        return DecodeResult(hidden=cur.clone(), copies=n_copies, h2d_bytes=b.value, routes=routes, scores=scores)
+
+    def end_session(self) -> SimReport:
+        sess = getattr(self, "_sess", None)
+        if sess is None:
+            raise ContractError("no open session")
+        self._sess = None
+        return sess["eng"].finish(with_events=False)
 
     def _issue(self, eng: Engine) -> int:
         n = C.c_int()

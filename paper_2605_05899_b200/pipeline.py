@@ -330,7 +330,7 @@ class Engine:
     def finish(self, with_events: bool) -> SimReport:
         r = EngineReport()
         check(self._L.vmm_engine_finish(self._h, C.byref(r)))
-        rows = []
+        rows = self.__dict__.setdefault("_rows", [])  # drained rows accumulate: finish() may be called again
         buf = np.empty((1024, 8), dtype=np.float64)
         while True:
             n = self._L.vmm_engine_layer_stats(self._h, buf.ctypes.data, 1024)

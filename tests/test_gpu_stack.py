@@ -205,3 +205,49 @@ def test_batched_requests_share_transfers_and_replay_exactly():
     for key in _F:
         assert got[key] == exp[key], key
     assert got["per_layer"] == exp["per_layer"]
+
+
+@pytest.mark.parametrize("pred", ["gate", "history"])
+def test_decode_steps_replay_exactly(pred):
+    """Prefill then D decode tokens with the cache persisting (pipeline.py:723-740);
+    the whole session's decisions replay exactly through the oracle engine."""
+    cfg = tiny_cfg(routing="live", predictor=pred, num_slabs=20)
+    tr = small_trace(cfg, seed=21)
+    stack = MoEStack(cfg)
+    x, sal, mod, _ = request(tr, cfg.hidden, seed=4)
+    res = stack.forward(x, sal, mod, record=True, keep_session=True)
+    D = 3
+    g = torch.Generator(device="cuda").manual_seed(9)
+    steps = [stack.decode_step(torch.randn((1, cfg.hidden), generator=g, device="cuda").to(torch.bfloat16),
+                               record=True) for _ in range(D)]
+    rep = stack.end_session()
+    T = tr.num_tokens
+    re = np.zeros((cfg.layers, T + D, cfg.k), dtype=np.int64)
+    re[:] = np.arange(cfg.k)
+    re[: cfg.l_pinned, :T] = res.prefix_routes.cpu().numpy()
+    for i, l in enumerate(range(cfg.l_pinned, cfg.layers)):
+        re[l, res.retained] = res.routes[i].cpu().numpy()
+    for s, st in enumerate(steps):
+        for l in range(cfg.layers):
+            re[l, T + s] = st.routes[l].cpu().numpy()[0]
+    merged = RoutingTrace(cfg.layers, cfg.experts, cfg.k, re, np.full(re.shape, 1.0 / cfg.k),
+                          np.r_[tr.saliency, np.ones(D)], np.r_[tr.modality, np.ones(D, np.uint8)],
+                          np.r_[tr.embedding, np.zeros((D, tr.embed_dim))], phase_marks=list(range(T, T + D)))
+    sd = _sim_dict(cfg)
+    sd["decode_steps"] = D
+    comp = dict(alpha=cfg.alpha, beta=cfg.beta, lam=cfg.lam, prefix=list(range(cfg.l_pinned)))
+    y_over = None
+    if pred == "gate":
+        sd["predictor"]["kind"] = "history"
+
+        def y_over(ctx, ids):
+            ids = list(ids)
+            if len(ids) == 1 and ids[0] >= T:
+                return steps[ids[0] - T].scores[ctx]
+            return res.scores[ctx]
+    exp = harness.simulate(merged, sd, comp, False, y_override=y_over)
+    got = rep.to_dict()
+    for key in _F + ("decode_ms_per_step",):
+        assert got[key] == exp[key], key
+    assert got["per_layer"] == exp["per_layer"]
+    assert sum(st.copies for st in steps) >= 0
