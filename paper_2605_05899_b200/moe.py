@@ -68,6 +68,7 @@ class StackConfig:
     compress_ms: float = 0.0
     bootstrap_ms: float = 0.0
     shared_experts: int = 0
+    router_corr: float = 0.8   # synthetic router weights: correlation between consecutive layers' gates
 
     @classmethod
     def from_workload(cls, w: Workload, **kw) -> "StackConfig":
@@ -127,7 +128,13 @@ class ExpertStore:
         for l in range(cfg.l_pinned):
             h = l % self.host_layers
             self.arena[l * E:(l + 1) * E].copy_(self.pool[h * E:(h + 1) * E], non_blocking=True)
-        self.router = (torch.randn((L, E, H), generator=g, device=dev) / math.sqrt(H)).to(torch.bfloat16)
+        # router: W[l] = rho W[l-1] + sqrt(1-rho^2) noise, so consecutive layers route
+        # alike (the inter-layer affinity lookahead prediction relies on; rho=0 -> independent)
+        rho = cfg.router_corr
+        r = torch.randn((L, E, H), generator=g, device=dev)
+        for l in range(1, L):
+            r[l] = rho * r[l - 1] + math.sqrt(1.0 - rho * rho) * r[l]
+        self.router = (r / math.sqrt(H)).to(torch.bfloat16)
         self.pinned_slot_of = (torch.arange(self.n_pinned_slots, dtype=torch.int32, device=dev).reshape(cfg.l_pinned, E)
                                if cfg.l_pinned else None)
         torch.cuda.synchronize(dev)
@@ -300,8 +307,8 @@ class MoEStack:
                 ids, gates, _ = kernels.route_topk(xn, self.store.router[l], k, counts=counts_pre[l], ids=prefix[l],
                                                    gates=bufs["gates"][:T])
             else:
-                prefix[l].copy_(trace["routes"][l])
-                ids, gates = prefix[l], trace["gates"][l]
+                prefix[l].copy_(trace["routes"][l, :T])  # the trace may carry decode tokens after row T
+                ids, gates = prefix[l], trace["gates"][l, :T]
                 kernels.demand_counts(trace["routes"], torch.tensor([l], dtype=torch.int32, device=dev),
                                       torch.arange(T, dtype=torch.int32, device=dev), E, out=counts_pre[l:l + 1])
             if l == lp - 1:
