@@ -120,6 +120,121 @@ route_kernel(const __nv_bfloat16 *__restrict__ x, const __nv_bfloat16 *__restric
   }
 }
 
+// ---- skinny path (decode-sized N): spread the gate rows over many CTAs ----
+constexpr int kSkinnyMaxN = 32;
+
+// logits[n][g] = x[n] . W[g] for g in [0, G): one warp per gate row, all N tokens
+__global__ void skinny_logits_kernel(const __nv_bfloat16 *__restrict__ x, const __nv_bfloat16 *__restrict__ w,
+                                     int N, int H, int G, float *__restrict__ logits) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= G) return;
+  const uint4 *wr = reinterpret_cast<const uint4 *>(w + (long long)warp * H);
+  const int nv = H / 8;
+  float acc[kSkinnyMaxN];
+#pragma unroll
+  for (int n = 0; n < kSkinnyMaxN; ++n) acc[n] = 0.f;
+  for (int c = lane; c < nv; c += 32) {
+    uint4 wv = __ldg(wr + c);
+    const __nv_bfloat16 *wh = reinterpret_cast<const __nv_bfloat16 *>(&wv);
+    float wf[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) wf[q] = __bfloat162float(wh[q]);
+#pragma unroll
+    for (int n = 0; n < kSkinnyMaxN; ++n) {
+      if (n < N) {
+        uint4 xv = __ldg(reinterpret_cast<const uint4 *>(x + (long long)n * H) + c);
+        const __nv_bfloat16 *xh = reinterpret_cast<const __nv_bfloat16 *>(&xv);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[n] = fmaf(__bfloat162float(xh[q]), wf[q], acc[n]);
+      }
+    }
+  }
+#pragma unroll
+  for (int n = 0; n < kSkinnyMaxN; ++n) {
+    if (n < N) {
+      float v = acc[n];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) logits[(long long)n * G + warp] = v;
+    }
+  }
+}
+
+// per (token, gate group): top-k by (logit desc, id asc) with a warp argmax per pick
+__global__ void skinny_topk_kernel(const float *__restrict__ logits, int N, int E, int NG, int k,
+                                   int32_t *__restrict__ ids, float *__restrict__ gates,
+                                   float *__restrict__ logits_out, uint32_t *__restrict__ counts,
+                                   uint32_t *__restrict__ la_counts) {
+  const int t = blockIdx.x;
+  const int g = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= N || g >= NG) return;
+  const float *row = logits + (long long)t * NG * E + (long long)g * E;
+  float v[kMaxE / 32];
+#pragma unroll
+  for (int j = 0; j < kMaxE / 32; ++j) {
+    int e = lane + 32 * j;
+    float f = e < E ? row[e] : -INFINITY;
+    if (f != f) f = -INFINITY;
+    v[j] = f;
+    if (g == 0 && logits_out && e < E) logits_out[(long long)t * E + e] = f;
+  }
+  unsigned taken[kMaxE / 32];
+#pragma unroll
+  for (int j = 0; j < kMaxE / 32; ++j) taken[j] = 0;
+  float vals[kMaxK];
+  int sel[kMaxK];
+  for (int s = 0; s < k; ++s) {
+    float best = -INFINITY;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int j = 0; j < kMaxE / 32; ++j) {
+      int e = lane + 32 * j;
+      if (e < E && !((taken[j] >> lane) & 1u) && (bi == 0x7fffffff || v[j] > best)) { best = v[j]; bi = e; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      float ov = __shfl_xor_sync(0xffffffffu, best, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (oi != 0x7fffffff && (bi == 0x7fffffff || ov > best || (ov == best && oi < bi))) { best = ov; bi = oi; }
+    }
+    if (bi == 0x7fffffff) bi = 0;
+    vals[s] = best;
+    sel[s] = bi;
+    if ((bi & 31) == lane) taken[bi >> 5] |= 1u << lane;
+  }
+  if (lane == 0) {
+    if (g == 0) {
+      float ex[kMaxK], sum = 0.f;
+      for (int s = 0; s < k; ++s) { ex[s] = expf(vals[s] - vals[0]); sum += ex[s]; }
+      for (int s = 0; s < k; ++s) {
+        if (ids) ids[(long long)t * k + s] = sel[s];
+        if (gates) gates[(long long)t * k + s] = ex[s] / sum;
+        if (counts) atomicAdd(&counts[sel[s]], 1u);
+      }
+    } else if (la_counts) {
+      for (int s = 0; s < k; ++s) atomicAdd(&la_counts[sel[s]], 1u);
+    }
+  }
+}
+
+int route_skinny(const void *x, const void *w, int N, int H, int E, int NG, int k, int32_t *ids, float *gates,
+                 float *logits_out, uint32_t *counts, uint32_t *la_counts, cudaStream_t s) {
+  static float *scratch = nullptr;  // [kSkinnyMaxN][2*kMaxE] fp32 logits
+  if (!scratch) {
+    cudaError_t e = cudaMalloc(&scratch, sizeof(float) * kSkinnyMaxN * 2 * kMaxE);
+    if (e != cudaSuccess) return vmm::cuda_status(e, "skinny scratch");
+  }
+  const int G = NG * E;
+  skinny_logits_kernel<<<(G * 32 + 255) / 256, 256, 0, s>>>((const __nv_bfloat16 *)x, (const __nv_bfloat16 *)w, N,
+                                                            H, G, scratch);
+  VMM_LAUNCH_CHECK("skinny_logits_kernel");
+  skinny_topk_kernel<<<N, 32 * NG, 0, s>>>(scratch, N, E, NG, k, ids, gates, logits_out, counts, la_counts);
+  VMM_LAUNCH_CHECK("skinny_topk_kernel");
+  return VMM_OK;
+}
+
 }  // namespace
 
 namespace vmm {
@@ -133,6 +248,9 @@ extern "C" int vmm_route_lookahead(const void *d_x, const void *d_router, int la
                                    void *stream) {
   if (N <= 0) return VMM_OK;
   if (layer < 0 || layer + 1 >= L) return vmm::fail(VMM_ECONTRACT, "lookahead needs a next layer");
+  if (N <= kSkinnyMaxN && H % 8 == 0 && E <= kMaxE && k <= kMaxK)  // decode-sized: gate rows over many CTAs
+    return route_skinny(d_x, (const __nv_bfloat16 *)d_router + (long long)layer * E * H, N, H, E, 2, k, d_ids,
+                        d_gates, nullptr, d_counts, d_la_counts, (cudaStream_t)stream);
   int st = vmm::route_sm100(d_x, d_router, layer * E, (long long)L * E, N, H, E, k, d_ids, d_gates, nullptr,
                             d_counts, d_la_counts, true, (cudaStream_t)stream);
   if (st == -1) return vmm::fail(VMM_EVALIDATION, "fused route+lookahead needs E in {16,32,64,128}, H % 64 == 0");
@@ -144,6 +262,8 @@ extern "C" int vmm_route_topk(const void *d_x, const void *d_wg, int N, int H, i
   if (N <= 0) return VMM_OK;
   if (E < 1 || E > kMaxE) return vmm::fail(VMM_EVALIDATION, "router: experts must lie in [1, 256]");
   if (k < 1 || k > kMaxK || k > E) return vmm::fail(VMM_EVALIDATION, "router: k must lie in [1, min(16, E)]");
+  if (N <= kSkinnyMaxN && H % 8 == 0)  // decode-sized: gate rows over many CTAs
+    return route_skinny(d_x, d_wg, N, H, E, 1, k, d_ids, d_gates, d_logits, d_counts, nullptr, (cudaStream_t)stream);
   int st = vmm::route_sm100(d_x, d_wg, 0, E, N, H, E, k, d_ids, d_gates, d_logits, d_counts, nullptr, false,
                             (cudaStream_t)stream);
   if (st != -1) return st;

@@ -4,10 +4,14 @@
 //
 // One CTA = 128 token rows (UMMA M=128).  B = the gate rows [EG x K] (or the
 // two adjacent gates of layers l and l+1, [2E x K], one TMA box since the
-// router weights are stored [L, E, H]).  Epilogue thread t owns row t: it pulls
-// its EG logits from TMEM (tcgen05.ld 32x32b.x16), selects the top-k by
-// (logit desc, id asc), softmaxes the selected logits, writes ids/gates and
-// adds the picks to a shared histogram (demand set / lookahead counts).
+// router weights are stored [L, E, H]).  Warp roles: 0 TMA, 1 TMEM alloc + MMA,
+// then one 4-warp epilogue group PER GATE (warps 2..5 gate 0, 6..9 gate 1), so
+// the two top-k selections run concurrently.  Epilogue thread t owns row t:
+// it pulls its EG logits from TMEM (tcgen05.ld 32x32b.x16) and keeps a
+// register-resident sorted top-K list (single pass, insertion only when a
+// logit beats the current K-th; strict > keeps the lower expert id first on
+// ties), softmaxes the selected logits, writes ids/gates and adds the picks to
+// a shared histogram (demand set / lookahead counts).
 // Contract as vmm_route_topk (trace.py:80-81; gates sum to 1, :375-382).
 #include <math.h>
 
@@ -19,12 +23,12 @@ using namespace sm100;
 
 constexpr int BM = 128, BK = 64;
 constexpr int kStages = 4;
-constexpr int kThreads = 192;
-constexpr int kMaxK = 16;
+constexpr int kMaxK = 8;
 
 template <int EG, int NG>
 struct RouteCfg {
   static constexpr int N = EG * NG;                          // UMMA N
+  static constexpr int kThreads = 64 + 128 * NG;
   static constexpr uint32_t kA = BM * BK * 2;                // 16 KB
   static constexpr uint32_t kB = N * BK * 2;
   static constexpr uint32_t kStage = kA + kB;
@@ -32,8 +36,12 @@ struct RouteCfg {
   static constexpr size_t kSmem = (size_t)kStages * kStage + 1024 + 256 + 2 * EG * 4;
 };
 
-template <int EG>
-__device__ __forceinline__ void load_row(uint32_t taddr, float (&v)[EG]) {
+// one row's top-K by (logit desc, id asc): single pass over TMEM columns
+template <int EG, int K>
+__device__ __forceinline__ void topk_from_tmem(uint32_t taddr, int E, float (&tv)[K], int (&ti)[K],
+                                               float *logits_row) {
+#pragma unroll
+  for (int j = 0; j < K; ++j) { tv[j] = -INFINITY; ti[j] = -1; }
 #pragma unroll
   for (int c = 0; c < EG / 16; ++c) {
     uint32_t r[16];
@@ -41,40 +49,54 @@ __device__ __forceinline__ void load_row(uint32_t taddr, float (&v)[EG]) {
     tmem_wait_ld();
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      float f = __uint_as_float(r[i]);
-      v[c * 16 + i] = (f != f) ? -INFINITY : f;  // NaN ranks below every number
+      const int e = c * 16 + i;
+      float x = __uint_as_float(r[i]);
+      if (x != x) x = -INFINITY;  // NaN ranks below every number
+      if (e < E) {
+        if (logits_row) logits_row[e] = x;
+        if (x > tv[K - 1] || ti[K - 1] < 0) {
+          tv[K - 1] = x;
+          ti[K - 1] = e;
+#pragma unroll
+          for (int j = K - 1; j > 0; --j) {
+            if (tv[j] > tv[j - 1] || (ti[j - 1] < 0)) {  // strict: earlier (lower id) wins ties
+              float fv = tv[j]; tv[j] = tv[j - 1]; tv[j - 1] = fv;
+              int fi = ti[j]; ti[j] = ti[j - 1]; ti[j - 1] = fi;
+            }
+          }
+        }
+      }
     }
   }
 }
 
-// top-k by (value desc, id asc) over the first E of EG registers; returns picks in order
-template <int EG>
-__device__ __forceinline__ void topk_row(const float (&v)[EG], int E, int k, int (&sel)[kMaxK],
-                                         float (&val)[kMaxK]) {
-  uint32_t taken[(EG + 31) / 32];
+template <int EG, int NG, int K>
+__device__ __forceinline__ void epilogue(uint32_t t_base, int gate, int row, bool valid, int E,
+                                         int32_t *__restrict__ ids, float *__restrict__ gates,
+                                         float *__restrict__ logits_out, uint32_t *hist) {
+  float tv[K];
+  int ti[K];
+  float *lrow = (gate == 0 && valid && logits_out) ? logits_out + (long long)row * E : nullptr;
+  topk_from_tmem<EG, K>(t_base + gate * EG, E, tv, ti, lrow);
+  if (!valid) return;
+  if (gate == 0) {
+    float ex[K], sum = 0.f;
 #pragma unroll
-  for (int w = 0; w < (EG + 31) / 32; ++w) taken[w] = 0;
-  for (int s = 0; s < k; ++s) {
-    float best = -INFINITY;
-    int bi = -1;
+    for (int s = 0; s < K; ++s) { ex[s] = expf(tv[s] - tv[0]); sum += ex[s]; }
 #pragma unroll
-    for (int e = 0; e < EG; ++e) {
-      bool free_ = e < E && !((taken[e >> 5] >> (e & 31)) & 1u);
-      if (free_ && (v[e] > best || bi < 0)) { best = v[e]; bi = e; }
+    for (int s = 0; s < K; ++s) {
+      if (ids) ids[(long long)row * K + s] = ti[s];
+      if (gates) gates[(long long)row * K + s] = ex[s] / sum;
     }
-    if (bi < 0) bi = 0;  // unreachable for k <= E
-#pragma unroll
-    for (int e = 0; e < EG; ++e)
-      if (e == bi) taken[e >> 5] |= 1u << (e & 31);
-    sel[s] = bi;
-    val[s] = best;
   }
+#pragma unroll
+  for (int s = 0; s < K; ++s) atomicAdd(&hist[gate * EG + ti[s]], 1u);
 }
 
-template <int EG, int NG>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int EG, int NG, int K>
+__global__ void __launch_bounds__(RouteCfg<EG, NG>::kThreads, 1)
 route_sm100_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w, int w_row0,
-                   int N, int K, int E, int k, int32_t *__restrict__ ids, float *__restrict__ gates,
+                   int N, int Kdim, int E, int32_t *__restrict__ ids, float *__restrict__ gates,
                    float *__restrict__ logits_out, uint32_t *__restrict__ counts, uint32_t *__restrict__ la_counts) {
   using Cfg = RouteCfg<EG, NG>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -88,7 +110,7 @@ route_sm100_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_const
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row0 = blockIdx.x * BM;
-  const int nk = K / BK;
+  const int nk = Kdim / BK;
 
   for (int i = threadIdx.x; i < NG * EG; i += blockDim.x) hist[i] = 0;
   if (warp == 0 && lane == 0) {
@@ -137,42 +159,14 @@ route_sm100_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_const
     }
     __syncwarp();
   } else {
+    // warp w may only touch TMEM lanes [32*(w%4), +32); gate group = (w-2)/4
     const int q = warp & 3;
+    const int gate = (warp - 2) >> 2;
     const int row = row0 + q * 32 + lane;
-    const bool valid = row < N;
     mbar_wait(tmem_full, 0);
     tc_fence_after();
     const uint32_t t_base = tmem + ((uint32_t)(q * 32) << 16);
-    {
-      float v[EG];
-      load_row<EG>(t_base, v);
-      int sel[kMaxK];
-      float val[kMaxK];
-      topk_row<EG>(v, E, k, sel, val);
-      if (valid) {
-        if (logits_out) {
-#pragma unroll
-          for (int e = 0; e < EG; ++e)
-            if (e < E) logits_out[(long long)row * E + e] = v[e];
-        }
-        float ex[kMaxK], sum = 0.f;
-        for (int s = 0; s < k; ++s) { ex[s] = expf(val[s] - val[0]); sum += ex[s]; }
-        for (int s = 0; s < k; ++s) {
-          if (ids) ids[(long long)row * k + s] = sel[s];
-          if (gates) gates[(long long)row * k + s] = ex[s] / sum;
-          atomicAdd(&hist[sel[s]], 1u);
-        }
-      }
-    }
-    if constexpr (NG == 2) {
-      float v[EG];
-      load_row<EG>(t_base + EG, v);
-      int sel[kMaxK];
-      float val[kMaxK];
-      topk_row<EG>(v, E, k, sel, val);
-      if (valid)
-        for (int s = 0; s < k; ++s) atomicAdd(&hist[EG + sel[s]], 1u);
-    }
+    epilogue<EG, NG, K>(t_base, gate, row, row < N, E, ids, gates, logits_out, hist);
   }
   tc_fence_before();
   __syncthreads();
@@ -186,14 +180,14 @@ route_sm100_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_const
   }
 }
 
-template <int EG, int NG>
-int launch(const void *x, const void *wg, int w_row0, long long w_rows, int N, int H, int E, int k, int32_t *ids,
+template <int EG, int NG, int K>
+int launch(const void *x, const void *wg, int w_row0, long long w_rows, int N, int H, int E, int32_t *ids,
            float *gates, float *logits, uint32_t *counts, uint32_t *la_counts, cudaStream_t s) {
   using Cfg = RouteCfg<EG, NG>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(route_sm100_kernel<EG, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)Cfg::kSmem);
+    cudaError_t e = cudaFuncSetAttribute(route_sm100_kernel<EG, NG, K>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
     if (e != cudaSuccess) return vmm::cuda_status(e, "route_sm100 attr");
     attr = true;
   }
@@ -212,10 +206,22 @@ int launch(const void *x, const void *wg, int w_row0, long long w_rows, int N, i
     if ((st = make_map(&mw, wg, 2, dims, str, box))) return st;
   }
   int grid = (N + BM - 1) / BM;
-  route_sm100_kernel<EG, NG><<<grid, kThreads, Cfg::kSmem, s>>>(mx, mw, w_row0, N, H, E, k, ids, gates, logits,
-                                                                counts, la_counts);
+  route_sm100_kernel<EG, NG, K><<<grid, Cfg::kThreads, Cfg::kSmem, s>>>(mx, mw, w_row0, N, H, E, ids, gates, logits,
+                                                                       counts, la_counts);
   VMM_LAUNCH_CHECK("route_sm100_kernel");
   return VMM_OK;
+}
+
+template <int EG, int NG>
+int launch_k(int k, const void *x, const void *wg, int w_row0, long long w_rows, int N, int H, int E, int32_t *ids,
+             float *gates, float *logits, uint32_t *counts, uint32_t *la_counts, cudaStream_t s) {
+  switch (k) {
+#define VMM_K(KK) \
+  case KK: return launch<EG, NG, KK>(x, wg, w_row0, w_rows, N, H, E, ids, gates, logits, counts, la_counts, s);
+    VMM_K(1) VMM_K(2) VMM_K(3) VMM_K(4) VMM_K(5) VMM_K(6) VMM_K(7) VMM_K(8)
+#undef VMM_K
+    default: return -1;
+  }
 }
 
 }  // namespace
@@ -225,20 +231,20 @@ namespace vmm {
 int route_sm100(const void *x, const void *wg_base, int w_row0, long long w_rows, int N, int H, int E, int k,
                 int32_t *ids, float *gates, float *logits, uint32_t *counts, uint32_t *la_counts, bool fused,
                 cudaStream_t s) {
-  if (H % BK || k > kMaxK || E > 128 || N <= 0) return -1;
+  if (H % BK || k > kMaxK || k < 1 || E > 128 || N <= 0) return -1;
   if (fused) {
-    if (E % 16) return -1;
     switch (E) {
-      case 16: return launch<16, 2>(x, wg_base, w_row0, w_rows, N, H, E, k, ids, gates, logits, counts, la_counts, s);
-      case 32: return launch<32, 2>(x, wg_base, w_row0, w_rows, N, H, E, k, ids, gates, logits, counts, la_counts, s);
-      case 64: return launch<64, 2>(x, wg_base, w_row0, w_rows, N, H, E, k, ids, gates, logits, counts, la_counts, s);
-      case 128: return launch<128, 2>(x, wg_base, w_row0, w_rows, N, H, E, k, ids, gates, logits, counts, la_counts, s);
+      case 16: return launch_k<16, 2>(k, x, wg_base, w_row0, w_rows, N, H, E, ids, gates, logits, counts, la_counts, s);
+      case 32: return launch_k<32, 2>(k, x, wg_base, w_row0, w_rows, N, H, E, ids, gates, logits, counts, la_counts, s);
+      case 64: return launch_k<64, 2>(k, x, wg_base, w_row0, w_rows, N, H, E, ids, gates, logits, counts, la_counts, s);
+      case 128:
+        return launch_k<128, 2>(k, x, wg_base, w_row0, w_rows, N, H, E, ids, gates, logits, counts, la_counts, s);
       default: return -1;
     }
   }
-  if (E <= 16) return launch<16, 1>(x, wg_base, w_row0, w_rows, N, H, E, k, ids, gates, logits, counts, nullptr, s);
-  if (E <= 32) return launch<32, 1>(x, wg_base, w_row0, w_rows, N, H, E, k, ids, gates, logits, counts, nullptr, s);
-  if (E <= 64) return launch<64, 1>(x, wg_base, w_row0, w_rows, N, H, E, k, ids, gates, logits, counts, nullptr, s);
-  return launch<128, 1>(x, wg_base, w_row0, w_rows, N, H, E, k, ids, gates, logits, counts, nullptr, s);
+  if (E <= 16) return launch_k<16, 1>(k, x, wg_base, w_row0, w_rows, N, H, E, ids, gates, logits, counts, nullptr, s);
+  if (E <= 32) return launch_k<32, 1>(k, x, wg_base, w_row0, w_rows, N, H, E, ids, gates, logits, counts, nullptr, s);
+  if (E <= 64) return launch_k<64, 1>(k, x, wg_base, w_row0, w_rows, N, H, E, ids, gates, logits, counts, nullptr, s);
+  return launch_k<128, 1>(k, x, wg_base, w_row0, w_rows, N, H, E, ids, gates, logits, counts, nullptr, s);
 }
 }  // namespace vmm

@@ -112,3 +112,23 @@ def test_fused_route_and_lookahead_exact_on_integer_inputs():
         nid, _, _ = moe_ref.route(x, router[layer + 1], k)
         assert torch.equal(la.cpu().long(), torch.bincount(nid.reshape(-1).long(), minlength=E))
         assert torch.equal(counts.cpu().long(), torch.bincount(rid.reshape(-1).long(), minlength=E))
+
+
+@pytest.mark.parametrize("N", [1, 5, 32])
+def test_skinny_router_decode_sizes_exact(N):
+    g = torch.Generator().manual_seed(N)
+    L, H, E, k = 3, 2048, 128, 8
+    x = torch.randint(-4, 5, (N, H), generator=g).to(torch.bfloat16)
+    router = torch.randint(-1, 2, (L, E, H), generator=g).to(torch.bfloat16)
+    counts = torch.zeros(E, dtype=torch.int32, device="cuda")
+    ids, gates, logits = kernels.route_topk(x.cuda(), router[1].cuda(), k, counts=counts, want_logits=True)
+    rid, rg, rl = moe_ref.route(x, router[1], k)
+    assert torch.equal(logits.cpu().double(), rl)
+    assert torch.equal(ids.cpu(), rid)
+    assert (gates.cpu() - rg).abs().max().item() <= 1e-6
+    c2 = torch.zeros(E, dtype=torch.int32, device="cuda")
+    la = torch.zeros(E, dtype=torch.int32, device="cuda")
+    ids2, _ = kernels.route_lookahead(x.cuda(), router.cuda(), 1, k, c2, la)
+    assert torch.equal(ids2.cpu(), rid)
+    nid, _, _ = moe_ref.route(x, router[2], k)
+    assert torch.equal(la.cpu().long(), torch.bincount(nid.reshape(-1).long(), minlength=E))
