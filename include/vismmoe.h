@@ -286,6 +286,63 @@ int vmm_xfer_join(vmm_xfer *x, void *compute_stream);
 int vmm_xfer_stats(vmm_xfer *x, double *bytes, double *busy_ms, long long *copies);
 void *vmm_xfer_stream(vmm_xfer *x);
 
+/* ------------------------------------------------------------------------
+ * Native layer-loop executor (the per-layer body of pipeline.py:709-740 on
+ * the device): rmsnorm -> route (+ fused gate lookahead) -> scores -> ONE
+ * sync -> engine decisions -> copies -> slot table + fence -> permute ->
+ * grouped SwiGLU -> combine -> reader event -> deferred emission.  All
+ * buffers are caller-owned; the executor holds pointers only.
+ * ------------------------------------------------------------------------ */
+int vmm_gather_i32(const int32_t *d_src, const int32_t *d_rows, int n, int width, int32_t *d_dst, void *stream);
+int vmm_gather_f32(const float *d_src, const int32_t *d_rows, int n, int width, float *d_dst, void *stream);
+
+typedef struct {
+  int layers, experts, k, hidden, inter, l_pinned;
+  long long n_pinned_slots, n_slots;
+  size_t slot_bytes;
+  int host_layers;
+  int cap_rows;              /* capacity of the row scratch buffers */
+  int routing;               /* 0 live, 1 trace */
+  int predictor;             /* 0 none, 1 history, 2 gate lookahead, 3 oracle table */
+  int counts_preset;         /* trace routing: counts rows already filled by the caller */
+  void *arena;               /* d bf16 [n_slots][3*I*H] */
+  const void *pool;          /* h pinned bf16 [host_layers*E][3*I*H] */
+  const void *router;        /* d bf16 [L][E][H] */
+  const int32_t *pinned_slot_of; /* d [l_pinned][E] */
+  const int32_t *layer_ids;  /* d [L] = 0..L-1 */
+  const double *pow_table;   /* d [L+1] history decay powers */
+  const double *oracle_table;/* d [L][E] (predictor 3), row = context layer */
+  const int32_t *trace_routes; /* d [L][trace_tokens][k] (routing 1) */
+  const float *trace_gates;    /* d [L][trace_tokens][k] */
+  int trace_tokens;
+  void *xn, *xp, *h1, *y, *out0, *out1; /* d scratch: [cap][H], [cap*k][H], [cap*k][I], [cap*k][H], [cap][H] x2 */
+  int32_t *ids; float *gates;           /* d [cap][k] */
+  int32_t *off, *src, *pos;             /* d [E+1], [cap*k], [cap*k] */
+  uint32_t *counts;                     /* d [L][E] demand counts (history input) */
+  uint32_t *la_counts;                  /* d [E] */
+  double *y_dev;                        /* d [E] */
+  int32_t *slot_dev;                    /* d [L][E] */
+  int32_t *counts_host;                 /* h pinned [L][E] */
+  double *y_host;                       /* h pinned [L][E] scores per context layer */
+  int32_t *slot_host;                   /* h pinned [L][E] */
+} vmm_stack_desc;
+
+typedef struct {
+  const void *x_out;         /* device rows after the last layer (one of out0/out1) */
+  int copies;                /* expert transfers issued */
+  int32_t *routes;           /* nullable d [l1-l0][n_rows][k]: record of the routes used */
+  void **ffn_start, **ffn_end; /* nullable cudaEvent_t arrays [l1-l0] around the grouped SwiGLU */
+  int *n_demand;             /* nullable h [l1-l0] demanded experts per layer */
+} vmm_stack_out;
+
+typedef struct vmm_stack vmm_stack;
+int vmm_stack_create(const vmm_stack_desc *desc, vmm_stack **out);
+void vmm_stack_destroy(vmm_stack *s);
+/* run layers [l0, l1) on n_rows rows starting from d_x (phase 0 prefill / 1
+ * decode, decode step `step`); d_rows = trace rows of these tokens (routing 1) */
+int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_x, int n_rows, int l0, int l1,
+                     int phase, int step, const int32_t *d_rows, void *stream, vmm_stack_out *out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -45,6 +45,24 @@ class EngineReport(C.Structure):
     ]
 
 
+class StackDesc(C.Structure):
+    _fields_ = [
+        ("layers", I32), ("experts", I32), ("k", I32), ("hidden", I32), ("inter", I32), ("l_pinned", I32),
+        ("n_pinned_slots", I64), ("n_slots", I64), ("slot_bytes", SZ), ("host_layers", I32), ("cap_rows", I32),
+        ("routing", I32), ("predictor", I32), ("counts_preset", I32),
+        ("arena", P), ("pool", P), ("router", P), ("pinned_slot_of", P), ("layer_ids", P), ("pow_table", P),
+        ("oracle_table", P), ("trace_routes", P), ("trace_gates", P), ("trace_tokens", I32),
+        ("xn", P), ("xp", P), ("h1", P), ("y", P), ("out0", P), ("out1", P),
+        ("ids", P), ("gates", P), ("off", P), ("src", P), ("pos", P),
+        ("counts", P), ("la_counts", P), ("y_dev", P), ("slot_dev", P),
+        ("counts_host", P), ("y_host", P), ("slot_host", P),
+    ]
+
+
+class StackOut(C.Structure):
+    _fields_ = [("x_out", P), ("copies", I32), ("routes", P), ("ffn_start", P), ("ffn_end", P), ("n_demand", P)]
+
+
 _SIGS = {
     "vmm_last_error": (C.c_char_p, []),
     "vmm_abi_version": (I32, []),
@@ -104,6 +122,11 @@ _SIGS = {
     "vmm_xfer_reset_stats": (I32, [P]),
     "vmm_xfer_stream": (P, [P]),
     "vmm_xfer_issue_engine": (I32, [P, P, P, I32, I32, P, I64, SZ, PI32]),
+    "vmm_gather_i32": (I32, [P, P, I32, I32, P, P]),
+    "vmm_gather_f32": (I32, [P, P, I32, I32, P, P]),
+    "vmm_stack_create": (I32, [C.POINTER(StackDesc), C.POINTER(P)]),
+    "vmm_stack_destroy": (None, [P]),
+    "vmm_stack_layers": (I32, [P, P, P, P, I32, I32, I32, I32, I32, P, P, C.POINTER(StackOut)]),
 }
 
 _lock = threading.Lock()

@@ -30,7 +30,7 @@ CU = {
     "permute.cu": [],
     "ffn_sm100.cu": [],
 }
-CPP = ["engine.cpp", "xfer.cpp", "capi.cpp"]
+CPP = ["engine.cpp", "xfer.cpp", "capi.cpp", "stack.cpp"]
 
 
 def _nvcc() -> str:

@@ -211,3 +211,38 @@ extern "C" int vmm_combine(const void *d_y, const int32_t *d_pos, const float *d
   VMM_LAUNCH_CHECK("combine_kernel");
   return VMM_OK;
 }
+
+namespace {
+template <class T>
+__global__ void gather_elems_kernel(const T *__restrict__ src, const int32_t *__restrict__ rows, int n, int width,
+                                    T *__restrict__ dst) {
+  long long total = (long long)n * width;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    int r = (int)(i / width), c = (int)(i % width);
+    dst[i] = src[(long long)rows[r] * width + c];
+  }
+}
+}  // namespace
+
+extern "C" int vmm_gather_i32(const int32_t *d_src, const int32_t *d_rows, int n, int width, int32_t *d_dst,
+                              void *stream) {
+  if (n <= 0) return VMM_OK;
+  long long total = (long long)n * width;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 1184) blocks = 1184;
+  gather_elems_kernel<int32_t><<<blocks, 256, 0, (cudaStream_t)stream>>>(d_src, d_rows, n, width, d_dst);
+  VMM_LAUNCH_CHECK("gather_elems_kernel<i32>");
+  return VMM_OK;
+}
+
+extern "C" int vmm_gather_f32(const float *d_src, const int32_t *d_rows, int n, int width, float *d_dst,
+                              void *stream) {
+  if (n <= 0) return VMM_OK;
+  long long total = (long long)n * width;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 1184) blocks = 1184;
+  gather_elems_kernel<float><<<blocks, 256, 0, (cudaStream_t)stream>>>(d_src, d_rows, n, width, d_dst);
+  VMM_LAUNCH_CHECK("gather_elems_kernel<f32>");
+  return VMM_OK;
+}

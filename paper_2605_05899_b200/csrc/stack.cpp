@@ -1,0 +1,183 @@
+// Native layer-loop executor: the per-layer body of the reference engine
+// (pkg/src/moesim/pipeline.py:709-740) driving the device kernels, the
+// decision engine and the copy stream without returning to Python.
+//
+// Per layer l (prefill rows or one decode token):
+//   rmsnorm -> route (live: tcgen05/skinny router, fused with the gate
+//   lookahead when emitting; trace: gather the contract routes) -> predictor
+//   scores -> D2H demand counts (+ scores) -> ONE stream sync -> engine
+//   decisions -> expert copies -> slot table + fence -> permute -> grouped
+//   SwiGLU (tcgen05) -> combine -> reader event -> deferred emission ->
+//   prefetch copies.
+// The host only waits once per layer (the decisions need the layer's demand
+// set); everything else is asynchronous on the caller's compute stream and the
+// xfer copy stream.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/vismmoe.h"
+
+namespace vmm {
+int fail(int code, const std::string &msg);
+}
+
+namespace {
+int cuda_status(cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return VMM_OK;
+  return vmm::fail(VMM_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define VMM_TRY(x)           \
+  do {                       \
+    int _st = (x);           \
+    if (_st) return _st;     \
+  } while (0)
+#define VMM_CUDA(x, what)                          \
+  do {                                             \
+    cudaError_t _e = (x);                          \
+    if (_e != cudaSuccess) return cuda_status(_e, what); \
+  } while (0)
+}  // namespace
+
+extern "C" {
+int vmm_engine_slots(const vmm_engine *e, int layer, const int32_t *h_demand, int n, int32_t *h_slabs);
+int vmm_engine_emit(vmm_engine *e, int layer, const double *h_y);
+int vmm_xfer_issue_engine(vmm_xfer *x, vmm_engine *e, const void *h_pool, int host_layers, int experts,
+                          void *d_arena, long long slab_offset, size_t slot_bytes, int *n_issued);
+int vmm_gather_i32(const int32_t *d_src, const int32_t *d_rows, int n, int width, int32_t *d_dst, void *stream);
+int vmm_gather_f32(const float *d_src, const int32_t *d_rows, int n, int width, float *d_dst, void *stream);
+}
+
+struct vmm_stack {
+  vmm_stack_desc d;
+};
+
+extern "C" {
+
+int vmm_stack_create(const vmm_stack_desc *desc, vmm_stack **out) {
+  if (!desc || !out) return vmm::fail(VMM_ECONTRACT, "null argument");
+  if (desc->experts < 1 || desc->experts > VMM_MAX_EXPERTS) return vmm::fail(VMM_EVALIDATION, "bad expert count");
+  auto *s = new vmm_stack();
+  s->d = *desc;
+  *out = s;
+  return VMM_OK;
+}
+
+void vmm_stack_destroy(vmm_stack *s) { delete s; }
+
+int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_x, int n_rows, int l0, int l1,
+                     int phase, int step, const int32_t *d_rows, void *stream, vmm_stack_out *out) {
+  const vmm_stack_desc &d = s->d;
+  const int E = d.experts, k = d.k, H = d.hidden, I = d.inter, L = d.layers, lp = d.l_pinned;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n_rows <= 0 || n_rows > d.cap_rows) return vmm::fail(VMM_ECONTRACT, "row count outside the buffers");
+  const size_t row_bytes = (size_t)H * 2;
+  const void *cur = d_x;
+  int ping = 0, copies = 0;
+  std::vector<int32_t> demand, slabs;
+  for (int l = l0; l < l1; ++l) {
+    void *xn = d.xn;
+    VMM_TRY(vmm_rmsnorm(cur, nullptr, n_rows, H, 1e-6f, xn, stream));
+    const int emits = vmm_engine_emits(eng, l, phase);
+    uint32_t *cnt = d.counts + (size_t)l * E;
+    bool la_done = false;
+    if (d.routing == 0) {
+      VMM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * E, st), "counts memset");
+      if (emits && d.predictor == 2 && l + 1 < L && (E % 16 == 0) && E <= 128) {
+        VMM_CUDA(cudaMemsetAsync(d.la_counts, 0, sizeof(uint32_t) * E, st), "lookahead memset");
+        VMM_TRY(vmm_route_lookahead(xn, d.router, l, L, n_rows, H, E, k, d.ids, d.gates, cnt, d.la_counts, stream));
+        la_done = true;
+      } else {
+        VMM_TRY(vmm_route_topk(xn, (const char *)d.router + (size_t)l * E * H * 2, n_rows, H, E, k, d.ids, d.gates,
+                               nullptr, cnt, stream));
+      }
+    } else {
+      const int32_t *tr = d.trace_routes + (size_t)l * d.trace_tokens * k;
+      const float *tg = d.trace_gates + (size_t)l * d.trace_tokens * k;
+      VMM_TRY(vmm_gather_i32(tr, d_rows, n_rows, k, d.ids, stream));
+      VMM_TRY(vmm_gather_f32(tg, d_rows, n_rows, k, d.gates, stream));
+      if (!d.counts_preset) {
+        int32_t lay = l;
+        (void)lay;
+        VMM_TRY(vmm_demand_counts(d.trace_routes, L, d.trace_tokens, k, E, d.layer_ids + l, 1, d_rows, n_rows, cnt,
+                                  stream));
+      }
+    }
+    if (out && out->routes)
+      VMM_CUDA(cudaMemcpyAsync(out->routes + (size_t)(l - l0) * n_rows * k, d.ids, sizeof(int32_t) * n_rows * k,
+                               cudaMemcpyDeviceToDevice, st), "record routes");
+    double *yh = d.y_host + (size_t)l * E;
+    if (emits) {
+      const double *ysrc = nullptr;
+      if (la_done) {
+        VMM_TRY(vmm_normalize_counts(d.la_counts, E, (double)n_rows * k, d.y_dev, stream));
+        ysrc = d.y_dev;
+      } else if (d.predictor == 1) {
+        VMM_TRY(vmm_history(d.counts, L, E, d.layer_ids + l, 1, d.pow_table, d.y_dev, stream));
+        ysrc = d.y_dev;
+      } else if (d.predictor == 2) {
+        VMM_TRY(vmm_gate_lookahead(xn, (const char *)d.router + (size_t)(l + 1) * E * H * 2, n_rows, H, E, k,
+                                   d.la_counts, d.y_dev, stream));
+        ysrc = d.y_dev;
+      } else if (d.predictor == 3) {
+        ysrc = d.oracle_table + (size_t)l * E;
+      } else {
+        return vmm::fail(VMM_ECONTRACT, "emitting layer without a predictor");
+      }
+      VMM_CUDA(cudaMemcpyAsync(yh, ysrc, sizeof(double) * E, cudaMemcpyDeviceToHost, st), "scores D2H");
+    }
+    int32_t *ch = d.counts_host + (size_t)l * E;
+    VMM_CUDA(cudaMemcpyAsync(ch, cnt, sizeof(uint32_t) * E, cudaMemcpyDeviceToHost, st), "counts D2H");
+    VMM_CUDA(cudaStreamSynchronize(st), "layer sync");
+    demand.clear();
+    for (int e = 0; e < E; ++e)
+      if (ch[e]) demand.push_back(e);
+    VMM_TRY(vmm_engine_layer(eng, l, demand.data(), (int)demand.size(), phase, step, nullptr));
+    int n = 0;
+    VMM_TRY(vmm_xfer_issue_engine(xf, eng, d.pool, d.host_layers, E, d.arena, d.n_pinned_slots, d.slot_bytes, &n));
+    copies += n;
+    const int32_t *slot_of;
+    if (l < lp) {
+      slot_of = d.pinned_slot_of + (size_t)l * E;
+    } else {
+      slabs.resize(demand.size());
+      VMM_TRY(vmm_engine_slots(eng, l, demand.data(), (int)demand.size(), slabs.data()));
+      int32_t *row = d.slot_host + (size_t)l * E;
+      std::memset(row, 0, sizeof(int32_t) * E);
+      for (size_t i = 0; i < demand.size(); ++i) row[demand[i]] = slabs[i] + (int32_t)d.n_pinned_slots;
+      int32_t *drow = d.slot_dev + (size_t)l * E;
+      VMM_CUDA(cudaMemcpyAsync(drow, row, sizeof(int32_t) * E, cudaMemcpyHostToDevice, st), "slot table H2D");
+      VMM_TRY(vmm_xfer_fence(xf, slabs.data(), (int)slabs.size(), stream));
+      slot_of = drow;
+    }
+    const int M = n_rows * k;
+    VMM_TRY(vmm_permute_plan(d.ids, n_rows, k, E, d.off, d.src, d.pos, stream));
+    VMM_TRY(vmm_permute_rows(xn, d.src, M, H, d.xp, stream));
+    if (out && out->ffn_start)
+      VMM_CUDA(cudaEventRecord((cudaEvent_t)out->ffn_start[l - l0], st), "ffn start event");
+    VMM_TRY(vmm_grouped_swiglu(d.xp, d.off, E, M, H, I, d.arena, (const char *)d.arena + (size_t)2 * I * H * 2,
+                               (long long)3 * I * H, d.n_slots, slot_of, d.h1, d.y, stream));
+    if (out && out->ffn_end) VMM_CUDA(cudaEventRecord((cudaEvent_t)out->ffn_end[l - l0], st), "ffn end event");
+    void *dst = ping ? d.out1 : d.out0;
+    VMM_TRY(vmm_combine(d.y, d.pos, d.gates, cur, n_rows, k, H, dst, stream));
+    cur = dst;
+    ping ^= 1;
+    if (out && out->n_demand) out->n_demand[l - l0] = (int)demand.size();
+    if (l >= lp) VMM_TRY(vmm_xfer_layer_done(xf, l, stream));
+    if (emits) {
+      VMM_TRY(vmm_engine_emit(eng, l, yh));
+      VMM_TRY(vmm_xfer_issue_engine(xf, eng, d.pool, d.host_layers, E, d.arena, d.n_pinned_slots, d.slot_bytes, &n));
+      copies += n;
+    }
+  }
+  if (out) {
+    out->x_out = cur;
+    out->copies = copies;
+  }
+  (void)row_bytes;
+  return VMM_OK;
+}
+
+}  // extern "C"

@@ -216,6 +216,8 @@ class MoEStack:
         self.counts_host = torch.zeros((L, E), dtype=torch.int32, pin_memory=True)
         self.y_host = torch.zeros((L + 1, E), dtype=torch.float64, pin_memory=True)
         self.pow = torch.tensor(pow_table(cfg.history_decay, L), dtype=torch.float64, device=self.device)
+        self.layer_ids = torch.arange(L, dtype=torch.int32, device=self.device)
+        self.step_counts = torch.zeros((L, E), dtype=torch.int32, device=self.device)
         self._bufs = {}
         self.profile = None  # list -> (start_ev, end_ev, bytes, flops) per grouped SwiGLU launch pair
 
@@ -346,9 +348,8 @@ class MoEStack:
         if c.predictor == "oracle":
             rl = trace["routes"]
             kernels.demand_counts(rl, torch.arange(L, dtype=torch.int32, device=dev), ret, E, out=counts_ret)
-            ctx = torch.arange(max(lp - 1, 0), L, dtype=torch.int32, device=dev)
             dec = torch.tensor(decay_table(c.gamma, c.window), dtype=torch.float64, device=dev)
-            oracle_table = kernels.oracle_targets(counts_ret, ctx, c.window, dec)
+            oracle_table = kernels.oracle_targets(counts_ret, self.layer_ids, c.window, dec)  # row = context layer
 
         cfg = c.sim_config()
         prefetching = c.predictor != "none" and c.budget > 0
@@ -363,7 +364,7 @@ class MoEStack:
                 yt = kernels.gate_lookahead(x_in, self.store.router[ctx + 1], k, scratch=bufs["scratch"],
                                             out=bufs["y_dev"])
             else:
-                yt = oracle_table[ctx - max(lp - 1, 0)]
+                yt = oracle_table[ctx]
             self.y_host[ctx].copy_(yt, non_blocking=True)
             return self.y_host[ctx]
 
@@ -381,56 +382,15 @@ class MoEStack:
         for l in range(lp):
             eng.layer(l, np.flatnonzero(cp[l]).astype(np.int32), 0, -1, None)
 
-        # --- cached layers on the retained tokens
-        routes = []
-        cur = xr
-        ping = 0
-        for l in range(lp, L):
-            xn = kernels.rmsnorm(cur, out=bufs["xn"][:n_r])
-            fused_la = (c.routing == "live" and c.predictor == "gate" and E % 16 == 0 and E <= 128
-                        and eng.emits(l, 0))
-            if fused_la:
-                # one tcgen05 GEMM against the adjacent gates of layers l and l+1
-                bufs["scratch"].zero_()
-                ids, gates = kernels.route_lookahead(xn, self.store.router, l, k, counts_ret[l], bufs["scratch"],
-                                                     ids=bufs["ids"][:n_r], gates=bufs["gates"][:n_r])
-            elif c.routing == "live":
-                ids, gates, _ = kernels.route_topk(xn, self.store.router[l], k, counts=counts_ret[l],
-                                                   ids=bufs["ids"][:n_r], gates=bufs["gates"][:n_r])
-            else:
-                ids = trace["routes"][l].index_select(0, ret.long())
-                gates = trace["gates"][l].index_select(0, ret.long())
-                if c.predictor != "oracle":
-                    kernels.demand_counts(trace["routes"], torch.tensor([l], dtype=torch.int32, device=dev), ret, E,
-                                          out=counts_ret[l:l + 1])
-            if record:
-                routes.append(ids.clone())
-            emits = eng.emits(l, 0)
-            if emits and fused_la:
-                yt = kernels.normalize_counts(bufs["scratch"], float(n_r * k), out=bufs["y_dev"])
-                self.y_host[l].copy_(yt, non_blocking=True)
-                y_row = self.y_host[l]
-            else:
-                y_row = predict(l, xn) if emits else None
-            self.counts_host[l].copy_(counts_ret[l], non_blocking=True)
-            stream.synchronize()
-            demand = np.flatnonzero(self.counts_host[l].numpy()).astype(np.int32)
-            eng.layer(l, demand, 0, -1, None)
-            n_copies += self._issue(eng)
-            slabs = np.empty(len(demand), dtype=np.int32)
-            check(self._L.vmm_engine_slots(eng._h, l, demand.ctypes.data, len(demand), slabs.ctypes.data))
-            row = self.slot_host[l].numpy()
-            row[:] = 0
-            row[demand] = slabs + self.store.n_pinned_slots
-            self.slot_dev[l].copy_(self.slot_host[l], non_blocking=True)
-            check(self._L.vmm_xfer_fence(self._x, slabs.ctypes.data, len(slabs), sp))
-            cur = self._layer_compute(cur, xn, ids, gates, self.slot_dev[l], bufs, outs[ping], n_experts=len(demand))
-            ping ^= 1
-            check(self._L.vmm_xfer_layer_done(self._x, l, sp))
-            if emits:
-                scores[l] = y_row.numpy().copy()
-                check(self._L.vmm_engine_emit(eng._h, l, scores[l].ctypes.data))
-                n_copies += self._issue(eng)
+        # --- cached layers on the retained tokens: the native layer loop
+        cur, n_cp, routes_t = self._native_layers(
+            eng, xr, n_r, lp, L, 0, -1, rows=ret if c.routing == "trace" else None, counts=counts_ret,
+            oracle_table=oracle_table, trace=trace, record=record)
+        n_copies += n_cp
+        for l in range(lp, L - 1):
+            if eng.emits(l, 0):
+                scores[l] = self.y_host[l].numpy().copy()
+        routes = [routes_t[i] for i in range(L - lp)] if record else []
         check(self._L.vmm_xfer_join(self._x, sp))  # the step ends when its last transfer has landed
         report = eng.finish(with_events=False)
         b, ms, cnt = C.c_double(), C.c_double(), C.c_longlong()
@@ -439,6 +399,63 @@ class MoEStack:
         return StackResult(hidden=cur, retained=ret.cpu().numpy(), report=report, prefix_routes=prefix[:lp],
                            routes=routes, scores=scores, copies=n_copies, h2d_bytes=b.value,
                            retained_offsets=ret_off)
+
+    def _native_layers(self, eng, x, n_rows, l0, l1, phase, step, rows=None, counts=None, oracle_table=None,
+                       trace=None, record=False):
+        """Run layers [l0, l1) through the native executor (csrc/stack.cpp)."""
+        c = self.cfg
+        L, E, k = c.layers, c.experts, c.k
+        bufs = self._buffers(n_rows)
+        st = self.store
+        pred = {"none": 0, "history": 1, "gate": 2, "oracle": 3}[c.predictor]
+        d = _lib.StackDesc(
+            layers=L, experts=E, k=k, hidden=c.hidden, inter=c.inter, l_pinned=c.l_pinned,
+            n_pinned_slots=st.n_pinned_slots, n_slots=int(st.arena.shape[0]), slot_bytes=c.slot_bytes,
+            host_layers=st.host_layers, cap_rows=int(bufs["n"]), routing=int(c.routing == "trace"), predictor=pred,
+            counts_preset=int(oracle_table is not None and c.routing == "trace"),
+            arena=st.arena.data_ptr(), pool=st.pool.data_ptr(), router=st.router.data_ptr(),
+            pinned_slot_of=st.pinned_slot_of.data_ptr() if st.pinned_slot_of is not None else None,
+            layer_ids=self.layer_ids.data_ptr(), pow_table=self.pow.data_ptr(),
+            oracle_table=oracle_table.data_ptr() if oracle_table is not None else None,
+            trace_routes=trace["routes"].data_ptr() if trace is not None else None,
+            trace_gates=trace["gates"].data_ptr() if trace is not None else None,
+            trace_tokens=int(trace["routes"].shape[1]) if trace is not None else 0,
+            xn=bufs["xn"].data_ptr(), xp=bufs["xp"].data_ptr(), h1=bufs["h1"].data_ptr(), y=bufs["y"].data_ptr(),
+            out0=bufs["out"].data_ptr(), out1=bufs["out2"].data_ptr(), ids=bufs["ids"].data_ptr(),
+            gates=bufs["gates"].data_ptr(), off=bufs["off"].data_ptr(), src=bufs["src"].data_ptr(),
+            pos=bufs["pos"].data_ptr(), counts=counts.data_ptr(), la_counts=bufs["scratch"].data_ptr(),
+            y_dev=bufs["y_dev"].data_ptr(), slot_dev=self.slot_dev.data_ptr(),
+            counts_host=self.counts_host.data_ptr(), y_host=self.y_host.data_ptr(),
+            slot_host=self.slot_host.data_ptr())
+        h = C.c_void_p()
+        check(self._L.vmm_stack_create(C.byref(d), C.byref(h)))
+        nl = l1 - l0
+        out = _lib.StackOut()
+        routes_t = torch.empty((nl, n_rows, k), dtype=torch.int32, device=self.device) if record else None
+        out.routes = routes_t.data_ptr() if record else None
+        evs = None
+        n_dem = np.zeros(nl, dtype=np.int32)
+        out.n_demand = n_dem.ctypes.data
+        if self.profile is not None:
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * nl)]
+            for e in evs:
+                e.record()  # materialise the CUDA events
+            arr = (C.c_void_p * (2 * nl))(*[e.cuda_event for e in evs])
+            out.ffn_start = C.cast(arr, C.c_void_p)
+            out.ffn_end = C.cast(C.byref(arr, nl * C.sizeof(C.c_void_p)), C.c_void_p)
+        try:
+            check(self._L.vmm_stack_layers(h, eng._h, self._x, x.data_ptr(), n_rows, l0, l1, phase, step,
+                                           rows.data_ptr() if rows is not None else None,
+                                           torch.cuda.current_stream().cuda_stream, C.byref(out)))
+        finally:
+            self._L.vmm_stack_destroy(h)
+        if self.profile is not None:
+            M = n_rows * k
+            for i in range(nl):
+                nbytes = int(n_dem[i]) * c.slot_bytes + M * c.hidden * 2 * 2 + M * c.inter * 2 * 2
+                self.profile.append((evs[i], evs[nl + i], nbytes, 6.0 * M * c.hidden * c.inter))
+        res = bufs["out"] if out.x_out == bufs["out"].data_ptr() else bufs["out2"]
+        return res[:n_rows], out.copies, routes_t
 
     # ------------------------------------------------------------------
     # decode phase (pipeline.py:723-740): one token per step, the prefill's
@@ -452,83 +469,32 @@ class MoEStack:
         if sess is None:
             raise ContractError("decode_step needs forward(..., keep_session=True) first")
         c = self.cfg
-        L, E, k, lp = c.layers, c.experts, c.k, c.l_pinned
+        L, E = c.layers, c.experts
         dev = self.device
         eng, s = sess["eng"], sess["step"]
-        stream = torch.cuda.current_stream()
-        sp = stream.cuda_stream
-        bufs = self._buffers(1)
         trace = sess["trace"]
         if c.routing == "trace" and tok is None:
             raise ContractError("routing='trace' decode needs the token's trace row")
         check(self._L.vmm_xfer_reset_stats(self._x))
-        counts = torch.zeros((L, E), dtype=torch.int32, device=dev)
-        ids_tok = None
+        counts = self.step_counts
+        rows, otab = None, None
         if c.routing == "trace":
-            ids_tok = trace["routes"][:, tok:tok + 1].contiguous()  # [L, 1, k]
-            one = torch.zeros(1, dtype=torch.int32, device=dev)
-            kernels.demand_counts(ids_tok, torch.arange(L, dtype=torch.int32, device=dev), one, E, out=counts)
+            rows = torch.tensor([tok], dtype=torch.int32, device=dev)
             if c.predictor == "oracle":
+                kernels.demand_counts(trace["routes"], self.layer_ids, rows, E, out=counts)
                 dec = torch.tensor(decay_table(c.gamma, c.window), dtype=torch.float64, device=dev)
-                otab = kernels.oracle_targets(counts, torch.arange(L, dtype=torch.int32, device=dev), c.window, dec)
-        outs = (bufs["out"], bufs["out2"])
-        cur, n_copies, routes, scores = x_tok, 0, [], {}
-        for l in range(L):
-            xn = kernels.rmsnorm(cur, out=bufs["xn"][:1])
-            emits = eng.emits(l, 1)
-            la = emits and c.routing == "live" and c.predictor == "gate" and E % 16 == 0 and E <= 128
-            if c.routing == "live":
-                if la:
-                    bufs["scratch"].zero_()
-                    ids, gates = kernels.route_lookahead(xn, self.store.router, l, k, counts[l], bufs["scratch"],
-                                                         ids=bufs["ids"][:1], gates=bufs["gates"][:1])
-                else:
-                    ids, gates, _ = kernels.route_topk(xn, self.store.router[l], k, counts=counts[l],
-                                                       ids=bufs["ids"][:1], gates=bufs["gates"][:1])
-            else:
-                ids, gates = ids_tok[l], trace["gates"][l, tok:tok + 1]
-            if record:
-                routes.append(ids.clone())
-            if emits:
-                if la:
-                    yt = kernels.normalize_counts(bufs["scratch"], float(k), out=bufs["y_dev"])
-                elif c.predictor == "history":
-                    yt = kernels.history(counts, torch.tensor([l], dtype=torch.int32, device=dev), self.pow)[0]
-                elif c.predictor == "oracle":
-                    yt = otab[l]
-                else:
-                    yt = kernels.gate_lookahead(xn, self.store.router[l + 1], k, scratch=bufs["scratch"],
-                                                out=bufs["y_dev"])
-                self.y_host[l].copy_(yt, non_blocking=True)
-            self.counts_host[l].copy_(counts[l], non_blocking=True)
-            stream.synchronize()
-            demand = np.flatnonzero(self.counts_host[l].numpy()).astype(np.int32)
-            eng.layer(l, demand, 1, s, None)
-            n_copies += self._issue(eng)
-            if l < lp:
-                cur = self._layer_compute(cur, xn, ids, gates, self.store.pinned_slot_of[l], bufs, outs[l % 2])
-            else:
-                slabs = np.empty(len(demand), dtype=np.int32)
-                check(self._L.vmm_engine_slots(eng._h, l, demand.ctypes.data, len(demand), slabs.ctypes.data))
-                row = self.slot_host[l].numpy()
-                row[:] = 0
-                row[demand] = slabs + self.store.n_pinned_slots
-                self.slot_dev[l].copy_(self.slot_host[l], non_blocking=True)
-                check(self._L.vmm_xfer_fence(self._x, slabs.ctypes.data, len(slabs), sp))
-                cur = self._layer_compute(cur, xn, ids, gates, self.slot_dev[l], bufs, outs[l % 2],
-                                          n_experts=len(demand))
-                check(self._L.vmm_xfer_layer_done(self._x, l, sp))
-            if emits:
-                y = self.y_host[l].numpy().copy()
-                scores[l] = y
-                check(self._L.vmm_engine_emit(eng._h, l, y.ctypes.data))
-                n_copies += self._issue(eng)
+                otab = kernels.oracle_targets(counts, self.layer_ids, c.window, dec)
+        cur, n_cp, routes_t = self._native_layers(eng, x_tok, 1, 0, L, 1, s, rows=rows, counts=counts,
+                                                  oracle_table=otab, trace=trace, record=record)
+        scores = {l: self.y_host[l].numpy().copy() for l in range(L) if eng.emits(l, 1)}
         eng.end_step()
         sess["step"] = s + 1
+        sp = torch.cuda.current_stream().cuda_stream
         check(self._L.vmm_xfer_join(self._x, sp))
         b, ms, cnt = C.c_double(), C.c_double(), C.c_longlong()
         check(self._L.vmm_xfer_stats(self._x, C.byref(b), C.byref(ms), C.byref(cnt)))
-        return DecodeResult(hidden=cur.clone(), copies=n_copies, h2d_bytes=b.value, routes=routes, scores=scores)
+        routes = [routes_t[i] for i in range(L)] if record else []
+        return DecodeResult(hidden=cur.clone(), copies=n_cp, h2d_bytes=b.value, routes=routes, scores=scores)
 
     def end_session(self) -> SimReport:
         sess = getattr(self, "_sess", None)
