@@ -131,6 +131,11 @@ int vmm_permute_plan(const int32_t *d_ids, int N, int k, int E, int32_t *d_offse
                      int32_t *d_src_row, int32_t *d_pos, void *stream);
 /* Xp[p] = X[src_row[p]] for the n_rows permuted rows (bf16 rows of H) */
 int vmm_permute_rows(const void *d_x, const int32_t *d_src_row, int n_rows, int H, void *d_xp, void *stream);
+/* combine plus S always-resident shared experts (unit weight; rows s*N + t of d_ys) */
+int vmm_combine_shared(const void *d_y, const int32_t *d_pos, const float *d_gates, const void *d_resid,
+                       int N, int k, int H, const void *d_ys, int S, void *d_out, void *stream);
+/* shared-expert plan: src[s*N + t] = t, offsets[s] = s*N (every token to each shared expert) */
+int vmm_shared_plan(int N, int S, int32_t *d_src, int32_t *d_offsets, void *stream);
 /* Pre-MoE RMSNorm of the token rows (the layer's router and experts see the
  * normalised rows, the residual is the raw row): y = x * rsqrt(mean(x^2)+eps) * w
  * (w nullable = ones). */
@@ -325,6 +330,10 @@ typedef struct {
   int32_t *counts_host;                 /* h pinned [L][E] */
   double *y_host;                       /* h pinned [L][E] scores per context layer */
   int32_t *slot_host;                   /* h pinned [L][E] */
+  int shared;                           /* S always-resident shared experts per layer (0: none) */
+  const int32_t *shared_slot_of;        /* d [L][S] arena slots of the shared experts */
+  int32_t *shared_src, *shared_off;     /* d [cap*S], [S+1] */
+  void *xs, *h1s, *ys;                  /* d [cap*S][H], [cap*S][I], [cap*S][H] */
 } vmm_stack_desc;
 
 typedef struct {

@@ -56,6 +56,8 @@ class StackDesc(C.Structure):
         ("ids", P), ("gates", P), ("off", P), ("src", P), ("pos", P),
         ("counts", P), ("la_counts", P), ("y_dev", P), ("slot_dev", P),
         ("counts_host", P), ("y_host", P), ("slot_host", P),
+        ("shared", I32), ("shared_slot_of", P), ("shared_src", P), ("shared_off", P),
+        ("xs", P), ("h1s", P), ("ys", P),
     ]
 
 
@@ -122,6 +124,8 @@ _SIGS = {
     "vmm_xfer_reset_stats": (I32, [P]),
     "vmm_xfer_stream": (P, [P]),
     "vmm_xfer_issue_engine": (I32, [P, P, P, I32, I32, P, I64, SZ, PI32]),
+    "vmm_combine_shared": (I32, [P, P, P, P, I32, I32, I32, P, I32, P, P]),
+    "vmm_shared_plan": (I32, [I32, I32, P, P, P]),
     "vmm_gather_i32": (I32, [P, P, I32, I32, P, P]),
     "vmm_gather_f32": (I32, [P, P, I32, I32, P, P]),
     "vmm_stack_create": (I32, [C.POINTER(StackDesc), C.POINTER(P)]),

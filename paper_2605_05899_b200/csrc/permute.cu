@@ -95,7 +95,7 @@ __global__ void permute_rows_kernel(const uint4 *__restrict__ x, const int32_t *
 // out[t] = resid[t] + sum_j gates[t,j] * Y[pos[t,j]]; each thread owns 8 columns
 __global__ void combine_kernel(const uint4 *__restrict__ y, const int32_t *__restrict__ pos,
                                const float *__restrict__ gates, const uint4 *__restrict__ resid, int N, int k,
-                               int row_vec, uint4 *__restrict__ out) {
+                               int row_vec, uint4 *__restrict__ out, const uint4 *__restrict__ ys, int S) {
   long long total = (long long)N * row_vec;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
@@ -110,6 +110,12 @@ __global__ void combine_kernel(const uint4 *__restrict__ y, const int32_t *__res
       const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&v);
 #pragma unroll
       for (int q = 0; q < 8; ++q) acc[q] = fmaf(g, __bfloat162float(h[q]), acc[q]);
+    }
+    for (int sx = 0; sx < S; ++sx) {  // shared experts: unit weight, row sx*N + t
+      uint4 v = __ldg(ys + ((long long)sx * N + t) * row_vec + c);
+      const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&v);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] += __bfloat162float(h[q]);
     }
     uint4 rv = resid ? __ldg(resid + i) : make_uint4(0, 0, 0, 0);
     const __nv_bfloat16 *rh = reinterpret_cast<const __nv_bfloat16 *>(&rv);
@@ -207,8 +213,47 @@ extern "C" int vmm_combine(const void *d_y, const int32_t *d_pos, const float *d
   int blocks = (int)((total + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
   combine_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((const uint4 *)d_y, d_pos, d_gates,
-                                                           (const uint4 *)d_resid, N, k, row_vec, (uint4 *)d_out);
+                                                           (const uint4 *)d_resid, N, k, row_vec, (uint4 *)d_out,
+                                                           nullptr, 0);
   VMM_LAUNCH_CHECK("combine_kernel");
+  return VMM_OK;
+}
+
+extern "C" int vmm_combine_shared(const void *d_y, const int32_t *d_pos, const float *d_gates, const void *d_resid,
+                                  int N, int k, int H, const void *d_ys, int S, void *d_out, void *stream) {
+  if (N <= 0) return VMM_OK;
+  if ((H * 2) % 16) return vmm::fail(VMM_EVALIDATION, "hidden size must be a multiple of 8");
+  int row_vec = H * 2 / 16;
+  long long total = (long long)N * row_vec;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  combine_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((const uint4 *)d_y, d_pos, d_gates,
+                                                           (const uint4 *)d_resid, N, k, row_vec, (uint4 *)d_out,
+                                                           (const uint4 *)d_ys, S);
+  VMM_LAUNCH_CHECK("combine_kernel");
+  return VMM_OK;
+}
+
+namespace {
+// shared-expert "routing": every token goes to each of the S shared experts:
+// src[s*N + t] = t, offsets[s] = s*N
+__global__ void shared_plan_kernel(int N, int S, int32_t *__restrict__ src, int32_t *__restrict__ offs) {
+  long long total = (long long)N * S;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x)
+    src[i] = (int32_t)(i % N);
+  if (blockIdx.x == 0 && threadIdx.x <= S) offs[threadIdx.x] = threadIdx.x * N;
+}
+}  // namespace
+
+extern "C" int vmm_shared_plan(int N, int S, int32_t *d_src, int32_t *d_offsets, void *stream) {
+  if (S <= 0 || N <= 0) return VMM_OK;
+  if (S > 255) return vmm::fail(VMM_EVALIDATION, "too many shared experts");
+  long long total = (long long)N * S;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 1184) blocks = 1184;
+  shared_plan_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(N, S, d_src, d_offsets);
+  VMM_LAUNCH_CHECK("shared_plan_kernel");
   return VMM_OK;
 }
 

@@ -161,7 +161,18 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
                                (long long)3 * I * H, d.n_slots, slot_of, d.h1, d.y, stream));
     if (out && out->ffn_end) VMM_CUDA(cudaEventRecord((cudaEvent_t)out->ffn_end[l - l0], st), "ffn end event");
     void *dst = ping ? d.out1 : d.out0;
-    VMM_TRY(vmm_combine(d.y, d.pos, d.gates, cur, n_rows, k, H, dst, stream));
+    if (d.shared > 0) {
+      // always-resident shared experts: every token through each, grouped GEMM over S groups
+      const int S = d.shared, MS = n_rows * S;
+      VMM_TRY(vmm_shared_plan(n_rows, S, d.shared_src, d.shared_off, stream));
+      VMM_TRY(vmm_permute_rows(xn, d.shared_src, MS, H, d.xs, stream));
+      VMM_TRY(vmm_grouped_swiglu(d.xs, d.shared_off, S, MS, H, I, d.arena,
+                                 (const char *)d.arena + (size_t)2 * I * H * 2, (long long)3 * I * H, d.n_slots,
+                                 d.shared_slot_of + (size_t)l * S, d.h1s, d.ys, stream));
+      VMM_TRY(vmm_combine_shared(d.y, d.pos, d.gates, cur, n_rows, k, H, d.ys, S, dst, stream));
+    } else {
+      VMM_TRY(vmm_combine(d.y, d.pos, d.gates, cur, n_rows, k, H, dst, stream));
+    }
     cur = dst;
     ping ^= 1;
     if (out && out->n_demand) out->n_demand[l - l0] = (int)demand.size();

@@ -211,6 +211,22 @@ def pack_expert(w_gate, w_up, w_down):
     return torch.cat([interleave_w13(w_gate, w_up).reshape(-1), w_down.reshape(-1)])
 
 
+def shared_plan(N: int, S: int, src, offsets, stream=None):
+    _n(1)
+    check(_lib.lib().vmm_shared_plan(N, S, ptr(src), ptr(offsets), stream_ptr(stream)))
+    return src[: N * S], offsets
+
+
+def combine_shared(y, pos, gates, resid, ys, S: int, stream=None, out=None):
+    N, k = (int(s) for s in gates.shape)
+    H = int(y.shape[1])
+    out = torch.empty(N, H, dtype=torch.bfloat16, device=y.device) if out is None else out
+    _n(1)
+    check(_lib.lib().vmm_combine_shared(ptr(y), ptr(pos), ptr(gates), ptr(resid), N, k, H, ptr(ys), S, ptr(out),
+                                        stream_ptr(stream)))
+    return out
+
+
 def rmsnorm(x, weight=None, eps: float = 1e-6, stream=None, out=None):
     n, H = (int(s) for s in x.shape)
     out = torch.empty_like(x) if out is None else out

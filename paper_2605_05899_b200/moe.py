@@ -123,11 +123,22 @@ class ExpertStore:
             w[:, 2 * I * H:] *= 1.0 / math.sqrt(I)
             self.pool[s0:s1].copy_(w.to(torch.bfloat16))
         self.n_pinned_slots = cfg.l_pinned * E
-        self.arena = torch.empty((self.n_pinned_slots + cfg.num_slabs, cfg.slot_elems), dtype=torch.bfloat16,
-                                 device=dev)
+        S = cfg.shared_experts
+        # arena: [pinned prefix experts | cache slabs | always-resident shared experts (L*S)]
+        self.arena = torch.empty((self.n_pinned_slots + cfg.num_slabs + L * S, cfg.slot_elems),
+                                 dtype=torch.bfloat16, device=dev)
         for l in range(cfg.l_pinned):
             h = l % self.host_layers
             self.arena[l * E:(l + 1) * E].copy_(self.pool[h * E:(h + 1) * E], non_blocking=True)
+        base = self.n_pinned_slots + cfg.num_slabs
+        for s0 in range(0, L * S, chunk):
+            s1 = min(L * S, s0 + chunk)
+            w = torch.randn((s1 - s0, cfg.slot_elems), generator=g, device=dev, dtype=torch.float32)
+            w[:, : 2 * I * H] *= 1.0 / math.sqrt(H)
+            w[:, 2 * I * H:] *= 1.0 / math.sqrt(I)
+            self.arena[base + s0: base + s1].copy_(w.to(torch.bfloat16))
+        self.shared_slot_of = (torch.arange(base, base + L * S, dtype=torch.int32, device=dev).reshape(L, S)
+                               if S else None)
         # router: W[l] = rho W[l-1] + sqrt(1-rho^2) noise, so consecutive layers route
         # alike (the inter-layer affinity lookahead prediction relies on; rho=0 -> independent)
         rho = cfg.router_corr
@@ -201,8 +212,6 @@ class MoEStack:
     def __init__(self, cfg: StackConfig, store: ExpertStore | None = None, seed: int = 0):
         if cfg.predictor == "oracle" and cfg.routing != "trace":
             raise ValidationError("the oracle predictor needs trace routing (future routes)")
-        if cfg.shared_experts:
-            raise ValidationError("shared experts are not supported by the live stack yet")
         self.cfg = cfg
         self.store = store or ExpertStore(cfg, seed)
         self.device = self.store.device
@@ -251,6 +260,12 @@ class MoEStack:
                 gates=torch.empty(n_tok, c.k, dtype=torch.float32, device=dev),
                 y_dev=torch.empty(c.experts, dtype=torch.float64, device=dev),
                 scratch=torch.empty(c.experts, dtype=torch.int32, device=dev),
+                # shared experts (S per layer, every token)
+                shared_src=torch.empty(max(n_tok * c.shared_experts, 1), dtype=torch.int32, device=dev),
+                shared_off=torch.empty(c.shared_experts + 1, dtype=torch.int32, device=dev),
+                xs=torch.empty(max(n_tok * c.shared_experts, 1), c.hidden, dtype=torch.bfloat16, device=dev),
+                h1s=torch.empty(max(n_tok * c.shared_experts, 1), c.inter, dtype=torch.bfloat16, device=dev),
+                ys=torch.empty(max(n_tok * c.shared_experts, 1), c.hidden, dtype=torch.bfloat16, device=dev),
             )
         return self._bufs
 
@@ -273,6 +288,14 @@ class MoEStack:
             nbytes = ne * c.slot_bytes + M * c.hidden * 2 * 2 + M * c.inter * 2 * 2
             flops = 6.0 * M * c.hidden * c.inter
             self.profile.append((e0, e1, nbytes, flops))
+        S = c.shared_experts
+        if S:
+            layer = self._cur_layer
+            src_s, off_s = kernels.shared_plan(N, S, bufs["shared_src"], bufs["shared_off"])
+            xs = kernels.permute_rows(xn, src_s, N * S, out=bufs["xs"][: N * S])
+            _, ys = kernels.grouped_swiglu(xs, off_s, self.store.arena, self.store.shared_slot_of[layer], c.inter,
+                                           h1=bufs["h1s"][: N * S], y=bufs["ys"][: N * S])
+            return kernels.combine_shared(y, pos, gates, x, ys, S, out=out[:N])
         return kernels.combine(y, pos, gates, x, out=out[:N])
 
     def forward(self, x, saliency, modality, trace=None, record: bool = False, req_off=None,
@@ -315,6 +338,7 @@ class MoEStack:
                                       torch.arange(T, dtype=torch.int32, device=dev), E, out=counts_pre[l:l + 1])
             if l == lp - 1:
                 x_ctx = xn  # normalised input of layer lp-1: context of the boot emission (gate predictor)
+            self._cur_layer = l
             cur = self._layer_compute(cur, xn, ids, gates, self.store.pinned_slot_of[l], bufs, outs[l % 2])
 
         # --- prune (token compression) on the prefix routes, one CTA per request
@@ -353,7 +377,8 @@ class MoEStack:
 
         cfg = c.sim_config()
         prefetching = c.predictor != "none" and c.budget > 0
-        eng = Engine(L, E, cfg, c.num_slabs, lp, 0, prefetching, False, c.compress_ms + (c.bootstrap_ms if prefetching else 0.0))
+        eng = Engine(L, E, cfg, c.num_slabs, lp, c.shared_experts, prefetching, False,
+                     c.compress_ms + (c.bootstrap_ms if prefetching else 0.0))
         scores = {}
 
         def predict(ctx: int, x_in):
@@ -426,7 +451,10 @@ class MoEStack:
             pos=bufs["pos"].data_ptr(), counts=counts.data_ptr(), la_counts=bufs["scratch"].data_ptr(),
             y_dev=bufs["y_dev"].data_ptr(), slot_dev=self.slot_dev.data_ptr(),
             counts_host=self.counts_host.data_ptr(), y_host=self.y_host.data_ptr(),
-            slot_host=self.slot_host.data_ptr())
+            slot_host=self.slot_host.data_ptr(), shared=c.shared_experts,
+            shared_slot_of=st.shared_slot_of.data_ptr() if st.shared_slot_of is not None else None,
+            shared_src=bufs["shared_src"].data_ptr(), shared_off=bufs["shared_off"].data_ptr(),
+            xs=bufs["xs"].data_ptr(), h1s=bufs["h1s"].data_ptr(), ys=bufs["ys"].data_ptr())
         h = C.c_void_p()
         check(self._L.vmm_stack_create(C.byref(d), C.byref(h)))
         nl = l1 - l0

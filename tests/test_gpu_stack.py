@@ -251,3 +251,54 @@ def test_decode_steps_replay_exactly(pred):
         assert got[key] == exp[key], key
     assert got["per_layer"] == exp["per_layer"]
     assert sum(st.copies for st in steps) >= 0
+
+
+def test_shared_experts_decisions_and_data_path():
+    """C4-style layer with 2 always-resident shared experts: decisions equal
+    simulate() with shared_experts=2 (pipeline.py:406,640-641) and the hidden
+    states equal a hand-run of the same kernels with every expert resident."""
+    from paper_2605_05899_b200 import kernels
+    cfg = tiny_cfg(layers=6, experts=16, k=4, inter=512, l_pinned=2, num_slabs=40, routing="trace",
+                   predictor="history", shared_experts=2)
+    tr = generate_trace(TraceGenConfig(n_visual=300, n_text=20, layers=6, experts=16, k=4, cluster_support=6,
+                                       visual_noise=0.3, seed=8, shared_experts=2))
+    stack = MoEStack(cfg)
+    x, sal, mod, dtr = request(tr, cfg.hidden, seed=6)
+    res = stack.forward(x, sal, mod, trace=dtr)
+    sim = cfg.sim_config()
+    plan = build_plan(tr, sim, CompressionConfig(cfg.alpha, cfg.beta, cfg.lam, tuple(range(cfg.l_pinned))))
+    rep = simulate(tr, plan, sim).to_dict()
+    got = res.report.to_dict()
+    for key in _F:
+        assert got[key] == rep[key], key
+    # hand-run with every routed expert resident
+    st = stack.store
+    E, S = cfg.experts, cfg.shared_experts
+    full = torch.cat([st.pool[(l % st.host_layers) * E:(l % st.host_layers + 1) * E] for l in range(cfg.layers)])
+    arena = torch.cat([full.cuda(), st.arena[st.shared_slot_of[0, 0]:]])  # routed slots 0..L*E-1, then shared
+    shared0 = cfg.layers * E
+    routes = dtr["routes"]
+    gts = dtr["gates"]
+    cur = x
+    rows = torch.arange(tr.num_tokens, dtype=torch.int32, device="cuda")
+    ret = torch.from_numpy(res.retained.astype(np.int32)).cuda()
+    for l in range(cfg.layers):
+        if l == cfg.l_pinned:
+            cur = kernels.gather_rows(cur, ret)
+            rows = ret
+        N = int(cur.shape[0])
+        xn = kernels.rmsnorm(cur)
+        ids = routes[l].index_select(0, rows.long()).contiguous()
+        gates = gts[l].index_select(0, rows.long()).contiguous()
+        off, src, pos = kernels.permute_plan(ids, E)
+        xp = kernels.permute_rows(xn, src, N * cfg.k)
+        _, y = kernels.grouped_swiglu(xp, off, arena, torch.arange(l * E, (l + 1) * E, dtype=torch.int32,
+                                                                   device="cuda"), cfg.inter)
+        ssrc = torch.arange(N, dtype=torch.int32, device="cuda").repeat(S)
+        soff = torch.tensor([s * N for s in range(S + 1)], dtype=torch.int32, device="cuda")
+        xs = kernels.permute_rows(xn, ssrc, N * S)
+        _, ys = kernels.grouped_swiglu(xs, soff, arena, torch.arange(shared0 + l * S, shared0 + (l + 1) * S,
+                                                                     dtype=torch.int32, device="cuda"), cfg.inter)
+        cur = kernels.combine_shared(y, pos, gates, cur, ys, S)
+    torch.cuda.synchronize()
+    assert torch.equal(res.hidden, cur)
