@@ -40,6 +40,8 @@ def parse():
     p.add_argument("--routing", default="live", choices=["live", "trace"])
     p.add_argument("--predictor", default=None)
     p.add_argument("--requests", type=int, default=1, help="requests per GPU per step (C5 batch sweep)")
+    p.add_argument("--source", default="host", choices=["host", "sharded"],
+                   help="miss source: pinned host pool over PCIe, or HBM home copies sharded over the GPUs (NVLink)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--out", default=None)
     return p.parse_args()
@@ -200,8 +202,15 @@ def main():
     from paper_2605_05899_b200.trace import generate_trace
 
     predictor = a.predictor or ("gate" if a.routing == "live" else "oracle")
-    cfg = StackConfig.from_workload(w, routing=a.routing, predictor=predictor, host_layers=8)
-    stack = MoEStack(cfg, seed=1000 + rank)
+    from paper_2605_05899_b200.moe import ExpertStore, ShardedHome
+
+    kw = dict(routing=a.routing, predictor=predictor, host_layers=8)
+    if a.source == "sharded":  # logical clock: one slot over NVLink (770 GB/s measured peer copy) or local D2D
+        kw["transfer_ms"] = w.expert_bytes / (770e9 if world > 1 else 3000e9) * 1e3
+    cfg = StackConfig.from_workload(w, **kw)
+    store = ExpertStore(cfg, seed=1000 + rank)
+    home = ShardedHome(store, rank, world) if a.source == "sharded" else None
+    stack = MoEStack(cfg, store=store, home=home)
     R = a.requests
     tr = generate_trace(w.trace_config(seed=rank * R))
     T1 = tr.num_tokens
@@ -308,7 +317,7 @@ def main():
         tj = json.load(open(tpath)).get(f"{w.name}/R{a.requests}")
         traffic = tj["dram_bytes_per_launch"] if tj else None
     res0 = results[-1][0]
-    h2d_peak = measure_h2d_peak(torch, dev)
+    h2d_peak = measure_h2d_peak(torch, dev) if a.source == "host" else (770.0 if world > 1 else None)
     h2d_bytes = res0.h2d_bytes
     rep = res0.report
     h2d_gbs = h2d_bytes / (ms * 1e-3) / 1e9
@@ -340,13 +349,17 @@ def main():
             "config": {"workload": w.name, "tokens": T, "layers": w.layers, "hidden": w.hidden, "experts": w.experts,
                        "top_k": w.k, "moe_inter": w.inter, "l_pinned": w.l_pinned, "num_slabs": w.num_slabs,
                        "routing": a.routing, "predictor": f"{predictor} B={w.budget} W={w.window}",
+                       "miss_source": a.source,
                        "parallelism": f"dp{world} (requests)", "requests_per_gpu_step": R,
                        "l2": "flushed (256 MB write) between timed steps"},
             "hit_rate": rep.hit_rate, "hits": rep.hits, "misses": rep.misses, "evictions": rep.evictions,
             "retained_tokens": int(res0.hidden.shape[0]),
             "h2d": {"gbs": h2d_gbs, "bytes_per_step": h2d_bytes, "copies_per_step": res0.copies,
                     "peak_gbs": h2d_peak, "frac": h2d_gbs / h2d_peak if h2d_peak else None,
-                    "peak_source": "measured pinned 1 GiB H2D in this run"},
+                    "link": "PCIe (pinned host pool)" if a.source == "host" else
+                            ("NVLink P2P + local D2D (sharded HBM home copies)" if world > 1 else "local D2D (HBM home)"),
+                    "peak_source": "measured pinned 1 GiB H2D in this run" if a.source == "host" else
+                                   "B200_PROFILING.md measured peer copy 770 GB/s"},
             "roofline": {"bound": bound, "kernel": "grouped_swiglu (tcgen05 GEMM1+GEMM2 per post-prefix layer)",
                          "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
                          "traffic": traffic, "launch_ms": float(np.mean(durs)),

@@ -279,6 +279,15 @@ int vmm_xfer_fence(vmm_xfer *x, const int32_t *h_slabs, int n, void *compute_str
 /* record the compute event closing the reads registered since the last call */
 int vmm_xfer_layer_done(vmm_xfer *x, int layer, void *compute_stream);
 int vmm_xfer_reset_stats(vmm_xfer *x);
+/* per-(layer, expert) source pointers [L*E] (sharded mode: local or IPC-mapped
+ * peer HBM home copies).  vmm_xfer_issue_engine with h_pool == NULL uses them. */
+int vmm_xfer_set_sources(vmm_xfer *x, const void *const *h_table, long long n);
+/* sharded expert cache plumbing: export / map a device allocation across
+ * processes (64-byte handle) and enable peer access over NVLink */
+int vmm_ipc_get(const void *d_ptr, void *h_handle64);
+int vmm_ipc_open(const void *h_handle64, void **d_ptr);
+int vmm_ipc_close(void *d_ptr);
+int vmm_peer_enable(int peer);
 /* drain the engine's transfer commands and enqueue each as one copy of
  * slot_bytes from the pinned host pool slot ((layer % host_layers)*experts +
  * expert) into arena slot (slab_offset + slab) */

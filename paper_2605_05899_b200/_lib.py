@@ -126,6 +126,11 @@ _SIGS = {
     "vmm_xfer_issue_engine": (I32, [P, P, P, I32, I32, P, I64, SZ, PI32]),
     "vmm_combine_shared": (I32, [P, P, P, P, I32, I32, I32, P, I32, P, P]),
     "vmm_shared_plan": (I32, [I32, I32, P, P, P]),
+    "vmm_xfer_set_sources": (I32, [P, P, I64]),
+    "vmm_ipc_get": (I32, [P, P]),
+    "vmm_ipc_open": (I32, [P, C.POINTER(P)]),
+    "vmm_ipc_close": (I32, [P]),
+    "vmm_peer_enable": (I32, [I32]),
     "vmm_gather_i32": (I32, [P, P, I32, I32, P, P]),
     "vmm_gather_f32": (I32, [P, P, I32, I32, P, P]),
     "vmm_stack_create": (I32, [C.POINTER(StackDesc), C.POINTER(P)]),

@@ -1,6 +1,7 @@
 // Error plumbing and device checks for the C-ABI (include/vismmoe.h).
 #include <cuda_runtime.h>
 
+#include <cstring>
 #include <string>
 
 #include "../../include/vismmoe.h"
@@ -27,6 +28,45 @@ int vmm_device_check(int dev) {
   if (p.major != 10 || p.minor != 0)
     return vmm::fail(VMM_ECUDA, "libvismmoe is built for sm_100a (B200); found sm_" + std::to_string(p.major) +
                                     std::to_string(p.minor));
+  return VMM_OK;
+}
+
+// ---- sharded expert cache plumbing: IPC-mapped peer HBM + peer access ----
+int vmm_ipc_get(const void *d_ptr, void *h_handle64) {
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void *>(d_ptr));
+  if (e != cudaSuccess) return vmm::fail(VMM_ECUDA, std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
+  static_assert(sizeof(h) == 64, "ipc handle size");
+  memcpy(h_handle64, &h, sizeof(h));
+  return VMM_OK;
+}
+
+int vmm_ipc_open(const void *h_handle64, void **d_ptr) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, h_handle64, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return vmm::fail(VMM_ECUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+  return VMM_OK;
+}
+
+int vmm_ipc_close(void *d_ptr) {
+  cudaError_t e = cudaIpcCloseMemHandle(d_ptr);
+  if (e != cudaSuccess) return vmm::fail(VMM_ECUDA, std::string("cudaIpcCloseMemHandle: ") + cudaGetErrorString(e));
+  return VMM_OK;
+}
+
+int vmm_peer_enable(int peer) {
+  int dev = 0, can = 0;
+  cudaGetDevice(&dev);
+  if (peer == dev) return VMM_OK;
+  cudaDeviceCanAccessPeer(&can, dev, peer);
+  if (!can) return vmm::fail(VMM_ECUDA, "no peer access to device " + std::to_string(peer));
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return VMM_OK;
+  }
+  if (e != cudaSuccess) return vmm::fail(VMM_ECUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
   return VMM_OK;
 }
 

@@ -42,6 +42,7 @@ struct vmm_xfer {
   long long copies = 0;
   cudaEvent_t t_first = nullptr, t_last = nullptr;
   bool timing_started = false;
+  std::vector<const void *> sources;  // optional per-(layer, expert) source pointers (sharded mode)
 };
 
 extern "C" {
@@ -94,7 +95,9 @@ int vmm_xfer_copy(vmm_xfer *x, int slab, const void *h_src, void *d_dst, size_t 
     cudaEventRecord(x->t_first, x->stream);
     x->timing_started = true;
   }
-  if ((e = cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyHostToDevice, x->stream)) != cudaSuccess)
+  // cudaMemcpyDefault: pinned host pool (PCIe), local HBM home copy (D2D) or a
+  // peer GPU's HBM home copy (NVLink P2P) -- UVA resolves the direction
+  if ((e = cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyDefault, x->stream)) != cudaSuccess)
     return cuda_status(e, "expert copy");
   x->fill_seq++;
   if ((e = cudaEventRecord(x->fill_ev[(x->fill_seq - 1) % kRing], x->stream)) != cudaSuccess)
@@ -163,6 +166,11 @@ int vmm_xfer_reset_stats(vmm_xfer *x) {
 
 void *vmm_xfer_stream(vmm_xfer *x) { return (void *)x->stream; }
 
+int vmm_xfer_set_sources(vmm_xfer *x, const void *const *h_table, long long n) {
+  x->sources.assign(h_table, h_table + n);
+  return VMM_OK;
+}
+
 int vmm_engine_copies(vmm_engine *e, int32_t *out, int cap);
 
 int vmm_xfer_issue_engine(vmm_xfer *x, vmm_engine *e, const void *h_pool, int host_layers, int experts,
@@ -174,7 +182,8 @@ int vmm_xfer_issue_engine(vmm_xfer *x, vmm_engine *e, const void *h_pool, int ho
     if (n <= 0) break;
     for (int i = 0; i < n; ++i) {
       int layer = buf[3 * i], expert = buf[3 * i + 1], slab = buf[3 * i + 2];
-      const char *src = (const char *)h_pool + ((size_t)(layer % host_layers) * experts + expert) * slot_bytes;
+      const char *src = h_pool ? (const char *)h_pool + ((size_t)(layer % host_layers) * experts + expert) * slot_bytes
+                               : (const char *)x->sources.at((size_t)layer * experts + expert);
       char *dst = (char *)d_arena + (size_t)(slab_offset + slab) * slot_bytes;
       int st = vmm_xfer_copy(x, slab, src, dst, slot_bytes, 0);
       if (st) return st;

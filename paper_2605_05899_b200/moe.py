@@ -206,19 +206,79 @@ class DecodeResult:
     scores: dict = None             # context layer -> predictor y of this step's emissions
 
 
+class ShardedHome:
+    """Home copies of every expert sharded over the ranks' HBM (SURVEY §8(e)
+    mode "sharded cache"): expert (l, e) lives on rank e % world.  A cache miss
+    on any rank is one copy-engine pull of the 9.44 MB slot from its home --
+    local D2D, or a peer GPU's HBM over NVLink (IPC-mapped, peer access
+    enabled) -- instead of a PCIe transfer from the pinned host pool.  No
+    collective on the critical path; one handle exchange at setup."""
+
+    def __init__(self, store: ExpertStore, rank: int = 0, world: int = 1):
+        import torch.distributed as dist
+
+        c = store.cfg
+        E, L = c.experts, c.layers
+        self.rank, self.world = rank, world
+        self.per = -(-E // world)
+        dev = store.device
+        self.arena = torch.empty((L * self.per, c.slot_elems), dtype=torch.bfloat16, device=dev)
+        mine = [e for e in range(E) if e % world == rank]
+        for l in range(L):
+            h = l % store.host_layers
+            rows = torch.tensor([h * E + e for e in mine], dtype=torch.long)
+            self.arena[l * self.per: l * self.per + len(mine)].copy_(store.pool.index_select(0, rows).to(dev))
+        torch.cuda.synchronize(dev)
+        L_ = _lib.lib()
+        bases = [self.arena.data_ptr()]
+        self._opened = []
+        if world > 1:
+            hdl = (C.c_char * 64)()
+            check(L_.vmm_ipc_get(self.arena.data_ptr(), hdl))
+            handles = [None] * world
+            dist.all_gather_object(handles, bytes(hdl))
+            bases = []
+            for r in range(world):
+                if r == rank:
+                    bases.append(self.arena.data_ptr())
+                    continue
+                check(L_.vmm_peer_enable(r))  # one process per GPU on one node: rank r <-> device r
+                p = C.c_void_p()
+                buf = (C.c_char * 64).from_buffer_copy(handles[r])
+                check(L_.vmm_ipc_open(buf, C.byref(p)))
+                self._opened.append(p.value)
+                bases.append(p.value)
+        self.table = np.zeros(L * E, dtype=np.uint64)
+        for l in range(L):
+            for e in range(E):
+                self.table[l * E + e] = bases[e % world] + (l * self.per + e // world) * c.slot_bytes
+
+    def close(self):
+        L_ = _lib.lib()
+        for p in self._opened:
+            L_.vmm_ipc_close(p)
+        self._opened = []
+
+
 class MoEStack:
     """One-request-at-a-time VL-MoE layer stack with the offloaded expert cache."""
 
-    def __init__(self, cfg: StackConfig, store: ExpertStore | None = None, seed: int = 0):
+    def __init__(self, cfg: StackConfig, store: ExpertStore | None = None, seed: int = 0,
+                 home: ShardedHome | None = None):
+        """home=None: misses are served from the pinned host pool over PCIe;
+        home=ShardedHome(...): from the sharded HBM home copies (D2D / NVLink)."""
         if cfg.predictor == "oracle" and cfg.routing != "trace":
             raise ValidationError("the oracle predictor needs trace routing (future routes)")
         self.cfg = cfg
         self.store = store or ExpertStore(cfg, seed)
         self.device = self.store.device
+        self.home = home
         self._L = _lib.lib()
         h = C.c_void_p()
         check(self._L.vmm_xfer_create(cfg.num_slabs, cfg.slot_bytes, cfg.layers, C.byref(h)))
         self._x = h
+        if home is not None:
+            check(self._L.vmm_xfer_set_sources(h, home.table.ctypes.data, len(home.table)))
         E, L = cfg.experts, cfg.layers
         self.slot_host = torch.zeros((L, E), dtype=torch.int32, pin_memory=True)
         self.slot_dev = torch.zeros((L, E), dtype=torch.int32, device=self.device)
@@ -438,7 +498,8 @@ class MoEStack:
             n_pinned_slots=st.n_pinned_slots, n_slots=int(st.arena.shape[0]), slot_bytes=c.slot_bytes,
             host_layers=st.host_layers, cap_rows=int(bufs["n"]), routing=int(c.routing == "trace"), predictor=pred,
             counts_preset=int(oracle_table is not None and c.routing == "trace"),
-            arena=st.arena.data_ptr(), pool=st.pool.data_ptr(), router=st.router.data_ptr(),
+            arena=st.arena.data_ptr(), pool=st.pool.data_ptr() if self.home is None else None,
+            router=st.router.data_ptr(),
             pinned_slot_of=st.pinned_slot_of.data_ptr() if st.pinned_slot_of is not None else None,
             layer_ids=self.layer_ids.data_ptr(), pow_table=self.pow.data_ptr(),
             oracle_table=oracle_table.data_ptr() if oracle_table is not None else None,
@@ -533,7 +594,8 @@ class MoEStack:
 
     def _issue(self, eng: Engine) -> int:
         n = C.c_int()
-        check(self._L.vmm_xfer_issue_engine(self._x, eng._h, self.store.pool.data_ptr(), self.store.host_layers,
+        pool = self.store.pool.data_ptr() if self.home is None else None
+        check(self._L.vmm_xfer_issue_engine(self._x, eng._h, pool, self.store.host_layers,
                                             self.cfg.experts, self.store.arena.data_ptr(),
                                             self.store.n_pinned_slots, self.cfg.slot_bytes, C.byref(n)))
         return n.value

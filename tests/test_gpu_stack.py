@@ -302,3 +302,23 @@ def test_shared_experts_decisions_and_data_path():
         cur = kernels.combine_shared(y, pos, gates, cur, ys, S)
     torch.cuda.synchronize()
     assert torch.equal(res.hidden, cur)
+
+
+def test_sharded_home_mode_bit_identical_to_host_pool_mode():
+    """Misses served from the HBM home copies (sharded mode, world=1 -> local
+    D2D pulls) give the same decisions and bit-identical hidden states as the
+    pinned-host-pool mode."""
+    from paper_2605_05899_b200.moe import ShardedHome
+    cfg = tiny_cfg(routing="live", predictor="gate")
+    store = ExpertStore(cfg, seed=3)
+    tr = small_trace(cfg, seed=31)
+    x, sal, mod, _ = request(tr, cfg.hidden, seed=5)
+    a = MoEStack(cfg, store=store).forward(x, sal, mod)
+    torch.cuda.synchronize()
+    ha = a.hidden.clone()
+    home = ShardedHome(store, 0, 1)
+    b = MoEStack(cfg, store=store, home=home).forward(x, sal, mod)
+    torch.cuda.synchronize()
+    assert b.copies == a.copies > 0
+    assert b.report.to_dict() == a.report.to_dict()
+    assert torch.equal(b.hidden, ha)
