@@ -275,11 +275,13 @@ def main():
     # warm-up
     timed(a.warmup)
     barrier()
-    launches0 = kernels.LAUNCHES[0]
+    from paper_2605_05899_b200 import _lib as vlib
+
+    launches0 = vlib.load().vmm_launch_count()
     with ClockSampler(os.path.join(ROOT, "gpurun_out", f"clocks_rank{rank}.csv")
                       if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else "/tmp/clocks.csv") as clk:
         times, results = timed(a.steps, prof=True)
-    launches = (kernels.LAUNCHES[0] - launches0) // max(a.steps, 1)
+    launches = (vlib.load().vmm_launch_count() - launches0) // max(a.steps, 1)
     e2e_times, e2e_results = timed(a.steps, e2e=True)
 
     def max_over_ranks(v):

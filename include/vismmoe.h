@@ -40,6 +40,8 @@ extern "C" {
 
 const char *vmm_last_error(void);
 int vmm_abi_version(void);
+/* number of kernels this library has launched in the process (all entry points) */
+long long vmm_launch_count(void);
 /* 0 if device `dev` is sm_100 and the kernels of this library can run there */
 int vmm_device_check(int dev);
 

@@ -68,6 +68,7 @@ class StackOut(C.Structure):
 _SIGS = {
     "vmm_last_error": (C.c_char_p, []),
     "vmm_abi_version": (I32, []),
+    "vmm_launch_count": (I64, []),
     "vmm_device_check": (I32, [I32]),
     "vmm_prune": (I32, [P, P, P, P, P, P, I32, I32, I32, I32, I32, F64, P, P, P, P, P, P, P, P, P]),
     "vmm_gather_rows": (I32, [P, P, I32, I32, P, P]),

@@ -6,7 +6,11 @@
 
 #include "../../include/vismmoe.h"
 
+#include <atomic>
+
 namespace vmm {
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 static thread_local std::string g_err;
 void set_error(const std::string &msg) { g_err = msg; }
 int fail(int code, const std::string &msg) {
@@ -20,6 +24,8 @@ extern "C" {
 const char *vmm_last_error(void) { return vmm::g_err.c_str(); }
 
 int vmm_abi_version(void) { return 1; }
+
+long long vmm_launch_count(void) { return vmm::g_launches.load(std::memory_order_relaxed); }
 
 int vmm_device_check(int dev) {
   cudaDeviceProp p;

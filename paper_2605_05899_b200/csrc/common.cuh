@@ -18,10 +18,14 @@ inline int cuda_status(cudaError_t e, const char *what) {
   return fail(VMM_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// every kernel launch of the library goes through this macro: it checks the
+// launch and counts it (vmm_launch_count, the bench's gpu_launches evidence)
+void count_launch();
 #define VMM_LAUNCH_CHECK(what)                                   \
   do {                                                           \
     cudaError_t _e = cudaGetLastError();                         \
     if (_e != cudaSuccess) return ::vmm::cuda_status(_e, what);  \
+    ::vmm::count_launch();                                       \
   } while (0)
 
 // Total order on doubles as unsigned keys: a < b  <=>  ord(a) < ord(b)
