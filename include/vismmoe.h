@@ -136,6 +136,11 @@ int vmm_permute_rows(const void *d_x, const int32_t *d_src_row, int n_rows, int 
 /* combine plus S always-resident shared experts (unit weight; rows s*N + t of d_ys) */
 int vmm_combine_shared(const void *d_y, const int32_t *d_pos, const float *d_gates, const void *d_resid,
                        int N, int k, int H, const void *d_ys, int S, void *d_out, void *stream);
+/* fused combine (+ shared experts, S may be 0) and the next layer's RMSNorm:
+ * bit-identical to vmm_combine_shared followed by vmm_rmsnorm(w = NULL) */
+int vmm_combine_norm(const void *d_y, const int32_t *d_pos, const float *d_gates, const void *d_resid,
+                     int N, int k, int H, const void *d_ys, int S, float eps, void *d_out, void *d_xn,
+                     void *stream);
 /* shared-expert plan: src[s*N + t] = t, offsets[s] = s*N (every token to each shared expert) */
 int vmm_shared_plan(int N, int S, int32_t *d_src, int32_t *d_offsets, void *stream);
 /* Pre-MoE RMSNorm of the token rows (the layer's router and experts see the

@@ -127,6 +127,7 @@ _SIGS = {
     "vmm_xfer_issue_engine": (I32, [P, P, P, I32, I32, P, I64, SZ, PI32]),
     "vmm_combine_shared": (I32, [P, P, P, P, I32, I32, I32, P, I32, P, P]),
     "vmm_shared_plan": (I32, [I32, I32, P, P, P]),
+    "vmm_combine_norm": (I32, [P, P, P, P, I32, I32, I32, P, I32, C.c_float, P, P, P]),
     "vmm_xfer_set_sources": (I32, [P, P, I64]),
     "vmm_ipc_get": (I32, [P, P]),
     "vmm_ipc_open": (I32, [P, C.POINTER(P)]),

@@ -214,6 +214,103 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_cons
   }
 }
 
+
+// ---- decode-sized batches: weight-streaming SwiGLU on CUDA cores -----------
+// With <= kSkinnyRows rows in the whole layer (one decode token: k rows) the
+// tensor-core tiles would be >90% padding and a 128x128 tile loop per expert is
+// latency-bound.  Instead every warp owns one output feature of one expert and
+// streams that feature's weight rows once (16-byte vector loads, coalesced),
+// dotting them with the expert's few token rows held in L1/L2.  HBM-bound on
+// the demanded experts' weights, spread over all SMs.
+constexpr int kSkinnyRows = 16;
+
+__global__ void skinny_gateup_kernel(const __nv_bfloat16 *__restrict__ xp, const int32_t *__restrict__ offsets,
+                                     const int32_t *__restrict__ slot_of, const __nv_bfloat16 *__restrict__ w13,
+                                     long long stride, int H, int I, __nv_bfloat16 *__restrict__ h1) {
+  const int e = blockIdx.y;
+  const int r0 = offsets[e], r1 = offsets[e + 1];
+  if (r1 <= r0) return;
+  const int f = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // output feature
+  const int lane = threadIdx.x & 31;
+  if (f >= I) return;
+  const __nv_bfloat16 *w = w13 + (long long)slot_of[e] * stride;
+  const int grow = (f >> 6) * 128 + (f & 63);  // interleaved 64|64 gate/up blocks
+  const uint4 *wg = reinterpret_cast<const uint4 *>(w + (long long)grow * H);
+  const uint4 *wu = reinterpret_cast<const uint4 *>(w + (long long)(grow + 64) * H);
+  const int nv = H / 8, nr = r1 - r0;
+  float ag[kSkinnyRows], au[kSkinnyRows];
+#pragma unroll
+  for (int m = 0; m < kSkinnyRows; ++m) { ag[m] = 0.f; au[m] = 0.f; }
+  for (int c = lane; c < nv; c += 32) {
+    uint4 gv = __ldg(wg + c), uv = __ldg(wu + c);
+    const __nv_bfloat16 *gh = reinterpret_cast<const __nv_bfloat16 *>(&gv);
+    const __nv_bfloat16 *uh = reinterpret_cast<const __nv_bfloat16 *>(&uv);
+#pragma unroll
+    for (int m = 0; m < kSkinnyRows; ++m) {
+      if (m < nr) {
+        uint4 xv = __ldg(reinterpret_cast<const uint4 *>(xp + (long long)(r0 + m) * H) + c);
+        const __nv_bfloat16 *xh = reinterpret_cast<const __nv_bfloat16 *>(&xv);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float xf = __bfloat162float(xh[q]);
+          ag[m] = fmaf(xf, __bfloat162float(gh[q]), ag[m]);
+          au[m] = fmaf(xf, __bfloat162float(uh[q]), au[m]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < kSkinnyRows; ++m) {
+    if (m < nr) {
+      float g = ag[m], u = au[m];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        g += __shfl_xor_sync(0xffffffffu, g, o);
+        u += __shfl_xor_sync(0xffffffffu, u, o);
+      }
+      if (lane == 0) h1[(long long)(r0 + m) * I + f] = __float2bfloat16(silu(g) * u);
+    }
+  }
+}
+
+__global__ void skinny_down_kernel(const __nv_bfloat16 *__restrict__ h1, const int32_t *__restrict__ offsets,
+                                   const int32_t *__restrict__ slot_of, const __nv_bfloat16 *__restrict__ w2,
+                                   long long stride, int H, int I, __nv_bfloat16 *__restrict__ y) {
+  const int e = blockIdx.y;
+  const int r0 = offsets[e], r1 = offsets[e + 1];
+  if (r1 <= r0) return;
+  const int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // output column
+  const int lane = threadIdx.x & 31;
+  if (n >= H) return;
+  const uint4 *wr = reinterpret_cast<const uint4 *>(w2 + (long long)slot_of[e] * stride + (long long)n * I);
+  const int nv = I / 8, nr = r1 - r0;
+  float acc[kSkinnyRows];
+#pragma unroll
+  for (int m = 0; m < kSkinnyRows; ++m) acc[m] = 0.f;
+  for (int c = lane; c < nv; c += 32) {
+    uint4 wv = __ldg(wr + c);
+    const __nv_bfloat16 *wh = reinterpret_cast<const __nv_bfloat16 *>(&wv);
+#pragma unroll
+    for (int m = 0; m < kSkinnyRows; ++m) {
+      if (m < nr) {
+        uint4 hv = __ldg(reinterpret_cast<const uint4 *>(h1 + (long long)(r0 + m) * I) + c);
+        const __nv_bfloat16 *hh = reinterpret_cast<const __nv_bfloat16 *>(&hv);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[m] = fmaf(__bfloat162float(hh[q]), __bfloat162float(wh[q]), acc[m]);
+      }
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < kSkinnyRows; ++m) {
+    if (m < nr) {
+      float v = acc[m];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) y[(long long)(r0 + m) * H + n] = __float2bfloat16(v);
+    }
+  }
+}
+
 // ---- CUDA-core cross-check path -------------------------------------------
 __device__ __forceinline__ int expert_of_row(const int32_t *offsets, int E, int row) {
   int lo = 0, hi = E - 1;
@@ -267,6 +364,20 @@ extern "C" int vmm_grouped_swiglu(const void *d_xp, const int32_t *d_offsets, in
     return vmm::fail(VMM_EVALIDATION, "grouped_swiglu: hidden must be a multiple of 128, inter of 64");
   if (E < 1 || E > VMM_MAX_EXPERTS) return vmm::fail(VMM_EVALIDATION, "experts must lie in [1, 256]");
   if (slot_stride % 8) return vmm::fail(VMM_EVALIDATION, "slot stride must be a multiple of 8 elements");
+  if (M_total <= kSkinnyRows) {  // decode-sized layer: every expert has <= 16 rows
+    cudaStream_t s = (cudaStream_t)stream;
+    constexpr int kWarps = 8;
+    dim3 g1((I + kWarps - 1) / kWarps, E), g2((H + kWarps - 1) / kWarps, E);
+    skinny_gateup_kernel<<<g1, 32 * kWarps, 0, s>>>((const __nv_bfloat16 *)d_xp, d_offsets, d_slot_of_expert,
+                                                     (const __nv_bfloat16 *)d_w13_arena, slot_stride, H, I,
+                                                     (__nv_bfloat16 *)d_h1);
+    VMM_LAUNCH_CHECK("skinny_gateup_kernel");
+    skinny_down_kernel<<<g2, 32 * kWarps, 0, s>>>((const __nv_bfloat16 *)d_h1, d_offsets, d_slot_of_expert,
+                                                   (const __nv_bfloat16 *)d_w2_arena, slot_stride, H, I,
+                                                   (__nv_bfloat16 *)d_y);
+    VMM_LAUNCH_CHECK("skinny_down_kernel");
+    return VMM_OK;
+  }
   static bool attr = false;
   if (!attr) {
     cudaError_t e1 = cudaFuncSetAttribute(grouped_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -291,3 +291,84 @@ extern "C" int vmm_gather_f32(const float *d_src, const int32_t *d_rows, int n, 
   VMM_LAUNCH_CHECK("gather_elems_kernel<f32>");
   return VMM_OK;
 }
+
+namespace {
+// Fused combine + next layer's RMSNorm: one warp per token row.  out = resid +
+// sum_j g_j Y[pos_j] (+ shared rows), rounded to bf16; then xn = out * rsqrt(
+// mean(out^2) + eps) from the ROUNDED values with the same lane->chunk order as
+// rmsnorm_kernel, so the result is bit-identical to combine followed by rmsnorm.
+constexpr int kRowVecMax = 64;  // H <= 64*32*8 = 16384
+__global__ void combine_norm_kernel(const uint4 *__restrict__ y, const int32_t *__restrict__ pos,
+                                    const float *__restrict__ gates, const uint4 *__restrict__ resid, int N, int k,
+                                    int row_vec, const uint4 *__restrict__ ys, int S, float eps,
+                                    uint4 *__restrict__ out, uint4 *__restrict__ xn) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = warp; t < N; t += nw) {
+    uint4 o[kRowVecMax / 32];
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < kRowVecMax / 32; ++i) {
+      const int c = lane + 32 * i;
+      if (c >= row_vec) break;
+      float acc[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+      for (int j = 0; j < k; ++j) {
+        float g = gates[(long long)t * k + j];
+        uint4 v = __ldg(y + (long long)pos[(long long)t * k + j] * row_vec + c);
+        const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&v);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = fmaf(g, __bfloat162float(h[q]), acc[q]);
+      }
+      for (int sx = 0; sx < S; ++sx) {
+        uint4 v = __ldg(ys + ((long long)sx * N + t) * row_vec + c);
+        const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&v);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] += __bfloat162float(h[q]);
+      }
+      uint4 rv = __ldg(resid + (long long)t * row_vec + c);
+      const __nv_bfloat16 *rh = reinterpret_cast<const __nv_bfloat16 *>(&rv);
+      __nv_bfloat16 *oh = reinterpret_cast<__nv_bfloat16 *>(&o[i]);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        oh[q] = __float2bfloat16(__bfloat162float(rh[q]) + acc[q]);
+        float f = __bfloat162float(oh[q]);
+        ss = fmaf(f, f, ss);
+      }
+      out[(long long)t * row_vec + c] = o[i];
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    const float inv = rsqrtf(ss / (float)(row_vec * 8) + eps);
+#pragma unroll
+    for (int i = 0; i < kRowVecMax / 32; ++i) {
+      const int c = lane + 32 * i;
+      if (c >= row_vec) break;
+      const __nv_bfloat16 *oh = reinterpret_cast<const __nv_bfloat16 *>(&o[i]);
+      uint4 nv;
+      __nv_bfloat16 *nh = reinterpret_cast<__nv_bfloat16 *>(&nv);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) nh[q] = __float2bfloat16(__bfloat162float(oh[q]) * inv);
+      xn[(long long)t * row_vec + c] = nv;
+    }
+  }
+}
+}  // namespace
+
+extern "C" int vmm_combine_norm(const void *d_y, const int32_t *d_pos, const float *d_gates, const void *d_resid,
+                                int N, int k, int H, const void *d_ys, int S, float eps, void *d_out, void *d_xn,
+                                void *stream) {
+  if (N <= 0) return VMM_OK;
+  if ((H * 2) % 16 || H * 2 / 16 > kRowVecMax) return vmm::fail(VMM_EVALIDATION, "hidden size unsupported");
+  int row_vec = H * 2 / 16;
+  int warps = N < 148 * 32 ? N : 148 * 32;
+  int blocks = (warps * 32 + 255) / 256;
+  combine_norm_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((const uint4 *)d_y, d_pos, d_gates,
+                                                                (const uint4 *)d_resid, N, k, row_vec,
+                                                                (const uint4 *)d_ys, S, eps, (uint4 *)d_out,
+                                                                (uint4 *)d_xn);
+  VMM_LAUNCH_CHECK("combine_norm_kernel");
+  return VMM_OK;
+}

@@ -77,9 +77,10 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
   const void *cur = d_x;
   int ping = 0, copies = 0;
   std::vector<int32_t> demand, slabs;
+  bool have_xn = false;  // the fused combine of the previous layer already produced this layer's xn
   for (int l = l0; l < l1; ++l) {
     void *xn = d.xn;
-    VMM_TRY(vmm_rmsnorm(cur, nullptr, n_rows, H, 1e-6f, xn, stream));
+    if (!have_xn) VMM_TRY(vmm_rmsnorm(cur, nullptr, n_rows, H, 1e-6f, xn, stream));
     const int emits = vmm_engine_emits(eng, l, phase);
     uint32_t *cnt = d.counts + (size_t)l * E;
     bool la_done = false;
@@ -161,14 +162,21 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
                                (long long)3 * I * H, d.n_slots, slot_of, d.h1, d.y, stream));
     if (out && out->ffn_end) VMM_CUDA(cudaEventRecord((cudaEvent_t)out->ffn_end[l - l0], st), "ffn end event");
     void *dst = ping ? d.out1 : d.out0;
-    if (d.shared > 0) {
+    const int S = d.shared;
+    if (S > 0) {
       // always-resident shared experts: every token through each, grouped GEMM over S groups
-      const int S = d.shared, MS = n_rows * S;
+      const int MS = n_rows * S;
       VMM_TRY(vmm_shared_plan(n_rows, S, d.shared_src, d.shared_off, stream));
       VMM_TRY(vmm_permute_rows(xn, d.shared_src, MS, H, d.xs, stream));
       VMM_TRY(vmm_grouped_swiglu(d.xs, d.shared_off, S, MS, H, I, d.arena,
                                  (const char *)d.arena + (size_t)2 * I * H * 2, (long long)3 * I * H, d.n_slots,
                                  d.shared_slot_of + (size_t)l * S, d.h1s, d.ys, stream));
+    }
+    if (l + 1 < l1) {  // combine fused with the next layer's RMSNorm (xn is free again: consumed above)
+      VMM_TRY(vmm_combine_norm(d.y, d.pos, d.gates, cur, n_rows, k, H, S > 0 ? d.ys : nullptr, S, 1e-6f, dst, xn,
+                               stream));
+      have_xn = true;
+    } else if (S > 0) {
       VMM_TRY(vmm_combine_shared(d.y, d.pos, d.gates, cur, n_rows, k, H, d.ys, S, dst, stream));
     } else {
       VMM_TRY(vmm_combine(d.y, d.pos, d.gates, cur, n_rows, k, H, dst, stream));

@@ -132,3 +132,52 @@ def test_skinny_router_decode_sizes_exact(N):
     assert torch.equal(ids2.cpu(), rid)
     nid, _, _ = moe_ref.route(x, router[2], k)
     assert torch.equal(la.cpu().long(), torch.bincount(nid.reshape(-1).long(), minlength=E))
+
+
+@pytest.mark.parametrize("shape", [(1, 2048, 768, 128, 8), (2, 2048, 1408, 64, 6), (1, 2560, 10240, 4, 2)])
+def test_decode_sized_swiglu_matches_fp32_restatement(shape):
+    """M_total <= 16 rows takes the weight-streaming CUDA-core path."""
+    _check_swiglu(shape)
+
+
+def _check_swiglu(shape):
+    N, H, I, E, k = shape
+    n_slots = E + 3
+    x, wg, wu, wd, arena, ids, slot_of = _expert_setup(N, H, I, E, k, n_slots, seed=N + E + 7)
+    off, src, pos = kernels.permute_plan(ids.cuda(), E)
+    M = N * k
+    xp = kernels.permute_rows(x.cuda(), src, M)
+    h1, y = kernels.grouped_swiglu(xp, off, arena.cuda(), slot_of.cuda(), I)
+    roff, rsrc, rpos = moe_ref.permute(ids, E)
+    xr = x[rsrc]
+    y_exp = torch.empty(M, H, dtype=torch.bfloat16)
+    for e in range(E):
+        a, b = int(roff[e]), int(roff[e + 1])
+        if b > a:
+            s = int(slot_of[e])
+            _, y_exp[a:b] = moe_ref.expert_ffn(xr[a:b], wg[s], wu[s], wd[s])
+    torch.testing.assert_close(y.cpu().float(), y_exp.float(), rtol=2e-2, atol=2e-2)
+    rel = (y.cpu().float() - y_exp.float()).norm() / y_exp.float().norm()
+    assert rel.item() <= 5e-3
+
+
+def test_fused_combine_norm_bit_identical_to_combine_then_rmsnorm():
+    g = torch.Generator().manual_seed(4)
+    N, k, H, S = 300, 6, 2048, 2
+    y = torch.randn(N * k, H, generator=g).to(torch.bfloat16).cuda()
+    ys = torch.randn(N * S, H, generator=g).to(torch.bfloat16).cuda()
+    pos = torch.randperm(N * k, generator=g).int().reshape(N, k).cuda()
+    gates = torch.softmax(torch.randn(N, k, generator=g), 1).cuda()
+    resid = torch.randn(N, H, generator=g).to(torch.bfloat16).cuda()
+    for shared in (0, S):
+        ref = kernels.combine_shared(y, pos, gates, resid, ys, shared) if shared else kernels.combine(y, pos, gates, resid)
+        refn = kernels.rmsnorm(ref)
+        out = torch.empty_like(resid)
+        xn = torch.empty_like(resid)
+        from paper_2605_05899_b200 import _lib
+        _lib.check(_lib.lib().vmm_combine_norm(y.data_ptr(), pos.data_ptr(), gates.data_ptr(), resid.data_ptr(), N, k,
+                                               H, ys.data_ptr() if shared else None, shared, 1e-6, out.data_ptr(),
+                                               xn.data_ptr(), torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
+        assert torch.equal(xn, refn)
