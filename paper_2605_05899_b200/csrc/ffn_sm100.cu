@@ -224,12 +224,37 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_cons
 // the demanded experts' weights, spread over all SMs.
 constexpr int kSkinnyRows = 16;
 
+// expert owning "active slot" j (the j-th expert with rows), or -1; warp-collective over E
+__device__ __forceinline__ int jth_active_expert(const int32_t *offsets, int E, int j) {
+  __shared__ int s_e;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int seen = 0, found = -1;
+    for (int c0 = 0; c0 < E && found < 0; c0 += 32) {
+      const int e = c0 + lane;
+      const bool act = e < E && offsets[e + 1] > offsets[e];
+      const unsigned bal = __ballot_sync(0xffffffffu, act);
+      const int cnt = __popc(bal);
+      if (j < seen + cnt) {
+        // position of the (j - seen)-th set bit
+        unsigned b = bal;
+        for (int r = 0; r < j - seen; ++r) b &= b - 1;
+        found = c0 + __ffs(b) - 1;
+      }
+      seen += cnt;
+    }
+    if (lane == 0) s_e = found;
+  }
+  __syncthreads();
+  return s_e;
+}
+
 __global__ void skinny_gateup_kernel(const __nv_bfloat16 *__restrict__ xp, const int32_t *__restrict__ offsets,
-                                     const int32_t *__restrict__ slot_of, const __nv_bfloat16 *__restrict__ w13,
+                                     int E, const int32_t *__restrict__ slot_of, const __nv_bfloat16 *__restrict__ w13,
                                      long long stride, int H, int I, __nv_bfloat16 *__restrict__ h1) {
-  const int e = blockIdx.y;
+  const int e = jth_active_expert(offsets, E, blockIdx.y);
+  if (e < 0) return;
   const int r0 = offsets[e], r1 = offsets[e + 1];
-  if (r1 <= r0) return;
   const int f = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // output feature
   const int lane = threadIdx.x & 31;
   if (f >= I) return;
@@ -274,11 +299,11 @@ __global__ void skinny_gateup_kernel(const __nv_bfloat16 *__restrict__ xp, const
 }
 
 __global__ void skinny_down_kernel(const __nv_bfloat16 *__restrict__ h1, const int32_t *__restrict__ offsets,
-                                   const int32_t *__restrict__ slot_of, const __nv_bfloat16 *__restrict__ w2,
+                                   int E, const int32_t *__restrict__ slot_of, const __nv_bfloat16 *__restrict__ w2,
                                    long long stride, int H, int I, __nv_bfloat16 *__restrict__ y) {
-  const int e = blockIdx.y;
+  const int e = jth_active_expert(offsets, E, blockIdx.y);
+  if (e < 0) return;
   const int r0 = offsets[e], r1 = offsets[e + 1];
-  if (r1 <= r0) return;
   const int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // output column
   const int lane = threadIdx.x & 31;
   if (n >= H) return;
@@ -367,12 +392,13 @@ extern "C" int vmm_grouped_swiglu(const void *d_xp, const int32_t *d_offsets, in
   if (M_total <= kSkinnyRows) {  // decode-sized layer: every expert has <= 16 rows
     cudaStream_t s = (cudaStream_t)stream;
     constexpr int kWarps = 8;
-    dim3 g1((I + kWarps - 1) / kWarps, E), g2((H + kWarps - 1) / kWarps, E);
-    skinny_gateup_kernel<<<g1, 32 * kWarps, 0, s>>>((const __nv_bfloat16 *)d_xp, d_offsets, d_slot_of_expert,
+    // grid.y = active-expert slots (at most M_total experts have rows)
+    dim3 g1((I + kWarps - 1) / kWarps, M_total), g2((H + kWarps - 1) / kWarps, M_total);
+    skinny_gateup_kernel<<<g1, 32 * kWarps, 0, s>>>((const __nv_bfloat16 *)d_xp, d_offsets, E, d_slot_of_expert,
                                                      (const __nv_bfloat16 *)d_w13_arena, slot_stride, H, I,
                                                      (__nv_bfloat16 *)d_h1);
     VMM_LAUNCH_CHECK("skinny_gateup_kernel");
-    skinny_down_kernel<<<g2, 32 * kWarps, 0, s>>>((const __nv_bfloat16 *)d_h1, d_offsets, d_slot_of_expert,
+    skinny_down_kernel<<<g2, 32 * kWarps, 0, s>>>((const __nv_bfloat16 *)d_h1, d_offsets, E, d_slot_of_expert,
                                                    (const __nv_bfloat16 *)d_w2_arena, slot_stride, H, I,
                                                    (__nv_bfloat16 *)d_y);
     VMM_LAUNCH_CHECK("skinny_down_kernel");

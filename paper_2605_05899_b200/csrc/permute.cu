@@ -297,7 +297,7 @@ namespace {
 // sum_j g_j Y[pos_j] (+ shared rows), rounded to bf16; then xn = out * rsqrt(
 // mean(out^2) + eps) from the ROUNDED values with the same lane->chunk order as
 // rmsnorm_kernel, so the result is bit-identical to combine followed by rmsnorm.
-constexpr int kRowVecMax = 64;  // H <= 64*32*8 = 16384
+constexpr int kRowVecMax = 512;  // H <= 512*8 = 4096 (16 x 16-byte vectors per lane)
 __global__ void combine_norm_kernel(const uint4 *__restrict__ y, const int32_t *__restrict__ pos,
                                     const float *__restrict__ gates, const uint4 *__restrict__ resid, int N, int k,
                                     int row_vec, const uint4 *__restrict__ ys, int S, float eps,
