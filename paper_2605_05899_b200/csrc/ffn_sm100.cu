@@ -266,8 +266,20 @@ __global__ void skinny_gateup_kernel(const __nv_bfloat16 *__restrict__ xp, const
   float ag[kSkinnyRows], au[kSkinnyRows];
 #pragma unroll
   for (int m = 0; m < kSkinnyRows; ++m) { ag[m] = 0.f; au[m] = 0.f; }
-  for (int c = lane; c < nv; c += 32) {
-    uint4 gv = __ldg(wg + c), uv = __ldg(wu + c);
+  // issue the lane's weight loads for 4 chunks at once (HBM latency hiding), then use them
+  for (int c0 = lane; c0 < nv; c0 += 32 * 4) {
+    uint4 gvs[4], uvs[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + 32 * u;
+      gvs[u] = c < nv ? __ldg(wg + c) : make_uint4(0, 0, 0, 0);
+      uvs[u] = c < nv ? __ldg(wu + c) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+    const int c = c0 + 32 * u;
+    if (c >= nv) break;
+    uint4 gv = gvs[u], uv = uvs[u];
     const __nv_bfloat16 *gh = reinterpret_cast<const __nv_bfloat16 *>(&gv);
     const __nv_bfloat16 *uh = reinterpret_cast<const __nv_bfloat16 *>(&uv);
 #pragma unroll
@@ -282,6 +294,7 @@ __global__ void skinny_gateup_kernel(const __nv_bfloat16 *__restrict__ xp, const
           au[m] = fmaf(xf, __bfloat162float(uh[q]), au[m]);
         }
       }
+    }
     }
   }
 #pragma unroll
@@ -312,8 +325,15 @@ __global__ void skinny_down_kernel(const __nv_bfloat16 *__restrict__ h1, const i
   float acc[kSkinnyRows];
 #pragma unroll
   for (int m = 0; m < kSkinnyRows; ++m) acc[m] = 0.f;
-  for (int c = lane; c < nv; c += 32) {
-    uint4 wv = __ldg(wr + c);
+  for (int c0 = lane; c0 < nv; c0 += 32 * 4) {
+    uint4 wvs[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) wvs[u] = (c0 + 32 * u) < nv ? __ldg(wr + c0 + 32 * u) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+    const int c = c0 + 32 * u;
+    if (c >= nv) break;
+    uint4 wv = wvs[u];
     const __nv_bfloat16 *wh = reinterpret_cast<const __nv_bfloat16 *>(&wv);
 #pragma unroll
     for (int m = 0; m < kSkinnyRows; ++m) {
@@ -323,6 +343,7 @@ __global__ void skinny_down_kernel(const __nv_bfloat16 *__restrict__ h1, const i
 #pragma unroll
         for (int q = 0; q < 8; ++q) acc[m] = fmaf(__bfloat162float(hh[q]), __bfloat162float(wh[q]), acc[m]);
       }
+    }
     }
   }
 #pragma unroll

@@ -127,37 +127,60 @@ __global__ void combine_kernel(const uint4 *__restrict__ y, const int32_t *__res
   }
 }
 
-// y[r] = x[r] * rsqrt(mean(x[r]^2) + eps) (* w), one warp per row, fp32 statistics
-__global__ void rmsnorm_kernel(const uint4 *__restrict__ x, const __nv_bfloat16 *__restrict__ w, int n, int row_vec,
-                               float eps, uint4 *__restrict__ y) {
-  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int r = warp; r < n; r += nw) {
+// Row statistics shared by rmsnorm and the fused combine+norm: one CTA of
+// kNormThreads threads per row; thread t owns 16-byte chunks t, t+256, ...;
+// fp32 partial sums in chunk order, warp xor-tree, then the 8 warp sums in
+// fixed order -> deterministic and identical in both kernels.
+constexpr int kNormThreads = 256;
+constexpr int kNormChunks = 2;  // chunks per thread: H <= 2*256*8 = 4096
+
+__device__ __forceinline__ float block_row_sum(float v) {
+  __shared__ float s_w[kNormThreads / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float t = 0.f;
+#pragma unroll
+  for (int w = 0; w < kNormThreads / 32; ++w) t += s_w[w];
+  __syncthreads();
+  return t;
+}
+
+// y[r] = x[r] * rsqrt(mean(x[r]^2) + eps) (* w)
+__global__ void __launch_bounds__(kNormThreads)
+rmsnorm_kernel(const uint4 *__restrict__ x, const __nv_bfloat16 *__restrict__ w, int n, int row_vec, float eps,
+               uint4 *__restrict__ y) {
+  for (int r = blockIdx.x; r < n; r += gridDim.x) {
     const uint4 *s = x + (long long)r * row_vec;
+    uint4 v[kNormChunks];
     float ss = 0.f;
-    for (int c = lane; c < row_vec; c += 32) {
-      uint4 v = __ldg(s + c);
-      const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&v);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) { float f = __bfloat162float(h[q]); ss = fmaf(f, f, ss); }
-    }
+    for (int i = 0; i < kNormChunks; ++i) {
+      const int c = threadIdx.x + kNormThreads * i;
+      if (c < row_vec) {
+        v[i] = __ldg(s + c);
+        const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&v[i]);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    const float inv = rsqrtf(ss / (float)(row_vec * 8) + eps);
-    uint4 *d = y + (long long)r * row_vec;
-    for (int c = lane; c < row_vec; c += 32) {
-      uint4 v = __ldg(s + c);
-      const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&v);
-      uint4 o;
-      __nv_bfloat16 *oh = reinterpret_cast<__nv_bfloat16 *>(&o);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        float f = __bfloat162float(h[q]) * inv;
-        if (w) f *= __bfloat162float(w[c * 8 + q]);
-        oh[q] = __float2bfloat16(f);
+        for (int q = 0; q < 8; ++q) { float f = __bfloat162float(h[q]); ss = fmaf(f, f, ss); }
       }
-      d[c] = o;
+    }
+    const float inv = rsqrtf(block_row_sum(ss) / (float)(row_vec * 8) + eps);
+#pragma unroll
+    for (int i = 0; i < kNormChunks; ++i) {
+      const int c = threadIdx.x + kNormThreads * i;
+      if (c < row_vec) {
+        const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&v[i]);
+        uint4 o;
+        __nv_bfloat16 *oh = reinterpret_cast<__nv_bfloat16 *>(&o);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float f = __bfloat162float(h[q]) * inv;
+          if (w) f *= __bfloat162float(w[c * 8 + q]);
+          oh[q] = __float2bfloat16(f);
+        }
+        y[(long long)r * row_vec + c] = o;
+      }
     }
   }
 }
@@ -168,17 +191,51 @@ extern "C" int vmm_rmsnorm(const void *d_x, const void *d_w, int n, int H, float
   if (n <= 0) return VMM_OK;
   if ((H * 2) % 16) return vmm::fail(VMM_EVALIDATION, "hidden size must be a multiple of 8");
   int row_vec = H * 2 / 16;
-  int warps = n < 148 * 32 ? n : 148 * 32;
-  int blocks = (warps * 32 + 255) / 256;
-  rmsnorm_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((const uint4 *)d_x, (const __nv_bfloat16 *)d_w, n, row_vec,
-                                                           eps, (uint4 *)d_y);
+  if (row_vec > kNormThreads * kNormChunks) return vmm::fail(VMM_EVALIDATION, "hidden size above 4096");
+  int blocks = n < 148 * 16 ? n : 148 * 16;
+  rmsnorm_kernel<<<blocks, kNormThreads, 0, (cudaStream_t)stream>>>((const uint4 *)d_x, (const __nv_bfloat16 *)d_w, n,
+                                                                    row_vec, eps, (uint4 *)d_y);
   VMM_LAUNCH_CHECK("rmsnorm_kernel");
   return VMM_OK;
 }
 
+namespace {
+// <= 32 picks (a decode token): one warp, one pick per lane; same stable order
+__global__ void permute_plan_warp_kernel(const int32_t *__restrict__ ids, int n_picks, int k, int E,
+                                         int32_t *__restrict__ offsets, int32_t *__restrict__ src_row,
+                                         int32_t *__restrict__ pos) {
+  const int lane = threadIdx.x;
+  const int e = lane < n_picks ? ids[lane] : 0x7fffffff;
+  // offsets: count picks with expert < x for every x, chunk by chunk over the expert ids
+  for (int c0 = 0; c0 <= E; c0 += 32) {
+    const int x = c0 + lane;
+    int below = 0;
+    for (int j = 0; j < n_picks; ++j) below += (__shfl_sync(0xffffffffu, e, j) < x);
+    if (x <= E) offsets[x] = below;
+  }
+  if (lane < n_picks) {
+    // stable rank: picks with a smaller expert, plus equal experts earlier in pick order
+    int p = 0;
+    for (int j = 0; j < n_picks; ++j) {
+      const int ej = __shfl_sync(0xffffffffu, e, j);  // all lanes participate below via the mask
+      p += (ej < e) || (ej == e && j < lane);
+    }
+    pos[lane] = p;
+    src_row[p] = lane / k;
+  } else {
+    for (int j = 0; j < n_picks; ++j) (void)__shfl_sync(0xffffffffu, e, j);
+  }
+}
+}  // namespace
+
 extern "C" int vmm_permute_plan(const int32_t *d_ids, int N, int k, int E, int32_t *d_offsets, int32_t *d_src_row,
                                 int32_t *d_pos, void *stream) {
   if (E < 1 || E > VMM_MAX_EXPERTS) return vmm::fail(VMM_EVALIDATION, "experts must lie in [1, 256]");
+  if (N * k <= 32) {
+    permute_plan_warp_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(d_ids, N * k, k, E, d_offsets, d_src_row, d_pos);
+    VMM_LAUNCH_CHECK("permute_plan_warp_kernel");
+    return VMM_OK;
+  }
   size_t smem = sizeof(int32_t) * ((size_t)kWarps * E + E);
   static bool attr = false;
   if (!attr) {
@@ -293,25 +350,21 @@ extern "C" int vmm_gather_f32(const float *d_src, const int32_t *d_rows, int n, 
 }
 
 namespace {
-// Fused combine + next layer's RMSNorm: one warp per token row.  out = resid +
-// sum_j g_j Y[pos_j] (+ shared rows), rounded to bf16; then xn = out * rsqrt(
-// mean(out^2) + eps) from the ROUNDED values with the same lane->chunk order as
-// rmsnorm_kernel, so the result is bit-identical to combine followed by rmsnorm.
-constexpr int kRowVecMax = 512;  // H <= 512*8 = 4096 (16 x 16-byte vectors per lane)
-__global__ void combine_norm_kernel(const uint4 *__restrict__ y, const int32_t *__restrict__ pos,
-                                    const float *__restrict__ gates, const uint4 *__restrict__ resid, int N, int k,
-                                    int row_vec, const uint4 *__restrict__ ys, int S, float eps,
-                                    uint4 *__restrict__ out, uint4 *__restrict__ xn) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int t = warp; t < N; t += nw) {
-    uint4 o[kRowVecMax / 32];
+// Fused combine + next layer's RMSNorm: one CTA per token row (same chunk map
+// and reduction as rmsnorm_kernel).  out = resid + sum_j g_j Y[pos_j] (+ shared
+// rows), rounded to bf16; xn = out * rsqrt(mean(out^2) + eps) from the ROUNDED
+// values, so the result is bit-identical to combine followed by rmsnorm.
+__global__ void __launch_bounds__(kNormThreads)
+combine_norm_kernel(const uint4 *__restrict__ y, const int32_t *__restrict__ pos, const float *__restrict__ gates,
+                    const uint4 *__restrict__ resid, int N, int k, int row_vec, const uint4 *__restrict__ ys, int S,
+                    float eps, uint4 *__restrict__ out, uint4 *__restrict__ xn) {
+  for (int t = blockIdx.x; t < N; t += gridDim.x) {
+    uint4 o[kNormChunks];
     float ss = 0.f;
 #pragma unroll
-    for (int i = 0; i < kRowVecMax / 32; ++i) {
-      const int c = lane + 32 * i;
-      if (c >= row_vec) break;
+    for (int i = 0; i < kNormChunks; ++i) {
+      const int c = threadIdx.x + kNormThreads * i;
+      if (c >= row_vec) continue;
       float acc[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) acc[q] = 0.f;
@@ -339,13 +392,11 @@ __global__ void combine_norm_kernel(const uint4 *__restrict__ y, const int32_t *
       }
       out[(long long)t * row_vec + c] = o[i];
     }
+    const float inv = rsqrtf(block_row_sum(ss) / (float)(row_vec * 8) + eps);
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
-    const float inv = rsqrtf(ss / (float)(row_vec * 8) + eps);
-#pragma unroll
-    for (int i = 0; i < kRowVecMax / 32; ++i) {
-      const int c = lane + 32 * i;
-      if (c >= row_vec) break;
+    for (int i = 0; i < kNormChunks; ++i) {
+      const int c = threadIdx.x + kNormThreads * i;
+      if (c >= row_vec) continue;
       const __nv_bfloat16 *oh = reinterpret_cast<const __nv_bfloat16 *>(&o[i]);
       uint4 nv;
       __nv_bfloat16 *nh = reinterpret_cast<__nv_bfloat16 *>(&nv);
@@ -361,11 +412,11 @@ extern "C" int vmm_combine_norm(const void *d_y, const int32_t *d_pos, const flo
                                 int N, int k, int H, const void *d_ys, int S, float eps, void *d_out, void *d_xn,
                                 void *stream) {
   if (N <= 0) return VMM_OK;
-  if ((H * 2) % 16 || H * 2 / 16 > kRowVecMax) return vmm::fail(VMM_EVALIDATION, "hidden size unsupported");
+  if ((H * 2) % 16 || H * 2 / 16 > kNormThreads * kNormChunks)
+    return vmm::fail(VMM_EVALIDATION, "hidden size unsupported");
   int row_vec = H * 2 / 16;
-  int warps = N < 148 * 32 ? N : 148 * 32;
-  int blocks = (warps * 32 + 255) / 256;
-  combine_norm_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((const uint4 *)d_y, d_pos, d_gates,
+  int blocks = N < 148 * 16 ? N : 148 * 16;
+  combine_norm_kernel<<<blocks, kNormThreads, 0, (cudaStream_t)stream>>>((const uint4 *)d_y, d_pos, d_gates,
                                                                 (const uint4 *)d_resid, N, k, row_vec,
                                                                 (const uint4 *)d_ys, S, eps, (uint4 *)d_out,
                                                                 (uint4 *)d_xn);

@@ -181,3 +181,14 @@ def test_fused_combine_norm_bit_identical_to_combine_then_rmsnorm():
         torch.cuda.synchronize()
         assert torch.equal(out, ref)
         assert torch.equal(xn, refn)
+
+
+@pytest.mark.parametrize("N,k,E", [(1, 8, 128), (2, 8, 128), (4, 6, 64), (1, 2, 4), (16, 2, 8)])
+def test_permute_plan_small_batches(N, k, E):
+    g = torch.Generator().manual_seed(N * 100 + k)
+    ids = torch.stack([torch.randperm(E, generator=g)[:k] for _ in range(N)]).int()
+    off, src, pos = kernels.permute_plan(ids.cuda(), E)
+    roff, rsrc, rpos = moe_ref.permute(ids, E)
+    assert torch.equal(off.cpu().long(), roff)
+    assert torch.equal(src.cpu().long()[: N * k], rsrc)
+    assert torch.equal(pos.cpu().long()[: N * k].reshape(N, k), rpos)
