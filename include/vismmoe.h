@@ -358,6 +358,7 @@ typedef struct {
   int32_t *routes;           /* nullable d [l1-l0][n_rows][k]: record of the routes used */
   void **ffn_start, **ffn_end; /* nullable cudaEvent_t arrays [l1-l0] around the grouped SwiGLU */
   int *n_demand;             /* nullable h [l1-l0] demanded experts per layer */
+  double host_us[4];         /* host time: launches before the sync, sync wait, decisions+copies, launches after */
 } vmm_stack_out;
 
 typedef struct vmm_stack vmm_stack;

@@ -14,6 +14,7 @@
 // xfer copy stream.
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -78,7 +79,13 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
   int ping = 0, copies = 0;
   std::vector<int32_t> demand, slabs;
   bool have_xn = false;  // the fused combine of the previous layer already produced this layer's xn
+  using clk = std::chrono::steady_clock;
+  double t_pre = 0, t_sync = 0, t_dec = 0, t_post = 0;  // host microseconds per phase
+  auto us = [](clk::time_point a, clk::time_point b) {
+    return std::chrono::duration<double, std::micro>(b - a).count();
+  };
   for (int l = l0; l < l1; ++l) {
+    auto c0 = clk::now();
     void *xn = d.xn;
     if (!have_xn) VMM_TRY(vmm_rmsnorm(cur, nullptr, n_rows, H, 1e-6f, xn, stream));
     const int emits = vmm_engine_emits(eng, l, phase);
@@ -131,7 +138,9 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
     }
     int32_t *ch = d.counts_host + (size_t)l * E;
     VMM_CUDA(cudaMemcpyAsync(ch, cnt, sizeof(uint32_t) * E, cudaMemcpyDeviceToHost, st), "counts D2H");
+    auto c1 = clk::now();
     VMM_CUDA(cudaStreamSynchronize(st), "layer sync");
+    auto c2 = clk::now();
     demand.clear();
     for (int e = 0; e < E; ++e)
       if (ch[e]) demand.push_back(e);
@@ -153,6 +162,7 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
       VMM_TRY(vmm_xfer_fence(xf, slabs.data(), (int)slabs.size(), stream));
       slot_of = drow;
     }
+    auto c3 = clk::now();
     const int M = n_rows * k;
     VMM_TRY(vmm_permute_plan(d.ids, n_rows, k, E, d.off, d.src, d.pos, stream));
     VMM_TRY(vmm_permute_rows(xn, d.src, M, H, d.xp, stream));
@@ -185,6 +195,11 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
     ping ^= 1;
     if (out && out->n_demand) out->n_demand[l - l0] = (int)demand.size();
     if (l >= lp) VMM_TRY(vmm_xfer_layer_done(xf, l, stream));
+    auto c4 = clk::now();
+    t_pre += us(c0, c1);
+    t_sync += us(c1, c2);
+    t_dec += us(c2, c3);
+    t_post += us(c3, c4);
     if (emits) {
       VMM_TRY(vmm_engine_emit(eng, l, yh));
       VMM_TRY(vmm_xfer_issue_engine(xf, eng, d.pool, d.host_layers, E, d.arena, d.n_pinned_slots, d.slot_bytes, &n));
@@ -192,6 +207,10 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
     }
   }
   if (out) {
+    out->host_us[0] = t_pre;
+    out->host_us[1] = t_sync;
+    out->host_us[2] = t_dec;
+    out->host_us[3] = t_post;
     out->x_out = cur;
     out->copies = copies;
   }

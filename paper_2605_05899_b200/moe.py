@@ -544,6 +544,7 @@ class MoEStack:
                 nbytes = int(n_dem[i]) * c.slot_bytes + M * c.hidden * 2 * 2 + M * c.inter * 2 * 2
                 self.profile.append((evs[i], evs[nl + i], nbytes, 6.0 * M * c.hidden * c.inter))
         res = bufs["out"] if out.x_out == bufs["out"].data_ptr() else bufs["out2"]
+        self.last_host_us = list(out.host_us)
         return res[:n_rows], out.copies, routes_t
 
     # ------------------------------------------------------------------

@@ -52,7 +52,7 @@ for pred in preds:
         t = 0.9 * t + (1 - 0.81) ** 0.5 * torch.randn((1, w.hidden), generator=g, device="cuda")
     res = stack.forward(x, sal, mod, trace=dtr, keep_session=True)
     pre = res.report
-    ms, copies = [], 0
+    ms, copies, host = [], 0, np.zeros(4)
     for s, tk in enumerate(toks):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -61,12 +61,15 @@ for pred in preds:
         e1.synchronize()
         ms.append(e0.elapsed_time(e1))
         copies += r.copies
+        host += np.asarray(stack.last_host_us)
     rep = stack.end_session()
     dh, dm = rep.hits - pre.hits, rep.misses - pre.misses
     steady = ms[1:] if D > 1 else ms
     out[pred] = dict(decode_ms_per_token=float(np.mean(steady)), decode_tokens_per_s=1e3 / float(np.mean(steady)),
                      decode_hit_rate=dh / max(dh + dm, 1), copies_per_token=copies / D,
-                     h2d_bytes_per_token=copies * cfg.slot_bytes / D, ms_first_token=ms[0])
+                     h2d_bytes_per_token=copies * cfg.slot_bytes / D, ms_first_token=ms[0],
+                     host_us_per_token=dict(zip(["launch_pre_sync", "sync_wait", "decisions_copies", "launch_post"],
+                                                (host / D).round(1).tolist())))
     print(pred, json.dumps(out[pred]), flush=True)
 base = out.get("none")
 if base:
