@@ -224,19 +224,22 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_cons
 // the demanded experts' weights, spread over all SMs.
 constexpr int kSkinnyRows = 16;
 
-// expert owning "active slot" j (the j-th expert with rows), or -1; warp-collective over E
+// expert owning "active slot" j (the j-th expert with rows), or -1.  The CTA
+// stages offsets[] in shared memory with one coalesced load, then warp 0 scans.
 __device__ __forceinline__ int jth_active_expert(const int32_t *offsets, int E, int j) {
+  __shared__ int s_off[VMM_MAX_EXPERTS + 1];
   __shared__ int s_e;
+  for (int i = threadIdx.x; i <= E; i += blockDim.x) s_off[i] = offsets[i];
+  __syncthreads();
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     int seen = 0, found = -1;
     for (int c0 = 0; c0 < E && found < 0; c0 += 32) {
       const int e = c0 + lane;
-      const bool act = e < E && offsets[e + 1] > offsets[e];
+      const bool act = e < E && s_off[e + 1] > s_off[e];
       const unsigned bal = __ballot_sync(0xffffffffu, act);
       const int cnt = __popc(bal);
       if (j < seen + cnt) {
-        // position of the (j - seen)-th set bit
         unsigned b = bal;
         for (int r = 0; r < j - seen; ++r) b &= b - 1;
         found = c0 + __ffs(b) - 1;

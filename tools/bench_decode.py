@@ -53,12 +53,17 @@ for pred in preds:
     res = stack.forward(x, sal, mod, trace=dtr, keep_session=True)
     pre = res.report
     ms, copies, host = [], 0, np.zeros(4)
+    ffn = []
     for s, tk in enumerate(toks):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        stack.profile = [] if s == D - 1 else None  # FFN events on the last token only
         e0.record()
         r = stack.decode_step(tk, tok=T + s if routing == "trace" else None)
         e1.record()
         e1.synchronize()
+        if stack.profile:
+            ffn = [a.elapsed_time(b) * 1e3 for a, b, _, _ in stack.profile]
+        stack.profile = None
         ms.append(e0.elapsed_time(e1))
         copies += r.copies
         host += np.asarray(stack.last_host_us)
@@ -68,6 +73,7 @@ for pred in preds:
     out[pred] = dict(decode_ms_per_token=float(np.mean(steady)), decode_tokens_per_s=1e3 / float(np.mean(steady)),
                      decode_hit_rate=dh / max(dh + dm, 1), copies_per_token=copies / D,
                      h2d_bytes_per_token=copies * cfg.slot_bytes / D, ms_first_token=ms[0],
+                     ffn_us_per_layer=float(np.mean(ffn)) if ffn else None,
                      host_us_per_token=dict(zip(["launch_pre_sync", "sync_wait", "decisions_copies", "launch_post"],
                                                 (host / D).round(1).tolist())))
     print(pred, json.dumps(out[pred]), flush=True)
