@@ -166,6 +166,20 @@ int vmm_combine(const void *d_y, const int32_t *d_pos, const float *d_gates, con
 int vmm_grouped_swiglu(const void *d_xp, const int32_t *d_offsets, int E, int M_total,
                        int H, int I, const void *d_w13_arena, const void *d_w2_arena, long long slot_stride,
                        long long n_slots, const int32_t *d_slot_of_expert, void *d_h1, void *d_y, void *stream);
+/* Same contraction as ONE persistent launch (GEMM1 and GEMM2 tiles interleaved,
+ * H1 dependencies resolved per 128-row block through d_done, a u32 scratch of
+ * ceil(M_total/128)+E words, zeroed by the call).  Bit-identical to
+ * vmm_grouped_swiglu.  Copy overlap: when d_need != NULL the GEMM tiles of
+ * expert e first wait until d_ready[slot_of[e] - ready_base] >= d_need[e]
+ * (u32 fill sequence numbers written by the copy stream after each fill, see
+ * vmm_xfer_ready), so the layer computes on landed experts while the misses
+ * still stream in.  need[e] == 0: no wait.  M_total <= 16 (decode) or
+ * d_done == NULL falls through to vmm_grouped_swiglu (d_need must be NULL). */
+int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offsets, int E, int M_total,
+                             int H, int I, const void *d_w13_arena, const void *d_w2_arena, long long slot_stride,
+                             long long n_slots, const int32_t *d_slot_of_expert, const uint32_t *d_need,
+                             const uint32_t *d_ready, int ready_base, uint32_t *d_done, void *d_h1, void *d_y,
+                             void *stream);
 /* Reference (CUDA-core, fp32) version of the same contraction for cross-checks. */
 int vmm_grouped_swiglu_simt(const void *d_xp, const int32_t *d_offsets, int E, int M_total,
                             int H, int I, const void *d_w13_arena, const void *d_w2_arena, long long slot_stride,
@@ -283,6 +297,14 @@ int vmm_xfer_copy(vmm_xfer *x, int slab, const void *h_src, void *d_dst, size_t 
  * (FIFO copy stream => covers all older fills) and register them as read by
  * the next layer */
 int vmm_xfer_fence(vmm_xfer *x, const int32_t *h_slabs, int n, void *compute_stream);
+/* device u32 [num_slabs] fill flags: after each fill of slab s the copy stream
+ * writes that fill's sequence number to ready[s] (stream memory op, ordered
+ * after the copy).  NULL when the device lacks stream memory ops. */
+const uint32_t *vmm_xfer_ready(vmm_xfer *x);
+/* flag-based alternative to vmm_xfer_fence (no stream wait): register the
+ * slabs as read by the next layer and write, per slab, the fill sequence number
+ * a reader must see in ready[] (0 = nothing pending) into h_need */
+int vmm_xfer_need(vmm_xfer *x, const int32_t *h_slabs, int n, uint32_t *h_need);
 /* record the compute event closing the reads registered since the last call */
 int vmm_xfer_layer_done(vmm_xfer *x, int layer, void *compute_stream);
 int vmm_xfer_reset_stats(vmm_xfer *x);
@@ -350,6 +372,9 @@ typedef struct {
   const int32_t *shared_slot_of;        /* d [L][S] arena slots of the shared experts */
   int32_t *shared_src, *shared_off;     /* d [cap*S], [S+1] */
   void *xs, *h1s, *ys;                  /* d [cap*S][H], [cap*S][I], [cap*S][H] */
+  uint32_t *need_host;                  /* nullable h pinned [L][E]: fill seq each expert's FFN waits for */
+  uint32_t *need_dev;                   /* nullable d [L][E] (with need_host: flag-based copy overlap) */
+  uint32_t *ffn_done;                   /* nullable d [cap*k/128 + E + 1] fused-FFN scratch (NULL: 2 launches) */
 } vmm_stack_desc;
 
 typedef struct {

@@ -58,6 +58,7 @@ class StackDesc(C.Structure):
         ("counts_host", P), ("y_host", P), ("slot_host", P),
         ("shared", I32), ("shared_slot_of", P), ("shared_src", P), ("shared_off", P),
         ("xs", P), ("h1s", P), ("ys", P),
+        ("need_host", P), ("need_dev", P), ("ffn_done", P),
     ]
 
 
@@ -86,6 +87,7 @@ _SIGS = {
     "vmm_combine": (I32, [P, P, P, P, I32, I32, I32, P, P]),
     "vmm_rmsnorm": (I32, [P, P, I32, I32, C.c_float, P, P]),
     "vmm_grouped_swiglu": (I32, [P, P, I32, I32, I32, I32, P, P, I64, I64, P, P, P, P]),
+    "vmm_grouped_swiglu_fused": (I32, [P, P, I32, I32, I32, I32, P, P, I64, I64, P, P, P, I32, P, P, P, P]),
     "vmm_grouped_swiglu_simt": (I32, [P, P, I32, I32, I32, I32, P, P, I64, P, P, P, P]),
     "vmm_engine_create": (I32, [C.POINTER(EngineConfig), C.POINTER(P)]),
     "vmm_engine_destroy": (None, [P]),
@@ -119,6 +121,8 @@ _SIGS = {
     "vmm_xfer_destroy": (None, [P]),
     "vmm_xfer_copy": (I32, [P, I32, P, P, SZ, I32]),
     "vmm_xfer_fence": (I32, [P, P, I32, P]),
+    "vmm_xfer_ready": (P, [P]),
+    "vmm_xfer_need": (I32, [P, P, I32, P]),
     "vmm_xfer_layer_done": (I32, [P, I32, P]),
     "vmm_xfer_sync": (I32, [P]),
     "vmm_xfer_join": (I32, [P, P]),

@@ -215,6 +215,247 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_cons
 }
 
 
+// ---- fused GEMM1 + GEMM2, expert-granular overlap with the copy stream -------
+// One persistent launch runs both contractions of a layer.  The tile space is a
+// sequence of blocks of (n1 + n2) tiles: block b holds the n1 GEMM1 tiles of
+// m-tile b and the n2 GEMM2 tiles of m-tile b - kLag, so a GEMM2 tile comes
+// ~2 waves after the GEMM1 tiles whose H1 rows it consumes.  Dependencies are
+// resolved with flags instead of kernel boundaries:
+//   * GEMM1 tile of expert e waits until the copy stream's fill of e's slot
+//     has landed (ready[slot - ready_base] >= need[e]; the copy stream writes
+//     the fill sequence number with a stream memory op after each copy), so
+//     the FFN of a layer starts on resident experts while misses stream in;
+//   * GEMM2 tile of m-tile r waits until all n1 GEMM1 tiles of r stored their
+//     H1 columns (done[r] == 4 * n1 epilogue-warp arrivals, release/acquire).
+// Tiles are assigned round-robin (static), every CTA is resident (grid <= SMs,
+// 1 CTA/SM) and a tile only waits on lower-index tiles or on copies, so the
+// lowest unfinished tile can always progress: no deadlock.
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(uint32_t *p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// spin until *p >= want (wrap-safe u32 sequence compare); a wait beyond 30 s
+// means a lost copy or a broken dependency: trap (error) instead of hanging the GPU
+__device__ __forceinline__ void wait_at_least(const uint32_t *p, uint32_t want, int sleep_ns) {
+  if ((int)(ld_acquire_u32(p) - want) >= 0) return;
+  const uint64_t t0 = global_ns();
+  while ((int)(ld_acquire_u32(p) - want) < 0) {
+    __nanosleep(sleep_ns);
+    if (global_ns() - t0 > 30ull * 1000000000ull) __trap();
+  }
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+struct FusedTile {
+  bool valid, gemm2;
+  int m_tile, n_tile;
+};
+__device__ __forceinline__ FusedTile fused_tile(int t, int n1, int n2, int MT, int lag) {
+  FusedTile f;
+  const int per = n1 + n2;
+  const int b = t / per, j = t - b * per;
+  f.gemm2 = j >= n1;
+  f.m_tile = f.gemm2 ? b - lag : b;
+  f.n_tile = f.gemm2 ? j - n1 : j;
+  f.valid = f.m_tile >= 0 && f.m_tile < MT;
+  return f;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+ffn_fused_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w13,
+                 const __grid_constant__ CUtensorMap map_h1, const __grid_constant__ CUtensorMap map_w2,
+                 const int32_t *__restrict__ offsets, const int32_t *__restrict__ slot_of,
+                 const uint32_t *__restrict__ need, const uint32_t *ready, int ready_base, uint32_t *done, int E,
+                 int H, int I, int lag, __nv_bfloat16 *__restrict__ h1, __nv_bfloat16 *__restrict__ y) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * kStageBytes);
+  uint64_t *empty = full + kStages;
+  uint64_t *tmem_full = empty + kStages;   // [2]
+  uint64_t *tmem_empty = tmem_full + 2;    // [2]
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 2);
+  __shared__ int s_offs[VMM_MAX_EXPERTS + 1], s_tile_base[VMM_MAX_EXPERTS + 1], s_slots[VMM_MAX_EXPERTS];
+  __shared__ uint32_t s_need[VMM_MAX_EXPERTS];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int e = threadIdx.x; e <= E; e += blockDim.x) s_offs[e] = offsets[e];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    s_slots[e] = slot_of[e];
+    s_need[e] = need ? need[e] : 0u;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int e = 0; e < E; ++e) {
+      s_tile_base[e] = acc;
+      acc += (s_offs[e + 1] - s_offs[e] + BM - 1) / BM;
+    }
+    s_tile_base[E] = acc;
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&map_x);
+    prefetch_tmap(&map_w13);
+    prefetch_tmap(&map_h1);
+    prefetch_tmap(&map_w2);
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tmem_full[b], 1); mbar_init(&tmem_empty[b], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int MT = s_tile_base[E];
+  const int n1 = (2 * I) / BN, n2 = H / BN;
+  const int total = (MT + lag) * (n1 + n2);
+  const int nk1 = H / BK, nk2 = I / BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const FusedTile f = fused_tile(t, n1, n2, MT, lag);
+        if (!f.valid) continue;
+        const TileInfo ti = tile_info(f.m_tile * n1, n1, s_tile_base, s_offs, s_slots, E);
+        const uint32_t nd = s_need[ti.expert];
+        // the expert's slot fill must have landed (copy stream -> ready flag)
+        if (nd) wait_at_least(ready + (ti.slot - ready_base), nd, 256);
+        // GEMM2: H1 rows of this m-tile complete (all GEMM1 n-tiles stored)
+        if (f.gemm2) wait_at_least(done + f.m_tile, 4u * (uint32_t)n1, 64);
+        if (nd || f.gemm2) fence_proxy_async_global();
+        const CUtensorMap *ma = f.gemm2 ? &map_h1 : &map_x;
+        const CUtensorMap *mb = f.gemm2 ? &map_w2 : &map_w13;
+        const int nk = f.gemm2 ? nk2 : nk1;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % kStages;
+          if (it >= kStages) mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
+          unsigned char *a_dst = smem + s * kStageBytes;
+          mbar_expect_tx(&full[s], kStageBytes);
+          tma_load_2d(ma, &full[s], a_dst, kb * BK, ti.row0);
+          tma_load_3d(mb, &full[s], a_dst + kTileBytes, kb * BK, f.n_tile * BN, ti.slot);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int it = 0, local = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const FusedTile f = fused_tile(t, n1, n2, MT, lag);
+        if (!f.valid) continue;
+        const int nk = f.gemm2 ? nk2 : nk1;
+        const int b = local & 1, use = local >> 1;
+        if (use > 0) mbar_wait(&tmem_empty[b], (use - 1) & 1);
+        tc_fence_after();
+        const uint32_t acc = tmem + b * BN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % kStages;
+          mbar_wait(&full[s], (it / kStages) & 1);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + s * kStageBytes);
+          const uint32_t b_addr = a_addr + kTileBytes;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            umma_bf16(acc, sw128_desc(a_addr + kk * 32), sw128_desc(b_addr + kk * 32), idesc_bf16(BM, BN),
+                      (kb | kk) != 0);
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tmem_full[b]);
+        ++local;
+      }
+    }
+    __syncwarp();
+  } else {
+    const int q = warp & 3;
+    int local = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const FusedTile f = fused_tile(t, n1, n2, MT, lag);
+      if (!f.valid) continue;
+      const TileInfo ti = tile_info(f.m_tile * n1, n1, s_tile_base, s_offs, s_slots, E);
+      const int b = local & 1, use = local >> 1;
+      ++local;
+      const int row = ti.row0 + q * 32 + lane;
+      mbar_wait(&tmem_full[b], use & 1);
+      tc_fence_after();
+      const uint32_t t_base = tmem + b * BN + ((uint32_t)(q * 32) << 16);
+      if (!f.gemm2) {
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          float g[32], u[32];
+          tmem_ld32(t_base + half * 32, g);
+          tmem_ld32(t_base + 64 + half * 32, u);
+          if (half == 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tmem_empty[b]);
+          }
+          if (row < ti.row_end) {
+            uint4 *dst = reinterpret_cast<uint4 *>(h1 + (long long)row * I + f.n_tile * (BN / 2) + half * 32);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              uint4 o;
+              o.x = pack_bf16(silu(g[8 * v + 0]) * u[8 * v + 0], silu(g[8 * v + 1]) * u[8 * v + 1]);
+              o.y = pack_bf16(silu(g[8 * v + 2]) * u[8 * v + 2], silu(g[8 * v + 3]) * u[8 * v + 3]);
+              o.z = pack_bf16(silu(g[8 * v + 4]) * u[8 * v + 4], silu(g[8 * v + 5]) * u[8 * v + 5]);
+              o.w = pack_bf16(silu(g[8 * v + 6]) * u[8 * v + 6], silu(g[8 * v + 7]) * u[8 * v + 7]);
+              dst[v] = o;
+            }
+          }
+        }
+        // publish this warp's 32 H1 rows of the tile to the GEMM2 TMA readers
+        fence_proxy_async_global();
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) red_release_add(done + f.m_tile, 1u);
+      } else {
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c) {
+          float a[32];
+          tmem_ld32(t_base + c * 32, a);
+          if (c == BN / 32 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tmem_empty[b]);
+          }
+          if (row < ti.row_end) {
+            uint4 *dst = reinterpret_cast<uint4 *>(y + (long long)row * H + f.n_tile * BN + c * 32);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              uint4 o;
+              o.x = pack_bf16(a[8 * v + 0], a[8 * v + 1]);
+              o.y = pack_bf16(a[8 * v + 2], a[8 * v + 3]);
+              o.z = pack_bf16(a[8 * v + 4], a[8 * v + 5]);
+              o.w = pack_bf16(a[8 * v + 6], a[8 * v + 7]);
+              dst[v] = o;
+            }
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+  }
+}
+
 // ---- decode-sized batches: weight-streaming SwiGLU on CUDA cores -----------
 // With <= kSkinnyRows rows in the whole layer (one decode token: k rows) the
 // tensor-core tiles would be >90% padding and a 128x128 tile loop per expert is
@@ -481,6 +722,73 @@ extern "C" int vmm_grouped_swiglu(const void *d_xp, const int32_t *d_offsets, in
   grouped_gemm_kernel<false><<<g2, kThreads, kSmemBytes, s>>>(ma2, mb2, d_offsets, d_slot_of_expert, E, I, n2,
                                                               (__nv_bfloat16 *)d_y, H);
   VMM_LAUNCH_CHECK("grouped_gemm_kernel<down>");
+  return VMM_OK;
+}
+
+extern "C" int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offsets, int E, int M_total, int H, int I,
+                                        const void *d_w13_arena, const void *d_w2_arena, long long slot_stride,
+                                        long long n_slots, const int32_t *d_slot_of_expert, const uint32_t *d_need,
+                                        const uint32_t *d_ready, int ready_base, uint32_t *d_done, void *d_h1,
+                                        void *d_y, void *stream) {
+  if (M_total <= 0) return VMM_OK;
+  if (M_total <= kSkinnyRows || d_done == nullptr)  // decode-sized: skinny path (callers fence on events)
+    return d_need ? vmm::fail(VMM_ECONTRACT, "ready flags need the fused tensor-core path (M > 16, scratch)")
+                  : vmm_grouped_swiglu(d_xp, d_offsets, E, M_total, H, I, d_w13_arena, d_w2_arena, slot_stride,
+                                       n_slots, d_slot_of_expert, d_h1, d_y, stream);
+  if (H % BN || H % BK || I % 64 || I % BK || (2 * I) % BN)
+    return vmm::fail(VMM_EVALIDATION, "grouped_swiglu: hidden must be a multiple of 128, inter of 64");
+  if (E < 1 || E > VMM_MAX_EXPERTS) return vmm::fail(VMM_EVALIDATION, "experts must lie in [1, 256]");
+  if (slot_stride % 8) return vmm::fail(VMM_EVALIDATION, "slot stride must be a multiple of 8 elements");
+  if (d_need && !d_ready) return vmm::fail(VMM_ECONTRACT, "need[] without ready flags");
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e1 = cudaFuncSetAttribute(ffn_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)kSmemBytes);
+    if (e1 != cudaSuccess) return vmm::cuda_status(e1, "ffn fused attr");
+    attr = true;
+  }
+  CUtensorMap mx, mw13, mh1, mw2;
+  int st;
+  {
+    uint64_t dims[2] = {(uint64_t)H, (uint64_t)M_total};
+    uint64_t str[1] = {(uint64_t)H * 2};
+    uint32_t box[2] = {BK, BM};
+    if ((st = make_map(&mx, d_xp, 2, dims, str, box))) return st;
+  }
+  {
+    uint64_t dims[3] = {(uint64_t)H, (uint64_t)2 * I, (uint64_t)n_slots};
+    uint64_t str[2] = {(uint64_t)H * 2, (uint64_t)slot_stride * 2};
+    uint32_t box[3] = {BK, BN, 1};
+    if ((st = make_map(&mw13, d_w13_arena, 3, dims, str, box))) return st;
+  }
+  {
+    uint64_t dims[2] = {(uint64_t)I, (uint64_t)M_total};
+    uint64_t str[1] = {(uint64_t)I * 2};
+    uint32_t box[2] = {BK, BM};
+    if ((st = make_map(&mh1, d_h1, 2, dims, str, box))) return st;
+  }
+  {
+    uint64_t dims[3] = {(uint64_t)I, (uint64_t)H, (uint64_t)n_slots};
+    uint64_t str[2] = {(uint64_t)I * 2, (uint64_t)slot_stride * 2};
+    uint32_t box[3] = {BK, BN, 1};
+    if ((st = make_map(&mw2, d_w2_arena, 3, dims, str, box))) return st;
+  }
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int max_m_tiles = (M_total + BM - 1) / BM + E;
+  const int n1 = (2 * I) / BN, n2 = H / BN;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t ce = cudaMemsetAsync(d_done, 0, sizeof(uint32_t) * max_m_tiles, s);
+  if (ce != cudaSuccess) return vmm::cuda_status(ce, "ffn done memset");
+  const int grid = g_num_sms < max_m_tiles * (n1 + n2) ? g_num_sms : max_m_tiles * (n1 + n2);
+  const int lag = (2 * grid + n1 + n2 - 1) / (n1 + n2);  // GEMM2 tiles ~2 waves behind their GEMM1 tiles
+  ffn_fused_kernel<<<grid, kThreads, kSmemBytes, s>>>(mx, mw13, mh1, mw2, d_offsets, d_slot_of_expert, d_need,
+                                                      d_ready, ready_base, d_done, E, H, I, lag,
+                                                      (__nv_bfloat16 *)d_h1, (__nv_bfloat16 *)d_y);
+  VMM_LAUNCH_CHECK("ffn_fused_kernel");
   return VMM_OK;
 }
 

@@ -88,7 +88,16 @@ __global__ void permute_rows_kernel(const uint4 *__restrict__ x, const int32_t *
   for (int r = warp; r < n; r += nw) {
     const uint4 *s = x + (long long)src_row[r] * row_vec;
     uint4 *d = xp + (long long)r * row_vec;
-    for (int c = lane; c < row_vec; c += 32) d[c] = __ldg(s + c);
+    // 8 independent 16-byte loads in flight per lane before the stores (a 4 KB row per warp pass)
+    for (int c0 = lane; c0 < row_vec; c0 += 32 * 8) {
+      uint4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (c0 + 32 * u < row_vec) v[u] = __ldg(s + c0 + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (c0 + 32 * u < row_vec) d[c0 + 32 * u] = v[u];
+    }
   }
 }
 
@@ -201,6 +210,108 @@ extern "C" int vmm_rmsnorm(const void *d_x, const void *d_w, int n, int H, float
 
 namespace {
 // <= 32 picks (a decode token): one warp, one pick per lane; same stable order
+// ---- multi-CTA stable counting sort (large batches) --------------------------
+// Picks are split into contiguous chunks of kChunk (one CTA each, 8 warps of
+// kChunk/8 picks), so block order, warp order and lane order together are the
+// pick order and the sort stays stable:
+//   1. plan_count   : per-CTA expert counts           blk[b][e]
+//   2. plan_scan    : expert offsets + per-CTA bases  blk[b][e] <- offsets[e] + sum_{b'<b} cnt[b'][e]
+//   3. plan_scatter : per-warp bases inside the CTA, ranks by match_any -> pos/src_row
+constexpr int kChunk = 8192, kPT = 256, kPW = kPT / 32;
+
+__device__ __forceinline__ void chunk_warp_counts(const int32_t *__restrict__ ids, int n_picks, int32_t *cnt, int E) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < kPW * E; i += kPT) cnt[i] = 0;
+  __syncthreads();
+  const int lo = blockIdx.x * kChunk + warp * (kChunk / kPW);
+  const int hi = min(n_picks, lo + kChunk / kPW);
+  for (int c0 = lo; c0 < hi; c0 += 32) {
+    const int i = c0 + lane;
+    const int e = (i < hi) ? __ldg(ids + i) : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    if (e >= 0 && lane == __ffs(peers) - 1) cnt[warp * E + e] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kPT) plan_count_kernel(const int32_t *__restrict__ ids, int n_picks, int E,
+                                                         int32_t *__restrict__ blk) {
+  __shared__ int32_t cnt[kPW * VMM_MAX_EXPERTS];
+  chunk_warp_counts(ids, n_picks, cnt, E);
+  for (int e = threadIdx.x; e < E; e += kPT) {
+    int s = 0;
+#pragma unroll
+    for (int w = 0; w < kPW; ++w) s += cnt[w * E + e];
+    blk[(long long)blockIdx.x * E + e] = s;
+  }
+}
+
+__global__ void __launch_bounds__(VMM_MAX_EXPERTS) plan_scan_kernel(int32_t *__restrict__ blk, int G, int E,
+                                                                   int32_t *__restrict__ offsets) {
+  __shared__ int32_t tot[VMM_MAX_EXPERTS + 1];
+  const int e = threadIdx.x;
+  int s = 0;
+  if (e < E)
+    for (int b = 0; b < G; ++b) s += blk[(long long)b * E + e];
+  tot[e] = s;
+  __syncthreads();
+  if (e == 0) {
+    int run = 0;
+    for (int x = 0; x < E; ++x) {
+      const int t = tot[x];
+      tot[x] = run;
+      offsets[x] = run;
+      run += t;
+    }
+    offsets[E] = run;
+  }
+  __syncthreads();
+  if (e < E) {
+    int run = tot[e];
+    for (int b = 0; b < G; ++b) {
+      const int c = blk[(long long)b * E + e];
+      blk[(long long)b * E + e] = run;
+      run += c;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kPT) plan_scatter_kernel(const int32_t *__restrict__ ids, int n_picks, int k, int E,
+                                                           const int32_t *__restrict__ blk,
+                                                           int32_t *__restrict__ src_row, int32_t *__restrict__ pos) {
+  __shared__ int32_t cnt[kPW * VMM_MAX_EXPERTS];
+  chunk_warp_counts(ids, n_picks, cnt, E);
+  for (int e = threadIdx.x; e < E; e += kPT) {
+    int run = blk[(long long)blockIdx.x * E + e];
+#pragma unroll
+    for (int w = 0; w < kPW; ++w) {
+      const int c = cnt[w * E + e];
+      cnt[w * E + e] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lo = blockIdx.x * kChunk + warp * (kChunk / kPW);
+  const int hi = min(n_picks, lo + kChunk / kPW);
+  for (int c0 = lo; c0 < hi; c0 += 32) {
+    const int i = c0 + lane;
+    const int e = (i < hi) ? __ldg(ids + i) : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    const int leader = __ffs(peers) - 1;
+    const int basep = (e >= 0) ? cnt[warp * E + e] : 0;
+    if (e >= 0) {
+      const int p = basep + __popc(peers & ((1u << lane) - 1u));
+      pos[i] = p;
+      src_row[p] = i / k;
+    }
+    __syncwarp();
+    if (e >= 0 && lane == leader) cnt[warp * E + e] = basep + __popc(peers);
+    __syncwarp();
+  }
+}
+
 __global__ void permute_plan_warp_kernel(const int32_t *__restrict__ ids, int n_picks, int k, int E,
                                          int32_t *__restrict__ offsets, int32_t *__restrict__ src_row,
                                          int32_t *__restrict__ pos) {
@@ -234,6 +345,30 @@ extern "C" int vmm_permute_plan(const int32_t *d_ids, int N, int k, int E, int32
   if (N * k <= 32) {
     permute_plan_warp_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(d_ids, N * k, k, E, d_offsets, d_src_row, d_pos);
     VMM_LAUNCH_CHECK("permute_plan_warp_kernel");
+    return VMM_OK;
+  }
+  const int n_picks = N * k;
+  if (n_picks > kChunk) {  // multi-CTA stable sort; per-CTA counts in a library scratch (per device)
+    const int G = (n_picks + kChunk - 1) / kChunk;
+    static int32_t *scratch[64] = {nullptr};
+    static size_t cap[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const size_t need = (size_t)G * E;
+    if (dev < 0 || dev >= 64) return vmm::fail(VMM_ECUDA, "device index out of range");
+    if (cap[dev] < need) {
+      if (scratch[dev]) cudaFree(scratch[dev]);
+      cudaError_t e = cudaMalloc(&scratch[dev], sizeof(int32_t) * need * 2);
+      if (e != cudaSuccess) { scratch[dev] = nullptr; cap[dev] = 0; return vmm::cuda_status(e, "permute scratch"); }
+      cap[dev] = need * 2;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    plan_count_kernel<<<G, kPT, 0, st>>>(d_ids, n_picks, E, scratch[dev]);
+    VMM_LAUNCH_CHECK("plan_count_kernel");
+    plan_scan_kernel<<<1, VMM_MAX_EXPERTS, 0, st>>>(scratch[dev], G, E, d_offsets);
+    VMM_LAUNCH_CHECK("plan_scan_kernel");
+    plan_scatter_kernel<<<G, kPT, 0, st>>>(d_ids, n_picks, k, E, scratch[dev], d_src_row, d_pos);
+    VMM_LAUNCH_CHECK("plan_scatter_kernel");
     return VMM_OK;
   }
   size_t smem = sizeof(int32_t) * ((size_t)kWarps * E + E);

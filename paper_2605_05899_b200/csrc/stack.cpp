@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -49,6 +50,8 @@ int vmm_xfer_issue_engine(vmm_xfer *x, vmm_engine *e, const void *h_pool, int ho
                           void *d_arena, long long slab_offset, size_t slot_bytes, int *n_issued);
 int vmm_gather_i32(const int32_t *d_src, const int32_t *d_rows, int n, int width, int32_t *d_dst, void *stream);
 int vmm_gather_f32(const float *d_src, const int32_t *d_rows, int n, int width, float *d_dst, void *stream);
+const uint32_t *vmm_xfer_ready(vmm_xfer *x);
+int vmm_xfer_need(vmm_xfer *x, const int32_t *h_slabs, int n, uint32_t *h_need);
 }
 
 struct vmm_stack {
@@ -78,6 +81,12 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
   const void *cur = d_x;
   int ping = 0, copies = 0;
   std::vector<int32_t> demand, slabs;
+  std::vector<uint32_t> need;
+  const uint32_t *ready = vmm_xfer_ready(xf);
+  // tensor-core FFN with per-expert ready flags: the layer's FFN starts while its misses still stream in
+  // (VMM_FFN_FENCE=1: whole-layer event fence instead, e.g. under a serialising profiler)
+  static const bool force_fence = std::getenv("VMM_FFN_FENCE") != nullptr;
+  const bool flagged = !force_fence && ready && d.need_host && d.need_dev && d.ffn_done && n_rows * k > 16;
   bool have_xn = false;  // the fused combine of the previous layer already produced this layer's xn
   using clk = std::chrono::steady_clock;
   double t_pre = 0, t_sync = 0, t_dec = 0, t_post = 0;  // host microseconds per phase
@@ -149,6 +158,7 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
     VMM_TRY(vmm_xfer_issue_engine(xf, eng, d.pool, d.host_layers, E, d.arena, d.n_pinned_slots, d.slot_bytes, &n));
     copies += n;
     const int32_t *slot_of;
+    const uint32_t *need_of = nullptr;
     if (l < lp) {
       slot_of = d.pinned_slot_of + (size_t)l * E;
     } else {
@@ -159,7 +169,18 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
       for (size_t i = 0; i < demand.size(); ++i) row[demand[i]] = slabs[i] + (int32_t)d.n_pinned_slots;
       int32_t *drow = d.slot_dev + (size_t)l * E;
       VMM_CUDA(cudaMemcpyAsync(drow, row, sizeof(int32_t) * E, cudaMemcpyHostToDevice, st), "slot table H2D");
-      VMM_TRY(vmm_xfer_fence(xf, slabs.data(), (int)slabs.size(), stream));
+      if (flagged) {
+        need.resize(demand.size());
+        VMM_TRY(vmm_xfer_need(xf, slabs.data(), (int)slabs.size(), need.data()));
+        uint32_t *nrow = d.need_host + (size_t)l * E;
+        std::memset(nrow, 0, sizeof(uint32_t) * E);
+        for (size_t i = 0; i < demand.size(); ++i) nrow[demand[i]] = need[i];
+        uint32_t *ndev = d.need_dev + (size_t)l * E;
+        VMM_CUDA(cudaMemcpyAsync(ndev, nrow, sizeof(uint32_t) * E, cudaMemcpyHostToDevice, st), "need H2D");
+        need_of = ndev;
+      } else {
+        VMM_TRY(vmm_xfer_fence(xf, slabs.data(), (int)slabs.size(), stream));
+      }
       slot_of = drow;
     }
     auto c3 = clk::now();
@@ -168,8 +189,9 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
     VMM_TRY(vmm_permute_rows(xn, d.src, M, H, d.xp, stream));
     if (out && out->ffn_start)
       VMM_CUDA(cudaEventRecord((cudaEvent_t)out->ffn_start[l - l0], st), "ffn start event");
-    VMM_TRY(vmm_grouped_swiglu(d.xp, d.off, E, M, H, I, d.arena, (const char *)d.arena + (size_t)2 * I * H * 2,
-                               (long long)3 * I * H, d.n_slots, slot_of, d.h1, d.y, stream));
+    VMM_TRY(vmm_grouped_swiglu_fused(d.xp, d.off, E, M, H, I, d.arena, (const char *)d.arena + (size_t)2 * I * H * 2,
+                                     (long long)3 * I * H, d.n_slots, slot_of, need_of, ready,
+                                     (int)d.n_pinned_slots, d.ffn_done, d.h1, d.y, stream));
     if (out && out->ffn_end) VMM_CUDA(cudaEventRecord((cudaEvent_t)out->ffn_end[l - l0], st), "ffn end event");
     void *dst = ping ? d.out1 : d.out0;
     const int S = d.shared;
@@ -178,9 +200,10 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
       const int MS = n_rows * S;
       VMM_TRY(vmm_shared_plan(n_rows, S, d.shared_src, d.shared_off, stream));
       VMM_TRY(vmm_permute_rows(xn, d.shared_src, MS, H, d.xs, stream));
-      VMM_TRY(vmm_grouped_swiglu(d.xs, d.shared_off, S, MS, H, I, d.arena,
-                                 (const char *)d.arena + (size_t)2 * I * H * 2, (long long)3 * I * H, d.n_slots,
-                                 d.shared_slot_of + (size_t)l * S, d.h1s, d.ys, stream));
+      VMM_TRY(vmm_grouped_swiglu_fused(d.xs, d.shared_off, S, MS, H, I, d.arena,
+                                       (const char *)d.arena + (size_t)2 * I * H * 2, (long long)3 * I * H, d.n_slots,
+                                       d.shared_slot_of + (size_t)l * S, nullptr, nullptr, 0, d.ffn_done, d.h1s,
+                                       d.ys, stream));
     }
     if (l + 1 < l1) {  // combine fused with the next layer's RMSNorm (xn is free again: consumed above)
       VMM_TRY(vmm_combine_norm(d.y, d.pos, d.gates, cur, n_rows, k, H, S > 0 ? d.ys : nullptr, S, 1e-6f, dst, xn,

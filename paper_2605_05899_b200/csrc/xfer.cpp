@@ -10,8 +10,10 @@
 //   * a slab is never overwritten while a layer may still read it: the copy
 //     into slab s first waits for the compute event of the last layer fenced
 //     on s (again one wait per newer reader, FIFO on the compute stream).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -30,7 +32,22 @@ int cuda_status(cudaError_t e, const char *what) {
 
 namespace {
 constexpr int kRing = 8192;
+
+// cuStreamWriteValue32 through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*WriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WriteValue32Fn write_value_fn() {
+  static WriteValue32Fn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<WriteValue32Fn>(p);
+  });
+  return fn;
 }
+}  // namespace
 
 struct vmm_xfer {
   cudaStream_t stream = nullptr;
@@ -43,6 +60,7 @@ struct vmm_xfer {
   cudaEvent_t t_first = nullptr, t_last = nullptr;
   bool timing_started = false;
   std::vector<const void *> sources;  // optional per-(layer, expert) source pointers (sharded mode)
+  uint32_t *ready = nullptr;          // d [num_slabs] fill sequence flags (stream memory op after each fill)
 };
 
 extern "C" {
@@ -66,6 +84,13 @@ int vmm_xfer_create(int num_slabs, size_t slab_bytes, int max_layers, vmm_xfer *
   if (e != cudaSuccess) { vmm_xfer_destroy(x); return cuda_status(e, "copy events"); }
   x->slab_fill_seq.assign(num_slabs, 0);
   x->slab_read_seq.assign(num_slabs, 0);
+  if (write_value_fn() && num_slabs > 0) {
+    if ((e = cudaMalloc(&x->ready, sizeof(uint32_t) * num_slabs)) != cudaSuccess ||
+        (e = cudaMemset(x->ready, 0, sizeof(uint32_t) * num_slabs)) != cudaSuccess) {
+      vmm_xfer_destroy(x);
+      return cuda_status(e, "ready flags");
+    }
+  }
   *out = x;
   return VMM_OK;
 }
@@ -78,6 +103,7 @@ void vmm_xfer_destroy(vmm_xfer *x) {
   if (x->t_first) cudaEventDestroy(x->t_first);
   if (x->t_last) cudaEventDestroy(x->t_last);
   if (x->stream) cudaStreamDestroy(x->stream);
+  if (x->ready) cudaFree(x->ready);
   delete x;
 }
 
@@ -103,6 +129,10 @@ int vmm_xfer_copy(vmm_xfer *x, int slab, const void *h_src, void *d_dst, size_t 
   if ((e = cudaEventRecord(x->fill_ev[(x->fill_seq - 1) % kRing], x->stream)) != cudaSuccess)
     return cuda_status(e, "fill event");
   x->slab_fill_seq[slab] = x->fill_seq;
+  if (x->ready) {  // ordered after the copy, with a memory barrier: readers polling ready[] see the data
+    CUresult r = write_value_fn()((CUstream)x->stream, (CUdeviceptr)(x->ready + slab), (cuuint32_t)x->fill_seq, 0);
+    if (r != CUDA_SUCCESS) return vmm::fail(VMM_ECUDA, "cuStreamWriteValue32 failed (" + std::to_string((int)r) + ")");
+  }
   x->bytes += (double)bytes;
   x->copies++;
   return VMM_OK;
@@ -119,6 +149,19 @@ int vmm_xfer_fence(vmm_xfer *x, const int32_t *slabs, int n, void *compute_strea
   if (need > 0) {
     cudaError_t e = cudaStreamWaitEvent((cudaStream_t)compute_stream, x->fill_ev[(need - 1) % kRing], 0);
     if (e != cudaSuccess) return cuda_status(e, "fence wait");
+  }
+  return VMM_OK;
+}
+
+const uint32_t *vmm_xfer_ready(vmm_xfer *x) { return x->ready; }
+
+int vmm_xfer_need(vmm_xfer *x, const int32_t *slabs, int n, uint32_t *need) {
+  if (!x->ready) return vmm::fail(VMM_ECONTRACT, "no ready flags (stream memory ops unavailable)");
+  for (int i = 0; i < n; ++i) {
+    int s = slabs[i];
+    if (s < 0 || s >= (int)x->slab_fill_seq.size()) return vmm::fail(VMM_ECONTRACT, "slab out of range");
+    need[i] = (uint32_t)x->slab_fill_seq[s];
+    x->pending_readers.push_back(s);
   }
   return VMM_OK;
 }

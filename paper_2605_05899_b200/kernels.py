@@ -182,9 +182,14 @@ def permute_rows(x, src_row, n_rows: int, stream=None, out=None):
     return out
 
 
-def grouped_swiglu(xp, offsets, arena, slot_of, inter: int, stream=None, h1=None, y=None, simt: bool = False):
-    """Grouped SwiGLU over expert-contiguous rows of xp (tcgen05 path unless simt).
+def grouped_swiglu(xp, offsets, arena, slot_of, inter: int, stream=None, h1=None, y=None, simt: bool = False,
+                   fused: bool = True, need=None, ready=None, ready_base: int = 0):
+    """Grouped SwiGLU over expert-contiguous rows of xp.
 
+    Default: the fused persistent tcgen05 kernel (GEMM1+GEMM2 in one launch);
+    fused=False: two tcgen05 launches; simt=True: CUDA-core cross-check.
+    need/ready: optional per-expert fill sequence numbers / device flags
+    (vmm_grouped_swiglu_fused's copy overlap).
     arena: bf16 [n_slots, 3*I*H] -- per slot W13 ([2I,H], interleaved) then W2 ([H,I])."""
     M, H = (int(s) for s in xp.shape)
     E = int(offsets.shape[0]) - 1
@@ -199,6 +204,12 @@ def grouped_swiglu(xp, offsets, arena, slot_of, inter: int, stream=None, h1=None
         _n(2)
         check(L.vmm_grouped_swiglu_simt(ptr(xp), ptr(offsets), E, M, H, inter, ptr(arena), w2_base, stride,
                                         ptr(slot_of), ptr(h1), ptr(y), stream_ptr(stream)))
+    elif fused:
+        _n(1 if M > 16 else 2)
+        done = torch.empty(M // 128 + E + 1, dtype=torch.int32, device=xp.device)
+        check(L.vmm_grouped_swiglu_fused(ptr(xp), ptr(offsets), E, M, H, inter, ptr(arena), w2_base, stride,
+                                         n_slots, ptr(slot_of), ptr(need), ptr(ready), ready_base, ptr(done),
+                                         ptr(h1), ptr(y), stream_ptr(stream)))
     else:
         _n(2)
         check(L.vmm_grouped_swiglu(ptr(xp), ptr(offsets), E, M, H, inter, ptr(arena), w2_base, stride, n_slots,

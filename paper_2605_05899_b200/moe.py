@@ -282,6 +282,9 @@ class MoEStack:
         E, L = cfg.experts, cfg.layers
         self.slot_host = torch.zeros((L, E), dtype=torch.int32, pin_memory=True)
         self.slot_dev = torch.zeros((L, E), dtype=torch.int32, device=self.device)
+        # per-expert fill sequence numbers the fused FFN waits for (copy/compute overlap)
+        self.need_host = torch.zeros((L, E), dtype=torch.int32, pin_memory=True)
+        self.need_dev = torch.zeros((L, E), dtype=torch.int32, device=self.device)
         self.counts_host = torch.zeros((L, E), dtype=torch.int32, pin_memory=True)
         self.y_host = torch.zeros((L + 1, E), dtype=torch.float64, pin_memory=True)
         self.pow = torch.tensor(pow_table(cfg.history_decay, L), dtype=torch.float64, device=self.device)
@@ -326,6 +329,7 @@ class MoEStack:
                 xs=torch.empty(max(n_tok * c.shared_experts, 1), c.hidden, dtype=torch.bfloat16, device=dev),
                 h1s=torch.empty(max(n_tok * c.shared_experts, 1), c.inter, dtype=torch.bfloat16, device=dev),
                 ys=torch.empty(max(n_tok * c.shared_experts, 1), c.hidden, dtype=torch.bfloat16, device=dev),
+                ffn_done=torch.empty(M // 128 + c.experts + 1, dtype=torch.int32, device=dev),
             )
         return self._bufs
 
@@ -416,8 +420,13 @@ class MoEStack:
             raise ValidationError("saliency entries must be finite and >= 0")
         if R == 1:
             ret = pr["retained"][: int(n_ret[0])]
-        else:  # request-local ids -> global row ids, requests in order
-            ret = torch.cat([pr["retained"][offs[r]: offs[r] + int(n_ret[r])] + offs[r] for r in range(R)])
+        else:  # request-local ids -> global row ids, requests in order (constant launch count in R)
+            starts = torch.tensor(offs[:-1], dtype=torch.int32, device=dev)
+            lens = torch.tensor([offs[r + 1] - offs[r] for r in range(R)], dtype=torch.int64, device=dev)
+            seg = torch.repeat_interleave(torch.arange(R, device=dev), lens, output_size=T)
+            local = torch.arange(T, dtype=torch.int32, device=dev) - starts[seg]
+            valid = local < torch.from_numpy(n_ret.astype(np.int32)).to(dev)[seg]
+            ret = (pr["retained"][:T] + starts[seg])[valid]
         n_r = int(ret.shape[0])
         ret_off = np.concatenate([[0], np.cumsum(n_ret)]).astype(np.int64)
         xr = kernels.gather_rows(cur, ret, out=bufs["xp"][:n_r])  # scratch until permute of layer lp
@@ -515,7 +524,9 @@ class MoEStack:
             slot_host=self.slot_host.data_ptr(), shared=c.shared_experts,
             shared_slot_of=st.shared_slot_of.data_ptr() if st.shared_slot_of is not None else None,
             shared_src=bufs["shared_src"].data_ptr(), shared_off=bufs["shared_off"].data_ptr(),
-            xs=bufs["xs"].data_ptr(), h1s=bufs["h1s"].data_ptr(), ys=bufs["ys"].data_ptr())
+            xs=bufs["xs"].data_ptr(), h1s=bufs["h1s"].data_ptr(), ys=bufs["ys"].data_ptr(),
+            need_host=self.need_host.data_ptr(), need_dev=self.need_dev.data_ptr(),
+            ffn_done=bufs["ffn_done"].data_ptr())
         h = C.c_void_p()
         check(self._L.vmm_stack_create(C.byref(d), C.byref(h)))
         nl = l1 - l0

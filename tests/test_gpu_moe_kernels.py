@@ -41,14 +41,18 @@ def test_router_realistic_inputs_margin_aware():
     torch.testing.assert_close(gates.cpu()[safe], rg[safe], rtol=1e-4, atol=1e-5)
 
 
-def test_permute_plan_is_stable_counting_sort():
-    g = torch.Generator().manual_seed(3)
-    ids = torch.stack([torch.randperm(128, generator=g)[:8] for _ in range(1216)]).int()
-    off, src, pos = kernels.permute_plan(ids.cuda(), 128)
-    roff, rsrc, rpos = moe_ref.permute(ids, 128)
+@pytest.mark.parametrize("N,k,E", [(1216, 8, 128), (1000, 8, 128), (155648, 8, 128), (30000, 6, 64), (5000, 2, 4)])
+def test_permute_plan_is_stable_counting_sort(N, k, E):
+    """Single-CTA (<= 8192 picks) and multi-CTA (count / scan / scatter) paths."""
+    g = torch.Generator().manual_seed(3 + N)
+    # skewed, distinct ids per token (some experts empty at small E... all ids drawn from a biased order)
+    logits = torch.randn(N, E, generator=g) + torch.linspace(2, -2, E)
+    ids = torch.topk(logits, k, dim=1).indices.int()
+    off, src, pos = kernels.permute_plan(ids.cuda(), E)
+    roff, rsrc, rpos = moe_ref.permute(ids, E)
     assert torch.equal(off.cpu().long(), roff)
-    assert torch.equal(src.cpu().long(), rsrc)
-    assert torch.equal(pos.cpu().long().reshape(1216, 8), rpos)
+    assert torch.equal(src.cpu().long()[: N * k], rsrc)
+    assert torch.equal(pos.cpu().long()[: N * k].reshape(N, k), rpos)
 
 
 def _expert_setup(N, H, I, E, k, n_slots, seed):
@@ -192,3 +196,68 @@ def test_permute_plan_small_batches(N, k, E):
     assert torch.equal(off.cpu().long(), roff)
     assert torch.equal(src.cpu().long()[: N * k], rsrc)
     assert torch.equal(pos.cpu().long()[: N * k].reshape(N, k), rpos)
+
+
+@pytest.mark.parametrize("shape", [(1216, 2048, 768, 128, 8), (300, 256, 512, 8, 2), (640, 2048, 1408, 64, 6),
+                                   (9728, 2048, 768, 128, 8), (3, 2048, 768, 128, 8)])
+def test_fused_ffn_bit_identical_to_two_launches(shape):
+    """The one-launch persistent FFN (GEMM2 tiles gated on H1 block counters)
+    computes every tile exactly like the two-launch path."""
+    N, H, I, E, k = shape
+    n_slots = E + 3
+    x, wg, wu, wd, arena, ids, slot_of = _expert_setup(N, H, I, E, k, n_slots, seed=N + 2 * E)
+    off, src, pos = kernels.permute_plan(ids.cuda(), E)
+    xp = kernels.permute_rows(x.cuda(), src, N * k)
+    arena, slot_of = arena.cuda(), slot_of.cuda()
+    h1a, ya = kernels.grouped_swiglu(xp, off, arena, slot_of, I, fused=False)
+    h1b, yb = kernels.grouped_swiglu(xp, off, arena, slot_of, I, fused=True)
+    torch.cuda.synchronize()
+    assert torch.equal(h1a, h1b)
+    assert torch.equal(ya, yb)
+
+
+def test_fused_ffn_waits_for_copy_stream_fills():
+    """Copy overlap: the FFN is launched BEFORE its experts' weights are copied
+    in; each expert's tiles wait on the copy stream's ready flag.  The result
+    must equal the all-resident computation bit for bit."""
+    import ctypes as C
+
+    from paper_2605_05899_b200 import _lib
+
+    N, H, I, E, k = 1216, 2048, 768, 128, 8
+    x, wg, wu, wd, arena, ids, slot_of = _expert_setup(N, H, I, E, k, E, seed=77)
+    slot_of = torch.arange(E, dtype=torch.int32)  # expert e -> slab e
+    pool = arena.pin_memory()
+    L = _lib.lib()
+    xf = C.c_void_p()
+    _lib.check(L.vmm_xfer_create(E, arena.shape[1] * 2, 1, C.byref(xf)))
+    try:
+        ready = L.vmm_xfer_ready(xf)
+        assert ready
+        off, src, pos = kernels.permute_plan(ids.cuda(), E)
+        xp = kernels.permute_rows(x.cuda(), src, N * k)
+        dev_arena = torch.zeros_like(arena, device="cuda")
+        torch.cuda.synchronize()
+        need = torch.arange(1, E + 1, dtype=torch.int32, device="cuda")  # fill e is the (e+1)-th copy
+        ready_t = torch.empty(0)  # placeholder; pass the raw pointer below
+        h1 = torch.empty(N * k, I, dtype=torch.bfloat16, device="cuda")
+        y = torch.empty(N * k, H, dtype=torch.bfloat16, device="cuda")
+        done = torch.empty(N * k // 128 + E + 1, dtype=torch.int32, device="cuda")
+        w2 = dev_arena.data_ptr() + 2 * I * H * 2
+        _lib.check(L.vmm_grouped_swiglu_fused(xp.data_ptr(), off.data_ptr(), E, N * k, H, I, dev_arena.data_ptr(),
+                                              w2, 3 * I * H, E, slot_of.cuda().data_ptr(), need.data_ptr(), ready, 0,
+                                              done.data_ptr(), h1.data_ptr(), y.data_ptr(),
+                                              torch.cuda.current_stream().cuda_stream))
+        del ready_t
+        nbytes = arena.shape[1] * 2
+        for e in range(E):  # the copies are issued only now, while the FFN kernel already runs
+            _lib.check(L.vmm_xfer_copy(xf, e, pool[e].data_ptr(), dev_arena[e].data_ptr(), nbytes, 0))
+        torch.cuda.synchronize()
+        _lib.check(L.vmm_xfer_sync(xf))
+        h1r, yr = kernels.grouped_swiglu(xp, off, dev_arena, slot_of.cuda(), I, fused=False)
+        torch.cuda.synchronize()
+        assert torch.equal(dev_arena.cpu(), arena)
+        assert torch.equal(h1, h1r)
+        assert torch.equal(y, yr)
+    finally:
+        L.vmm_xfer_destroy(xf)

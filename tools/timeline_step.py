@@ -1,0 +1,48 @@
+"""Per-layer timeline of one batched prefill step (FFN events, host phases, copy stream).
+
+    python tools/timeline_step.py [requests] [workload]
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+from paper_2605_05899_b200.configs import WORKLOADS
+from paper_2605_05899_b200.moe import MoEStack, StackConfig
+from paper_2605_05899_b200.trace import generate_trace
+
+R = int(sys.argv[1]) if len(sys.argv) > 1 else 128
+w = WORKLOADS[sys.argv[2] if len(sys.argv) > 2 else "c3_qwen3vl"]
+cfg = StackConfig.from_workload(w, routing="live", predictor="gate", host_layers=8)
+stack = MoEStack(cfg, seed=1000)
+tr = generate_trace(w.trace_config(seed=0))
+T1 = tr.num_tokens
+x = torch.randn((T1 * R, w.hidden), device="cuda").to(torch.bfloat16)
+rng = np.random.default_rng(0)
+sal = torch.from_numpy(np.concatenate([tr.saliency] + [rng.gamma(2.0, 1.0, T1) for _ in range(R - 1)])).cuda()
+mod = torch.from_numpy(np.concatenate([tr.device_modality()] * R)).cuda()
+offs = [r * T1 for r in range(R + 1)]
+ITERS = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+for it in range(ITERS):
+    stack.profile = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    res = stack.forward(x, sal, mod, req_off=offs)
+    e1.record()
+    torch.cuda.synchronize()
+    prof = stack.profile
+    stack.profile = None
+total = e0.elapsed_time(e1)
+starts = [p[0] for p in prof]
+ffn = [p[0].elapsed_time(p[1]) for p in prof]
+lp = cfg.l_pinned
+print(f"R={R} step {total:.1f} ms, copies {res.copies}, h2d {res.h2d_bytes / 1e9:.1f} GB")
+print(f"prefix (start -> first cached FFN): {e0.elapsed_time(starts[lp]):.1f} ms; prefix FFN sum {sum(ffn[:lp]):.1f}")
+per = [starts[i].elapsed_time(starts[i + 1]) for i in range(lp, len(starts) - 1)]
+print(f"cached layers: period mean {np.mean(per):.2f} ms, FFN(incl. copy waits) mean {np.mean(ffn[lp:]):.2f} ms,"
+      f" non-FFN mean {np.mean(per) - np.mean(ffn[lp:-1]):.2f} ms")
+print("host us (pre, sync, decide, post) over cached layers:", [round(v / 1e3, 1) for v in stack.last_host_us])
+print("per-layer period:", [round(v, 1) for v in per])
+print("per-layer ffn   :", [round(v, 1) for v in ffn])
