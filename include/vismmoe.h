@@ -131,6 +131,11 @@ int vmm_gate_lookahead(const void *d_x, const void *d_wnext, int N, int H, int E
  * ------------------------------------------------------------------------ */
 int vmm_permute_plan(const int32_t *d_ids, int N, int k, int E, int32_t *d_offsets,
                      int32_t *d_src_row, int32_t *d_pos, void *stream);
+/* plan + row copy in one pass over the picks (token order: each X row is read
+ * once and stored to its k permuted positions): same outputs as
+ * vmm_permute_plan followed by vmm_permute_rows(d_x, d_src_row, N*k, H, d_xp) */
+int vmm_permute(const int32_t *d_ids, int N, int k, int E, const void *d_x, int H, int32_t *d_offsets,
+                int32_t *d_src_row, int32_t *d_pos, void *d_xp, void *stream);
 /* Xp[p] = X[src_row[p]] for the n_rows permuted rows (bf16 rows of H) */
 int vmm_permute_rows(const void *d_x, const int32_t *d_src_row, int n_rows, int H, void *d_xp, void *stream);
 /* combine plus S always-resident shared experts (unit weight; rows s*N + t of d_ys) */
@@ -173,12 +178,17 @@ int vmm_grouped_swiglu(const void *d_xp, const int32_t *d_offsets, int E, int M_
  * expert e first wait until d_ready[slot_of[e] - ready_base] >= d_need[e]
  * (u32 fill sequence numbers written by the copy stream after each fill, see
  * vmm_xfer_ready), so the layer computes on landed experts while the misses
- * still stream in.  need[e] == 0: no wait.  M_total <= 16 (decode) or
- * d_done == NULL falls through to vmm_grouped_swiglu (d_need must be NULL). */
+ * still stream in.  need[e] == 0: no wait.  Row gather: when d_src_row
+ * != NULL (the plan's [M_total] source rows) GEMM1 reads its A rows straight
+ * from d_x_rows [n_x_rows][H] with TMA tile::gather4 and d_xp is unused, so no
+ * permuted copy of the tokens is materialised.  M_total <= 16 (decode) or
+ * d_done == NULL falls through to vmm_grouped_swiglu (d_need and d_src_row
+ * must then be NULL). */
 int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offsets, int E, int M_total,
                              int H, int I, const void *d_w13_arena, const void *d_w2_arena, long long slot_stride,
                              long long n_slots, const int32_t *d_slot_of_expert, const uint32_t *d_need,
-                             const uint32_t *d_ready, int ready_base, uint32_t *d_done, void *d_h1, void *d_y,
+                             const uint32_t *d_ready, int ready_base, uint32_t *d_done,
+                             const void *d_x_rows, const int32_t *d_src_row, int n_x_rows, void *d_h1, void *d_y,
                              void *stream);
 /* Reference (CUDA-core, fp32) version of the same contraction for cross-checks. */
 int vmm_grouped_swiglu_simt(const void *d_xp, const int32_t *d_offsets, int E, int M_total,

@@ -84,10 +84,11 @@ _SIGS = {
     "vmm_gate_lookahead": (I32, [P, P, I32, I32, I32, I32, P, P, P]),
     "vmm_permute_plan": (I32, [P, I32, I32, I32, P, P, P, P]),
     "vmm_permute_rows": (I32, [P, P, I32, I32, P, P]),
+    "vmm_permute": (I32, [P, I32, I32, I32, P, I32, P, P, P, P, P]),
     "vmm_combine": (I32, [P, P, P, P, I32, I32, I32, P, P]),
     "vmm_rmsnorm": (I32, [P, P, I32, I32, C.c_float, P, P]),
     "vmm_grouped_swiglu": (I32, [P, P, I32, I32, I32, I32, P, P, I64, I64, P, P, P, P]),
-    "vmm_grouped_swiglu_fused": (I32, [P, P, I32, I32, I32, I32, P, P, I64, I64, P, P, P, I32, P, P, P, P]),
+    "vmm_grouped_swiglu_fused": (I32, [P, P, I32, I32, I32, I32, P, P, I64, I64, P, P, P, I32, P, P, P, I32, P, P, P]),
     "vmm_grouped_swiglu_simt": (I32, [P, P, I32, I32, I32, I32, P, P, I64, P, P, P, P]),
     "vmm_engine_create": (I32, [C.POINTER(EngineConfig), C.POINTER(P)]),
     "vmm_engine_destroy": (None, [P]),

@@ -16,6 +16,7 @@
 // A kStages-deep smem ring (full/empty mbarriers) overlaps TMA with MMA.
 #include <math.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "sm100.cuh"
@@ -272,17 +273,29 @@ __device__ __forceinline__ FusedTile fused_tile(int t, int n1, int n2, int MT, i
   return f;
 }
 
+// TN = N tile width (128 or 256): a 128x256 tile halves the A re-reads per FLOP
+// (L2->SMEM traffic is the limiter of a 128x128 tcgen05 tile).
+template <int TN>
+struct FusedCfg {
+  static constexpr int kStages = TN == 256 ? 4 : 6;
+  static constexpr uint32_t kATile = BM * BK * 2, kBTile = TN * BK * 2;
+  static constexpr uint32_t kStage = kATile + kBTile;
+  static constexpr size_t kSmem = (size_t)kStages * kStage + 1024 + 256;
+};
+
+template <int TN>
 __global__ void __launch_bounds__(kThreads, 1)
 ffn_fused_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w13,
                  const __grid_constant__ CUtensorMap map_h1, const __grid_constant__ CUtensorMap map_w2,
                  const int32_t *__restrict__ offsets, const int32_t *__restrict__ slot_of,
                  const uint32_t *__restrict__ need, const uint32_t *ready, int ready_base, uint32_t *done, int E,
-                 int H, int I, int lag, __nv_bfloat16 *__restrict__ h1, __nv_bfloat16 *__restrict__ y) {
+                 int H, int I, int lag, const int32_t *__restrict__ src_row, int M_total,
+                 __nv_bfloat16 *__restrict__ h1, __nv_bfloat16 *__restrict__ y) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * kStageBytes);
-  uint64_t *empty = full + kStages;
-  uint64_t *tmem_full = empty + kStages;   // [2]
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + FusedCfg<TN>::kStages * FusedCfg<TN>::kStage);
+  uint64_t *empty = full + FusedCfg<TN>::kStages;
+  uint64_t *tmem_full = empty + FusedCfg<TN>::kStages;   // [2]
   uint64_t *tmem_empty = tmem_full + 2;    // [2]
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 2);
   __shared__ int s_offs[VMM_MAX_EXPERTS + 1], s_tile_base[VMM_MAX_EXPERTS + 1], s_slots[VMM_MAX_EXPERTS];
@@ -308,13 +321,13 @@ ffn_fused_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
     prefetch_tmap(&map_w13);
     prefetch_tmap(&map_h1);
     prefetch_tmap(&map_w2);
-    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < FusedCfg<TN>::kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int b = 0; b < 2; ++b) { mbar_init(&tmem_full[b], 1); mbar_init(&tmem_empty[b], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(2 * BN));
+                 "r"(2 * TN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -322,33 +335,53 @@ ffn_fused_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int MT = s_tile_base[E];
-  const int n1 = (2 * I) / BN, n2 = H / BN;
+  const int n1 = (2 * I) / TN, n2 = H / TN;
   const int total = (MT + lag) * (n1 + n2);
   const int nk1 = H / BK, nk2 = I / BK;
 
   if (warp == 0) {
-    if (lane == 0) {
-      int it = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const FusedTile f = fused_tile(t, n1, n2, MT, lag);
-        if (!f.valid) continue;
-        const TileInfo ti = tile_info(f.m_tile * n1, n1, s_tile_base, s_offs, s_slots, E);
+    // TMA producer.  GEMM1 A rows come either from the permuted copy Xp (one
+    // box load) or -- src_row != NULL -- straight from the token rows X through
+    // tile::gather4 (each lane fetches 4 of the tile's 128 rows), which removes
+    // the permute_rows pass (Xp write + re-read) entirely.
+    int it = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const FusedTile f = fused_tile(t, n1, n2, MT, lag);
+      if (!f.valid) continue;
+      const TileInfo ti = tile_info(f.m_tile * n1, n1, s_tile_base, s_offs, s_slots, E);
+      if (lane == 0) {
         const uint32_t nd = s_need[ti.expert];
         // the expert's slot fill must have landed (copy stream -> ready flag)
         if (nd) wait_at_least(ready + (ti.slot - ready_base), nd, 256);
         // GEMM2: H1 rows of this m-tile complete (all GEMM1 n-tiles stored)
         if (f.gemm2) wait_at_least(done + f.m_tile, 4u * (uint32_t)n1, 64);
         if (nd || f.gemm2) fence_proxy_async_global();
-        const CUtensorMap *ma = f.gemm2 ? &map_h1 : &map_x;
-        const CUtensorMap *mb = f.gemm2 ? &map_w2 : &map_w13;
-        const int nk = f.gemm2 ? nk2 : nk1;
-        for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % kStages;
-          if (it >= kStages) mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
-          unsigned char *a_dst = smem + s * kStageBytes;
-          mbar_expect_tx(&full[s], kStageBytes);
-          tma_load_2d(ma, &full[s], a_dst, kb * BK, ti.row0);
-          tma_load_3d(mb, &full[s], a_dst + kTileBytes, kb * BK, f.n_tile * BN, ti.slot);
+      }
+      const bool gather = src_row != nullptr && !f.gemm2;
+      int g[4];
+      if (gather) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int p = ti.row0 + 4 * lane + j;  // rows past the layer end: any valid row (masked later)
+          g[j] = __ldg(src_row + (p < M_total ? p : M_total - 1));
+        }
+      }
+      __syncwarp();
+      const CUtensorMap *ma = f.gemm2 ? &map_h1 : &map_x;
+      const CUtensorMap *mb = f.gemm2 ? &map_w2 : &map_w13;
+      const int nk = f.gemm2 ? nk2 : nk1;
+      for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int s = it % FusedCfg<TN>::kStages;
+        unsigned char *a_dst = smem + s * FusedCfg<TN>::kStage;
+        if (lane == 0) {
+          if (it >= FusedCfg<TN>::kStages) mbar_wait(&empty[s], ((it / FusedCfg<TN>::kStages) - 1) & 1);
+          mbar_expect_tx(&full[s], FusedCfg<TN>::kStage);
+          tma_load_3d(mb, &full[s], a_dst + FusedCfg<TN>::kATile, kb * BK, f.n_tile * TN, ti.slot);
+          if (!gather) tma_load_2d(ma, &full[s], a_dst, kb * BK, ti.row0);
+        }
+        if (gather) {
+          __syncwarp();  // stage free + expect_tx posted before the gathers complete bytes
+          tma_gather4(ma, &full[s], a_dst + lane * 4 * BK * 2, kb * BK, g[0], g[1], g[2], g[3]);
         }
       }
     }
@@ -362,16 +395,16 @@ ffn_fused_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
         const int b = local & 1, use = local >> 1;
         if (use > 0) mbar_wait(&tmem_empty[b], (use - 1) & 1);
         tc_fence_after();
-        const uint32_t acc = tmem + b * BN;
+        const uint32_t acc = tmem + b * TN;
         for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % kStages;
-          mbar_wait(&full[s], (it / kStages) & 1);
+          const int s = it % FusedCfg<TN>::kStages;
+          mbar_wait(&full[s], (it / FusedCfg<TN>::kStages) & 1);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(smem + s * kStageBytes);
-          const uint32_t b_addr = a_addr + kTileBytes;
+          const uint32_t a_addr = smem_u32(smem + s * FusedCfg<TN>::kStage);
+          const uint32_t b_addr = a_addr + FusedCfg<TN>::kATile;
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk)
-            umma_bf16(acc, sw128_desc(a_addr + kk * 32), sw128_desc(b_addr + kk * 32), idesc_bf16(BM, BN),
+            umma_bf16(acc, sw128_desc(a_addr + kk * 32), sw128_desc(b_addr + kk * 32), idesc_bf16(BM, TN),
                       (kb | kk) != 0);
           umma_commit(&empty[s]);
         }
@@ -392,20 +425,23 @@ ffn_fused_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
       const int row = ti.row0 + q * 32 + lane;
       mbar_wait(&tmem_full[b], use & 1);
       tc_fence_after();
-      const uint32_t t_base = tmem + b * BN + ((uint32_t)(q * 32) << 16);
+      const uint32_t t_base = tmem + b * TN + ((uint32_t)(q * 32) << 16);
       if (!f.gemm2) {
+        // accumulator columns: TN/128 pairs of [64 gate | 64 up] -> 64 H1 columns each
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
+        for (int hc = 0; hc < TN / 64; ++hc) {
+          const int pair = hc >> 1, half = hc & 1;
           float g[32], u[32];
-          tmem_ld32(t_base + half * 32, g);
-          tmem_ld32(t_base + 64 + half * 32, u);
-          if (half == 1) {
+          tmem_ld32(t_base + pair * 128 + half * 32, g);
+          tmem_ld32(t_base + pair * 128 + 64 + half * 32, u);
+          if (hc == TN / 64 - 1) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tmem_empty[b]);
           }
           if (row < ti.row_end) {
-            uint4 *dst = reinterpret_cast<uint4 *>(h1 + (long long)row * I + f.n_tile * (BN / 2) + half * 32);
+            uint4 *dst = reinterpret_cast<uint4 *>(h1 + (long long)row * I + f.n_tile * (TN / 2) + pair * 64 +
+                                                   half * 32);
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
               uint4 o;
@@ -424,16 +460,16 @@ ffn_fused_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
         if (lane == 0) red_release_add(done + f.m_tile, 1u);
       } else {
 #pragma unroll
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = 0; c < TN / 32; ++c) {
           float a[32];
           tmem_ld32(t_base + c * 32, a);
-          if (c == BN / 32 - 1) {
+          if (c == TN / 32 - 1) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tmem_empty[b]);
           }
           if (row < ti.row_end) {
-            uint4 *dst = reinterpret_cast<uint4 *>(y + (long long)row * H + f.n_tile * BN + c * 32);
+            uint4 *dst = reinterpret_cast<uint4 *>(y + (long long)row * H + f.n_tile * TN + c * 32);
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
               uint4 o;
@@ -452,7 +488,7 @@ ffn_fused_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TN));
   }
 }
 
@@ -728,11 +764,13 @@ extern "C" int vmm_grouped_swiglu(const void *d_xp, const int32_t *d_offsets, in
 extern "C" int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offsets, int E, int M_total, int H, int I,
                                         const void *d_w13_arena, const void *d_w2_arena, long long slot_stride,
                                         long long n_slots, const int32_t *d_slot_of_expert, const uint32_t *d_need,
-                                        const uint32_t *d_ready, int ready_base, uint32_t *d_done, void *d_h1,
+                                        const uint32_t *d_ready, int ready_base, uint32_t *d_done,
+                                        const void *d_x_rows, const int32_t *d_src_row, int n_x_rows, void *d_h1,
                                         void *d_y, void *stream) {
   if (M_total <= 0) return VMM_OK;
   if (M_total <= kSkinnyRows || d_done == nullptr)  // decode-sized: skinny path (callers fence on events)
     return d_need ? vmm::fail(VMM_ECONTRACT, "ready flags need the fused tensor-core path (M > 16, scratch)")
+         : d_src_row ? vmm::fail(VMM_ECONTRACT, "row gather needs the fused tensor-core path (M > 16, scratch)")
                   : vmm_grouped_swiglu(d_xp, d_offsets, E, M_total, H, I, d_w13_arena, d_w2_arena, slot_stride,
                                        n_slots, d_slot_of_expert, d_h1, d_y, stream);
   if (H % BN || H % BK || I % 64 || I % BK || (2 * I) % BN)
@@ -740,16 +778,29 @@ extern "C" int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offse
   if (E < 1 || E > VMM_MAX_EXPERTS) return vmm::fail(VMM_EVALIDATION, "experts must lie in [1, 256]");
   if (slot_stride % 8) return vmm::fail(VMM_EVALIDATION, "slot stride must be a multiple of 8 elements");
   if (d_need && !d_ready) return vmm::fail(VMM_ECONTRACT, "need[] without ready flags");
+  // 128x256 tiles when the widths allow (H and 2I multiples of 256), else 128x128
+  static const bool force_narrow = std::getenv("VMM_FFN_TN128") != nullptr;  // A/B comparison knob
+  const bool wide = !force_narrow && (H % 256 == 0) && ((2 * I) % 256 == 0);
+  const int TN = wide ? 256 : 128;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e1 = cudaFuncSetAttribute(ffn_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)kSmemBytes);
+    cudaError_t e1 = cudaFuncSetAttribute(ffn_fused_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)FusedCfg<256>::kSmem);
+    if (e1 == cudaSuccess)
+      e1 = cudaFuncSetAttribute(ffn_fused_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)FusedCfg<128>::kSmem);
     if (e1 != cudaSuccess) return vmm::cuda_status(e1, "ffn fused attr");
     attr = true;
   }
   CUtensorMap mx, mw13, mh1, mw2;
   int st;
-  {
+  if (d_src_row) {  // A rows gathered from the token rows (tile::gather4: box of one row)
+    if (!d_x_rows || n_x_rows <= 0) return vmm::fail(VMM_ECONTRACT, "row gather needs the token rows");
+    uint64_t dims[2] = {(uint64_t)H, (uint64_t)n_x_rows};
+    uint64_t str[1] = {(uint64_t)H * 2};
+    uint32_t box[2] = {BK, 1};
+    if ((st = make_map(&mx, d_x_rows, 2, dims, str, box))) return st;
+  } else {
     uint64_t dims[2] = {(uint64_t)H, (uint64_t)M_total};
     uint64_t str[1] = {(uint64_t)H * 2};
     uint32_t box[2] = {BK, BM};
@@ -758,7 +809,7 @@ extern "C" int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offse
   {
     uint64_t dims[3] = {(uint64_t)H, (uint64_t)2 * I, (uint64_t)n_slots};
     uint64_t str[2] = {(uint64_t)H * 2, (uint64_t)slot_stride * 2};
-    uint32_t box[3] = {BK, BN, 1};
+    uint32_t box[3] = {BK, (uint32_t)TN, 1};
     if ((st = make_map(&mw13, d_w13_arena, 3, dims, str, box))) return st;
   }
   {
@@ -770,7 +821,7 @@ extern "C" int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offse
   {
     uint64_t dims[3] = {(uint64_t)I, (uint64_t)H, (uint64_t)n_slots};
     uint64_t str[2] = {(uint64_t)I * 2, (uint64_t)slot_stride * 2};
-    uint32_t box[3] = {BK, BN, 1};
+    uint32_t box[3] = {BK, (uint32_t)TN, 1};
     if ((st = make_map(&mw2, d_w2_arena, 3, dims, str, box))) return st;
   }
   if (!g_num_sms) {
@@ -779,15 +830,20 @@ extern "C" int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offse
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int max_m_tiles = (M_total + BM - 1) / BM + E;
-  const int n1 = (2 * I) / BN, n2 = H / BN;
+  const int n1 = (2 * I) / TN, n2 = H / TN;
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t ce = cudaMemsetAsync(d_done, 0, sizeof(uint32_t) * max_m_tiles, s);
   if (ce != cudaSuccess) return vmm::cuda_status(ce, "ffn done memset");
   const int grid = g_num_sms < max_m_tiles * (n1 + n2) ? g_num_sms : max_m_tiles * (n1 + n2);
   const int lag = (2 * grid + n1 + n2 - 1) / (n1 + n2);  // GEMM2 tiles ~2 waves behind their GEMM1 tiles
-  ffn_fused_kernel<<<grid, kThreads, kSmemBytes, s>>>(mx, mw13, mh1, mw2, d_offsets, d_slot_of_expert, d_need,
-                                                      d_ready, ready_base, d_done, E, H, I, lag,
-                                                      (__nv_bfloat16 *)d_h1, (__nv_bfloat16 *)d_y);
+  if (wide)
+    ffn_fused_kernel<256><<<grid, kThreads, FusedCfg<256>::kSmem, s>>>(
+        mx, mw13, mh1, mw2, d_offsets, d_slot_of_expert, d_need, d_ready, ready_base, d_done, E, H, I, lag,
+        d_src_row, M_total, (__nv_bfloat16 *)d_h1, (__nv_bfloat16 *)d_y);
+  else
+    ffn_fused_kernel<128><<<grid, kThreads, FusedCfg<128>::kSmem, s>>>(
+        mx, mw13, mh1, mw2, d_offsets, d_slot_of_expert, d_need, d_ready, ready_base, d_done, E, H, I, lag,
+        d_src_row, M_total, (__nv_bfloat16 *)d_h1, (__nv_bfloat16 *)d_y);
   VMM_LAUNCH_CHECK("ffn_fused_kernel");
   return VMM_OK;
 }

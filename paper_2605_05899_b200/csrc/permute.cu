@@ -217,14 +217,16 @@ namespace {
 //   1. plan_count   : per-CTA expert counts           blk[b][e]
 //   2. plan_scan    : expert offsets + per-CTA bases  blk[b][e] <- offsets[e] + sum_{b'<b} cnt[b'][e]
 //   3. plan_scatter : per-warp bases inside the CTA, ranks by match_any -> pos/src_row
+// chunk = picks per CTA (a multiple of 256, chosen by the host so the grid covers the SMs)
 constexpr int kChunk = 8192, kPT = 256, kPW = kPT / 32;
 
-__device__ __forceinline__ void chunk_warp_counts(const int32_t *__restrict__ ids, int n_picks, int32_t *cnt, int E) {
+__device__ __forceinline__ void chunk_warp_counts(const int32_t *__restrict__ ids, int n_picks, int chunk,
+                                                  int32_t *cnt, int E) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < kPW * E; i += kPT) cnt[i] = 0;
   __syncthreads();
-  const int lo = blockIdx.x * kChunk + warp * (kChunk / kPW);
-  const int hi = min(n_picks, lo + kChunk / kPW);
+  const int lo = blockIdx.x * chunk + warp * (chunk / kPW);
+  const int hi = min(n_picks, lo + chunk / kPW);
   for (int c0 = lo; c0 < hi; c0 += 32) {
     const int i = c0 + lane;
     const int e = (i < hi) ? __ldg(ids + i) : -1;
@@ -235,10 +237,10 @@ __device__ __forceinline__ void chunk_warp_counts(const int32_t *__restrict__ id
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kPT) plan_count_kernel(const int32_t *__restrict__ ids, int n_picks, int E,
-                                                         int32_t *__restrict__ blk) {
+__global__ void __launch_bounds__(kPT) plan_count_kernel(const int32_t *__restrict__ ids, int n_picks, int chunk,
+                                                         int E, int32_t *__restrict__ blk) {
   __shared__ int32_t cnt[kPW * VMM_MAX_EXPERTS];
-  chunk_warp_counts(ids, n_picks, cnt, E);
+  chunk_warp_counts(ids, n_picks, chunk, cnt, E);
   for (int e = threadIdx.x; e < E; e += kPT) {
     int s = 0;
 #pragma unroll
@@ -247,16 +249,29 @@ __global__ void __launch_bounds__(kPT) plan_count_kernel(const int32_t *__restri
   }
 }
 
-__global__ void __launch_bounds__(VMM_MAX_EXPERTS) plan_scan_kernel(int32_t *__restrict__ blk, int G, int E,
-                                                                   int32_t *__restrict__ offsets) {
+// one CTA of 1024 threads: S = 1024/E threads per expert, each owning a contiguous
+// range of CTAs (block order is pick order, so the per-CTA bases stay stable)
+__global__ void __launch_bounds__(1024) plan_scan_kernel(int32_t *__restrict__ blk, int G, int E,
+                                                         int32_t *__restrict__ offsets) {
+  __shared__ int32_t part[1024];
   __shared__ int32_t tot[VMM_MAX_EXPERTS + 1];
-  const int e = threadIdx.x;
+  const int S = 1024 / E;  // E <= 256 -> S >= 4
+  const int e = threadIdx.x % E, sl = threadIdx.x / E;
+  const bool active = sl < S;
+  const int per = (G + S - 1) / S;
+  const int b0 = sl * per, b1 = min(G, b0 + per);
   int s = 0;
-  if (e < E)
-    for (int b = 0; b < G; ++b) s += blk[(long long)b * E + e];
-  tot[e] = s;
+  if (active)
+    for (int b = b0; b < b1; ++b) s += blk[(long long)b * E + e];
+  part[threadIdx.x] = s;
   __syncthreads();
-  if (e == 0) {
+  if (threadIdx.x < E) {
+    int t = 0;
+    for (int j = 0; j < S; ++j) t += part[j * E + threadIdx.x];
+    tot[threadIdx.x] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
     int run = 0;
     for (int x = 0; x < E; ++x) {
       const int t = tot[x];
@@ -267,9 +282,10 @@ __global__ void __launch_bounds__(VMM_MAX_EXPERTS) plan_scan_kernel(int32_t *__r
     offsets[E] = run;
   }
   __syncthreads();
-  if (e < E) {
+  if (active) {
     int run = tot[e];
-    for (int b = 0; b < G; ++b) {
+    for (int j = 0; j < sl; ++j) run += part[j * E + e];
+    for (int b = b0; b < b1; ++b) {
       const int c = blk[(long long)b * E + e];
       blk[(long long)b * E + e] = run;
       run += c;
@@ -277,11 +293,17 @@ __global__ void __launch_bounds__(VMM_MAX_EXPERTS) plan_scan_kernel(int32_t *__r
   }
 }
 
-__global__ void __launch_bounds__(kPT) plan_scatter_kernel(const int32_t *__restrict__ ids, int n_picks, int k, int E,
-                                                           const int32_t *__restrict__ blk,
-                                                           int32_t *__restrict__ src_row, int32_t *__restrict__ pos) {
+// x/xp != NULL: also copy the rows (fused permute).  Picks are visited in token
+// order, so each token row is read from HBM once (into registers) and stored to
+// its k permuted positions -- a separate permute_rows pass re-reads the row per
+// pick in permuted order (k x the reads once X exceeds L2).
+__global__ void __launch_bounds__(kPT) plan_scatter_kernel(const int32_t *__restrict__ ids, int n_picks, int chunk,
+                                                           int k, int E, const int32_t *__restrict__ blk,
+                                                           int32_t *__restrict__ src_row, int32_t *__restrict__ pos,
+                                                           const uint4 *__restrict__ x, int row_vec,
+                                                           uint4 *__restrict__ xp) {
   __shared__ int32_t cnt[kPW * VMM_MAX_EXPERTS];
-  chunk_warp_counts(ids, n_picks, cnt, E);
+  chunk_warp_counts(ids, n_picks, chunk, cnt, E);
   for (int e = threadIdx.x; e < E; e += kPT) {
     int run = blk[(long long)blockIdx.x * E + e];
 #pragma unroll
@@ -293,22 +315,46 @@ __global__ void __launch_bounds__(kPT) plan_scatter_kernel(const int32_t *__rest
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int lo = blockIdx.x * kChunk + warp * (kChunk / kPW);
-  const int hi = min(n_picks, lo + kChunk / kPW);
+  const int lo = blockIdx.x * chunk + warp * (chunk / kPW);
+  const int hi = min(n_picks, lo + chunk / kPW);
   for (int c0 = lo; c0 < hi; c0 += 32) {
     const int i = c0 + lane;
     const int e = (i < hi) ? __ldg(ids + i) : -1;
     const unsigned peers = __match_any_sync(0xffffffffu, e);
     const int leader = __ffs(peers) - 1;
     const int basep = (e >= 0) ? cnt[warp * E + e] : 0;
+    const int p = (e >= 0) ? basep + __popc(peers & ((1u << lane) - 1u)) : -1;
     if (e >= 0) {
-      const int p = basep + __popc(peers & ((1u << lane) - 1u));
       pos[i] = p;
       src_row[p] = i / k;
     }
     __syncwarp();
     if (e >= 0 && lane == leader) cnt[warp * E + e] = basep + __popc(peers);
     __syncwarp();
+    if (xp != nullptr) {
+      int cur_t = -1;
+      uint4 v[8];  // the current token's row: 8 x 16 B per lane covers H <= 2048; longer rows loop
+      for (int j = 0; j < 32; ++j) {
+        const int pj = __shfl_sync(0xffffffffu, p, j);
+        if (pj < 0) continue;  // warp-uniform
+        const int t = (c0 + j) / k;
+        for (int c0v = 0; c0v < row_vec; c0v += 32 * 8) {
+          if (t != cur_t || row_vec > 32 * 8) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int c = c0v + lane + 32 * u;
+              if (c < row_vec) v[u] = __ldg(x + (long long)t * row_vec + c);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int c = c0v + lane + 32 * u;
+            if (c < row_vec) xp[(long long)pj * row_vec + c] = v[u];
+          }
+        }
+        cur_t = t;
+      }
+    }
   }
 }
 
@@ -339,8 +385,22 @@ __global__ void permute_plan_warp_kernel(const int32_t *__restrict__ ids, int n_
 }
 }  // namespace
 
+static int permute_impl(const int32_t *d_ids, int N, int k, int E, int32_t *d_offsets, int32_t *d_src_row,
+                        int32_t *d_pos, const void *d_x, int H, void *d_xp, void *stream);
+
 extern "C" int vmm_permute_plan(const int32_t *d_ids, int N, int k, int E, int32_t *d_offsets, int32_t *d_src_row,
                                 int32_t *d_pos, void *stream) {
+  return permute_impl(d_ids, N, k, E, d_offsets, d_src_row, d_pos, nullptr, 0, nullptr, stream);
+}
+
+extern "C" int vmm_permute(const int32_t *d_ids, int N, int k, int E, const void *d_x, int H, int32_t *d_offsets,
+                           int32_t *d_src_row, int32_t *d_pos, void *d_xp, void *stream) {
+  if ((H * 2) % 16) return vmm::fail(VMM_EVALIDATION, "hidden size must be a multiple of 8");
+  return permute_impl(d_ids, N, k, E, d_offsets, d_src_row, d_pos, d_x, H, d_xp, stream);
+}
+
+static int permute_impl(const int32_t *d_ids, int N, int k, int E, int32_t *d_offsets, int32_t *d_src_row,
+                        int32_t *d_pos, const void *d_x, int H, void *d_xp, void *stream) {
   if (E < 1 || E > VMM_MAX_EXPERTS) return vmm::fail(VMM_EVALIDATION, "experts must lie in [1, 256]");
   if (N * k <= 32) {
     permute_plan_warp_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(d_ids, N * k, k, E, d_offsets, d_src_row, d_pos);
@@ -348,8 +408,11 @@ extern "C" int vmm_permute_plan(const int32_t *d_ids, int N, int k, int E, int32
     return VMM_OK;
   }
   const int n_picks = N * k;
-  if (n_picks > kChunk) {  // multi-CTA stable sort; per-CTA counts in a library scratch (per device)
-    const int G = (n_picks + kChunk - 1) / kChunk;
+  if (n_picks > 2048) {  // multi-CTA stable sort; per-CTA counts in a library scratch (per device)
+    // ~4 CTAs per SM, chunks of 1024..8192 picks (multiple of 256: 8 warps x whole 32-pick rounds)
+    int chunk = (n_picks / (148 * 4) + 255) / 256 * 256;
+    chunk = chunk < 1024 ? 1024 : (chunk > kChunk ? kChunk : chunk);
+    const int G = (n_picks + chunk - 1) / chunk;
     static int32_t *scratch[64] = {nullptr};
     static size_t cap[64] = {0};
     int dev = 0;
@@ -363,13 +426,19 @@ extern "C" int vmm_permute_plan(const int32_t *d_ids, int N, int k, int E, int32
       cap[dev] = need * 2;
     }
     cudaStream_t st = (cudaStream_t)stream;
-    plan_count_kernel<<<G, kPT, 0, st>>>(d_ids, n_picks, E, scratch[dev]);
+    plan_count_kernel<<<G, kPT, 0, st>>>(d_ids, n_picks, chunk, E, scratch[dev]);
     VMM_LAUNCH_CHECK("plan_count_kernel");
-    plan_scan_kernel<<<1, VMM_MAX_EXPERTS, 0, st>>>(scratch[dev], G, E, d_offsets);
+    plan_scan_kernel<<<1, 1024, 0, st>>>(scratch[dev], G, E, d_offsets);
     VMM_LAUNCH_CHECK("plan_scan_kernel");
-    plan_scatter_kernel<<<G, kPT, 0, st>>>(d_ids, n_picks, k, E, scratch[dev], d_src_row, d_pos);
+    plan_scatter_kernel<<<G, kPT, 0, st>>>(d_ids, n_picks, chunk, k, E, scratch[dev], d_src_row, d_pos,
+                                           (const uint4 *)d_x, H * 2 / 16, (uint4 *)d_xp);
     VMM_LAUNCH_CHECK("plan_scatter_kernel");
     return VMM_OK;
+  }
+  if (d_xp) {  // small batches: plan, then the row copy
+    int st = permute_impl(d_ids, N, k, E, d_offsets, d_src_row, d_pos, nullptr, 0, nullptr, stream);
+    if (st) return st;
+    return vmm_permute_rows(d_x, d_src_row, n_picks, H, d_xp, stream);
   }
   size_t smem = sizeof(int32_t) * ((size_t)kWarps * E + E);
   static bool attr = false;

@@ -185,24 +185,34 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
     }
     auto c3 = clk::now();
     const int M = n_rows * k;
-    VMM_TRY(vmm_permute_plan(d.ids, n_rows, k, E, d.off, d.src, d.pos, stream));
-    VMM_TRY(vmm_permute_rows(xn, d.src, M, H, d.xp, stream));
+    // VMM_FFN_GATHER=1: the tensor-core FFN gathers its rows from xn (TMA gather4) instead of a
+    // permuted copy.  Measured slower on B200 (32 gather4 issues per 16 KB A stage: 20.0 vs 10.9 ms
+    // at 1.25M rows), so the permuted copy is the default.
+    static const bool gather_env = std::getenv("VMM_FFN_GATHER") != nullptr;
+    const bool gather = gather_env && d.ffn_done && M > 16;
+    if (gather)
+      VMM_TRY(vmm_permute_plan(d.ids, n_rows, k, E, d.off, d.src, d.pos, stream));
+    else
+      VMM_TRY(vmm_permute(d.ids, n_rows, k, E, xn, H, d.off, d.src, d.pos, d.xp, stream));
     if (out && out->ffn_start)
       VMM_CUDA(cudaEventRecord((cudaEvent_t)out->ffn_start[l - l0], st), "ffn start event");
     VMM_TRY(vmm_grouped_swiglu_fused(d.xp, d.off, E, M, H, I, d.arena, (const char *)d.arena + (size_t)2 * I * H * 2,
                                      (long long)3 * I * H, d.n_slots, slot_of, need_of, ready,
-                                     (int)d.n_pinned_slots, d.ffn_done, d.h1, d.y, stream));
+                                     (int)d.n_pinned_slots, d.ffn_done, gather ? xn : nullptr,
+                                     gather ? d.src : nullptr, n_rows, d.h1, d.y, stream));
     if (out && out->ffn_end) VMM_CUDA(cudaEventRecord((cudaEvent_t)out->ffn_end[l - l0], st), "ffn end event");
     void *dst = ping ? d.out1 : d.out0;
     const int S = d.shared;
     if (S > 0) {
       // always-resident shared experts: every token through each, grouped GEMM over S groups
       const int MS = n_rows * S;
+      const bool gather_s = gather_env && d.ffn_done && MS > 16;
       VMM_TRY(vmm_shared_plan(n_rows, S, d.shared_src, d.shared_off, stream));
-      VMM_TRY(vmm_permute_rows(xn, d.shared_src, MS, H, d.xs, stream));
+      if (!gather_s) VMM_TRY(vmm_permute_rows(xn, d.shared_src, MS, H, d.xs, stream));
       VMM_TRY(vmm_grouped_swiglu_fused(d.xs, d.shared_off, S, MS, H, I, d.arena,
                                        (const char *)d.arena + (size_t)2 * I * H * 2, (long long)3 * I * H, d.n_slots,
-                                       d.shared_slot_of + (size_t)l * S, nullptr, nullptr, 0, d.ffn_done, d.h1s,
+                                       d.shared_slot_of + (size_t)l * S, nullptr, nullptr, 0, d.ffn_done,
+                                       gather_s ? xn : nullptr, gather_s ? d.shared_src : nullptr, n_rows, d.h1s,
                                        d.ys, stream));
     }
     if (l + 1 < l1) {  // combine fused with the next layer's RMSNorm (xn is free again: consumed above)

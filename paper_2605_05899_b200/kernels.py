@@ -174,6 +174,22 @@ def permute_plan(ids, experts: int, stream=None, bufs=None):
     return offsets, src_row, pos
 
 
+def permute(ids, x, experts: int, stream=None, bufs=None, out=None):
+    """Fused plan + row copy: (offsets, src_row, pos, xp) with xp[p] = x[src_row[p]]."""
+    N, k = (int(s) for s in ids.shape)
+    H = int(x.shape[1])
+    if bufs is None:
+        bufs = (torch.empty(experts + 1, dtype=_i32, device=ids.device),
+                torch.empty(max(N * k, 1), dtype=_i32, device=ids.device),
+                torch.empty(max(N * k, 1), dtype=_i32, device=ids.device))
+    offsets, src_row, pos = bufs
+    out = torch.empty(N * k, H, dtype=x.dtype, device=x.device) if out is None else out
+    _n(3)
+    check(_lib.lib().vmm_permute(ptr(ids), N, k, experts, ptr(x), H, ptr(offsets), ptr(src_row), ptr(pos),
+                                 ptr(out), stream_ptr(stream)))
+    return offsets, src_row, pos, out
+
+
 def permute_rows(x, src_row, n_rows: int, stream=None, out=None):
     H = int(x.shape[1])
     out = torch.empty(n_rows, H, dtype=x.dtype, device=x.device) if out is None else out
@@ -183,22 +199,29 @@ def permute_rows(x, src_row, n_rows: int, stream=None, out=None):
 
 
 def grouped_swiglu(xp, offsets, arena, slot_of, inter: int, stream=None, h1=None, y=None, simt: bool = False,
-                   fused: bool = True, need=None, ready=None, ready_base: int = 0):
+                   fused: bool = True, need=None, ready=None, ready_base: int = 0, x_rows=None, src_row=None):
     """Grouped SwiGLU over expert-contiguous rows of xp.
 
     Default: the fused persistent tcgen05 kernel (GEMM1+GEMM2 in one launch);
     fused=False: two tcgen05 launches; simt=True: CUDA-core cross-check.
     need/ready: optional per-expert fill sequence numbers / device flags
-    (vmm_grouped_swiglu_fused's copy overlap).
+    (vmm_grouped_swiglu_fused's copy overlap).  x_rows/src_row: gather the
+    GEMM1 rows from the token rows (TMA gather4) -- xp may then be None and
+    only its row count matters (pass an int).
     arena: bf16 [n_slots, 3*I*H] -- per slot W13 ([2I,H], interleaved) then W2 ([H,I])."""
-    M, H = (int(s) for s in xp.shape)
+    if src_row is not None:
+        M, H = int(xp), int(x_rows.shape[1])
+        dev, xp = x_rows.device, None
+    else:
+        M, H = (int(s) for s in xp.shape)
+        dev = xp.device
     E = int(offsets.shape[0]) - 1
     n_slots, stride = (int(s) for s in arena.shape[:2])
     if stride != 3 * inter * H:
         raise ValueError("arena slot must hold W13 and W2 (3*I*H elements)")
     w2_base = arena.data_ptr() + 2 * inter * H * 2
-    h1 = torch.empty(M, inter, dtype=torch.bfloat16, device=xp.device) if h1 is None else h1
-    y = torch.empty(M, H, dtype=torch.bfloat16, device=xp.device) if y is None else y
+    h1 = torch.empty(M, inter, dtype=torch.bfloat16, device=dev) if h1 is None else h1
+    y = torch.empty(M, H, dtype=torch.bfloat16, device=dev) if y is None else y
     L = _lib.lib()
     if simt:
         _n(2)
@@ -206,9 +229,10 @@ def grouped_swiglu(xp, offsets, arena, slot_of, inter: int, stream=None, h1=None
                                         ptr(slot_of), ptr(h1), ptr(y), stream_ptr(stream)))
     elif fused:
         _n(1 if M > 16 else 2)
-        done = torch.empty(M // 128 + E + 1, dtype=torch.int32, device=xp.device)
+        done = torch.empty(M // 128 + E + 1, dtype=torch.int32, device=dev)
         check(L.vmm_grouped_swiglu_fused(ptr(xp), ptr(offsets), E, M, H, inter, ptr(arena), w2_base, stride,
-                                         n_slots, ptr(slot_of), ptr(need), ptr(ready), ready_base, ptr(done),
+                                         n_slots, ptr(slot_of), ptr(need), ready, ready_base, ptr(done),
+                                         ptr(x_rows), ptr(src_row), 0 if x_rows is None else int(x_rows.shape[0]),
                                          ptr(h1), ptr(y), stream_ptr(stream)))
     else:
         _n(2)

@@ -28,6 +28,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass, field, replace
 
 import numpy as np
@@ -40,6 +41,8 @@ from .configs import Workload
 from .errors import ContractError, ValidationError
 from .pipeline import Engine, PredictorSpec, SimConfig, SimReport
 from .predictor import decay_table, pow_table
+
+_GATHER = bool(os.environ.get("VMM_FFN_GATHER"))
 
 
 @dataclass
@@ -336,13 +339,19 @@ class MoEStack:
     def _layer_compute(self, x, xn, ids, gates, slot_of, bufs, out, n_experts=None):
         c = self.cfg
         N = int(x.shape[0])
-        off, src, pos = kernels.permute_plan(ids, c.experts, bufs=(bufs["off"], bufs["src"], bufs["pos"]))
-        xp = kernels.permute_rows(xn, src, N * c.k, out=bufs["xp"][: N * c.k])
+        M = N * c.k
+        gather = _GATHER and M > 16  # VMM_FFN_GATHER=1: rows gathered by TMA gather4 (slower, see stack.cpp)
+        if gather:
+            off, src, pos = kernels.permute_plan(ids, c.experts, bufs=(bufs["off"], bufs["src"], bufs["pos"]))
+            xp = M
+        else:
+            off, src, pos, xp = kernels.permute(ids, xn, c.experts, bufs=(bufs["off"], bufs["src"], bufs["pos"]),
+                                                out=bufs["xp"][:M])
         if self.profile is not None:
             e0 = torch.cuda.Event(enable_timing=True)
             e0.record()
-        _, y = kernels.grouped_swiglu(xp, off, self.store.arena, slot_of, c.inter, h1=bufs["h1"][: N * c.k],
-                                      y=bufs["y"][: N * c.k])
+        _, y = kernels.grouped_swiglu(xp, off, self.store.arena, slot_of, c.inter, h1=bufs["h1"][:M],
+                                      y=bufs["y"][:M], x_rows=xn if gather else None, src_row=src if gather else None)
         if self.profile is not None:
             e1 = torch.cuda.Event(enable_timing=True)
             e1.record()
@@ -356,9 +365,11 @@ class MoEStack:
         if S:
             layer = self._cur_layer
             src_s, off_s = kernels.shared_plan(N, S, bufs["shared_src"], bufs["shared_off"])
-            xs = kernels.permute_rows(xn, src_s, N * S, out=bufs["xs"][: N * S])
+            gs = _GATHER and N * S > 16
+            xs = N * S if gs else kernels.permute_rows(xn, src_s, N * S, out=bufs["xs"][: N * S])
             _, ys = kernels.grouped_swiglu(xs, off_s, self.store.arena, self.store.shared_slot_of[layer], c.inter,
-                                           h1=bufs["h1s"][: N * S], y=bufs["ys"][: N * S])
+                                           h1=bufs["h1s"][: N * S], y=bufs["ys"][: N * S],
+                                           x_rows=xn if gs else None, src_row=src_s if gs else None)
             return kernels.combine_shared(y, pos, gates, x, ys, S, out=out[:N])
         return kernels.combine(y, pos, gates, x, out=out[:N])
 

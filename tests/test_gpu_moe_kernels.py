@@ -53,6 +53,12 @@ def test_permute_plan_is_stable_counting_sort(N, k, E):
     assert torch.equal(off.cpu().long(), roff)
     assert torch.equal(src.cpu().long()[: N * k], rsrc)
     assert torch.equal(pos.cpu().long()[: N * k].reshape(N, k), rpos)
+    # fused plan + row copy
+    H = 2560 if E == 4 else 256
+    x = torch.randn(N, H, device="cuda").to(torch.bfloat16)
+    off2, src2, pos2, xp2 = kernels.permute(ids.cuda(), x, E)
+    assert torch.equal(off2, off) and torch.equal(src2, src) and torch.equal(pos2, pos)
+    assert torch.equal(xp2, x[rsrc.cuda()])
 
 
 def _expert_setup(N, H, I, E, k, n_slots, seed):
@@ -187,7 +193,7 @@ def test_fused_combine_norm_bit_identical_to_combine_then_rmsnorm():
         assert torch.equal(xn, refn)
 
 
-@pytest.mark.parametrize("N,k,E", [(1, 8, 128), (2, 8, 128), (4, 6, 64), (1, 2, 4), (16, 2, 8)])
+@pytest.mark.parametrize("N,k,E", [(1, 8, 128), (2, 8, 128), (4, 6, 64), (1, 2, 4), (16, 2, 8), (200, 8, 128)])
 def test_permute_plan_small_batches(N, k, E):
     g = torch.Generator().manual_seed(N * 100 + k)
     ids = torch.stack([torch.randperm(E, generator=g)[:k] for _ in range(N)]).int()
@@ -211,9 +217,13 @@ def test_fused_ffn_bit_identical_to_two_launches(shape):
     arena, slot_of = arena.cuda(), slot_of.cuda()
     h1a, ya = kernels.grouped_swiglu(xp, off, arena, slot_of, I, fused=False)
     h1b, yb = kernels.grouped_swiglu(xp, off, arena, slot_of, I, fused=True)
+    # A rows gathered from the token rows by TMA gather4 (no permuted copy)
+    h1c, yc = kernels.grouped_swiglu(N * k, off, arena, slot_of, I, x_rows=x.cuda(), src_row=src)
     torch.cuda.synchronize()
     assert torch.equal(h1a, h1b)
     assert torch.equal(ya, yb)
+    assert torch.equal(h1a, h1c)
+    assert torch.equal(ya, yc)
 
 
 def test_fused_ffn_waits_for_copy_stream_fills():
@@ -246,7 +256,7 @@ def test_fused_ffn_waits_for_copy_stream_fills():
         w2 = dev_arena.data_ptr() + 2 * I * H * 2
         _lib.check(L.vmm_grouped_swiglu_fused(xp.data_ptr(), off.data_ptr(), E, N * k, H, I, dev_arena.data_ptr(),
                                               w2, 3 * I * H, E, slot_of.cuda().data_ptr(), need.data_ptr(), ready, 0,
-                                              done.data_ptr(), h1.data_ptr(), y.data_ptr(),
+                                              done.data_ptr(), None, None, 0, h1.data_ptr(), y.data_ptr(),
                                               torch.cuda.current_stream().cuda_stream))
         del ready_t
         nbytes = arena.shape[1] * 2
