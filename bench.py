@@ -4,12 +4,15 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3_qwen3vl]
     python bench.py --impl reference ...     # the reference CPU path (oracle port)
 
-One step = one request (BASELINE.json configs[2], Qwen3-VL-30B-A3B shape:
-2304 visual + 64 text tokens, 48 MoE layers, 128 experts top-8, expert
-intermediate 768, 8 pinned layers, 826-slab expert cache) through the whole
-stack: live router -> prune -> lookahead predictor -> expert cache with real
-H2D expert transfers -> permute -> grouped SwiGLU (tcgen05) -> combine.
-Synthetic bf16 hidden states and random-init weights of that shape.
+One step = one batch of R requests per GPU (default R=256; BASELINE.json
+configs[4], the batch sweep of the configs[2] shape: Qwen3-VL-30B-A3B, each
+request 2304 visual + 64 text tokens, 48 MoE layers, 128 experts top-8,
+expert intermediate 768, 8 pinned layers, 826-slab expert cache) through the
+whole stack: live router -> prune (per request) -> lookahead predictor ->
+expert cache with real H2D expert transfers (shared by the batch) -> permute
+-> grouped SwiGLU (tcgen05) -> combine.  `--requests 1` is the single-request
+configs[2] line.  Synthetic bf16 hidden states and random-init weights of
+that shape.
 
 Multi-GPU (torchrun): requests are data-parallel, one engine + cache per GPU,
 no data-path collective ("scaling": "weak"); time = max over ranks.
@@ -39,7 +42,8 @@ def parse():
     p.add_argument("--workload", default="c3_qwen3vl")
     p.add_argument("--routing", default="live", choices=["live", "trace"])
     p.add_argument("--predictor", default=None)
-    p.add_argument("--requests", type=int, default=1, help="requests per GPU per step (C5 batch sweep)")
+    p.add_argument("--requests", type=int, default=256,
+                   help="requests per GPU per step (BASELINE configs[4] batch sweep; 1 = one request per step)")
     p.add_argument("--source", default="host", choices=["host", "sharded"],
                    help="miss source: pinned host pool over PCIe, or HBM home copies sharded over the GPUs (NVLink)")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -367,7 +371,7 @@ def main():
                 harness.simulate(tr, ref_sim_dict(w), comp, False)
                 n_req += 1
             dt = (time.perf_counter() - t0) / n_req
-            cpu = {"value": T / dt, "unit": "tokens/s", "cores": 1, "kind": "port",
+            cpu = {"value": T1 / dt, "unit": "tokens/s", "cores": 1, "kind": "port",
                    "sample": f"{n_req} x one {w.name} request (compress + simulate, oracle predictor), single thread"}
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "unit": "tokens/s", "cores": 1, "kind": "port", "sample": f"failed: {exc}"}

@@ -101,6 +101,43 @@ __global__ void permute_rows_kernel(const uint4 *__restrict__ x, const int32_t *
   }
 }
 
+// acc[0..7] = sum_j g_j * Y[pos_j][c] (j ascending) + sum_s Ys[s*N + t][c]: the
+// k row loads (and the pos/gate loads before them) are all issued up front so
+// each thread keeps k x 16 B in flight; the accumulation order is unchanged.
+__device__ __forceinline__ void combine_chunk(const uint4 *__restrict__ y, const int32_t *__restrict__ pos,
+                                              const float *__restrict__ gates, int t, int k, int row_vec, int c,
+                                              const uint4 *__restrict__ ys, int S, int N, float (&acc)[8]) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+  for (int j0 = 0; j0 < k; j0 += 8) {
+    int pj[8];
+    float gj[8];
+    uint4 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j0 + j < k) {
+        pj[j] = __ldg(pos + (long long)t * k + j0 + j);
+        gj[j] = __ldg(gates + (long long)t * k + j0 + j);
+      }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j0 + j < k) v[j] = __ldg(y + (long long)pj[j] * row_vec + c);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j0 + j < k) {
+        const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&v[j]);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = fmaf(gj[j], __bfloat162float(h[q]), acc[q]);
+      }
+  }
+  for (int sx = 0; sx < S; ++sx) {  // shared experts: unit weight, row sx*N + t
+    uint4 v = __ldg(ys + ((long long)sx * N + t) * row_vec + c);
+    const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&v);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] += __bfloat162float(h[q]);
+  }
+}
+
 // out[t] = resid[t] + sum_j gates[t,j] * Y[pos[t,j]]; each thread owns 8 columns
 __global__ void combine_kernel(const uint4 *__restrict__ y, const int32_t *__restrict__ pos,
                                const float *__restrict__ gates, const uint4 *__restrict__ resid, int N, int k,
@@ -111,21 +148,7 @@ __global__ void combine_kernel(const uint4 *__restrict__ y, const int32_t *__res
     int t = (int)(i / row_vec);
     int c = (int)(i % row_vec);
     float acc[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = 0.f;
-    for (int j = 0; j < k; ++j) {
-      float g = gates[(long long)t * k + j];
-      uint4 v = __ldg(y + (long long)pos[(long long)t * k + j] * row_vec + c);
-      const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&v);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) acc[q] = fmaf(g, __bfloat162float(h[q]), acc[q]);
-    }
-    for (int sx = 0; sx < S; ++sx) {  // shared experts: unit weight, row sx*N + t
-      uint4 v = __ldg(ys + ((long long)sx * N + t) * row_vec + c);
-      const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&v);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) acc[q] += __bfloat162float(h[q]);
-    }
+    combine_chunk(y, pos, gates, t, k, row_vec, c, ys, S, N, acc);
     uint4 rv = resid ? __ldg(resid + i) : make_uint4(0, 0, 0, 0);
     const __nv_bfloat16 *rh = reinterpret_cast<const __nv_bfloat16 *>(&rv);
     uint4 o;
@@ -570,21 +593,7 @@ combine_norm_kernel(const uint4 *__restrict__ y, const int32_t *__restrict__ pos
       const int c = threadIdx.x + kNormThreads * i;
       if (c >= row_vec) continue;
       float acc[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) acc[q] = 0.f;
-      for (int j = 0; j < k; ++j) {
-        float g = gates[(long long)t * k + j];
-        uint4 v = __ldg(y + (long long)pos[(long long)t * k + j] * row_vec + c);
-        const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&v);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) acc[q] = fmaf(g, __bfloat162float(h[q]), acc[q]);
-      }
-      for (int sx = 0; sx < S; ++sx) {
-        uint4 v = __ldg(ys + ((long long)sx * N + t) * row_vec + c);
-        const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&v);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) acc[q] += __bfloat162float(h[q]);
-      }
+      combine_chunk(y, pos, gates, t, k, row_vec, c, ys, S, N, acc);
       uint4 rv = __ldg(resid + (long long)t * row_vec + c);
       const __nv_bfloat16 *rh = reinterpret_cast<const __nv_bfloat16 *>(&rv);
       __nv_bfloat16 *oh = reinterpret_cast<__nv_bfloat16 *>(&o[i]);

@@ -77,6 +77,10 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
   const int E = d.experts, k = d.k, H = d.hidden, I = d.inter, L = d.layers, lp = d.l_pinned;
   cudaStream_t st = (cudaStream_t)stream;
   if (n_rows <= 0 || n_rows > d.cap_rows) return vmm::fail(VMM_ECONTRACT, "row count outside the buffers");
+  // eng == NULL: pinned-prefix mode (layers < l_pinned on resident experts): no decisions,
+  // no copies, no host sync -- the whole range is enqueued asynchronously
+  const bool pinned_only = eng == nullptr;
+  if (pinned_only && l1 > lp) return vmm::fail(VMM_ECONTRACT, "engine-less run must stay inside the pinned prefix");
   const size_t row_bytes = (size_t)H * 2;
   const void *cur = d_x;
   int ping = 0, copies = 0;
@@ -97,7 +101,7 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
     auto c0 = clk::now();
     void *xn = d.xn;
     if (!have_xn) VMM_TRY(vmm_rmsnorm(cur, nullptr, n_rows, H, 1e-6f, xn, stream));
-    const int emits = vmm_engine_emits(eng, l, phase);
+    const int emits = pinned_only ? 0 : vmm_engine_emits(eng, l, phase);
     uint32_t *cnt = d.counts + (size_t)l * E;
     bool la_done = false;
     if (d.routing == 0) {
@@ -146,17 +150,20 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
       VMM_CUDA(cudaMemcpyAsync(yh, ysrc, sizeof(double) * E, cudaMemcpyDeviceToHost, st), "scores D2H");
     }
     int32_t *ch = d.counts_host + (size_t)l * E;
-    VMM_CUDA(cudaMemcpyAsync(ch, cnt, sizeof(uint32_t) * E, cudaMemcpyDeviceToHost, st), "counts D2H");
-    auto c1 = clk::now();
-    VMM_CUDA(cudaStreamSynchronize(st), "layer sync");
-    auto c2 = clk::now();
-    demand.clear();
-    for (int e = 0; e < E; ++e)
-      if (ch[e]) demand.push_back(e);
-    VMM_TRY(vmm_engine_layer(eng, l, demand.data(), (int)demand.size(), phase, step, nullptr));
+    auto c1 = clk::now(), c2 = c1;
     int n = 0;
-    VMM_TRY(vmm_xfer_issue_engine(xf, eng, d.pool, d.host_layers, E, d.arena, d.n_pinned_slots, d.slot_bytes, &n));
-    copies += n;
+    demand.clear();
+    if (!pinned_only) {
+      VMM_CUDA(cudaMemcpyAsync(ch, cnt, sizeof(uint32_t) * E, cudaMemcpyDeviceToHost, st), "counts D2H");
+      c1 = clk::now();
+      VMM_CUDA(cudaStreamSynchronize(st), "layer sync");
+      c2 = clk::now();
+      for (int e = 0; e < E; ++e)
+        if (ch[e]) demand.push_back(e);
+      VMM_TRY(vmm_engine_layer(eng, l, demand.data(), (int)demand.size(), phase, step, nullptr));
+      VMM_TRY(vmm_xfer_issue_engine(xf, eng, d.pool, d.host_layers, E, d.arena, d.n_pinned_slots, d.slot_bytes, &n));
+      copies += n;
+    }
     const int32_t *slot_of;
     const uint32_t *need_of = nullptr;
     if (l < lp) {
@@ -227,7 +234,7 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
     cur = dst;
     ping ^= 1;
     if (out && out->n_demand) out->n_demand[l - l0] = (int)demand.size();
-    if (l >= lp) VMM_TRY(vmm_xfer_layer_done(xf, l, stream));
+    if (l >= lp && !pinned_only) VMM_TRY(vmm_xfer_layer_done(xf, l, stream));
     auto c4 = clk::now();
     t_pre += us(c0, c1);
     t_sync += us(c1, c2);

@@ -28,7 +28,6 @@ from __future__ import annotations
 
 import ctypes as C
 import math
-import os
 from dataclasses import dataclass, field, replace
 
 import numpy as np
@@ -41,8 +40,6 @@ from .configs import Workload
 from .errors import ContractError, ValidationError
 from .pipeline import Engine, PredictorSpec, SimConfig, SimReport
 from .predictor import decay_table, pow_table
-
-_GATHER = bool(os.environ.get("VMM_FFN_GATHER"))
 
 
 @dataclass
@@ -336,43 +333,6 @@ class MoEStack:
             )
         return self._bufs
 
-    def _layer_compute(self, x, xn, ids, gates, slot_of, bufs, out, n_experts=None):
-        c = self.cfg
-        N = int(x.shape[0])
-        M = N * c.k
-        gather = _GATHER and M > 16  # VMM_FFN_GATHER=1: rows gathered by TMA gather4 (slower, see stack.cpp)
-        if gather:
-            off, src, pos = kernels.permute_plan(ids, c.experts, bufs=(bufs["off"], bufs["src"], bufs["pos"]))
-            xp = M
-        else:
-            off, src, pos, xp = kernels.permute(ids, xn, c.experts, bufs=(bufs["off"], bufs["src"], bufs["pos"]),
-                                                out=bufs["xp"][:M])
-        if self.profile is not None:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e0.record()
-        _, y = kernels.grouped_swiglu(xp, off, self.store.arena, slot_of, c.inter, h1=bufs["h1"][:M],
-                                      y=bufs["y"][:M], x_rows=xn if gather else None, src_row=src if gather else None)
-        if self.profile is not None:
-            e1 = torch.cuda.Event(enable_timing=True)
-            e1.record()
-            M = N * c.k
-            ne = c.experts if n_experts is None else n_experts
-            # algorithmic bytes: weights of the active experts once + Xp read + H1 write/read + Y write
-            nbytes = ne * c.slot_bytes + M * c.hidden * 2 * 2 + M * c.inter * 2 * 2
-            flops = 6.0 * M * c.hidden * c.inter
-            self.profile.append((e0, e1, nbytes, flops))
-        S = c.shared_experts
-        if S:
-            layer = self._cur_layer
-            src_s, off_s = kernels.shared_plan(N, S, bufs["shared_src"], bufs["shared_off"])
-            gs = _GATHER and N * S > 16
-            xs = N * S if gs else kernels.permute_rows(xn, src_s, N * S, out=bufs["xs"][: N * S])
-            _, ys = kernels.grouped_swiglu(xs, off_s, self.store.arena, self.store.shared_slot_of[layer], c.inter,
-                                           h1=bufs["h1s"][: N * S], y=bufs["ys"][: N * S],
-                                           x_rows=xn if gs else None, src_row=src_s if gs else None)
-            return kernels.combine_shared(y, pos, gates, x, ys, S, out=out[:N])
-        return kernels.combine(y, pos, gates, x, out=out[:N])
-
     def forward(self, x, saliency, modality, trace=None, record: bool = False, req_off=None,
                 keep_session: bool = False) -> StackResult:
         """Prefill a batch of requests through the whole stack.
@@ -395,26 +355,17 @@ class MoEStack:
             raise ContractError("routing='trace' needs the trace's device routes")
         check(self._L.vmm_xfer_reset_stats(self._x))
 
-        # --- pinned prefix: all prefill tokens, resident experts, no cache decisions
+        # --- pinned prefix: all prefill tokens, resident experts, no cache decisions:
+        # the native executor in engine-less mode (no host sync inside the prefix)
         prefix = torch.empty((max(lp, 1), T, k), dtype=torch.int32, device=dev)
         counts_pre = torch.zeros((max(lp, 1), E), dtype=torch.int32, device=dev)
         x_ctx = None
         cur = x
-        outs = (bufs["out"], bufs["out2"])
-        for l in range(lp):
-            xn = kernels.rmsnorm(cur, out=bufs["xn"][:T])
-            if c.routing == "live":
-                ids, gates, _ = kernels.route_topk(xn, self.store.router[l], k, counts=counts_pre[l], ids=prefix[l],
-                                                   gates=bufs["gates"][:T])
-            else:
-                prefix[l].copy_(trace["routes"][l, :T])  # the trace may carry decode tokens after row T
-                ids, gates = prefix[l], trace["gates"][l, :T]
-                kernels.demand_counts(trace["routes"], torch.tensor([l], dtype=torch.int32, device=dev),
-                                      torch.arange(T, dtype=torch.int32, device=dev), E, out=counts_pre[l:l + 1])
-            if l == lp - 1:
-                x_ctx = xn  # normalised input of layer lp-1: context of the boot emission (gate predictor)
-            self._cur_layer = l
-            cur = self._layer_compute(cur, xn, ids, gates, self.store.pinned_slot_of[l], bufs, outs[l % 2])
+        if lp:
+            rows_all = torch.arange(T, dtype=torch.int32, device=dev) if c.routing == "trace" else None
+            cur, _, _ = self._native_layers(None, x, T, 0, lp, 0, -1, rows=rows_all, counts=counts_pre, trace=trace,
+                                            record_into=prefix[:lp])
+            x_ctx = bufs["xn"][:T]  # normalised input of layer lp-1: context of the boot emission (gate predictor)
 
         # --- prune (token compression) on the prefix routes, one CTA per request
         offs = [0, T] if req_off is None else [int(v) for v in req_off]
@@ -506,8 +457,9 @@ class MoEStack:
                            retained_offsets=ret_off)
 
     def _native_layers(self, eng, x, n_rows, l0, l1, phase, step, rows=None, counts=None, oracle_table=None,
-                       trace=None, record=False):
-        """Run layers [l0, l1) through the native executor (csrc/stack.cpp)."""
+                       trace=None, record=False, record_into=None):
+        """Run layers [l0, l1) through the native executor (csrc/stack.cpp).
+        eng=None: pinned-prefix mode (no decisions / copies / host syncs)."""
         c = self.cfg
         L, E, k = c.layers, c.experts, c.k
         bufs = self._buffers(n_rows)
@@ -542,7 +494,10 @@ class MoEStack:
         check(self._L.vmm_stack_create(C.byref(d), C.byref(h)))
         nl = l1 - l0
         out = _lib.StackOut()
-        routes_t = torch.empty((nl, n_rows, k), dtype=torch.int32, device=self.device) if record else None
+        if record_into is not None:
+            routes_t, record = record_into, True
+        else:
+            routes_t = torch.empty((nl, n_rows, k), dtype=torch.int32, device=self.device) if record else None
         out.routes = routes_t.data_ptr() if record else None
         evs = None
         n_dem = np.zeros(nl, dtype=np.int32)
@@ -555,7 +510,8 @@ class MoEStack:
             out.ffn_start = C.cast(arr, C.c_void_p)
             out.ffn_end = C.cast(C.byref(arr, nl * C.sizeof(C.c_void_p)), C.c_void_p)
         try:
-            check(self._L.vmm_stack_layers(h, eng._h, self._x, x.data_ptr(), n_rows, l0, l1, phase, step,
+            check(self._L.vmm_stack_layers(h, None if eng is None else eng._h, self._x, x.data_ptr(), n_rows, l0, l1,
+                                           phase, step,
                                            rows.data_ptr() if rows is not None else None,
                                            torch.cuda.current_stream().cuda_stream, C.byref(out)))
         finally:
@@ -563,7 +519,8 @@ class MoEStack:
         if self.profile is not None:
             M = n_rows * k
             for i in range(nl):
-                nbytes = int(n_dem[i]) * c.slot_bytes + M * c.hidden * 2 * 2 + M * c.inter * 2 * 2
+                ne = c.experts if eng is None else int(n_dem[i])  # pinned prefix: every expert resident
+                nbytes = ne * c.slot_bytes + M * c.hidden * 2 * 2 + M * c.inter * 2 * 2
                 self.profile.append((evs[i], evs[nl + i], nbytes, 6.0 * M * c.hidden * c.inter))
         res = bufs["out"] if out.x_out == bufs["out"].data_ptr() else bufs["out2"]
         self.last_host_us = list(out.host_us)
