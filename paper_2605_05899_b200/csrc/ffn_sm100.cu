@@ -166,7 +166,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_cons
           if (half == 1) {  // accumulator fully read: hand the buffer back to the MMA warp
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tmem_empty[b]);
+            if (lane == 0) mbar_arrive_relaxed(&tmem_empty[b]);
           }
           if (row < ti.row_end) {
             uint4 *dst = reinterpret_cast<uint4 *>(out + (long long)row * ld_out + ti.n_tile * (BN / 2) + half * 32);
@@ -189,7 +189,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_cons
           if (c == BN / 32 - 1) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tmem_empty[b]);
+            if (lane == 0) mbar_arrive_relaxed(&tmem_empty[b]);
           }
           if (row < ti.row_end) {
             uint4 *dst = reinterpret_cast<uint4 *>(out + (long long)row * ld_out + ti.n_tile * BN + c * 32);
@@ -437,7 +437,7 @@ ffn_fused_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
           if (hc == TN / 64 - 1) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tmem_empty[b]);
+            if (lane == 0) mbar_arrive_relaxed(&tmem_empty[b]);
           }
           if (row < ti.row_end) {
             uint4 *dst = reinterpret_cast<uint4 *>(h1 + (long long)row * I + f.n_tile * (TN / 2) + pair * 64 +
@@ -466,7 +466,7 @@ ffn_fused_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
           if (c == TN / 32 - 1) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tmem_empty[b]);
+            if (lane == 0) mbar_arrive_relaxed(&tmem_empty[b]);
           }
           if (row < ti.row_end) {
             uint4 *dst = reinterpret_cast<uint4 *>(y + (long long)row * H + f.n_tile * TN + c * 32);
@@ -489,6 +489,225 @@ ffn_fused_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TN));
+  }
+}
+
+// ---- CTA-pair variant: 256 x 256 tiles with tcgen05 cta_group::2 ------------
+// A cluster of 2 CTAs (one TPC) owns a 256-row x 256-column tile: each CTA
+// stages its own 128 A rows and half (128 rows) of the B tile, the leader CTA
+// issues M=256 N=256 pair MMAs over both CTAs' smem, and each CTA's TMEM
+// receives its 128 accumulator rows.  Per FLOP this moves 1/3 less L2->SMEM
+// data than the 128x256 single-CTA tile.  Same fused GEMM1/GEMM2 tile order,
+// copy ready flags and H1 block counters as ffn_fused_kernel.
+constexpr int BM2 = 256, TN2 = 256, kStages2 = 6;
+constexpr uint32_t kHalf2 = 128 * BK * 2;  // 16 KB: 128 rows x 64 K of A or of B
+constexpr uint32_t kStage2 = 2 * kHalf2;
+constexpr size_t kSmem2 = (size_t)kStages2 * kStage2 + 1024 + 256;
+
+__device__ __forceinline__ TileInfo pair_tile_info(int m_tile, const int *tile_base, const int *offs, const int *slots,
+                                                   int E) {
+  TileInfo ti;
+  int lo = 0, hi = E - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (tile_base[mid] <= m_tile) lo = mid; else hi = mid - 1;
+  }
+  while (lo + 1 < E && tile_base[lo + 1] <= m_tile) ++lo;
+  ti.expert = lo;
+  ti.row0 = offs[lo] + (m_tile - tile_base[lo]) * BM2;
+  ti.row_end = offs[lo + 1];
+  ti.slot = slots[lo];
+  ti.n_tile = 0;
+  return ti;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w13,
+                const __grid_constant__ CUtensorMap map_h1, const __grid_constant__ CUtensorMap map_w2,
+                const int32_t *__restrict__ offsets, const int32_t *__restrict__ slot_of,
+                const uint32_t *__restrict__ need, const uint32_t *ready, int ready_base, uint32_t *done, int E, int H,
+                int I, int lag, __nv_bfloat16 *__restrict__ h1, __nv_bfloat16 *__restrict__ y) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages2 * kStage2);
+  uint64_t *empty = full + kStages2;
+  uint64_t *tmem_full = empty + kStages2;  // [2]
+  uint64_t *tmem_empty = tmem_full + 2;    // [2] (the leader's counts 8 epilogue warps of the pair)
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 2);
+  __shared__ int s_offs[VMM_MAX_EXPERTS + 1], s_tile_base[VMM_MAX_EXPERTS + 1], s_slots[VMM_MAX_EXPERTS];
+  __shared__ uint32_t s_need[VMM_MAX_EXPERTS];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  for (int e = threadIdx.x; e <= E; e += blockDim.x) s_offs[e] = offsets[e];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    s_slots[e] = slot_of[e];
+    s_need[e] = need ? need[e] : 0u;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int e = 0; e < E; ++e) {
+      s_tile_base[e] = acc;
+      acc += (s_offs[e + 1] - s_offs[e] + BM2 - 1) / BM2;
+    }
+    s_tile_base[E] = acc;
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&map_x);
+    prefetch_tmap(&map_w13);
+    prefetch_tmap(&map_h1);
+    prefetch_tmap(&map_w2);
+    for (int s = 0; s < kStages2; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tmem_full[b], 1); mbar_init(&tmem_empty[b], 8); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {  // both CTAs: the pair allocation (same columns in each CTA's TMEM)
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * TN2));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // both CTAs' barriers initialised and TMEM allocated before any cross-CTA use
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int MT = s_tile_base[E];
+  const int n1 = (2 * I) / TN2, n2 = H / TN2;
+  const int total = (MT + lag) * (n1 + n2);
+  const int nk1 = H / BK, nk2 = I / BK;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int t = cid; t < total; t += ncl) {
+        const FusedTile f = fused_tile(t, n1, n2, MT, lag);
+        if (!f.valid) continue;
+        const TileInfo ti = pair_tile_info(f.m_tile, s_tile_base, s_offs, s_slots, E);
+        const uint32_t nd = s_need[ti.expert];
+        if (nd) wait_at_least(ready + (ti.slot - ready_base), nd, 256);
+        if (f.gemm2) wait_at_least(done + f.m_tile, 8u * (uint32_t)n1, 64);
+        if (nd || f.gemm2) fence_proxy_async_global();
+        const CUtensorMap *ma = f.gemm2 ? &map_h1 : &map_x;
+        const CUtensorMap *mb = f.gemm2 ? &map_w2 : &map_w13;
+        const int nk = f.gemm2 ? nk2 : nk1;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % kStages2;
+          if (it >= kStages2) mbar_wait_watchdog(&empty[s], ((it / kStages2) - 1) & 1);
+          unsigned char *a_dst = smem + s * kStage2;
+          if (leader) mbar_expect_tx(&full[s], 2 * kStage2);  // both CTAs' bytes land on the leader's barrier
+          const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
+          tma_load_2d_cg2(ma, fb, a_dst, kb * BK, ti.row0 + 128 * (int)rank);
+          tma_load_3d_cg2(mb, fb, a_dst + kHalf2, kb * BK, f.n_tile * TN2 + 128 * (int)rank, ti.slot);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      int it = 0, local = 0;
+      for (int t = cid; t < total; t += ncl) {
+        const FusedTile f = fused_tile(t, n1, n2, MT, lag);
+        if (!f.valid) continue;
+        const int nk = f.gemm2 ? nk2 : nk1;
+        const int b = local & 1, use = local >> 1;
+        if (use > 0) mbar_wait_watchdog(&tmem_empty[b], (use - 1) & 1);
+        tc_fence_after();
+        const uint32_t acc = tmem + b * TN2;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % kStages2;
+          mbar_wait_watchdog(&full[s], (it / kStages2) & 1);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + s * kStage2);
+          const uint32_t b_addr = a_addr + kHalf2;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            umma_bf16_cg2(acc, sw128_desc(a_addr + kk * 32), sw128_desc(b_addr + kk * 32), idesc_bf16(BM2, TN2),
+                          (kb | kk) != 0);
+          umma_commit_mc2(&empty[s]);
+        }
+        umma_commit_mc2(&tmem_full[b]);
+        ++local;
+      }
+    }
+    __syncwarp();
+  } else {
+    const int q = warp & 3;
+    int local = 0;
+    const uint32_t te_leader[2] = {mapa_shared(smem_u32(&tmem_empty[0]), 0), mapa_shared(smem_u32(&tmem_empty[1]), 0)};
+    for (int t = cid; t < total; t += ncl) {
+      const FusedTile f = fused_tile(t, n1, n2, MT, lag);
+      if (!f.valid) continue;
+      const TileInfo ti = pair_tile_info(f.m_tile, s_tile_base, s_offs, s_slots, E);
+      const int b = local & 1, use = local >> 1;
+      ++local;
+      const int row = ti.row0 + 128 * (int)rank + q * 32 + lane;
+      mbar_wait_watchdog(&tmem_full[b], use & 1);
+      tc_fence_after();
+      const uint32_t t_base = tmem + b * TN2 + ((uint32_t)(q * 32) << 16);
+      if (!f.gemm2) {
+#pragma unroll
+        for (int hc = 0; hc < TN2 / 64; ++hc) {
+          const int pair = hc >> 1, half = hc & 1;
+          float g[32], u[32];
+          tmem_ld32(t_base + pair * 128 + half * 32, g);
+          tmem_ld32(t_base + pair * 128 + 64 + half * 32, u);
+          if (hc == TN2 / 64 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_relaxed_cluster(te_leader[b]);
+          }
+          if (row < ti.row_end) {
+            uint4 *dst = reinterpret_cast<uint4 *>(h1 + (long long)row * I + f.n_tile * (TN2 / 2) + pair * 64 +
+                                                   half * 32);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              uint4 o;
+              o.x = pack_bf16(silu(g[8 * v + 0]) * u[8 * v + 0], silu(g[8 * v + 1]) * u[8 * v + 1]);
+              o.y = pack_bf16(silu(g[8 * v + 2]) * u[8 * v + 2], silu(g[8 * v + 3]) * u[8 * v + 3]);
+              o.z = pack_bf16(silu(g[8 * v + 4]) * u[8 * v + 4], silu(g[8 * v + 5]) * u[8 * v + 5]);
+              o.w = pack_bf16(silu(g[8 * v + 6]) * u[8 * v + 6], silu(g[8 * v + 7]) * u[8 * v + 7]);
+              dst[v] = o;
+            }
+          }
+        }
+        fence_proxy_async_global();
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) red_release_add(done + f.m_tile, 1u);
+      } else {
+#pragma unroll
+        for (int c = 0; c < TN2 / 32; ++c) {
+          float a[32];
+          tmem_ld32(t_base + c * 32, a);
+          if (c == TN2 / 32 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_relaxed_cluster(te_leader[b]);
+          }
+          if (row < ti.row_end) {
+            uint4 *dst = reinterpret_cast<uint4 *>(y + (long long)row * H + f.n_tile * TN2 + c * 32);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              uint4 o;
+              o.x = pack_bf16(a[8 * v + 0], a[8 * v + 1]);
+              o.y = pack_bf16(a[8 * v + 2], a[8 * v + 3]);
+              o.z = pack_bf16(a[8 * v + 4], a[8 * v + 5]);
+              o.w = pack_bf16(a[8 * v + 6], a[8 * v + 7]);
+              dst[v] = o;
+            }
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // every pair MMA into either CTA has been consumed before TMEM is freed
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TN2));
   }
 }
 
@@ -782,6 +1001,10 @@ extern "C" int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offse
   static const bool force_narrow = std::getenv("VMM_FFN_TN128") != nullptr;  // A/B comparison knob
   const bool wide = !force_narrow && (H % 256 == 0) && ((2 * I) % 256 == 0);
   const int TN = wide ? 256 : 128;
+  // CTA pairs (256x256 tiles) once the average expert has >= 256 rows: tensor-bound batches
+  static const bool no_pair = std::getenv("VMM_FFN_NO_PAIR") != nullptr;
+  const bool pair = wide && !no_pair && d_src_row == nullptr && M_total >= 256 * E;
+  const uint32_t b_rows = pair ? 128u : (uint32_t)TN;  // a pair CTA stages half of the 256-row B tile
   static bool attr = false;
   if (!attr) {
     cudaError_t e1 = cudaFuncSetAttribute(ffn_fused_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -809,7 +1032,7 @@ extern "C" int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offse
   {
     uint64_t dims[3] = {(uint64_t)H, (uint64_t)2 * I, (uint64_t)n_slots};
     uint64_t str[2] = {(uint64_t)H * 2, (uint64_t)slot_stride * 2};
-    uint32_t box[3] = {BK, (uint32_t)TN, 1};
+    uint32_t box[3] = {BK, b_rows, 1};
     if ((st = make_map(&mw13, d_w13_arena, 3, dims, str, box))) return st;
   }
   {
@@ -821,7 +1044,7 @@ extern "C" int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offse
   {
     uint64_t dims[3] = {(uint64_t)I, (uint64_t)H, (uint64_t)n_slots};
     uint64_t str[2] = {(uint64_t)I * 2, (uint64_t)slot_stride * 2};
-    uint32_t box[3] = {BK, (uint32_t)TN, 1};
+    uint32_t box[3] = {BK, b_rows, 1};
     if ((st = make_map(&mw2, d_w2_arena, 3, dims, str, box))) return st;
   }
   if (!g_num_sms) {
@@ -836,6 +1059,25 @@ extern "C" int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offse
   if (ce != cudaSuccess) return vmm::cuda_status(ce, "ffn done memset");
   const int grid = g_num_sms < max_m_tiles * (n1 + n2) ? g_num_sms : max_m_tiles * (n1 + n2);
   const int lag = (2 * grid + n1 + n2 - 1) / (n1 + n2);  // GEMM2 tiles ~2 waves behind their GEMM1 tiles
+  if (pair) {
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaError_t e2 = cudaFuncSetAttribute(ffn_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2);
+      if (e2 != cudaSuccess) return vmm::cuda_status(e2, "ffn pair attr");
+      attr2 = true;
+    }
+    const int max_pair_tiles = (M_total + BM2 - 1) / BM2 + E;
+    int gridp = g_num_sms & ~1;
+    if (gridp > 2 * max_pair_tiles * (n1 + n2)) gridp = 2 * max_pair_tiles * (n1 + n2);
+    const int ncl = gridp / 2;
+    static const int lag_waves = std::getenv("VMM_FFN_LAG") ? std::atoi(std::getenv("VMM_FFN_LAG")) : 4;
+    const int lagp = (lag_waves * ncl + n1 + n2 - 1) / (n1 + n2);
+    ffn_pair_kernel<<<gridp, kThreads, kSmem2, s>>>(mx, mw13, mh1, mw2, d_offsets, d_slot_of_expert, d_need, d_ready,
+                                                   ready_base, d_done, E, H, I, lagp, (__nv_bfloat16 *)d_h1,
+                                                   (__nv_bfloat16 *)d_y);
+    VMM_LAUNCH_CHECK("ffn_pair_kernel");
+    return VMM_OK;
+  }
   if (wide)
     ffn_fused_kernel<256><<<grid, kThreads, FusedCfg<256>::kSmem, s>>>(
         mx, mw13, mh1, mw2, d_offsets, d_slot_of_expert, d_need, d_ready, ready_base, d_done, E, H, I, lag,

@@ -205,10 +205,12 @@ def test_permute_plan_small_batches(N, k, E):
 
 
 @pytest.mark.parametrize("shape", [(1216, 2048, 768, 128, 8), (300, 256, 512, 8, 2), (640, 2048, 1408, 64, 6),
-                                   (9728, 2048, 768, 128, 8), (3, 2048, 768, 128, 8)])
+                                   (9728, 2048, 768, 128, 8), (3, 2048, 768, 128, 8), (40000, 2048, 768, 128, 8),
+                                   (9000, 2048, 1408, 64, 6)])
 def test_fused_ffn_bit_identical_to_two_launches(shape):
-    """The one-launch persistent FFN (GEMM2 tiles gated on H1 block counters)
-    computes every tile exactly like the two-launch path."""
+    """The one-launch persistent FFN (GEMM2 tiles gated on H1 block counters;
+    CTA-pair 256x256 tiles once experts average >= 256 rows) computes every
+    tile exactly like the two-launch path."""
     N, H, I, E, k = shape
     n_slots = E + 3
     x, wg, wu, wd, arena, ids, slot_of = _expert_setup(N, H, I, E, k, n_slots, seed=N + 2 * E)
