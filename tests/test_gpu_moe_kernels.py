@@ -228,15 +228,17 @@ def test_fused_ffn_bit_identical_to_two_launches(shape):
     assert torch.equal(ya, yc)
 
 
-def test_fused_ffn_waits_for_copy_stream_fills():
+@pytest.mark.parametrize("N", [1216, 5000])
+def test_fused_ffn_waits_for_copy_stream_fills(N):
     """Copy overlap: the FFN is launched BEFORE its experts' weights are copied
     in; each expert's tiles wait on the copy stream's ready flag.  The result
-    must equal the all-resident computation bit for bit."""
+    must equal the all-resident computation bit for bit (N=1216: single-CTA
+    128x256 tiles; N=5000: CTA-pair 256x256 tiles)."""
     import ctypes as C
 
     from paper_2605_05899_b200 import _lib
 
-    N, H, I, E, k = 1216, 2048, 768, 128, 8
+    H, I, E, k = 2048, 768, 128, 8
     x, wg, wu, wd, arena, ids, slot_of = _expert_setup(N, H, I, E, k, E, seed=77)
     slot_of = torch.arange(E, dtype=torch.int32)  # expert e -> slab e
     pool = arena.pin_memory()

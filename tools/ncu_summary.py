@@ -10,7 +10,8 @@ want = ["Kernel Name", "Grid Size", "Block Size", "gpu__time_duration.sum", "dra
         "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
         "lts__t_bytes.sum", "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic",
-        "sm__warps_active.avg.pct_of_peak_sustained_active", "l1tex__data_pipe_tc_wavefronts_mem_shared.sum"]
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "l1tex__data_pipe_tc_wavefronts_mem_shared.sum",
+        "gpc__cycles_elapsed.max.per_second", "lts__throughput.avg.pct_of_peak_sustained_elapsed"]
 print(title)
 for r in rows[2:]:
     for w in want:
