@@ -124,6 +124,26 @@ int vmm_gate_lookahead(const void *d_x, const void *d_wnext, int N, int H, int E
                        uint32_t *d_scratch_counts /* [E] */, double *d_y, void *stream);
 
 /* ------------------------------------------------------------------------
+ * Attention-derived saliency (Alg. 1: s = Mean_h(A^h); the input the
+ * reference reads precomputed from the trace, trace.py:49 / compress.py:145-148)
+ * d_q bf16 [R][Hh][Q][D] (query rows: CLS or text tokens), d_k bf16 [R][Hh][N][D]
+ * (the request's N tokens), scale = 1/sqrt(D) usually.  A = softmax(q k^T *
+ * scale) per (request, head, query) in fp32 into d_probs f32 [R*Hh*Q][N];
+ * d_s f64 [R*N] = mean over heads and queries, summed in ascending (h, q)
+ * order.  vmm_attn_map_saliency does the mean for given maps [R*HQ][N].
+ * ------------------------------------------------------------------------ */
+int vmm_attn_saliency(const void *d_q, const void *d_k, int R, int Hh, int Q, int N, int D, float scale,
+                      float *d_probs, double *d_s, void *stream);
+int vmm_attn_map_saliency(const float *d_maps, int R, int HQ, int N, double *d_s, void *stream);
+
+/* GPU routing diagnostics (metrics.py:25-67), bit-identical to the reference:
+ * from per-layer expert histograms d_counts u32 [L][E] of a token subset of
+ * size n_subset (vmm_demand_counts), write d_out f64 [L][4] = {working set,
+ * top-`top` coverage, cosine(l, l+1), jaccard(l, l+1)} (last layer: NaN). */
+int vmm_routing_diagnostics(const uint32_t *d_counts, int L, int E, int n_subset, int k, int top, double *d_out,
+                            void *stream);
+
+/* ------------------------------------------------------------------------
  * Expert permutation and combine (no reference numerics; pipeline.py:573 order)
  * plan: stable counting sort of the N*k (token, slot) picks by expert.
  *   d_offsets [E+1] i32, d_src_row [N*k] i32 (token of each permuted row),

@@ -84,6 +84,9 @@ _SIGS = {
     "vmm_gate_lookahead": (I32, [P, P, I32, I32, I32, I32, P, P, P]),
     "vmm_permute_plan": (I32, [P, I32, I32, I32, P, P, P, P]),
     "vmm_permute_rows": (I32, [P, P, I32, I32, P, P]),
+    "vmm_attn_saliency": (I32, [P, P, I32, I32, I32, I32, I32, C.c_float, P, P, P]),
+    "vmm_attn_map_saliency": (I32, [P, I32, I32, I32, P, P]),
+    "vmm_routing_diagnostics": (I32, [P, I32, I32, I32, I32, I32, P, P]),
     "vmm_permute": (I32, [P, I32, I32, I32, P, I32, P, P, P, P, P]),
     "vmm_combine": (I32, [P, P, P, P, I32, I32, I32, P, P]),
     "vmm_rmsnorm": (I32, [P, P, I32, I32, C.c_float, P, P]),

@@ -29,6 +29,7 @@ CU = {
     "sm100.cu": [],
     "permute.cu": [],
     "ffn_sm100.cu": [],
+    "diag.cu": ["-fmad=false"],
 }
 CPP = ["engine.cpp", "xfer.cpp", "capi.cpp", "stack.cpp"]
 

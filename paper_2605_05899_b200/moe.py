@@ -334,7 +334,7 @@ class MoEStack:
         return self._bufs
 
     def forward(self, x, saliency, modality, trace=None, record: bool = False, req_off=None,
-                keep_session: bool = False) -> StackResult:
+                keep_session: bool = False, attn_qk=None) -> StackResult:
         """Prefill a batch of requests through the whole stack.
 
         x bf16 [T, H] (device), saliency f64 [T], modality u8 [T] (0 visual,
@@ -343,11 +343,21 @@ class MoEStack:
         own (one prune CTA per request) and the layers then run on the union of
         the retained rows, so expert transfers are shared by the batch.
         `trace` (device routes i32 [L,T,k], gates f32 [L,T,k]) is required for
-        routing="trace"."""
+        routing="trace".  saliency=None with attn_qk=(q [R,Hh,Q,D], k [R,Hh,T/R,D])
+        derives the saliency on the device from the vision encoder's attention
+        (head-averaged CLS/text->token attention, saliency.attention_saliency)."""
         c = self.cfg
         L, E, k, lp = c.layers, c.experts, c.k, c.l_pinned
         dev = self.device
         T = int(x.shape[0])
+        if saliency is None:
+            if attn_qk is None:
+                raise ContractError("forward needs saliency or attn_qk")
+            from .saliency import attention_saliency
+
+            saliency = attention_saliency(*attn_qk)
+            if int(saliency.shape[0]) != T:
+                raise ContractError("attn_qk keys must cover every token row (R requests x T/R tokens)")
         stream = torch.cuda.current_stream()
         sp = stream.cuda_stream
         bufs = self._buffers(T)

@@ -391,7 +391,75 @@ def trace_digest(trace: RoutingTrace) -> str:
     return h.hexdigest()
 
 
+# ---------------------------------------------------------------------------
+# Binary trace ingest: replaces the JSON-Lines format of
+# trace.py:390-503 for the device path.  One little-endian file:
+#   magic b"VMMTRACE" | u32 version | u32 L, E, k, N, D, shared, n_marks
+#   | i32 phase_marks[n_marks] | u8 modality[N] | f64 saliency[N]
+#   | i64 cluster[N] | f64 embedding[N*D] | i32 route_experts[L*N*k]
+#   | f64 route_gates[L*N*k]
+# Arrays are stored in the device layout (routes layer-major i32), so loading is
+# a few np.fromfile reads (memory-mapped on request) and one H2D per array,
+# instead of ~L*N JSON records.  Gates keep full fp64 (exact round trip).
+# ---------------------------------------------------------------------------
+BIN_MAGIC = b"VMMTRACE"
+BIN_VERSION = 1
+
+
+def save_trace_bin(trace: RoutingTrace, path: str) -> None:
+    hdr = np.array([BIN_VERSION, trace.layers, trace.experts, trace.k, trace.num_tokens, trace.embed_dim,
+                    trace.shared_experts, len(trace.phase_marks)], dtype="<u4")
+    with open(path, "wb") as f:
+        f.write(BIN_MAGIC)
+        f.write(hdr.tobytes())
+        f.write(np.asarray(trace.phase_marks, dtype="<i4").tobytes())
+        f.write(np.ascontiguousarray(trace.modality, dtype="u1").tobytes())
+        f.write(np.ascontiguousarray(trace.saliency, dtype="<f8").tobytes())
+        f.write(np.ascontiguousarray(trace.cluster, dtype="<i8").tobytes())
+        f.write(np.ascontiguousarray(trace.embedding, dtype="<f8").tobytes())
+        f.write(np.ascontiguousarray(trace.route_experts, dtype="<i4").tobytes())
+        f.write(np.ascontiguousarray(trace.route_gates, dtype="<f8").tobytes())
+
+
+def load_trace_bin(path: str, mmap: bool = False) -> RoutingTrace:
+    """Parse a binary trace; ParseError on a malformed file, ValidationError on
+    invariant violations (the same checks as the reference's load_trace)."""
+    from .errors import ParseError
+
+    with open(path, "rb") as f:
+        head = f.read(8 + 4 * 8)
+    if len(head) < 40 or head[:8] != BIN_MAGIC:
+        raise ParseError(f"{path}: not a VMMTRACE file")
+    ver, L, E, k, N, D, shared, nm = (int(v) for v in np.frombuffer(head[8:], dtype="<u4"))
+    if ver != BIN_VERSION:
+        raise ParseError(f"{path}: unsupported version {ver}")
+    sizes = [("marks", "<i4", nm), ("modality", "u1", N), ("saliency", "<f8", N), ("cluster", "<i8", N),
+             ("embedding", "<f8", N * D), ("routes", "<i4", L * N * k), ("gates", "<f8", L * N * k)]
+    total = 40 + sum(np.dtype(dt).itemsize * n for _, dt, n in sizes)
+    import os
+
+    if os.path.getsize(path) != total:
+        raise ParseError(f"{path}: size {os.path.getsize(path)} != {total} implied by the header")
+    arrs, off = {}, 40
+    for name, dt, n in sizes:
+        if mmap:
+            arrs[name] = np.memmap(path, dtype=dt, mode="r", offset=off, shape=(n,))
+        else:
+            arrs[name] = np.fromfile(path, dtype=dt, count=n, offset=off)
+        off += np.dtype(dt).itemsize * n
+    if arrs["modality"].size and int(arrs["modality"].max()) > 1:
+        raise ParseError(f"{path}: modality code out of range")
+    tr = RoutingTrace(L, E, k, arrs["routes"].reshape(L, N, k), arrs["gates"].reshape(L, N, k), arrs["saliency"],
+                      arrs["modality"], arrs["embedding"].reshape(N, D), arrs["cluster"],
+                      [int(m) for m in arrs["marks"]], shared)
+    bad = validate_trace(tr)
+    if bad:
+        raise ValidationError("; ".join(bad[:5]))
+    return tr
+
+
 __all__ = [
     "ExpertRef", "Modality", "RoutingTrace", "Token", "TraceGenConfig", "generate_trace",
     "validate_trace", "trace_digest", "MOD_VISUAL", "MOD_TEXT", "MOD_DECODE", "TRACE_VERSION",
+    "save_trace_bin", "load_trace_bin",
 ]
