@@ -391,6 +391,8 @@ def main():
             "hit_rate": rep.hit_rate, "hits": rep.hits, "misses": rep.misses, "evictions": rep.evictions,
             "retained_tokens": int(res0.hidden.shape[0]),
             "h2d": {"gbs": h2d_gbs, "bytes_per_step": h2d_bytes, "copies_per_step": res0.copies,
+                    "window_ms": res0.h2d_ms,
+                    "window_gbs": h2d_bytes / (res0.h2d_ms * 1e-3) / 1e9 if res0.h2d_ms else None,
                     "peak_gbs": h2d_peak, "frac": h2d_gbs / h2d_peak if h2d_peak else None,
                     "link": "PCIe (pinned host pool)" if a.source == "host" else
                             ("NVLink P2P + local D2D (sharded HBM home copies)" if world > 1 else "local D2D (HBM home)"),

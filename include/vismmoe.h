@@ -414,6 +414,8 @@ typedef struct {
   void **ffn_start, **ffn_end; /* nullable cudaEvent_t arrays [l1-l0] around the grouped SwiGLU */
   int *n_demand;             /* nullable h [l1-l0] demanded experts per layer */
   double host_us[4];         /* host time: launches before the sync, sync wait, decisions+copies, launches after */
+  void **copy_marks;         /* nullable cudaEvent_t [3*(l1-l0)] on the copy stream: before the layer's demand
+                                copies, after them, after its emission copies */
 } vmm_stack_out;
 
 typedef struct vmm_stack vmm_stack;

@@ -64,7 +64,7 @@ class StackDesc(C.Structure):
 
 class StackOut(C.Structure):
     _fields_ = [("x_out", P), ("copies", I32), ("routes", P), ("ffn_start", P), ("ffn_end", P), ("n_demand", P),
-                ("host_us", F64 * 4)]
+                ("host_us", F64 * 4), ("copy_marks", P)]
 
 
 _SIGS = {

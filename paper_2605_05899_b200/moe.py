@@ -195,6 +195,7 @@ class StackResult:
     copies: int                     # expert transfers issued
     h2d_bytes: float
     retained_offsets: np.ndarray = None  # [R+1] rows of each request in `hidden`
+    h2d_ms: float = 0.0                  # copy stream: first copy issued -> last copy landed (events)
 
 
 @dataclass
@@ -464,7 +465,7 @@ class MoEStack:
         self._sess = dict(eng=eng, step=0, trace=trace) if keep_session else None
         return StackResult(hidden=cur, retained=ret.cpu().numpy(), report=report, prefix_routes=prefix[:lp],
                            routes=routes, scores=scores, copies=n_copies, h2d_bytes=b.value,
-                           retained_offsets=ret_off)
+                           retained_offsets=ret_off, h2d_ms=ms.value)
 
     def _native_layers(self, eng, x, n_rows, l0, l1, phase, step, rows=None, counts=None, oracle_table=None,
                        trace=None, record=False, record_into=None):
@@ -512,6 +513,7 @@ class MoEStack:
         evs = None
         n_dem = np.zeros(nl, dtype=np.int32)
         out.n_demand = n_dem.ctypes.data
+        cmarks = None
         if self.profile is not None:
             evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * nl)]
             for e in evs:
@@ -519,6 +521,12 @@ class MoEStack:
             arr = (C.c_void_p * (2 * nl))(*[e.cuda_event for e in evs])
             out.ffn_start = C.cast(arr, C.c_void_p)
             out.ffn_end = C.cast(C.byref(arr, nl * C.sizeof(C.c_void_p)), C.c_void_p)
+            if eng is not None:
+                cmarks = [torch.cuda.Event(enable_timing=True) for _ in range(3 * nl)]
+                for e in cmarks:
+                    e.record()
+                carr = (C.c_void_p * (3 * nl))(*[e.cuda_event for e in cmarks])
+                out.copy_marks = C.cast(carr, C.c_void_p)
         try:
             check(self._L.vmm_stack_layers(h, None if eng is None else eng._h, self._x, x.data_ptr(), n_rows, l0, l1,
                                            phase, step,
@@ -534,6 +542,7 @@ class MoEStack:
                 self.profile.append((evs[i], evs[nl + i], nbytes, 6.0 * M * c.hidden * c.inter))
         res = bufs["out"] if out.x_out == bufs["out"].data_ptr() else bufs["out2"]
         self.last_host_us = list(out.host_us)
+        self.last_copy_marks = cmarks
         return res[:n_rows], out.copies, routes_t
 
     # ------------------------------------------------------------------

@@ -44,5 +44,15 @@ per = [starts[i].elapsed_time(starts[i + 1]) for i in range(lp, len(starts) - 1)
 print(f"cached layers: period mean {np.mean(per):.2f} ms, FFN(incl. copy waits) mean {np.mean(ffn[lp:]):.2f} ms,"
       f" non-FFN mean {np.mean(per) - np.mean(ffn[lp:-1]):.2f} ms")
 print("host us (pre, sync, decide, post) over cached layers:", [round(v / 1e3, 1) for v in stack.last_host_us])
+print(f"copy stream: {res.copies} copies, {res.h2d_bytes / 1e9:.1f} GB, first->last copy {res.h2d_ms:.1f} ms "
+      f"= {res.h2d_bytes / res.h2d_ms / 1e6:.1f} GB/s over the copy window")
+cm = stack.last_copy_marks
+if cm:
+    nl = len(cm) // 3
+    dem = [cm[3 * i].elapsed_time(cm[3 * i + 1]) for i in range(nl)]
+    emi = [cm[3 * i + 1].elapsed_time(cm[3 * i + 2]) for i in range(nl)]
+    idle = [cm[3 * (i - 1) + 2].elapsed_time(cm[3 * i]) for i in range(1, nl)]
+    print(f"copy stream per cached layer: demand {np.mean(dem):.2f} ms, emission prefetch {np.mean(emi):.2f} ms, "
+          f"gap before next demand {np.mean(idle):.2f} ms (mean)")
 print("per-layer period:", [round(v, 1) for v in per])
 print("per-layer ffn   :", [round(v, 1) for v in ffn])
