@@ -93,6 +93,30 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
   static const bool force_fence = std::getenv("VMM_FFN_FENCE") != nullptr;
   const bool flagged = !force_fence && ready && d.need_host && d.need_dev && d.ffn_done && n_rows * k > 16;
   bool have_xn = false;  // the fused combine of the previous layer already produced this layer's xn
+  // Early decisions (live routing, large batches): the previous layer's combine ->
+  // norm -> this layer's route run on the first n_split rows first; their expert
+  // set is a subset of the layer's demand set, and at prefill sizes it already
+  // contains every expert -- then it IS the demand set, the host decides and the
+  // copies start while the other 7/8 of the combine/norm/route work is still
+  // running.  Otherwise the host waits for the full counts (same decisions
+  // either way; VMM_NO_EARLY_DECIDE=1 disables the split).
+  static const bool no_split = std::getenv("VMM_NO_EARLY_DECIDE") != nullptr;
+  const int n_split = (!pinned_only && !no_split && d.routing == 0 && d.shared == 0 && n_rows >= 8192) ? n_rows / 8 : 0;
+  bool pending_rest = false;  // previous layer's combine covered rows [0, n_split) only
+  const void *rest_resid = nullptr;
+  void *rest_dst = nullptr;
+  cudaEvent_t ev_part = nullptr, ev_y = nullptr;
+  struct EvGuard {
+    cudaEvent_t *a, *b;
+    ~EvGuard() {
+      if (*a) cudaEventDestroy(*a);
+      if (*b) cudaEventDestroy(*b);
+    }
+  } ev_guard{&ev_part, &ev_y};
+  if (n_split) {
+    VMM_CUDA(cudaEventCreateWithFlags(&ev_part, cudaEventDisableTiming), "event");
+    VMM_CUDA(cudaEventCreateWithFlags(&ev_y, cudaEventDisableTiming), "event");
+  }
   using clk = std::chrono::steady_clock;
   double t_pre = 0, t_sync = 0, t_dec = 0, t_post = 0;  // host microseconds per phase
   auto us = [](clk::time_point a, clk::time_point b) {
@@ -105,16 +129,37 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
     const int emits = pinned_only ? 0 : vmm_engine_emits(eng, l, phase);
     uint32_t *cnt = d.counts + (size_t)l * E;
     bool la_done = false;
+    int32_t *ch = d.counts_host + (size_t)l * E;
+    const bool split_now = pending_rest;
     if (d.routing == 0) {
       VMM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * E, st), "counts memset");
-      if (emits && d.predictor == 2 && l + 1 < L && (E % 16 == 0) && E <= 128) {
-        VMM_CUDA(cudaMemsetAsync(d.la_counts, 0, sizeof(uint32_t) * E, st), "lookahead memset");
-        VMM_TRY(vmm_route_lookahead(xn, d.router, l, L, n_rows, H, E, k, d.ids, d.gates, cnt, d.la_counts, stream));
-        la_done = true;
+      const bool fused_la = emits && d.predictor == 2 && l + 1 < L && (E % 16 == 0) && E <= 128;
+      if (fused_la) VMM_CUDA(cudaMemsetAsync(d.la_counts, 0, sizeof(uint32_t) * E, st), "lookahead memset");
+      // rows [r0, r1) of this layer's router (counts accumulate over the launches)
+      auto route_rows = [&](int r0, int r1) -> int {
+        const char *x0 = (const char *)xn + (size_t)r0 * H * 2;
+        if (fused_la)
+          return vmm_route_lookahead(x0, d.router, l, L, r1 - r0, H, E, k, d.ids + (size_t)r0 * k,
+                                     d.gates + (size_t)r0 * k, cnt, d.la_counts, stream);
+        return vmm_route_topk(x0, (const char *)d.router + (size_t)l * E * H * 2, r1 - r0, H, E, k,
+                              d.ids + (size_t)r0 * k, d.gates + (size_t)r0 * k, nullptr, cnt, stream);
+      };
+      if (split_now) {
+        VMM_TRY(route_rows(0, n_split));
+        VMM_CUDA(cudaMemcpyAsync(ch, cnt, sizeof(uint32_t) * E, cudaMemcpyDeviceToHost, st), "partial counts D2H");
+        VMM_CUDA(cudaEventRecord(ev_part, st), "partial event");
+        // the rest of the previous layer's combine (its gates/pos/Y rows are untouched by chunk 1)
+        const int nr = n_rows - n_split;
+        VMM_TRY(vmm_combine_norm(d.y, d.pos + (size_t)n_split * k, d.gates + (size_t)n_split * k,
+                                 (const char *)rest_resid + (size_t)n_split * H * 2, nr, k, H, nullptr, 0, 1e-6f,
+                                 (char *)rest_dst + (size_t)n_split * H * 2, (char *)xn + (size_t)n_split * H * 2,
+                                 stream));
+        VMM_TRY(route_rows(n_split, n_rows));
+        pending_rest = false;
       } else {
-        VMM_TRY(vmm_route_topk(xn, (const char *)d.router + (size_t)l * E * H * 2, n_rows, H, E, k, d.ids, d.gates,
-                               nullptr, cnt, stream));
+        VMM_TRY(route_rows(0, n_rows));
       }
+      la_done = fused_la;
     } else {
       const int32_t *tr = d.trace_routes + (size_t)l * d.trace_tokens * k;
       const float *tg = d.trace_gates + (size_t)l * d.trace_tokens * k;
@@ -149,18 +194,31 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
         return vmm::fail(VMM_ECONTRACT, "emitting layer without a predictor");
       }
       VMM_CUDA(cudaMemcpyAsync(yh, ysrc, sizeof(double) * E, cudaMemcpyDeviceToHost, st), "scores D2H");
+      if (split_now) VMM_CUDA(cudaEventRecord(ev_y, st), "scores event");
     }
-    int32_t *ch = d.counts_host + (size_t)l * E;
     auto c1 = clk::now(), c2 = c1;
     int n = 0;
     demand.clear();
     if (!pinned_only) {
-      VMM_CUDA(cudaMemcpyAsync(ch, cnt, sizeof(uint32_t) * E, cudaMemcpyDeviceToHost, st), "counts D2H");
-      c1 = clk::now();
-      VMM_CUDA(cudaStreamSynchronize(st), "layer sync");
-      c2 = clk::now();
-      for (int e = 0; e < E; ++e)
-        if (ch[e]) demand.push_back(e);
+      bool known = false;
+      if (split_now) {  // the first chunk's experts: the whole demand set if they are all E
+        c1 = clk::now();
+        VMM_CUDA(cudaEventSynchronize(ev_part), "partial sync");
+        c2 = clk::now();
+        int n_act = 0;
+        for (int e = 0; e < E; ++e) n_act += ch[e] != 0;
+        known = n_act == E;
+        if (known)
+          for (int e = 0; e < E; ++e) demand.push_back(e);
+      }
+      if (!known) {
+        VMM_CUDA(cudaMemcpyAsync(ch, cnt, sizeof(uint32_t) * E, cudaMemcpyDeviceToHost, st), "counts D2H");
+        c1 = clk::now();
+        VMM_CUDA(cudaStreamSynchronize(st), "layer sync");
+        c2 = clk::now();
+        for (int e = 0; e < E; ++e)
+          if (ch[e]) demand.push_back(e);
+      }
       VMM_TRY(vmm_engine_layer(eng, l, demand.data(), (int)demand.size(), phase, step, nullptr));
       if (out && out->copy_marks)
         VMM_CUDA(cudaEventRecord((cudaEvent_t)out->copy_marks[3 * (l - l0)], (cudaStream_t)vmm_xfer_stream(xf)),
@@ -229,9 +287,19 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
                                        gather_s ? xn : nullptr, gather_s ? d.shared_src : nullptr, n_rows, d.h1s,
                                        d.ys, stream));
     }
+    if (out && out->n_demand) out->n_demand[l - l0] = (int)demand.size();
+    // the slabs this layer read are free for refills once its FFNs are done
+    if (l >= lp && !pinned_only) VMM_TRY(vmm_xfer_layer_done(xf, l, stream));
     if (l + 1 < l1) {  // combine fused with the next layer's RMSNorm (xn is free again: consumed above)
-      VMM_TRY(vmm_combine_norm(d.y, d.pos, d.gates, cur, n_rows, k, H, S > 0 ? d.ys : nullptr, S, 1e-6f, dst, xn,
-                               stream));
+      if (n_split) {  // first chunk only; the rest runs after the next layer's first-chunk route
+        VMM_TRY(vmm_combine_norm(d.y, d.pos, d.gates, cur, n_split, k, H, nullptr, 0, 1e-6f, dst, xn, stream));
+        pending_rest = true;
+        rest_resid = cur;
+        rest_dst = dst;
+      } else {
+        VMM_TRY(vmm_combine_norm(d.y, d.pos, d.gates, cur, n_rows, k, H, S > 0 ? d.ys : nullptr, S, 1e-6f, dst, xn,
+                                 stream));
+      }
       have_xn = true;
     } else if (S > 0) {
       VMM_TRY(vmm_combine_shared(d.y, d.pos, d.gates, cur, n_rows, k, H, d.ys, S, dst, stream));
@@ -240,14 +308,13 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
     }
     cur = dst;
     ping ^= 1;
-    if (out && out->n_demand) out->n_demand[l - l0] = (int)demand.size();
-    if (l >= lp && !pinned_only) VMM_TRY(vmm_xfer_layer_done(xf, l, stream));
     auto c4 = clk::now();
     t_pre += us(c0, c1);
     t_sync += us(c1, c2);
     t_dec += us(c2, c3);
     t_post += us(c3, c4);
     if (emits) {
+      if (split_now) VMM_CUDA(cudaEventSynchronize(ev_y), "scores sync");  // yh landed (after the full route)
       VMM_TRY(vmm_engine_emit(eng, l, yh));
       VMM_TRY(vmm_xfer_issue_engine(xf, eng, d.pool, d.host_layers, E, d.arena, d.n_pinned_slots, d.slot_bytes, &n));
       copies += n;

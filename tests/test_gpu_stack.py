@@ -164,14 +164,16 @@ def test_cached_run_bit_identical_to_all_resident_run():
     torch.testing.assert_close(res.hidden.cpu()[rows].float(), acc[rows], rtol=3e-2, atol=3e-2)
 
 
-def test_batched_requests_share_transfers_and_replay_exactly():
+@pytest.mark.parametrize("n_req", [3, 44])
+def test_batched_requests_share_transfers_and_replay_exactly(n_req):
     """R requests in one pass: each request is compressed on its own (prune CTA
     per request, identical to the oracle's per-request compress) and the
     layers run on the union of retained rows; the batch's decisions replay
-    exactly through the oracle engine on the merged routes."""
+    exactly through the oracle engine on the merged routes.  44 requests give
+    > 8192 retained rows: the executor's early-decision split path."""
     from oracle import compress_ref
     cfg = tiny_cfg(routing="live", predictor="gate")
-    trs = [small_trace(cfg, seed=s) for s in (11, 12, 13)]
+    trs = [small_trace(cfg, seed=s) for s in range(11, 11 + n_req)]
     stack = MoEStack(cfg)
     xs, sals, mods = [], [], []
     for i, tr in enumerate(trs):
@@ -322,3 +324,35 @@ def test_sharded_home_mode_bit_identical_to_host_pool_mode():
     assert b.copies == a.copies > 0
     assert b.report.to_dict() == a.report.to_dict()
     assert torch.equal(b.hidden, ha)
+
+
+def test_batched_split_path_bit_identical_to_all_resident_layers():
+    """> 8192 retained rows: early decisions split each layer's combine/norm/route
+    into two launches; the hidden states still equal a layer-by-layer run on
+    resident experts bit for bit."""
+    cfg = tiny_cfg(routing="live", predictor="history", num_slabs=24)
+    store = ExpertStore(cfg, seed=9)
+    trs = [small_trace(cfg, seed=s) for s in range(40, 84)]
+    xs, sals, mods = [], [], []
+    for i, tr in enumerate(trs):
+        x, sal, mod, _ = request(tr, cfg.hidden, seed=100 + i)
+        xs.append(x), sals.append(sal), mods.append(mod)
+    offs = np.cumsum([0] + [t.num_tokens for t in trs]).tolist()
+    x = torch.cat(xs)
+    res = MoEStack(cfg, store=store).forward(x, torch.cat(sals), torch.cat(mods), req_off=offs)
+    torch.cuda.synchronize()
+    assert len(res.retained) >= 8192
+    from paper_2605_05899_b200 import kernels
+    from paper_2605_05899_b200.moe import moe_layer_forward
+    E = cfg.experts
+    arena = torch.stack([store.pool[(l % store.host_layers) * E + e] for l in range(cfg.layers) for e in range(E)]).cuda()
+    cur = x
+    for l in range(cfg.layers):
+        if l == cfg.l_pinned:
+            cur = kernels.gather_rows(cur, torch.from_numpy(res.retained.astype(np.int32)).cuda())
+        xn = kernels.rmsnorm(cur)
+        ids, gates, _ = kernels.route_topk(xn, store.router[l], cfg.k)
+        cur = moe_layer_forward(cur, ids, gates, arena, torch.arange(l * E, (l + 1) * E, dtype=torch.int32,
+                                                                      device="cuda"), cfg.inter, E, xn=xn)
+    torch.cuda.synchronize()
+    assert torch.equal(res.hidden, cur)
