@@ -44,7 +44,7 @@ def parse():
     p.add_argument("--predictor", default=None)
     p.add_argument("--requests", type=int, default=256,
                    help="requests per GPU per step (BASELINE configs[4] batch sweep; 1 = one request per step)")
-    p.add_argument("--source", default="host", choices=["host", "sharded"],
+    p.add_argument("--source", default="host", choices=["host", "sharded", "ep"],
                    help="miss source: pinned host pool over PCIe, or HBM home copies sharded over the GPUs (NVLink)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--out", default=None)
@@ -167,6 +167,14 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+class _EPResult:
+    """EP mode has no cache: no transfers, no decisions."""
+
+    def __init__(self, hidden):
+        self.hidden, self.h2d_bytes, self.h2d_ms, self.copies = hidden, 0.0, 0.0, 0
+        self.report = type("R", (), dict(hit_rate=None, hits=0, misses=0, evictions=0))()
+
+
 def measure_h2d_peak(torch, dev):
     n = 1 << 30
     src = torch.empty(n, dtype=torch.uint8, pin_memory=True)
@@ -211,11 +219,21 @@ def main():
     kw = dict(routing=a.routing, predictor=predictor, host_layers=8)
     if a.source == "sharded":  # logical clock: one slot over NVLink (770 GB/s measured peer copy) or local D2D
         kw["transfer_ms"] = w.expert_bytes / (770e9 if world > 1 else 3000e9) * 1e3
+    if a.source == "ep":
+        kw.update(predictor="none", budget=0)
+        predictor = "none (expert-parallel: no cache)"
     cfg = StackConfig.from_workload(w, **kw)
-    store = ExpertStore(cfg, seed=1000 + rank)
-    home = ShardedHome(store, rank, world) if a.source == "sharded" else None
-    stack = MoEStack(cfg, store=store, home=home)
     R = a.requests
+    # one model for the whole job: every rank builds the same weights (the pinned prefix and router are
+    # replicated; sharded/EP modes keep each expert's home copy on rank e % world)
+    store = ExpertStore(cfg, seed=1000)
+    home = ShardedHome(store, rank, world) if a.source == "sharded" else None
+    if a.source == "ep":
+        from paper_2605_05899_b200.ep import EPStack
+
+        stack = EPStack(cfg, store=store, rank=rank, world=world, max_rows=R * (w.n_visual // 2 + w.n_text) + 64)
+    else:
+        stack = MoEStack(cfg, store=store, home=home)
     tr = generate_trace(w.trace_config(seed=rank * R))
     T1 = tr.num_tokens
     T = T1 * R
@@ -254,7 +272,11 @@ def main():
             md = mod_h.to(dev, non_blocking=True)
         else:
             xd, sd, md = x, sal, mod
-        res = stack.forward(xd, sd, md, trace=dtr, req_off=req_off)
+        if a.source == "ep":
+            h, ret, _ = stack.forward(xd, sd, md, req_off=req_off)
+            res = _EPResult(h)
+        else:
+            res = stack.forward(xd, sd, md, trace=dtr, req_off=req_off)
         if e2e:
             n = int(res.hidden.shape[0])
             if out_h[0] is None or out_h[0].shape[0] < n:  # pinned result buffer, allocated once
@@ -309,20 +331,23 @@ def main():
     # expert offsets, slot table) with every expert resident, L2 flushed before
     # each replay, CUDA events on the launching stream.
     prof = [p for _, pl, _ in results for p in pl[w.l_pinned:]]
-    live_ms = float(np.mean([p[0].elapsed_time(p[1]) for p in prof]))
+    live_ms = float(np.mean([p[0].elapsed_time(p[1]) for p in prof])) if prof else None
     bufs = stack._bufs
-    n_r = int(results[-1][0].hidden.shape[0])
-    M = n_r * w.k
-    off = bufs["off"]
-    slot_row = stack.slot_dev[w.layers - 1]
+    if a.source == "ep":  # the owner-side FFN of the last layer: the rows this rank received
+        xp_r, off, last_l, M = stack.last_ffn
+        arena_r, slot_row = stack.owner.arena, stack.local_slots[last_l]
+    else:
+        n_r = int(results[-1][0].hidden.shape[0])
+        M = n_r * w.k
+        off = bufs["off"]
+        xp_r, arena_r, slot_row = bufs["xp"][:M], stack.store.arena, stack.slot_dev[w.layers - 1]
     ne = int((off[1:] - off[:-1] > 0).sum().item())
     durs = []
     for _ in range(5):
         flush.zero_()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record()
-        kernels.grouped_swiglu(bufs["xp"][:M], off, stack.store.arena, slot_row, w.inter, h1=bufs["h1"][:M],
-                               y=bufs["y"][:M])
+        kernels.grouped_swiglu(xp_r, off, arena_r, slot_row, w.inter, h1=bufs["h1"][:M], y=bufs["y"][:M])
         f1.record()
         f1.synchronize()
         durs.append(f0.elapsed_time(f1))
@@ -353,7 +378,8 @@ def main():
         tj = json.load(open(tpath)).get(f"{w.name}/R{a.requests}")
         traffic = tj["dram_bytes_per_launch"] if tj else None
     res0 = results[-1][0]
-    h2d_peak = measure_h2d_peak(torch, dev) if a.source == "host" else (770.0 if world > 1 else None)
+    h2d_peak = measure_h2d_peak(torch, dev) if a.source == "host" else (770.0 if world > 1 and a.source == "sharded"
+                                                                          else None)
     h2d_bytes = res0.h2d_bytes
     rep = res0.report
     h2d_gbs = h2d_bytes / (ms * 1e-3) / 1e9
@@ -395,7 +421,9 @@ def main():
                     "window_gbs": h2d_bytes / (res0.h2d_ms * 1e-3) / 1e9 if res0.h2d_ms else None,
                     "peak_gbs": h2d_peak, "frac": h2d_gbs / h2d_peak if h2d_peak else None,
                     "link": "PCIe (pinned host pool)" if a.source == "host" else
-                            ("NVLink P2P + local D2D (sharded HBM home copies)" if world > 1 else "local D2D (HBM home)"),
+                            ("none: expert-parallel, token rows over peer memory" if a.source == "ep" else
+                             ("NVLink P2P + local D2D (sharded HBM home copies)" if world > 1 else
+                              "local D2D (HBM home)")),
                     "peak_source": "measured pinned 1 GiB H2D in this run" if a.source == "host" else
                                    "B200_PROFILING.md measured peer copy 770 GB/s"},
             "roofline": {"bound": bound,

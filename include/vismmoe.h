@@ -345,6 +345,8 @@ int vmm_xfer_set_sources(vmm_xfer *x, const void *const *h_table, long long n);
  * processes (64-byte handle) and enable peer access over NVLink */
 int vmm_ipc_get(const void *d_ptr, void *h_handle64);
 int vmm_ipc_open(const void *h_handle64, void **d_ptr);
+/* byte offset of d_ptr inside its allocation (the opener of a handle gets the base) */
+int vmm_ipc_offset(const void *d_ptr, long long *off);
 int vmm_ipc_close(void *d_ptr);
 int vmm_peer_enable(int peer);
 /* drain the engine's transfer commands and enqueue each as one copy of
@@ -358,6 +360,28 @@ int vmm_xfer_join(vmm_xfer *x, void *compute_stream);
 /* copy-stream accounting: bytes issued and wall ms between first and last copy (events) */
 int vmm_xfer_stats(vmm_xfer *x, double *bytes, double *busy_ms, long long *copies);
 void *vmm_xfer_stream(vmm_xfer *x);
+
+/* ------------------------------------------------------------------------
+ * Expert-parallel token exchange over peer memory: the
+ * alternative to weight pulls -- experts stay on their owner rank (e % G) and
+ * token rows move.  Tables are device arrays of G peer pointers (IPC-mapped
+ * allocations; the own rank's entry is local).  The host exchanges the
+ * per-layer (source rank, expert) counts and orders the phases (stream sync +
+ * process barrier between dispatch, expert compute and return).
+ *   vmm_ep_dispatch: pick i (expert e = d_ids[i], owner e % G) -> its row of
+ *                    d_xn [N][H] into the owner's rows buffer at
+ *                    d_base[e] + (d_pos[i] - d_my_off[e]) (d_pos / d_my_off:
+ *                    this rank's vmm_permute_plan by expert), meta (int2) =
+ *                    {source rank, i}: the owner's buffer is already grouped
+ *                    by expert for vmm_grouped_swiglu_fused
+ *   vmm_ep_return:   received row r's output -> source meta[r].x's return
+ *                    buffer at pick index meta[r].y (pick order)
+ * ------------------------------------------------------------------------ */
+int vmm_ep_dispatch(const void *d_xn, int H, const int32_t *d_ids, int k, const int32_t *d_pos,
+                    const int32_t *d_my_off, const int32_t *d_base, const void *d_rows_tab, const void *d_meta_tab,
+                    int G, int rank, int M, void *stream);
+int vmm_ep_return(const void *d_y_local, int H, const void *d_meta, const void *d_back_tab, int n_recv,
+                  void *stream);
 
 /* ------------------------------------------------------------------------
  * Native layer-loop executor (the per-layer body of pipeline.py:709-740 on

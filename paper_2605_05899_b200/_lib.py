@@ -87,6 +87,8 @@ _SIGS = {
     "vmm_attn_saliency": (I32, [P, P, I32, I32, I32, I32, I32, C.c_float, P, P, P]),
     "vmm_attn_map_saliency": (I32, [P, I32, I32, I32, P, P]),
     "vmm_routing_diagnostics": (I32, [P, I32, I32, I32, I32, I32, P, P]),
+    "vmm_ep_dispatch": (I32, [P, I32, P, I32, P, P, P, P, P, I32, I32, I32, P]),
+    "vmm_ep_return": (I32, [P, I32, P, P, I32, P]),
     "vmm_permute": (I32, [P, I32, I32, I32, P, I32, P, P, P, P, P]),
     "vmm_combine": (I32, [P, P, P, P, I32, I32, I32, P, P]),
     "vmm_rmsnorm": (I32, [P, P, I32, I32, C.c_float, P, P]),
@@ -140,6 +142,7 @@ _SIGS = {
     "vmm_xfer_set_sources": (I32, [P, P, I64]),
     "vmm_ipc_get": (I32, [P, P]),
     "vmm_ipc_open": (I32, [P, C.POINTER(P)]),
+    "vmm_ipc_offset": (I32, [P, C.POINTER(I64)]),
     "vmm_ipc_close": (I32, [P]),
     "vmm_peer_enable": (I32, [I32]),
     "vmm_gather_i32": (I32, [P, P, I32, I32, P, P]),
@@ -209,3 +212,23 @@ def stream_ptr(stream=None) -> int:
 
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream
+
+
+def ipc_export(dptr: int) -> bytes:
+    """64-byte IPC handle + 8-byte offset of a device pointer inside its allocation."""
+    L = lib()
+    h = (C.c_char * 64)()
+    check(L.vmm_ipc_get(dptr, h))
+    off = C.c_longlong()
+    check(L.vmm_ipc_offset(dptr, C.byref(off)))
+    return bytes(h) + int(off.value).to_bytes(8, "little")
+
+
+def ipc_import(blob: bytes) -> tuple[int, int]:
+    """Map a peer's exported pointer: (mapped base to close later, pointer)."""
+    L = lib()
+    q = C.c_void_p()
+    buf = (C.c_char * 64).from_buffer_copy(blob[:64])
+    check(L.vmm_ipc_open(buf, C.byref(q)))
+    return q.value, q.value + int.from_bytes(blob[64:72], "little")
+

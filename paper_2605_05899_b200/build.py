@@ -30,6 +30,7 @@ CU = {
     "permute.cu": [],
     "ffn_sm100.cu": [],
     "diag.cu": ["-fmad=false"],
+    "ep.cu": [],
 }
 CPP = ["engine.cpp", "xfer.cpp", "capi.cpp", "stack.cpp"]
 

@@ -1,4 +1,5 @@
 // Error plumbing and device checks for the C-ABI (include/vismmoe.h).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstring>
@@ -44,6 +45,26 @@ int vmm_ipc_get(const void *d_ptr, void *h_handle64) {
   if (e != cudaSuccess) return vmm::fail(VMM_ECUDA, std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
   static_assert(sizeof(h) == 64, "ipc handle size");
   memcpy(h_handle64, &h, sizeof(h));
+  return VMM_OK;
+}
+
+int vmm_ipc_offset(const void *d_ptr, long long *off) {
+  // an IPC handle maps the whole allocation: the opener adds the pointer's offset from its base
+  typedef CUresult (*RangeFn)(CUdeviceptr *, size_t *, CUdeviceptr);
+  static RangeFn fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return vmm::fail(VMM_ECUDA, "cuMemGetAddressRange unavailable");
+    fn = reinterpret_cast<RangeFn>(p);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  CUresult r = fn(&base, &size, (CUdeviceptr)d_ptr);
+  if (r != CUDA_SUCCESS) return vmm::fail(VMM_ECUDA, "cuMemGetAddressRange failed (" + std::to_string((int)r) + ")");
+  *off = (long long)((CUdeviceptr)d_ptr - base);
   return VMM_OK;
 }
 

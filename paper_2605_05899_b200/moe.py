@@ -215,7 +215,9 @@ class ShardedHome:
     enabled) -- instead of a PCIe transfer from the pinned host pool.  No
     collective on the critical path; one handle exchange at setup."""
 
-    def __init__(self, store: ExpertStore, rank: int = 0, world: int = 1):
+    def __init__(self, store: ExpertStore, rank: int = 0, world: int = 1, device_of_rank=None):
+        """device_of_rank: CUDA device of each rank (default: rank r on device r,
+        one process per GPU; several ranks may share one device in tests)."""
         import torch.distributed as dist
 
         c = store.cfg
@@ -234,21 +236,17 @@ class ShardedHome:
         bases = [self.arena.data_ptr()]
         self._opened = []
         if world > 1:
-            hdl = (C.c_char * 64)()
-            check(L_.vmm_ipc_get(self.arena.data_ptr(), hdl))
             handles = [None] * world
-            dist.all_gather_object(handles, bytes(hdl))
+            dist.all_gather_object(handles, _lib.ipc_export(self.arena.data_ptr()))
             bases = []
             for r in range(world):
                 if r == rank:
                     bases.append(self.arena.data_ptr())
                     continue
-                check(L_.vmm_peer_enable(r))  # one process per GPU on one node: rank r <-> device r
-                p = C.c_void_p()
-                buf = (C.c_char * 64).from_buffer_copy(handles[r])
-                check(L_.vmm_ipc_open(buf, C.byref(p)))
-                self._opened.append(p.value)
-                bases.append(p.value)
+                check(L_.vmm_peer_enable(r if device_of_rank is None else int(device_of_rank[r])))
+                base, p = _lib.ipc_import(handles[r])
+                self._opened.append(base)
+                bases.append(p)
         self.table = np.zeros(L * E, dtype=np.uint64)
         for l in range(L):
             for e in range(E):
@@ -366,44 +364,8 @@ class MoEStack:
             raise ContractError("routing='trace' needs the trace's device routes")
         check(self._L.vmm_xfer_reset_stats(self._x))
 
-        # --- pinned prefix: all prefill tokens, resident experts, no cache decisions:
-        # the native executor in engine-less mode (no host sync inside the prefix)
-        prefix = torch.empty((max(lp, 1), T, k), dtype=torch.int32, device=dev)
-        counts_pre = torch.zeros((max(lp, 1), E), dtype=torch.int32, device=dev)
-        x_ctx = None
-        cur = x
-        if lp:
-            rows_all = torch.arange(T, dtype=torch.int32, device=dev) if c.routing == "trace" else None
-            cur, _, _ = self._native_layers(None, x, T, 0, lp, 0, -1, rows=rows_all, counts=counts_pre, trace=trace,
-                                            record_into=prefix[:lp])
-            x_ctx = bufs["xn"][:T]  # normalised input of layer lp-1: context of the boot emission (gate predictor)
-
-        # --- prune (token compression) on the prefix routes, one CTA per request
-        offs = [0, T] if req_off is None else [int(v) for v in req_off]
-        R = len(offs) - 1
-        mod_h = modality.cpu().numpy() if isinstance(modality, torch.Tensor) else np.asarray(modality)
-        ccfg = CompressionConfig(c.alpha, c.beta, c.lam, tuple(range(lp)) if lp else (0,))
-        budgets = [ccfg.budgets(int((mod_h[offs[r]:offs[r + 1]] == 0).sum())) for r in range(R)]
-        pr = kernels.prune(saliency, modality, prefix[:max(lp, 1)],
-                           torch.tensor(offs, dtype=torch.int32, device=dev),
-                           torch.tensor([b[0] for b in budgets], dtype=torch.int32, device=dev),
-                           torch.tensor([b[1] for b in budgets], dtype=torch.int32, device=dev), E, c.lam)
-        n_ret = pr["n_retained"].cpu().numpy()
-        if (pr["status"].cpu().numpy() != 0).any():
-            raise ValidationError("saliency entries must be finite and >= 0")
-        if R == 1:
-            ret = pr["retained"][: int(n_ret[0])]
-        else:  # request-local ids -> global row ids, requests in order (constant launch count in R)
-            starts = torch.tensor(offs[:-1], dtype=torch.int32, device=dev)
-            lens = torch.tensor([offs[r + 1] - offs[r] for r in range(R)], dtype=torch.int64, device=dev)
-            seg = torch.repeat_interleave(torch.arange(R, device=dev), lens, output_size=T)
-            local = torch.arange(T, dtype=torch.int32, device=dev) - starts[seg]
-            valid = local < torch.from_numpy(n_ret.astype(np.int32)).to(dev)[seg]
-            ret = (pr["retained"][:T] + starts[seg])[valid]
-        n_r = int(ret.shape[0])
-        ret_off = np.concatenate([[0], np.cumsum(n_ret)]).astype(np.int64)
-        xr = kernels.gather_rows(cur, ret, out=bufs["xp"][:n_r])  # scratch until permute of layer lp
-        xr = xr.clone()
+        cur, x_ctx, prefix, counts_pre, ret, n_r, ret_off, xr = self._prefix_and_prune(
+            x, saliency, modality, trace, req_off, bufs)
 
         # --- per-layer demand counts over the retained tokens
         counts_ret = torch.zeros((L, E), dtype=torch.int32, device=dev)
@@ -466,6 +428,57 @@ class MoEStack:
         return StackResult(hidden=cur, retained=ret.cpu().numpy(), report=report, prefix_routes=prefix[:lp],
                            routes=routes, scores=scores, copies=n_copies, h2d_bytes=b.value,
                            retained_offsets=ret_off, h2d_ms=ms.value)
+
+    def _prefix_and_prune(self, x, saliency, modality, trace, req_off, bufs):
+        """Pinned prefix on all T rows (resident experts, engine-less executor,
+        no host sync) then per-request compression on the prefix routes.
+        Returns (rows after the prefix, xn of layer lp-1, prefix routes,
+        prefix counts, retained ids, N_r, per-request retained offsets,
+        retained rows)."""
+        c = self.cfg
+        L, E, k, lp = c.layers, c.experts, c.k, c.l_pinned
+        dev = self.device
+        T = int(x.shape[0])
+        # --- pinned prefix: all prefill tokens, resident experts, no cache decisions:
+        # the native executor in engine-less mode (no host sync inside the prefix)
+        prefix = torch.empty((max(lp, 1), T, k), dtype=torch.int32, device=dev)
+        counts_pre = torch.zeros((max(lp, 1), E), dtype=torch.int32, device=dev)
+        x_ctx = None
+        cur = x
+        if lp:
+            rows_all = torch.arange(T, dtype=torch.int32, device=dev) if c.routing == "trace" else None
+            cur, _, _ = self._native_layers(None, x, T, 0, lp, 0, -1, rows=rows_all, counts=counts_pre, trace=trace,
+                                            record_into=prefix[:lp])
+            x_ctx = bufs["xn"][:T]  # normalised input of layer lp-1: context of the boot emission (gate predictor)
+
+        # --- prune (token compression) on the prefix routes, one CTA per request
+        offs = [0, T] if req_off is None else [int(v) for v in req_off]
+        R = len(offs) - 1
+        mod_h = modality.cpu().numpy() if isinstance(modality, torch.Tensor) else np.asarray(modality)
+        ccfg = CompressionConfig(c.alpha, c.beta, c.lam, tuple(range(lp)) if lp else (0,))
+        budgets = [ccfg.budgets(int((mod_h[offs[r]:offs[r + 1]] == 0).sum())) for r in range(R)]
+        pr = kernels.prune(saliency, modality, prefix[:max(lp, 1)],
+                           torch.tensor(offs, dtype=torch.int32, device=dev),
+                           torch.tensor([b[0] for b in budgets], dtype=torch.int32, device=dev),
+                           torch.tensor([b[1] for b in budgets], dtype=torch.int32, device=dev), E, c.lam)
+        n_ret = pr["n_retained"].cpu().numpy()
+        if (pr["status"].cpu().numpy() != 0).any():
+            raise ValidationError("saliency entries must be finite and >= 0")
+        if R == 1:
+            ret = pr["retained"][: int(n_ret[0])]
+        else:  # request-local ids -> global row ids, requests in order (constant launch count in R)
+            starts = torch.tensor(offs[:-1], dtype=torch.int32, device=dev)
+            lens = torch.tensor([offs[r + 1] - offs[r] for r in range(R)], dtype=torch.int64, device=dev)
+            seg = torch.repeat_interleave(torch.arange(R, device=dev), lens, output_size=T)
+            local = torch.arange(T, dtype=torch.int32, device=dev) - starts[seg]
+            valid = local < torch.from_numpy(n_ret.astype(np.int32)).to(dev)[seg]
+            ret = (pr["retained"][:T] + starts[seg])[valid]
+        n_r = int(ret.shape[0])
+        ret_off = np.concatenate([[0], np.cumsum(n_ret)]).astype(np.int64)
+        xr = kernels.gather_rows(cur, ret, out=bufs["xp"][:n_r])  # scratch until permute of layer lp
+        xr = xr.clone()
+        return cur, x_ctx, prefix, counts_pre, ret, n_r, ret_off, xr
+
 
     def _native_layers(self, eng, x, n_rows, l0, l1, phase, step, rows=None, counts=None, oracle_table=None,
                        trace=None, record=False, record_into=None):

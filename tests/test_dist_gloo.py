@@ -80,3 +80,54 @@ def test_data_parallel_world2_gloo():
         seen.update(results)
         assert tot == [float(sum(v[1] for v in single.values())), float(sum(v[2] for v in single.values()))]
     assert seen == single
+
+
+def _ep_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_05899_b200.ep import ep_layout
+
+    vdist.init("gloo")
+    E = 10  # not a multiple of the world size on purpose
+    rng = np.random.default_rng(rank)
+    mine = torch.from_numpy(rng.integers(0, 50, size=E).astype(np.int64))
+    allc = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(allc, mine)
+    counts = np.stack([a.numpy() for a in allc])
+    q.put((rank, counts, ep_layout(counts, rank)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ep_count_exchange_and_layout_gloo(world):
+    """EP host plan: after the (source, expert) count exchange, every source's
+    block of every expert lands at a disjoint range of the owner's buffer, the
+    blocks are expert-major then source-ordered, and tile the buffer exactly."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ep_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = {r: (c, lay) for r, c, lay in (q.get(timeout=120) for _ in range(world))}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    counts = outs[0][0]
+    G, E = counts.shape
+    for r in range(world):
+        assert np.array_equal(outs[r][0], counts)
+    for d in range(world):
+        _, off_local, n_recv = outs[d][1]
+        assert n_recv == int(counts[:, d::G].sum())
+        expect = 0
+        for j, e in enumerate(range(d, E, G)):
+            assert off_local[j] == expect
+            for s in range(world):
+                base, _, _ = outs[s][1]
+                assert base[e] == expect  # source s's block of expert e starts here
+                expect += int(counts[s, e])
+        assert expect == n_recv == off_local[-1]
