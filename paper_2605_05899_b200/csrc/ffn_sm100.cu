@@ -748,9 +748,68 @@ __device__ __forceinline__ int jth_active_expert(const int32_t *offsets, int E, 
   return s_e;
 }
 
-__global__ void skinny_gateup_kernel(const __nv_bfloat16 *__restrict__ xp, const int32_t *__restrict__ offsets,
-                                     int E, const int32_t *__restrict__ slot_of, const __nv_bfloat16 *__restrict__ w13,
-                                     long long stride, int H, int I, __nv_bfloat16 *__restrict__ h1) {
+// Two weight rows per warp, streamed in 4 KB segments: every lane issues its
+// 2 x 8 sixteen-byte loads of a segment before touching any of them (8 KB in
+// flight per warp, several warps per SM), then dots them with the expert's
+// token rows (RC rows per pass, re-reading the weights from L2 if an expert
+// has more than RC rows -- at decode it has one).
+constexpr int kSeg = 8;   // uint4 per lane per weight row per segment
+constexpr int kRC = 4;    // token rows per pass
+
+__device__ __forceinline__ void bf16x8_fma(const uint4 &w, const uint4 &x, float &acc) {
+  const __nv_bfloat16 *wh = reinterpret_cast<const __nv_bfloat16 *>(&w);
+  const __nv_bfloat16 *xh = reinterpret_cast<const __nv_bfloat16 *>(&x);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc = fmaf(__bfloat162float(xh[q]), __bfloat162float(wh[q]), acc);
+}
+
+// acc[r][0|1] = <x row m0+r, weight row 0|1> over a row of row_vec uint4, lane partials
+__device__ __forceinline__ void warp_dot2(const uint4 *__restrict__ w0, const uint4 *__restrict__ w1, int row_vec,
+                                          const uint4 *__restrict__ x, int x_stride, int nrows,
+                                          float (&acc)[kRC][2]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int r = 0; r < kRC; ++r) acc[r][0] = acc[r][1] = 0.f;
+  for (int s0 = 0; s0 < row_vec; s0 += 32 * kSeg) {
+    uint4 a[kSeg], b[kSeg];
+#pragma unroll
+    for (int u = 0; u < kSeg; ++u) {
+      const int c = s0 + lane + 32 * u;
+      if (c < row_vec) {
+        a[u] = __ldg(w0 + c);
+        b[u] = __ldg(w1 + c);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kRC; ++r) {
+      if (r < nrows) {
+#pragma unroll
+        for (int u = 0; u < kSeg; ++u) {
+          const int c = s0 + lane + 32 * u;
+          if (c < row_vec) {
+            const uint4 xv = __ldg(x + (long long)r * x_stride + c);
+            bf16x8_fma(a[u], xv, acc[r][0]);
+            bf16x8_fma(b[u], xv, acc[r][1]);
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < kRC; ++r)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      acc[r][0] += __shfl_xor_sync(0xffffffffu, acc[r][0], o);
+      acc[r][1] += __shfl_xor_sync(0xffffffffu, acc[r][1], o);
+    }
+}
+
+// warp = one output feature f of one active expert: gate row and up row of W13
+__global__ void __launch_bounds__(256) skinny_gateup_kernel(const __nv_bfloat16 *__restrict__ xp,
+                                                            const int32_t *__restrict__ offsets, int E,
+                                                            const int32_t *__restrict__ slot_of,
+                                                            const __nv_bfloat16 *__restrict__ w13, long long stride,
+                                                            int H, int I, __nv_bfloat16 *__restrict__ h1) {
   const int e = jth_active_expert(offsets, E, blockIdx.y);
   if (e < 0) return;
   const int r0 = offsets[e], r1 = offsets[e + 1];
@@ -759,100 +818,44 @@ __global__ void skinny_gateup_kernel(const __nv_bfloat16 *__restrict__ xp, const
   if (f >= I) return;
   const __nv_bfloat16 *w = w13 + (long long)slot_of[e] * stride;
   const int grow = (f >> 6) * 128 + (f & 63);  // interleaved 64|64 gate/up blocks
-  const uint4 *wg = reinterpret_cast<const uint4 *>(w + (long long)grow * H);
-  const uint4 *wu = reinterpret_cast<const uint4 *>(w + (long long)(grow + 64) * H);
-  const int nv = H / 8, nr = r1 - r0;
-  float ag[kSkinnyRows], au[kSkinnyRows];
+  const int rv = H / 8;
+  for (int m0 = r0; m0 < r1; m0 += kRC) {
+    float acc[kRC][2];
+    warp_dot2(reinterpret_cast<const uint4 *>(w + (long long)grow * H),
+              reinterpret_cast<const uint4 *>(w + (long long)(grow + 64) * H), rv,
+              reinterpret_cast<const uint4 *>(xp + (long long)m0 * H), rv, min(kRC, r1 - m0), acc);
+    if (lane == 0)
 #pragma unroll
-  for (int m = 0; m < kSkinnyRows; ++m) { ag[m] = 0.f; au[m] = 0.f; }
-  // issue the lane's weight loads for 4 chunks at once (HBM latency hiding), then use them
-  for (int c0 = lane; c0 < nv; c0 += 32 * 4) {
-    uint4 gvs[4], uvs[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int c = c0 + 32 * u;
-      gvs[u] = c < nv ? __ldg(wg + c) : make_uint4(0, 0, 0, 0);
-      uvs[u] = c < nv ? __ldg(wu + c) : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-    const int c = c0 + 32 * u;
-    if (c >= nv) break;
-    uint4 gv = gvs[u], uv = uvs[u];
-    const __nv_bfloat16 *gh = reinterpret_cast<const __nv_bfloat16 *>(&gv);
-    const __nv_bfloat16 *uh = reinterpret_cast<const __nv_bfloat16 *>(&uv);
-#pragma unroll
-    for (int m = 0; m < kSkinnyRows; ++m) {
-      if (m < nr) {
-        uint4 xv = __ldg(reinterpret_cast<const uint4 *>(xp + (long long)(r0 + m) * H) + c);
-        const __nv_bfloat16 *xh = reinterpret_cast<const __nv_bfloat16 *>(&xv);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          float xf = __bfloat162float(xh[q]);
-          ag[m] = fmaf(xf, __bfloat162float(gh[q]), ag[m]);
-          au[m] = fmaf(xf, __bfloat162float(uh[q]), au[m]);
-        }
-      }
-    }
-    }
-  }
-#pragma unroll
-  for (int m = 0; m < kSkinnyRows; ++m) {
-    if (m < nr) {
-      float g = ag[m], u = au[m];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        g += __shfl_xor_sync(0xffffffffu, g, o);
-        u += __shfl_xor_sync(0xffffffffu, u, o);
-      }
-      if (lane == 0) h1[(long long)(r0 + m) * I + f] = __float2bfloat16(silu(g) * u);
-    }
+      for (int r = 0; r < kRC; ++r)
+        if (m0 + r < r1) h1[(long long)(m0 + r) * I + f] = __float2bfloat16(silu(acc[r][0]) * acc[r][1]);
   }
 }
 
-__global__ void skinny_down_kernel(const __nv_bfloat16 *__restrict__ h1, const int32_t *__restrict__ offsets,
-                                   int E, const int32_t *__restrict__ slot_of, const __nv_bfloat16 *__restrict__ w2,
-                                   long long stride, int H, int I, __nv_bfloat16 *__restrict__ y) {
+// warp = two output columns (n, n+1) of one active expert: rows n, n+1 of W2
+__global__ void __launch_bounds__(256) skinny_down_kernel(const __nv_bfloat16 *__restrict__ h1,
+                                                          const int32_t *__restrict__ offsets, int E,
+                                                          const int32_t *__restrict__ slot_of,
+                                                          const __nv_bfloat16 *__restrict__ w2, long long stride,
+                                                          int H, int I, __nv_bfloat16 *__restrict__ y) {
   const int e = jth_active_expert(offsets, E, blockIdx.y);
   if (e < 0) return;
   const int r0 = offsets[e], r1 = offsets[e + 1];
-  const int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // output column
+  const int n = 2 * (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));  // output columns n, n+1
   const int lane = threadIdx.x & 31;
   if (n >= H) return;
-  const uint4 *wr = reinterpret_cast<const uint4 *>(w2 + (long long)slot_of[e] * stride + (long long)n * I);
-  const int nv = I / 8, nr = r1 - r0;
-  float acc[kSkinnyRows];
+  const __nv_bfloat16 *w = w2 + (long long)slot_of[e] * stride;
+  const int rv = I / 8;
+  for (int m0 = r0; m0 < r1; m0 += kRC) {
+    float acc[kRC][2];
+    warp_dot2(reinterpret_cast<const uint4 *>(w + (long long)n * I),
+              reinterpret_cast<const uint4 *>(w + (long long)(n + 1) * I), rv,
+              reinterpret_cast<const uint4 *>(h1 + (long long)m0 * I), rv, min(kRC, r1 - m0), acc);
+    if (lane == 0)
 #pragma unroll
-  for (int m = 0; m < kSkinnyRows; ++m) acc[m] = 0.f;
-  for (int c0 = lane; c0 < nv; c0 += 32 * 4) {
-    uint4 wvs[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) wvs[u] = (c0 + 32 * u) < nv ? __ldg(wr + c0 + 32 * u) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-    const int c = c0 + 32 * u;
-    if (c >= nv) break;
-    uint4 wv = wvs[u];
-    const __nv_bfloat16 *wh = reinterpret_cast<const __nv_bfloat16 *>(&wv);
-#pragma unroll
-    for (int m = 0; m < kSkinnyRows; ++m) {
-      if (m < nr) {
-        uint4 hv = __ldg(reinterpret_cast<const uint4 *>(h1 + (long long)(r0 + m) * I) + c);
-        const __nv_bfloat16 *hh = reinterpret_cast<const __nv_bfloat16 *>(&hv);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) acc[m] = fmaf(__bfloat162float(hh[q]), __bfloat162float(wh[q]), acc[m]);
-      }
-    }
-    }
-  }
-#pragma unroll
-  for (int m = 0; m < kSkinnyRows; ++m) {
-    if (m < nr) {
-      float v = acc[m];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) y[(long long)(r0 + m) * H + n] = __float2bfloat16(v);
-    }
+      for (int r = 0; r < kRC; ++r)
+        if (m0 + r < r1)
+          *reinterpret_cast<__nv_bfloat162 *>(y + (long long)(m0 + r) * H + n) =
+              __floats2bfloat162_rn(acc[r][0], acc[r][1]);
   }
 }
 
@@ -913,7 +916,7 @@ extern "C" int vmm_grouped_swiglu(const void *d_xp, const int32_t *d_offsets, in
     cudaStream_t s = (cudaStream_t)stream;
     constexpr int kWarps = 8;
     // grid.y = active-expert slots (at most M_total experts have rows)
-    dim3 g1((I + kWarps - 1) / kWarps, M_total), g2((H + kWarps - 1) / kWarps, M_total);
+    dim3 g1((I + kWarps - 1) / kWarps, M_total), g2((H / 2 + kWarps - 1) / kWarps, M_total);
     skinny_gateup_kernel<<<g1, 32 * kWarps, 0, s>>>((const __nv_bfloat16 *)d_xp, d_offsets, E, d_slot_of_expert,
                                                      (const __nv_bfloat16 *)d_w13_arena, slot_stride, H, I,
                                                      (__nv_bfloat16 *)d_h1);
