@@ -201,9 +201,11 @@ int vmm_grouped_swiglu(const void *d_xp, const int32_t *d_offsets, int E, int M_
  * still stream in.  need[e] == 0: no wait.  Row gather: when d_src_row
  * != NULL (the plan's [M_total] source rows) GEMM1 reads its A rows straight
  * from d_x_rows [n_x_rows][H] with TMA tile::gather4 and d_xp is unused, so no
- * permuted copy of the tokens is materialised.  M_total <= 16 (decode) or
- * d_done == NULL falls through to vmm_grouped_swiglu (d_need and d_src_row
- * must then be NULL). */
+ * permuted copy of the tokens is materialised.  M_total <= 16 (decode): one
+ * persistent weight-streaming CUDA-core launch (both projections, grid-wide
+ * barrier between them), which honours d_need/d_ready as well.  d_done ==
+ * NULL with M_total > 16 falls through to vmm_grouped_swiglu (d_need and
+ * d_src_row must then be NULL). */
 int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offsets, int E, int M_total,
                              int H, int I, const void *d_w13_arena, const void *d_w2_arena, long long slot_stride,
                              long long n_slots, const int32_t *d_slot_of_expert, const uint32_t *d_need,

@@ -720,41 +720,18 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
 // the demanded experts' weights, spread over all SMs.
 constexpr int kSkinnyRows = 16;
 
-// expert owning "active slot" j (the j-th expert with rows), or -1.  The CTA
-// stages offsets[] in shared memory with one coalesced load, then warp 0 scans.
-__device__ __forceinline__ int jth_active_expert(const int32_t *offsets, int E, int j) {
-  __shared__ int s_off[VMM_MAX_EXPERTS + 1];
-  __shared__ int s_e;
-  for (int i = threadIdx.x; i <= E; i += blockDim.x) s_off[i] = offsets[i];
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    int seen = 0, found = -1;
-    for (int c0 = 0; c0 < E && found < 0; c0 += 32) {
-      const int e = c0 + lane;
-      const bool act = e < E && s_off[e + 1] > s_off[e];
-      const unsigned bal = __ballot_sync(0xffffffffu, act);
-      const int cnt = __popc(bal);
-      if (j < seen + cnt) {
-        unsigned b = bal;
-        for (int r = 0; r < j - seen; ++r) b &= b - 1;
-        found = c0 + __ffs(b) - 1;
-      }
-      seen += cnt;
-    }
-    if (lane == 0) s_e = found;
-  }
-  __syncthreads();
-  return s_e;
-}
-
-// Two weight rows per warp, streamed in 4 KB segments: every lane issues its
-// 2 x 8 sixteen-byte loads of a segment before touching any of them (8 KB in
-// flight per warp, several warps per SM), then dots them with the expert's
-// token rows (RC rows per pass, re-reading the weights from L2 if an expert
-// has more than RC rows -- at decode it has one).
-constexpr int kSeg = 8;   // uint4 per lane per weight row per segment
-constexpr int kRC = 4;    // token rows per pass
+// One persistent launch (one 512-thread CTA per SM, all co-resident) runs both
+// phases, separated by a grid-wide barrier:
+//   phase 1: work item = (active expert, output feature f): its gate and up
+//            rows of W13 (2 x 4 KB at H=2048), dotted with the expert's token
+//            rows -> H1 = SiLU(g) * u;
+//   phase 2: work item = (active expert, 4 output columns): 4 rows of W2
+//            (4 x 1.5 KB), dotted with the expert's H1 rows -> Y.
+// Each lane issues all of its 16-byte loads of an item (NW rows x SEG chunks)
+// before touching any, so every warp keeps 6-8 KB of weights in flight and 16
+// warps per SM cover the HBM latency; the items of a phase stream through the
+// active experts' weights exactly once.
+constexpr int kRC = 4;  // token rows per pass (an expert has one row per decode token)
 
 __device__ __forceinline__ void bf16x8_fma(const uint4 &w, const uint4 &x, float &acc) {
   const __nv_bfloat16 *wh = reinterpret_cast<const __nv_bfloat16 *>(&w);
@@ -763,33 +740,36 @@ __device__ __forceinline__ void bf16x8_fma(const uint4 &w, const uint4 &x, float
   for (int q = 0; q < 8; ++q) acc = fmaf(__bfloat162float(xh[q]), __bfloat162float(wh[q]), acc);
 }
 
-// acc[r][0|1] = <x row m0+r, weight row 0|1> over a row of row_vec uint4, lane partials
-__device__ __forceinline__ void warp_dot2(const uint4 *__restrict__ w0, const uint4 *__restrict__ w1, int row_vec,
-                                          const uint4 *__restrict__ x, int x_stride, int nrows,
-                                          float (&acc)[kRC][2]) {
+// acc[r][i] = <x row r, weight row i> (lane partials reduced over the warp) for
+// NW weight rows of row_vec uint4; x rows read coherently (phase 2 reads H1
+// written earlier in the same launch)
+template <int NW, int SEG>
+__device__ __forceinline__ void warp_dot(const uint4 *const (&w)[NW], int row_vec, const uint4 *x, int x_stride,
+                                         int nrows, float (&acc)[kRC][NW]) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
-  for (int r = 0; r < kRC; ++r) acc[r][0] = acc[r][1] = 0.f;
-  for (int s0 = 0; s0 < row_vec; s0 += 32 * kSeg) {
-    uint4 a[kSeg], b[kSeg];
+  for (int r = 0; r < kRC; ++r)
 #pragma unroll
-    for (int u = 0; u < kSeg; ++u) {
-      const int c = s0 + lane + 32 * u;
-      if (c < row_vec) {
-        a[u] = __ldg(w0 + c);
-        b[u] = __ldg(w1 + c);
+    for (int i = 0; i < NW; ++i) acc[r][i] = 0.f;
+  for (int s0 = 0; s0 < row_vec; s0 += 32 * SEG) {
+    uint4 a[NW][SEG];
+#pragma unroll
+    for (int i = 0; i < NW; ++i)
+#pragma unroll
+      for (int u = 0; u < SEG; ++u) {
+        const int c = s0 + lane + 32 * u;
+        if (c < row_vec) a[i][u] = __ldg(w[i] + c);
       }
-    }
 #pragma unroll
     for (int r = 0; r < kRC; ++r) {
       if (r < nrows) {
 #pragma unroll
-        for (int u = 0; u < kSeg; ++u) {
+        for (int u = 0; u < SEG; ++u) {
           const int c = s0 + lane + 32 * u;
           if (c < row_vec) {
-            const uint4 xv = __ldg(x + (long long)r * x_stride + c);
-            bf16x8_fma(a[u], xv, acc[r][0]);
-            bf16x8_fma(b[u], xv, acc[r][1]);
+            const uint4 xv = __ldcg(x + (long long)r * x_stride + c);
+#pragma unroll
+            for (int i = 0; i < NW; ++i) bf16x8_fma(a[i][u], xv, acc[r][i]);
           }
         }
       }
@@ -798,64 +778,96 @@ __device__ __forceinline__ void warp_dot2(const uint4 *__restrict__ w0, const ui
 #pragma unroll
   for (int r = 0; r < kRC; ++r)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      acc[r][0] += __shfl_xor_sync(0xffffffffu, acc[r][0], o);
-      acc[r][1] += __shfl_xor_sync(0xffffffffu, acc[r][1], o);
+    for (int i = 0; i < NW; ++i)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[r][i] += __shfl_xor_sync(0xffffffffu, acc[r][i], o);
+}
+
+constexpr int kSkinnyThreads = 512;
+
+__global__ void __launch_bounds__(kSkinnyThreads, 1)
+skinny_ffn_kernel(const __nv_bfloat16 *__restrict__ xp, const int32_t *__restrict__ offsets, int E,
+                  const int32_t *__restrict__ slot_of, const __nv_bfloat16 *__restrict__ w13,
+                  const __nv_bfloat16 *__restrict__ w2, long long stride, int H, int I, const uint32_t *need,
+                  const uint32_t *ready, int ready_base, unsigned int *grid_bar, unsigned int bar_target,
+                  __nv_bfloat16 *h1, __nv_bfloat16 *__restrict__ y) {
+  __shared__ int s_act[kSkinnyRows], s_r0[kSkinnyRows], s_r1[kSkinnyRows];
+  __shared__ int s_nact;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {  // active experts in ascending id order (at most M_total <= 16 of them)
+    int seen = 0;
+    for (int c0 = 0; c0 < E; c0 += 32) {
+      const int e = c0 + lane;
+      const bool act = e < E && offsets[e + 1] > offsets[e];
+      const unsigned bal = __ballot_sync(0xffffffffu, act);
+      if (act) {
+        const int j = seen + __popc(bal & ((1u << lane) - 1u));
+        if (j < kSkinnyRows) {
+          s_act[j] = e;
+          s_r0[j] = offsets[e];
+          s_r1[j] = offsets[e + 1];
+        }
+      }
+      seen += __popc(bal);
     }
-}
-
-// warp = one output feature f of one active expert: gate row and up row of W13
-__global__ void __launch_bounds__(256) skinny_gateup_kernel(const __nv_bfloat16 *__restrict__ xp,
-                                                            const int32_t *__restrict__ offsets, int E,
-                                                            const int32_t *__restrict__ slot_of,
-                                                            const __nv_bfloat16 *__restrict__ w13, long long stride,
-                                                            int H, int I, __nv_bfloat16 *__restrict__ h1) {
-  const int e = jth_active_expert(offsets, E, blockIdx.y);
-  if (e < 0) return;
-  const int r0 = offsets[e], r1 = offsets[e + 1];
-  const int f = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // output feature
-  const int lane = threadIdx.x & 31;
-  if (f >= I) return;
-  const __nv_bfloat16 *w = w13 + (long long)slot_of[e] * stride;
-  const int grow = (f >> 6) * 128 + (f & 63);  // interleaved 64|64 gate/up blocks
-  const int rv = H / 8;
-  for (int m0 = r0; m0 < r1; m0 += kRC) {
-    float acc[kRC][2];
-    warp_dot2(reinterpret_cast<const uint4 *>(w + (long long)grow * H),
-              reinterpret_cast<const uint4 *>(w + (long long)(grow + 64) * H), rv,
-              reinterpret_cast<const uint4 *>(xp + (long long)m0 * H), rv, min(kRC, r1 - m0), acc);
-    if (lane == 0)
-#pragma unroll
-      for (int r = 0; r < kRC; ++r)
-        if (m0 + r < r1) h1[(long long)(m0 + r) * I + f] = __float2bfloat16(silu(acc[r][0]) * acc[r][1]);
+    if (lane == 0) s_nact = seen < kSkinnyRows ? seen : kSkinnyRows;
   }
-}
-
-// warp = two output columns (n, n+1) of one active expert: rows n, n+1 of W2
-__global__ void __launch_bounds__(256) skinny_down_kernel(const __nv_bfloat16 *__restrict__ h1,
-                                                          const int32_t *__restrict__ offsets, int E,
-                                                          const int32_t *__restrict__ slot_of,
-                                                          const __nv_bfloat16 *__restrict__ w2, long long stride,
-                                                          int H, int I, __nv_bfloat16 *__restrict__ y) {
-  const int e = jth_active_expert(offsets, E, blockIdx.y);
-  if (e < 0) return;
-  const int r0 = offsets[e], r1 = offsets[e + 1];
-  const int n = 2 * (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));  // output columns n, n+1
-  const int lane = threadIdx.x & 31;
-  if (n >= H) return;
-  const __nv_bfloat16 *w = w2 + (long long)slot_of[e] * stride;
-  const int rv = I / 8;
-  for (int m0 = r0; m0 < r1; m0 += kRC) {
-    float acc[kRC][2];
-    warp_dot2(reinterpret_cast<const uint4 *>(w + (long long)n * I),
-              reinterpret_cast<const uint4 *>(w + (long long)(n + 1) * I), rv,
-              reinterpret_cast<const uint4 *>(h1 + (long long)m0 * I), rv, min(kRC, r1 - m0), acc);
-    if (lane == 0)
+  __syncthreads();
+  const int nact = s_nact;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + warp, nwarps = gridDim.x * (blockDim.x >> 5);
+  // phase 1: gate/up
+  const int rv1 = H / 8;
+  for (int it = gw; it < nact * I; it += nwarps) {
+    const int j = it / I, f = it - j * I;
+    const int e = s_act[j];
+    if (need && need[e] && lane == 0) wait_at_least(ready + (slot_of[e] - ready_base), need[e], 128);
+    __syncwarp();
+    const __nv_bfloat16 *w = w13 + (long long)slot_of[e] * stride;
+    const int grow = (f >> 6) * 128 + (f & 63);  // interleaved 64|64 gate/up blocks
+    const uint4 *rows[2] = {reinterpret_cast<const uint4 *>(w + (long long)grow * H),
+                            reinterpret_cast<const uint4 *>(w + (long long)(grow + 64) * H)};
+    for (int m0 = s_r0[j]; m0 < s_r1[j]; m0 += kRC) {
+      float acc[kRC][2];
+      warp_dot<2, 8>(rows, rv1, reinterpret_cast<const uint4 *>(xp + (long long)m0 * H), rv1,
+                     min(kRC, s_r1[j] - m0), acc);
+      if (lane == 0)
 #pragma unroll
-      for (int r = 0; r < kRC; ++r)
-        if (m0 + r < r1)
-          *reinterpret_cast<__nv_bfloat162 *>(y + (long long)(m0 + r) * H + n) =
-              __floats2bfloat162_rn(acc[r][0], acc[r][1]);
+        for (int r = 0; r < kRC; ++r)
+          if (m0 + r < s_r1[j]) h1[(long long)(m0 + r) * I + f] = __float2bfloat16(silu(acc[r][0]) * acc[r][1]);
+    }
+  }
+  // grid-wide barrier (all CTAs co-resident: one per SM): H1 complete before phase 2
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicAdd(grid_bar, 1u);
+    wait_at_least(grid_bar, bar_target, 32);
+  }
+  __syncthreads();
+  // phase 2: down projection, 4 output columns per item
+  const int rv2 = I / 8;
+  const int ncol4 = H / 4;
+  for (int it = gw; it < nact * ncol4; it += nwarps) {
+    const int j = it / ncol4, n = 4 * (it - j * ncol4);
+    const int e = s_act[j];
+    const __nv_bfloat16 *w = w2 + (long long)slot_of[e] * stride;
+    const uint4 *rows[4] = {reinterpret_cast<const uint4 *>(w + (long long)(n + 0) * I),
+                            reinterpret_cast<const uint4 *>(w + (long long)(n + 1) * I),
+                            reinterpret_cast<const uint4 *>(w + (long long)(n + 2) * I),
+                            reinterpret_cast<const uint4 *>(w + (long long)(n + 3) * I)};
+    for (int m0 = s_r0[j]; m0 < s_r1[j]; m0 += kRC) {
+      float acc[kRC][4];
+      warp_dot<4, 4>(rows, rv2, reinterpret_cast<const uint4 *>(h1 + (long long)m0 * I), rv2,
+                     min(kRC, s_r1[j] - m0), acc);
+      if (lane == 0)
+#pragma unroll
+        for (int r = 0; r < kRC; ++r)
+          if (m0 + r < s_r1[j]) {
+            __nv_bfloat162 *dst = reinterpret_cast<__nv_bfloat162 *>(y + (long long)(m0 + r) * H + n);
+            dst[0] = __floats2bfloat162_rn(acc[r][0], acc[r][1]);
+            dst[1] = __floats2bfloat162_rn(acc[r][2], acc[r][3]);
+          }
+    }
   }
 }
 
@@ -903,6 +915,35 @@ __global__ void simt_gemm2_kernel(const __nv_bfloat16 *__restrict__ h1, const in
 
 }  // namespace
 
+// per-device grid-barrier counter for the persistent decode FFN (monotonic:
+// each launch waits for its own epoch's target, so it is never reset)
+static int skinny_launch(const void *d_xp, const int32_t *d_offsets, int E, int M_total, int H, int I,
+                         const void *d_w13, const void *d_w2, long long stride, const int32_t *d_slot_of,
+                         const uint32_t *d_need, const uint32_t *d_ready, int ready_base, void *d_h1, void *d_y,
+                         void *stream) {
+  if (H % 8 || I % 8 || H % 4) return vmm::fail(VMM_EVALIDATION, "decode FFN: hidden/inter must be multiples of 8");
+  static unsigned int *bar[64] = {nullptr};
+  static unsigned long long epoch[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return vmm::fail(VMM_ECUDA, "device index out of range");
+  if (!bar[dev]) {
+    cudaError_t e = cudaMalloc(&bar[dev], sizeof(unsigned int));
+    if (e == cudaSuccess) e = cudaMemset(bar[dev], 0, sizeof(unsigned int));
+    if (e != cudaSuccess) return vmm::cuda_status(e, "decode FFN barrier");
+  }
+  if (!g_num_sms) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = g_num_sms;
+  epoch[dev] += 1;
+  const unsigned int target = (unsigned int)(epoch[dev] * (unsigned long long)grid);  // wraps consistently
+  skinny_ffn_kernel<<<grid, kSkinnyThreads, 0, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16 *)d_xp, d_offsets, E, d_slot_of, (const __nv_bfloat16 *)d_w13,
+      (const __nv_bfloat16 *)d_w2, stride, H, I, d_need, d_ready, ready_base, bar[dev], target,
+      (__nv_bfloat16 *)d_h1, (__nv_bfloat16 *)d_y);
+  VMM_LAUNCH_CHECK("skinny_ffn_kernel");
+  return VMM_OK;
+}
+
 extern "C" int vmm_grouped_swiglu(const void *d_xp, const int32_t *d_offsets, int E, int M_total, int H, int I,
                                   const void *d_w13_arena, const void *d_w2_arena, long long slot_stride,
                                   long long n_slots, const int32_t *d_slot_of_expert, void *d_h1, void *d_y,
@@ -913,19 +954,8 @@ extern "C" int vmm_grouped_swiglu(const void *d_xp, const int32_t *d_offsets, in
   if (E < 1 || E > VMM_MAX_EXPERTS) return vmm::fail(VMM_EVALIDATION, "experts must lie in [1, 256]");
   if (slot_stride % 8) return vmm::fail(VMM_EVALIDATION, "slot stride must be a multiple of 8 elements");
   if (M_total <= kSkinnyRows) {  // decode-sized layer: every expert has <= 16 rows
-    cudaStream_t s = (cudaStream_t)stream;
-    constexpr int kWarps = 8;
-    // grid.y = active-expert slots (at most M_total experts have rows)
-    dim3 g1((I + kWarps - 1) / kWarps, M_total), g2((H / 2 + kWarps - 1) / kWarps, M_total);
-    skinny_gateup_kernel<<<g1, 32 * kWarps, 0, s>>>((const __nv_bfloat16 *)d_xp, d_offsets, E, d_slot_of_expert,
-                                                     (const __nv_bfloat16 *)d_w13_arena, slot_stride, H, I,
-                                                     (__nv_bfloat16 *)d_h1);
-    VMM_LAUNCH_CHECK("skinny_gateup_kernel");
-    skinny_down_kernel<<<g2, 32 * kWarps, 0, s>>>((const __nv_bfloat16 *)d_h1, d_offsets, E, d_slot_of_expert,
-                                                   (const __nv_bfloat16 *)d_w2_arena, slot_stride, H, I,
-                                                   (__nv_bfloat16 *)d_y);
-    VMM_LAUNCH_CHECK("skinny_down_kernel");
-    return VMM_OK;
+    return skinny_launch(d_xp, d_offsets, E, M_total, H, I, d_w13_arena, d_w2_arena, slot_stride, d_slot_of_expert,
+                         nullptr, nullptr, 0, d_h1, d_y, stream);
   }
   static bool attr = false;
   if (!attr) {
@@ -990,9 +1020,15 @@ extern "C" int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offse
                                         const void *d_x_rows, const int32_t *d_src_row, int n_x_rows, void *d_h1,
                                         void *d_y, void *stream) {
   if (M_total <= 0) return VMM_OK;
-  if (M_total <= kSkinnyRows || d_done == nullptr)  // decode-sized: skinny path (callers fence on events)
-    return d_need ? vmm::fail(VMM_ECONTRACT, "ready flags need the fused tensor-core path (M > 16, scratch)")
-         : d_src_row ? vmm::fail(VMM_ECONTRACT, "row gather needs the fused tensor-core path (M > 16, scratch)")
+  if (M_total <= kSkinnyRows) {  // decode-sized: persistent weight-streaming kernel (waits on flags too)
+    if (d_src_row) return vmm::fail(VMM_ECONTRACT, "row gather needs the tensor-core path (M > 16)");
+    if (d_need && !d_ready) return vmm::fail(VMM_ECONTRACT, "need[] without ready flags");
+    return skinny_launch(d_xp, d_offsets, E, M_total, H, I, d_w13_arena, d_w2_arena, slot_stride, d_slot_of_expert,
+                         d_need, d_ready, ready_base, d_h1, d_y, stream);
+  }
+  if (d_done == nullptr)
+    return d_need ? vmm::fail(VMM_ECONTRACT, "ready flags need the fused path's scratch")
+         : d_src_row ? vmm::fail(VMM_ECONTRACT, "row gather needs the fused path's scratch")
                   : vmm_grouped_swiglu(d_xp, d_offsets, E, M_total, H, I, d_w13_arena, d_w2_arena, slot_stride,
                                        n_slots, d_slot_of_expert, d_h1, d_y, stream);
   if (H % BN || H % BK || I % 64 || I % BK || (2 * I) % BN)

@@ -91,7 +91,7 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
   // tensor-core FFN with per-expert ready flags: the layer's FFN starts while its misses still stream in
   // (VMM_FFN_FENCE=1: whole-layer event fence instead, e.g. under a serialising profiler)
   static const bool force_fence = std::getenv("VMM_FFN_FENCE") != nullptr;
-  const bool flagged = !force_fence && ready && d.need_host && d.need_dev && d.ffn_done && n_rows * k > 16;
+  const bool flagged = !force_fence && ready && d.need_host && d.need_dev && d.ffn_done;
   bool have_xn = false;  // the fused combine of the previous layer already produced this layer's xn
   // Early decisions (live routing, large batches): the previous layer's combine ->
   // norm -> this layer's route run on the first n_split rows first; their expert

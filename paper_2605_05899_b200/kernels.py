@@ -228,14 +228,14 @@ def grouped_swiglu(xp, offsets, arena, slot_of, inter: int, stream=None, h1=None
         check(L.vmm_grouped_swiglu_simt(ptr(xp), ptr(offsets), E, M, H, inter, ptr(arena), w2_base, stride,
                                         ptr(slot_of), ptr(h1), ptr(y), stream_ptr(stream)))
     elif fused:
-        _n(1 if M > 16 else 2)
+        _n(1)
         done = torch.empty(M // 128 + E + 1, dtype=torch.int32, device=dev)
         check(L.vmm_grouped_swiglu_fused(ptr(xp), ptr(offsets), E, M, H, inter, ptr(arena), w2_base, stride,
                                          n_slots, ptr(slot_of), ptr(need), ready, ready_base, ptr(done),
                                          ptr(x_rows), ptr(src_row), 0 if x_rows is None else int(x_rows.shape[0]),
                                          ptr(h1), ptr(y), stream_ptr(stream)))
     else:
-        _n(2)
+        _n(1 if M <= 16 else 2)
         check(L.vmm_grouped_swiglu(ptr(xp), ptr(offsets), E, M, H, inter, ptr(arena), w2_base, stride, n_slots,
                                    ptr(slot_of), ptr(h1), ptr(y), stream_ptr(stream)))
     return h1, y

@@ -228,12 +228,12 @@ def test_fused_ffn_bit_identical_to_two_launches(shape):
     assert torch.equal(ya, yc)
 
 
-@pytest.mark.parametrize("N", [1216, 5000])
+@pytest.mark.parametrize("N", [1, 2, 1216, 5000])
 def test_fused_ffn_waits_for_copy_stream_fills(N):
     """Copy overlap: the FFN is launched BEFORE its experts' weights are copied
     in; each expert's tiles wait on the copy stream's ready flag.  The result
-    must equal the all-resident computation bit for bit (N=1216: single-CTA
-    128x256 tiles; N=5000: CTA-pair 256x256 tiles)."""
+    must equal the all-resident computation bit for bit (N=1, 2: the persistent
+    decode kernel; N=1216: single-CTA 128x256 tiles; N=5000: CTA-pair 256x256)."""
     import ctypes as C
 
     from paper_2605_05899_b200 import _lib
