@@ -13,7 +13,7 @@ import threading
 from .errors import DeviceError, raise_status
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libvismmoe.so")
+LIB_PATH = os.environ.get("VMM_LIB") or os.path.join(HERE, "libvismmoe.so")  # VMM_LIB: dev override
 
 P = C.c_void_p
 I32 = C.c_int

@@ -251,7 +251,11 @@ __device__ __forceinline__ void wait_at_least(const uint32_t *p, uint32_t want, 
   const uint64_t t0 = global_ns();
   while ((int)(ld_acquire_u32(p) - want) < 0) {
     __nanosleep(sleep_ns);
-    if (global_ns() - t0 > 30ull * 1000000000ull) __trap();
+    if (global_ns() - t0 > 30ull * 1000000000ull) {
+      printf("vmm watchdog: block %d thread %d stuck on flag %p (%u < %u)\n", blockIdx.x, threadIdx.x, p,
+             ld_acquire_u32(p), want);
+      __trap();
+    }
   }
 }
 __device__ __forceinline__ void fence_proxy_async_global() {
@@ -521,12 +525,22 @@ __device__ __forceinline__ TileInfo pair_tile_info(int m_tile, const int *tile_b
   return ti;
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+// GATHER: GEMM1's A rows are gathered straight from the token rows x (one row
+// per gather thread, 8 x 16-byte cp.async per k-block into the SW128 layout)
+// instead of TMA box loads of a permuted copy -- no permute pass over HBM.
+// Bit-identical, but measured 2.6x slower than permute + TMA on B200 (25.6 vs
+// 9.9 ms at 1.25M rows: scattered 128-byte row pieces, ~3 stages in flight per
+// thread), so it is opt-in (VMM_FFN_GATHER=1) and kept as the measured
+// alternative.
+// Warps 6..9 gather and publish each stage to the leader's full barrier.
+template <bool GATHER>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GATHER ? kThreads + 128 : kThreads, 1)
 ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w13,
                 const __grid_constant__ CUtensorMap map_h1, const __grid_constant__ CUtensorMap map_w2,
                 const int32_t *__restrict__ offsets, const int32_t *__restrict__ slot_of,
                 const uint32_t *__restrict__ need, const uint32_t *ready, int ready_base, uint32_t *done, int E, int H,
-                int I, int lag, __nv_bfloat16 *__restrict__ h1, __nv_bfloat16 *__restrict__ y) {
+                int I, int lag, const __nv_bfloat16 *__restrict__ xg, const int32_t *__restrict__ src_row,
+                int M_total, __nv_bfloat16 *__restrict__ h1, __nv_bfloat16 *__restrict__ y) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages2 * kStage2);
@@ -555,11 +569,12 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
     s_tile_base[E] = acc;
   }
   if (warp == 0 && lane == 0) {
-    prefetch_tmap(&map_x);
+    if (!GATHER) prefetch_tmap(&map_x);  // (gather mode passes no A map for GEMM1)
     prefetch_tmap(&map_w13);
     prefetch_tmap(&map_h1);
     prefetch_tmap(&map_w2);
-    for (int s = 0; s < kStages2; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    // full: the leader producer's expect_tx arrival (+ the two CTAs' gather relays)
+    for (int s = 0; s < kStages2; ++s) { mbar_init(&full[s], GATHER ? 9 : 1); mbar_init(&empty[s], 1); }
     for (int b = 0; b < 2; ++b) { mbar_init(&tmem_full[b], 1); mbar_init(&tmem_empty[b], 8); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -597,9 +612,11 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
           const int s = it % kStages2;
           if (it >= kStages2) mbar_wait_watchdog(&empty[s], ((it / kStages2) - 1) & 1);
           unsigned char *a_dst = smem + s * kStage2;
-          if (leader) mbar_expect_tx(&full[s], 2 * kStage2);  // both CTAs' bytes land on the leader's barrier
+          const bool a_tma = !GATHER || f.gemm2;
+          // both CTAs' TMA bytes land on the leader's barrier
+          if (leader) mbar_expect_tx(&full[s], a_tma ? 2 * kStage2 : 2 * kHalf2);
           const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
-          tma_load_2d_cg2(ma, fb, a_dst, kb * BK, ti.row0 + 128 * (int)rank);
+          if (a_tma) tma_load_2d_cg2(ma, fb, a_dst, kb * BK, ti.row0 + 128 * (int)rank);
           tma_load_3d_cg2(mb, fb, a_dst + kHalf2, kb * BK, f.n_tile * TN2 + 128 * (int)rank, ti.slot);
         }
       }
@@ -618,6 +635,7 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % kStages2;
           mbar_wait_watchdog(&full[s], (it / kStages2) & 1);
+          if (GATHER) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem + s * kStage2);
           const uint32_t b_addr = a_addr + kHalf2;
@@ -632,7 +650,64 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
       }
     }
     __syncwarp();
-  } else {
+  } else if (GATHER && warp >= 6 && warp < 10) {
+    // gather: thread t owns row t of this CTA's 128-row A half (8 x 16 B per k-block) via cp.async
+    // groups; a stage's completion is published per warp (wait_group, proxy fence, lane 0 arrives on
+    // the leader's full barrier: 4 warps x 2 CTAs + the producer's expect_tx arrival).  kGD stages
+    // stay in flight per thread (kGD < kStages2, so a blocking empty wait never waits on a stage
+    // this warp has not published yet).
+    constexpr int kGD = 3;
+    const int t = threadIdx.x - 192;
+    int it = 0, pend[kGD + 1], np = 0;
+    auto publish = [&](int ps) {
+      __syncwarp();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&full[ps]), 0));
+    };
+    auto flush_to = [&](int keep) {  // publish all but the newest `keep` pending stages
+      while (np > keep) {
+        if (keep == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
+        else if (keep == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
+        else asm volatile("cp.async.wait_group 0;" ::: "memory");
+        publish(pend[0]);
+        for (int i = 1; i < np; ++i) pend[i - 1] = pend[i];
+        --np;
+      }
+    };
+    for (int tt = cid; tt < total; tt += ncl) {
+      const FusedTile f = fused_tile(tt, n1, n2, MT, lag);
+      if (!f.valid) continue;
+      if (f.gemm2) {  // no gather: publish the stages after their previous round was consumed
+        for (int kb = 0; kb < nk2; ++kb, ++it) {
+          const int s = it % kStages2;
+          if (it >= kStages2) mbar_wait_watchdog(&empty[s], ((it / kStages2) - 1) & 1);
+          if (np == kGD) flush_to(kGD - 1);
+          pend[np++] = s;
+          asm volatile("cp.async.commit_group;" ::: "memory");  // empty group keeps the group count aligned
+        }
+        continue;
+      }
+      const TileInfo ti = pair_tile_info(f.m_tile, s_tile_base, s_offs, s_slots, E);
+      const int r = ti.row0 + 128 * (int)rank + t;
+      const int tok = src_row[r < M_total ? r : M_total - 1];
+      const char *src = reinterpret_cast<const char *>(xg + (long long)tok * H);
+      for (int kb = 0; kb < nk1; ++kb, ++it) {
+        const int s = it % kStages2;
+        if (it >= kStages2) mbar_wait_watchdog(&empty[s], ((it / kStages2) - 1) & 1);
+        const uint32_t dst = smem_u32(smem + s * kStage2) + t * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + ((c ^ (t & 7)) << 4)),
+                       "l"(src + (size_t)kb * BK * 2 + c * 16)
+                       : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (np == kGD) flush_to(kGD - 1);
+        pend[np++] = s;
+      }
+    }
+    flush_to(0);
+  } else if (warp >= 2 && warp < 6) {
     const int q = warp & 3;
     int local = 0;
     const uint32_t te_leader[2] = {mapa_shared(smem_u32(&tmem_empty[0]), 0), mapa_shared(smem_u32(&tmem_empty[1]), 0)};
@@ -1042,7 +1117,7 @@ extern "C" int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offse
   const int TN = wide ? 256 : 128;
   // CTA pairs (256x256 tiles) once the average expert has >= 256 rows: tensor-bound batches
   static const bool no_pair = std::getenv("VMM_FFN_NO_PAIR") != nullptr;
-  const bool pair = wide && !no_pair && d_src_row == nullptr && M_total >= 256 * E;
+  const bool pair = wide && !no_pair && M_total >= 256 * E;
   const uint32_t b_rows = pair ? 128u : (uint32_t)TN;  // a pair CTA stages half of the 256-row B tile
   static bool attr = false;
   if (!attr) {
@@ -1056,12 +1131,14 @@ extern "C" int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offse
   }
   CUtensorMap mx, mw13, mh1, mw2;
   int st;
-  if (d_src_row) {  // A rows gathered from the token rows (tile::gather4: box of one row)
+  if (d_src_row && !pair) {  // A rows gathered from the token rows (tile::gather4: box of one row)
     if (!d_x_rows || n_x_rows <= 0) return vmm::fail(VMM_ECONTRACT, "row gather needs the token rows");
     uint64_t dims[2] = {(uint64_t)H, (uint64_t)n_x_rows};
     uint64_t str[1] = {(uint64_t)H * 2};
     uint32_t box[2] = {BK, 1};
     if ((st = make_map(&mx, d_x_rows, 2, dims, str, box))) return st;
+  } else if (d_src_row) {  // pair + gather: GEMM1 rows come from cp.async; the map is never used
+    mx = CUtensorMap{};
   } else {
     uint64_t dims[2] = {(uint64_t)H, (uint64_t)M_total};
     uint64_t str[1] = {(uint64_t)H * 2};
@@ -1101,7 +1178,10 @@ extern "C" int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offse
   if (pair) {
     static bool attr2 = false;
     if (!attr2) {
-      cudaError_t e2 = cudaFuncSetAttribute(ffn_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2);
+      cudaError_t e2 = cudaFuncSetAttribute(ffn_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)kSmem2);
+      if (e2 == cudaSuccess)
+        e2 = cudaFuncSetAttribute(ffn_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2);
       if (e2 != cudaSuccess) return vmm::cuda_status(e2, "ffn pair attr");
       attr2 = true;
     }
@@ -1111,9 +1191,14 @@ extern "C" int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offse
     const int ncl = gridp / 2;
     static const int lag_waves = std::getenv("VMM_FFN_LAG") ? std::atoi(std::getenv("VMM_FFN_LAG")) : 4;
     const int lagp = (lag_waves * ncl + n1 + n2 - 1) / (n1 + n2);
-    ffn_pair_kernel<<<gridp, kThreads, kSmem2, s>>>(mx, mw13, mh1, mw2, d_offsets, d_slot_of_expert, d_need, d_ready,
-                                                   ready_base, d_done, E, H, I, lagp, (__nv_bfloat16 *)d_h1,
-                                                   (__nv_bfloat16 *)d_y);
+    if (d_src_row)
+      ffn_pair_kernel<true><<<gridp, kThreads + 128, kSmem2, s>>>(
+          mx, mw13, mh1, mw2, d_offsets, d_slot_of_expert, d_need, d_ready, ready_base, d_done, E, H, I, lagp,
+          (const __nv_bfloat16 *)d_x_rows, d_src_row, M_total, (__nv_bfloat16 *)d_h1, (__nv_bfloat16 *)d_y);
+    else
+      ffn_pair_kernel<false><<<gridp, kThreads, kSmem2, s>>>(
+          mx, mw13, mh1, mw2, d_offsets, d_slot_of_expert, d_need, d_ready, ready_base, d_done, E, H, I, lagp,
+          nullptr, nullptr, M_total, (__nv_bfloat16 *)d_h1, (__nv_bfloat16 *)d_y);
     VMM_LAUNCH_CHECK("ffn_pair_kernel");
     return VMM_OK;
   }

@@ -55,7 +55,11 @@ __device__ __forceinline__ void mbar_wait_watchdog(uint64_t *bar, uint32_t parit
     if ((n & 1023) == 0) {
       uint64_t t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      if (t - t0 > 20ull * 1000000000ull) __trap();
+      if (t - t0 > 20ull * 1000000000ull) {
+        printf("vmm watchdog: block %d thread %d stuck on mbarrier smem+0x%x parity %u\n", blockIdx.x, threadIdx.x,
+               smem_u32(bar) & 0xfffff, parity);
+        __trap();
+      }
     }
   }
 }
