@@ -12,6 +12,7 @@
 // The host only waits once per layer (the decisions need the layer's demand
 // set); everything else is asynchronous on the caller's compute stream and the
 // xfer copy stream.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <chrono>
@@ -58,6 +59,65 @@ int vmm_xfer_need(vmm_xfer *x, const int32_t *h_slabs, int n, uint32_t *h_need);
 struct vmm_stack {
   vmm_stack_desc d;
 };
+
+namespace {
+// Low-latency host wait: the compute stream writes an epoch into a mapped
+// pinned word (stream memory op, ordered after the preceding D2H copies) and
+// the host spins on it -- a few microseconds less per layer than waking up from
+// cudaStreamSynchronize, which matters for decode (one host decision per layer).
+typedef CUresult (*WriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+struct HostFlag {
+  volatile uint32_t *h = nullptr;
+  CUdeviceptr d = 0;
+  uint32_t epoch = 0;
+  WriteValue32Fn wv = nullptr;
+  bool ok = false;
+  HostFlag() {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return;
+    wv = reinterpret_cast<WriteValue32Fn>(p);
+    void *hp = nullptr, *dp = nullptr;
+    if (cudaHostAlloc(&hp, 64, cudaHostAllocMapped) != cudaSuccess) return;
+    if (cudaHostGetDevicePointer(&dp, hp, 0) != cudaSuccess) return;
+    h = reinterpret_cast<volatile uint32_t *>(hp);
+    *h = 0;
+    d = (CUdeviceptr)dp;
+    ok = true;
+  }
+};
+HostFlag &host_flag() {
+  thread_local HostFlag f;  // one per host thread (handles are single-owner)
+  return f;
+}
+// enqueue the marker after the work already in `st`
+int host_mark(cudaStream_t st, uint32_t *epoch_out) {
+  HostFlag &f = host_flag();
+  if (!f.ok) return 1;
+  const uint32_t e = ++f.epoch;
+  if (f.wv((CUstream)st, f.d, e, 0) != CUDA_SUCCESS) return 1;
+  *epoch_out = e;
+  return 0;
+}
+// spin until the marker lands; every few thousand polls ask the stream whether it
+// failed (a trapped kernel never writes the marker) -> returns the CUDA error
+cudaError_t host_spin(cudaStream_t st, uint32_t epoch) {
+  HostFlag &f = host_flag();
+  for (uint32_t n = 1; (int32_t)(*f.h - epoch) < 0; ++n) {
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+    if ((n & 4095) == 0) {
+      const cudaError_t e = cudaStreamQuery(st);
+      if (e != cudaSuccess && e != cudaErrorNotReady) return e;
+      if (e == cudaSuccess && (int32_t)(*f.h - epoch) < 0) return cudaErrorUnknown;  // drained, no marker
+    }
+  }
+  return cudaSuccess;
+}
+}  // namespace
 
 extern "C" {
 
@@ -131,6 +191,8 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
     bool la_done = false;
     int32_t *ch = d.counts_host + (size_t)l * E;
     const bool split_now = pending_rest;
+    bool part_flag = false;
+    uint32_t part_epoch = 0;
     if (d.routing == 0) {
       VMM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * E, st), "counts memset");
       const bool fused_la = emits && d.predictor == 2 && l + 1 < L && (E % 16 == 0) && E <= 128;
@@ -148,6 +210,7 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
         VMM_TRY(route_rows(0, n_split));
         VMM_CUDA(cudaMemcpyAsync(ch, cnt, sizeof(uint32_t) * E, cudaMemcpyDeviceToHost, st), "partial counts D2H");
         VMM_CUDA(cudaEventRecord(ev_part, st), "partial event");
+        part_flag = host_mark(st, &part_epoch) == 0;
         // the rest of the previous layer's combine (its gates/pos/Y rows are untouched by chunk 1)
         const int nr = n_rows - n_split;
         VMM_TRY(vmm_combine_norm(d.y, d.pos + (size_t)n_split * k, d.gates + (size_t)n_split * k,
@@ -203,7 +266,8 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
       bool known = false;
       if (split_now) {  // the first chunk's experts: the whole demand set if they are all E
         c1 = clk::now();
-        VMM_CUDA(cudaEventSynchronize(ev_part), "partial sync");
+        if (part_flag) VMM_CUDA(host_spin(st, part_epoch), "partial sync");
+        else VMM_CUDA(cudaEventSynchronize(ev_part), "partial sync");
         c2 = clk::now();
         int n_act = 0;
         for (int e = 0; e < E; ++e) n_act += ch[e] != 0;
@@ -214,7 +278,9 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
       if (!known) {
         VMM_CUDA(cudaMemcpyAsync(ch, cnt, sizeof(uint32_t) * E, cudaMemcpyDeviceToHost, st), "counts D2H");
         c1 = clk::now();
-        VMM_CUDA(cudaStreamSynchronize(st), "layer sync");
+        uint32_t ep = 0;
+        if (host_mark(st, &ep) == 0) VMM_CUDA(host_spin(st, ep), "layer sync");  // counts (and scores) landed
+        else VMM_CUDA(cudaStreamSynchronize(st), "layer sync");
         c2 = clk::now();
         for (int e = 0; e < E; ++e)
           if (ch[e]) demand.push_back(e);
