@@ -265,18 +265,40 @@ def main():
 
     out_h = [None]
 
+    # e2e: the batch's hidden states cross PCIe in request-aligned chunks on a side
+    # stream, and the pinned prefix starts on each chunk as it lands (x_ready)
+    side = torch.cuda.Stream(device=dev)
+    n_chunks = 8 if (R >= 8 and a.source != "ep") else 1
+    bounds = [req_off[(R * (c + 1)) // n_chunks] for c in range(n_chunks)]
+    x_dev = torch.empty_like(x)  # device landing buffer (allocation is not a transfer)
+
     def step(e2e=False):
+        x_ready = None
         if e2e:
-            xd = x_h.to(dev, non_blocking=True)
             sd = sal_h.to(dev, non_blocking=True)
             md = mod_h.to(dev, non_blocking=True)
+            side.wait_stream(torch.cuda.current_stream())
+            x_ready, r0 = [], 0
+            with torch.cuda.stream(side):
+                for r1 in bounds:
+                    x_dev[r0:r1].copy_(x_h[r0:r1], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(side)
+                    x_ready.append((r1, ev))
+                    r0 = r1
+            xd = x_dev
         else:
             xd, sd, md = x, sal, mod
         if a.source == "ep":
+            if x_ready:
+                torch.cuda.current_stream().wait_event(x_ready[-1][1])
             h, ret, _ = stack.forward(xd, sd, md, req_off=req_off)
             res = _EPResult(h)
         else:
-            res = stack.forward(xd, sd, md, trace=dtr, req_off=req_off)
+            if x_ready and n_chunks == 1:  # one chunk: simply order the step after its copy
+                torch.cuda.current_stream().wait_event(x_ready[-1][1])
+                x_ready = None
+            res = stack.forward(xd, sd, md, trace=dtr, req_off=req_off, x_ready=x_ready)
         if e2e:
             n = int(res.hidden.shape[0])
             if out_h[0] is None or out_h[0].shape[0] < n:  # pinned result buffer, allocated once

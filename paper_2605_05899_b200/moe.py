@@ -290,6 +290,7 @@ class MoEStack:
         self.layer_ids = torch.arange(L, dtype=torch.int32, device=self.device)
         self.step_counts = torch.zeros((L, E), dtype=torch.int32, device=self.device)
         self._bufs = {}
+        self._pbufs = {}  # chunked-prefix outputs (x_ready)
         self.profile = None  # list -> (start_ev, end_ev, bytes, flops) per grouped SwiGLU launch pair
 
     def __del__(self):
@@ -333,7 +334,7 @@ class MoEStack:
         return self._bufs
 
     def forward(self, x, saliency, modality, trace=None, record: bool = False, req_off=None,
-                keep_session: bool = False, attn_qk=None) -> StackResult:
+                keep_session: bool = False, attn_qk=None, x_ready=None) -> StackResult:
         """Prefill a batch of requests through the whole stack.
 
         x bf16 [T, H] (device), saliency f64 [T], modality u8 [T] (0 visual,
@@ -344,7 +345,11 @@ class MoEStack:
         `trace` (device routes i32 [L,T,k], gates f32 [L,T,k]) is required for
         routing="trace".  saliency=None with attn_qk=(q [R,Hh,Q,D], k [R,Hh,T/R,D])
         derives the saliency on the device from the vision encoder's attention
-        (head-averaged CLS/text->token attention, saliency.attention_saliency)."""
+        (head-averaged CLS/text->token attention, saliency.attention_saliency).
+        x_ready: optional [(row_end, cuda.Event)] -- rows [prev_end, row_end) of x
+        are valid once the event fires (a host->device copy in flight on another
+        stream): the pinned prefix then runs chunk by chunk as the rows land
+        (rows are independent in the prefix, so the result is identical)."""
         c = self.cfg
         L, E, k, lp = c.layers, c.experts, c.k, c.l_pinned
         dev = self.device
@@ -365,7 +370,7 @@ class MoEStack:
         check(self._L.vmm_xfer_reset_stats(self._x))
 
         cur, x_ctx, prefix, counts_pre, ret, n_r, ret_off, xr = self._prefix_and_prune(
-            x, saliency, modality, trace, req_off, bufs)
+            x, saliency, modality, trace, req_off, bufs, x_ready=x_ready)
 
         # --- per-layer demand counts over the retained tokens
         counts_ret = torch.zeros((L, E), dtype=torch.int32, device=dev)
@@ -429,7 +434,7 @@ class MoEStack:
                            routes=routes, scores=scores, copies=n_copies, h2d_bytes=b.value,
                            retained_offsets=ret_off, h2d_ms=ms.value)
 
-    def _prefix_and_prune(self, x, saliency, modality, trace, req_off, bufs):
+    def _prefix_and_prune(self, x, saliency, modality, trace, req_off, bufs, x_ready=None):
         """Pinned prefix on all T rows (resident experts, engine-less executor,
         no host sync) then per-request compression on the prefix routes.
         Returns (rows after the prefix, xn of layer lp-1, prefix routes,
@@ -445,7 +450,33 @@ class MoEStack:
         counts_pre = torch.zeros((max(lp, 1), E), dtype=torch.int32, device=dev)
         x_ctx = None
         cur = x
-        if lp:
+        if lp and x_ready:
+            # chunk by chunk as the rows land (request-aligned chunks from the caller)
+            if self._pbufs.get("n", 0) < T:
+                self._pbufs = dict(n=T, cur=torch.empty_like(x), xn=torch.empty_like(x))
+            cur_full, xn_full = self._pbufs["cur"][:T], self._pbufs["xn"][:T]
+            stream = torch.cuda.current_stream()
+            r0 = 0
+            for r1, ev in x_ready:
+                stream.wait_event(ev)
+                n = int(r1) - r0
+                if n <= 0:
+                    continue
+                routes_c = torch.empty((lp, n, k), dtype=torch.int32, device=dev)
+                counts_c = torch.zeros((lp, E), dtype=torch.int32, device=dev)
+                rows_c = torch.arange(r0, r1, dtype=torch.int32, device=dev) if c.routing == "trace" else None
+                out_c, _, _ = self._native_layers(None, x[r0:r1], n, 0, lp, 0, -1, rows=rows_c, counts=counts_c,
+                                                  trace=trace, record_into=routes_c)
+                cur_full[r0:r1].copy_(out_c)
+                if c.predictor == "gate":  # the boot emission's context rows (layer lp-1 input)
+                    xn_full[r0:r1].copy_(bufs["xn"][:n])
+                prefix[:lp, r0:r1].copy_(routes_c)
+                counts_pre[:lp] += counts_c
+                r0 = int(r1)
+            if r0 != T:
+                raise ContractError("x_ready chunks must cover every row")
+            cur, x_ctx = cur_full, xn_full
+        elif lp:
             rows_all = torch.arange(T, dtype=torch.int32, device=dev) if c.routing == "trace" else None
             cur, _, _ = self._native_layers(None, x, T, 0, lp, 0, -1, rows=rows_all, counts=counts_pre, trace=trace,
                                             record_into=prefix[:lp])

@@ -41,7 +41,8 @@ def test_router_realistic_inputs_margin_aware():
     torch.testing.assert_close(gates.cpu()[safe], rg[safe], rtol=1e-4, atol=1e-5)
 
 
-@pytest.mark.parametrize("N,k,E", [(1216, 8, 128), (1000, 8, 128), (155648, 8, 128), (30000, 6, 64), (5000, 2, 4)])
+@pytest.mark.parametrize("N,k,E", [(1216, 8, 128), (1000, 8, 128), (155648, 8, 128), (30000, 6, 64), (5000, 2, 4),
+                                   (3000, 8, 256), (4097, 1, 16)])
 def test_permute_plan_is_stable_counting_sort(N, k, E):
     """Single-CTA (<= 8192 picks) and multi-CTA (count / scan / scatter) paths."""
     g = torch.Generator().manual_seed(3 + N)
@@ -206,7 +207,7 @@ def test_permute_plan_small_batches(N, k, E):
 
 @pytest.mark.parametrize("shape", [(1216, 2048, 768, 128, 8), (300, 256, 512, 8, 2), (640, 2048, 1408, 64, 6),
                                    (9728, 2048, 768, 128, 8), (3, 2048, 768, 128, 8), (40000, 2048, 768, 128, 8),
-                                   (9000, 2048, 1408, 64, 6)])
+                                   (9000, 2048, 1408, 64, 6), (2000, 256, 512, 256, 8), (70000, 256, 512, 256, 8)])
 def test_fused_ffn_bit_identical_to_two_launches(shape):
     """The one-launch persistent FFN (GEMM2 tiles gated on H1 block counters;
     CTA-pair 256x256 tiles once experts average >= 256 rows) computes every

@@ -356,3 +356,37 @@ def test_batched_split_path_bit_identical_to_all_resident_layers():
                                                                       device="cuda"), cfg.inter, E, xn=xn)
     torch.cuda.synchronize()
     assert torch.equal(res.hidden, cur)
+
+
+def test_chunked_prefix_as_rows_land_is_bit_identical():
+    """forward(x_ready=...): the pinned prefix runs chunk by chunk as the rows
+    arrive from a side-stream H2D; outputs and decisions equal the one-shot run."""
+    cfg = tiny_cfg(routing="live", predictor="gate")
+    store = ExpertStore(cfg, seed=3)
+    trs = [small_trace(cfg, seed=s) for s in range(60, 66)]
+    xs, sals, mods = [], [], []
+    for i, tr in enumerate(trs):
+        x, sal, mod, _ = request(tr, cfg.hidden, seed=200 + i)
+        xs.append(x), sals.append(sal), mods.append(mod)
+    offs = np.cumsum([0] + [t.num_tokens for t in trs]).tolist()
+    x = torch.cat(xs)
+    sal, mod = torch.cat(sals), torch.cat(mods)
+    a = MoEStack(cfg, store=store).forward(x, sal, mod, req_off=offs)
+    ha, reta, repa = a.hidden.clone(), a.retained.copy(), a.report.to_dict()
+    x_h = x.cpu().pin_memory()
+    x_dev = torch.empty_like(x)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    ready, r0 = [], 0
+    with torch.cuda.stream(side):
+        for r1 in (offs[2], offs[4], offs[6]):
+            x_dev[r0:r1].copy_(x_h[r0:r1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(side)
+            ready.append((r1, ev))
+            r0 = r1
+    b = MoEStack(cfg, store=store).forward(x_dev, sal, mod, req_off=offs, x_ready=ready)
+    torch.cuda.synchronize()
+    assert np.array_equal(reta, b.retained)
+    assert torch.equal(ha, b.hidden)
+    assert b.report.to_dict() == repa
