@@ -205,9 +205,13 @@ def main():
     from paper_2605_05899_b200 import dist as vdist
 
     rank, world, local = vdist.env_rank_world()
+    # VMM_SHARE_GPU=1 (test only): every rank on device 0 with gloo collectives, to exercise the
+    # multi-rank paths on a one-GPU box (NCCL refuses two ranks on one GPU)
+    share = bool(os.environ.get("VMM_SHARE_GPU"))
+    local = 0 if share else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    vdist.init("nccl", dev)
+    vdist.init("gloo" if share else "nccl", dev)
 
     from paper_2605_05899_b200 import kernels
     from paper_2605_05899_b200.moe import MoEStack, StackConfig
@@ -216,7 +220,10 @@ def main():
     predictor = a.predictor or ("gate" if a.routing == "live" else "oracle")
     from paper_2605_05899_b200.moe import ExpertStore, ShardedHome
 
-    kw = dict(routing=a.routing, predictor=predictor, host_layers=8)
+    # pinned host pool: layer l is served from pool layer l % host_layers (every byte moved is a real
+    # PCIe transfer); one process per GPU each pins its own pool, so shrink it as N grows (8 ranks x 9.7 GB
+    # would pin ~78 GB of host memory)
+    kw = dict(routing=a.routing, predictor=predictor, host_layers=max(1, 8 // world))
     if a.source == "sharded":  # logical clock: one slot over NVLink (770 GB/s measured peer copy) or local D2D
         kw["transfer_ms"] = w.expert_bytes / (770e9 if world > 1 else 3000e9) * 1e3
     if a.source == "ep":
@@ -227,11 +234,13 @@ def main():
     # one model for the whole job: every rank builds the same weights (the pinned prefix and router are
     # replicated; sharded/EP modes keep each expert's home copy on rank e % world)
     store = ExpertStore(cfg, seed=1000)
-    home = ShardedHome(store, rank, world) if a.source == "sharded" else None
+    home = ShardedHome(store, rank, world, device_of_rank=[0] * world if share else None) \
+        if a.source == "sharded" else None
     if a.source == "ep":
         from paper_2605_05899_b200.ep import EPStack
 
-        stack = EPStack(cfg, store=store, rank=rank, world=world, max_rows=R * (w.n_visual // 2 + w.n_text) + 64)
+        stack = EPStack(cfg, store=store, rank=rank, world=world, max_rows=R * (w.n_visual // 2 + w.n_text) + 64,
+                        device_of_rank=[0] * world if share else None)
     else:
         stack = MoEStack(cfg, store=store, home=home)
     tr = generate_trace(w.trace_config(seed=rank * R))

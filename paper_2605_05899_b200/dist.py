@@ -33,10 +33,15 @@ def shard_requests(n_requests: int, rank: int, world: int) -> list[int]:
     return [r for r in range(n_requests) if r % world == rank]
 
 
+def _coll_device(device):
+    """gloo collectives run on CPU tensors"""
+    return torch.device("cpu") if dist.get_backend() == "gloo" else device
+
+
 def max_over_ranks(value: float, device=None) -> float:
     if not dist.is_initialized() or dist.get_world_size() == 1:
         return float(value)
-    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=_coll_device(device))
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -44,7 +49,7 @@ def max_over_ranks(value: float, device=None) -> float:
 def sum_over_ranks(values, device=None) -> list[float]:
     if not dist.is_initialized() or dist.get_world_size() == 1:
         return [float(v) for v in values]
-    t = torch.tensor([float(v) for v in values], dtype=torch.float64, device=device)
+    t = torch.tensor([float(v) for v in values], dtype=torch.float64, device=_coll_device(device))
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return t.tolist()
 
