@@ -361,7 +361,7 @@ def main():
     # by replaying the LAST layer's FFN launch on its real inputs (permuted rows,
     # expert offsets, slot table) with every expert resident, L2 flushed before
     # each replay, CUDA events on the launching stream.
-    prof = [p for _, pl, _ in results for p in pl[w.l_pinned:]]
+    prof = [p for _, pl, _ in results for p in pl if not p[4]]  # cached layers (not the pinned prefix)
     live_ms = float(np.mean([p[0].elapsed_time(p[1]) for p in prof])) if prof else None
     bufs = stack._bufs
     if a.source == "ep":  # the owner-side FFN of the last layer: the rows this rank received

@@ -5,6 +5,8 @@
 // a layer are stably counting-sorted by expert (ties by (token, slot)) so each
 // expert's rows are contiguous for the grouped FFN, and the combine reduces
 // the k expert outputs per token in slot order (deterministic, no atomics).
+#include <mutex>
+
 #include "common.cuh"
 
 namespace {
@@ -447,24 +449,44 @@ static int permute_impl(const int32_t *d_ids, int N, int k, int E, int32_t *d_of
     int chunk = (n_picks / (148 * 4) + 255) / 256 * 256;
     chunk = chunk < 1024 ? 1024 : (chunk > kChunk ? kChunk : chunk);
     const int G = (n_picks + chunk - 1) / chunk;
-    static int32_t *scratch[64] = {nullptr};
-    static size_t cap[64] = {0};
+    // per-CTA count scratch, one per (device, stream): plans on different streams may run concurrently
+    struct Scratch {
+      int dev;
+      void *stream;
+      int32_t *ptr;
+      size_t cap;
+    };
+    static Scratch tab[64];
+    static int ntab = 0;
+    static std::mutex mu;
     int dev = 0;
     cudaGetDevice(&dev);
     const size_t need = (size_t)G * E;
-    if (dev < 0 || dev >= 64) return vmm::fail(VMM_ECUDA, "device index out of range");
-    if (cap[dev] < need) {
-      if (scratch[dev]) cudaFree(scratch[dev]);
-      cudaError_t e = cudaMalloc(&scratch[dev], sizeof(int32_t) * need * 2);
-      if (e != cudaSuccess) { scratch[dev] = nullptr; cap[dev] = 0; return vmm::cuda_status(e, "permute scratch"); }
-      cap[dev] = need * 2;
+    int32_t *scr = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      Scratch *ent = nullptr;
+      for (int i = 0; i < ntab; ++i)
+        if (tab[i].dev == dev && tab[i].stream == stream) ent = &tab[i];
+      if (!ent) {
+        if (ntab == 64) return vmm::fail(VMM_ECUDA, "too many streams for the permute scratch");
+        ent = &tab[ntab++];
+        *ent = Scratch{dev, stream, nullptr, 0};
+      }
+      if (ent->cap < need) {
+        if (ent->ptr) cudaFree(ent->ptr);
+        cudaError_t e = cudaMalloc(&ent->ptr, sizeof(int32_t) * need * 2);
+        if (e != cudaSuccess) { ent->ptr = nullptr; ent->cap = 0; return vmm::cuda_status(e, "permute scratch"); }
+        ent->cap = need * 2;
+      }
+      scr = ent->ptr;
     }
     cudaStream_t st = (cudaStream_t)stream;
-    plan_count_kernel<<<G, kPT, 0, st>>>(d_ids, n_picks, chunk, E, scratch[dev]);
+    plan_count_kernel<<<G, kPT, 0, st>>>(d_ids, n_picks, chunk, E, scr);
     VMM_LAUNCH_CHECK("plan_count_kernel");
-    plan_scan_kernel<<<1, 1024, 0, st>>>(scratch[dev], G, E, d_offsets);
+    plan_scan_kernel<<<1, 1024, 0, st>>>(scr, G, E, d_offsets);
     VMM_LAUNCH_CHECK("plan_scan_kernel");
-    plan_scatter_kernel<<<G, kPT, 0, st>>>(d_ids, n_picks, chunk, k, E, scratch[dev], d_src_row, d_pos,
+    plan_scatter_kernel<<<G, kPT, 0, st>>>(d_ids, n_picks, chunk, k, E, scr, d_src_row, d_pos,
                                            (const uint4 *)d_x, H * 2 / 16, (uint4 *)d_xp);
     VMM_LAUNCH_CHECK("plan_scatter_kernel");
     return VMM_OK;

@@ -291,7 +291,7 @@ class MoEStack:
         self.step_counts = torch.zeros((L, E), dtype=torch.int32, device=self.device)
         self._bufs = {}
         self._pbufs = {}  # chunked-prefix outputs (x_ready)
-        self.profile = None  # list -> (start_ev, end_ev, bytes, flops) per grouped SwiGLU launch pair
+        self.profile = None  # list -> (start_ev, end_ev, bytes, flops, is_prefix) per FFN launch
 
     def __del__(self):
         h = getattr(self, "_x", None)
@@ -450,31 +450,57 @@ class MoEStack:
         counts_pre = torch.zeros((max(lp, 1), E), dtype=torch.int32, device=dev)
         x_ctx = None
         cur = x
+        offs_req = [0, T] if req_off is None else [int(v) for v in req_off]
+        if lp and not x_ready and len(offs_req) > 2 and T >= 16384:
+            # two request-aligned halves on two streams: one half's memory-bound kernels
+            # (combine, permute, route) overlap the other half's tensor-core FFN
+            mid = min(offs_req[1:-1], key=lambda v: abs(2 * v - T))
+            x_ready = [(mid, None), (T, None)]
         if lp and x_ready:
-            # chunk by chunk as the rows land (request-aligned chunks from the caller)
+            # chunk by chunk (as the rows land, or the two halves), alternating over two streams
             if self._pbufs.get("n", 0) < T:
                 self._pbufs = dict(n=T, cur=torch.empty_like(x), xn=torch.empty_like(x))
             cur_full, xn_full = self._pbufs["cur"][:T], self._pbufs["xn"][:T]
-            stream = torch.cuda.current_stream()
-            r0 = 0
+            main = torch.cuda.current_stream()
+            if not hasattr(self, "_pstreams"):
+                self._pstreams = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
+            bounds, r0 = [], 0
             for r1, ev in x_ready:
-                stream.wait_event(ev)
-                n = int(r1) - r0
-                if n <= 0:
-                    continue
-                routes_c = torch.empty((lp, n, k), dtype=torch.int32, device=dev)
-                counts_c = torch.zeros((lp, E), dtype=torch.int32, device=dev)
-                rows_c = torch.arange(r0, r1, dtype=torch.int32, device=dev) if c.routing == "trace" else None
-                out_c, _, _ = self._native_layers(None, x[r0:r1], n, 0, lp, 0, -1, rows=rows_c, counts=counts_c,
-                                                  trace=trace, record_into=routes_c)
-                cur_full[r0:r1].copy_(out_c)
-                if c.predictor == "gate":  # the boot emission's context rows (layer lp-1 input)
-                    xn_full[r0:r1].copy_(bufs["xn"][:n])
-                prefix[:lp, r0:r1].copy_(routes_c)
-                counts_pre[:lp] += counts_c
+                bounds.append((r0, int(r1), ev))
                 r0 = int(r1)
             if r0 != T:
                 raise ContractError("x_ready chunks must cover every row")
+            caps = [max([b - a for i, (a, b, _) in enumerate(bounds) if i % 2 == j] or [0]) for j in range(2)]
+            two = caps[0] + caps[1] <= int(bufs["n"])
+            if not two:
+                caps = [max(b - a for a, b, _ in bounds), 0]
+            base = [0, caps[0]]
+            counts_lane = [torch.zeros((lp, E), dtype=torch.int32, device=dev) for _ in range(2)]
+            for sp_ in self._pstreams:
+                sp_.wait_stream(main)
+            for i, (r0, r1, ev) in enumerate(bounds):
+                n = r1 - r0
+                if n <= 0:
+                    continue
+                lane = i % 2 if two else 0
+                side = self._pstreams[lane]
+                with torch.cuda.stream(side):
+                    if ev is not None:
+                        side.wait_event(ev)
+                    routes_c = torch.empty((lp, n, k), dtype=torch.int32, device=dev)
+                    counts_c = torch.zeros((lp, E), dtype=torch.int32, device=dev)
+                    rows_c = torch.arange(r0, r1, dtype=torch.int32, device=dev) if c.routing == "trace" else None
+                    out_c, _, _ = self._native_layers(None, x[r0:r1], n, 0, lp, 0, -1, rows=rows_c, counts=counts_c,
+                                                      trace=trace, record_into=routes_c,
+                                                      region=(base[lane], caps[lane], lane))
+                    cur_full[r0:r1].copy_(out_c)
+                    if c.predictor == "gate":  # the boot emission's context rows (layer lp-1 input)
+                        xn_full[r0:r1].copy_(bufs["xn"][base[lane]:base[lane] + n])
+                    prefix[:lp, r0:r1].copy_(routes_c)
+                    counts_lane[lane] += counts_c
+            for sp_ in self._pstreams:
+                main.wait_stream(sp_)
+            counts_pre[:lp] += counts_lane[0] + counts_lane[1]
             cur, x_ctx = cur_full, xn_full
         elif lp:
             rows_all = torch.arange(T, dtype=torch.int32, device=dev) if c.routing == "trace" else None
@@ -512,18 +538,34 @@ class MoEStack:
 
 
     def _native_layers(self, eng, x, n_rows, l0, l1, phase, step, rows=None, counts=None, oracle_table=None,
-                       trace=None, record=False, record_into=None):
+                       trace=None, record=False, record_into=None, region=None):
         """Run layers [l0, l1) through the native executor (csrc/stack.cpp).
-        eng=None: pinned-prefix mode (no decisions / copies / host syncs)."""
+        eng=None: pinned-prefix mode (no decisions / copies / host syncs).
+        region=(row_base, cap, lane): run in rows [row_base, row_base+cap) of the
+        scratch buffers with lane's own small buffers (two pinned-prefix chunks
+        on two streams at once; enqueued on the current stream)."""
         c = self.cfg
         L, E, k = c.layers, c.experts, c.k
         bufs = self._buffers(n_rows)
         st = self.store
         pred = {"none": 0, "history": 1, "gate": 2, "oracle": 3}[c.predictor]
+        rb, cap, lane = (0, int(bufs["n"]), 0) if region is None else region
+        if region is not None:
+            if eng is not None or rb + cap > int(bufs["n"]) or n_rows > cap:
+                raise ContractError("scratch region outside the buffers (pinned prefix only)")
+            if lane and "off_b" not in bufs:
+                bufs["off_b"] = torch.empty_like(bufs["off"])
+                bufs["ffn_done_b"] = torch.empty_like(bufs["ffn_done"])
+                bufs["shared_off_b"] = torch.empty_like(bufs["shared_off"])
+        H, I, S = c.hidden, c.inter, c.shared_experts
+
+        def at(name, row_bytes):  # pointer of row rb of a [rows, ...] scratch buffer
+            return bufs[name].data_ptr() + rb * row_bytes
+        b_off, b_done, b_soff = (("off_b", "ffn_done_b", "shared_off_b") if lane else ("off", "ffn_done", "shared_off"))
         d = _lib.StackDesc(
             layers=L, experts=E, k=k, hidden=c.hidden, inter=c.inter, l_pinned=c.l_pinned,
             n_pinned_slots=st.n_pinned_slots, n_slots=int(st.arena.shape[0]), slot_bytes=c.slot_bytes,
-            host_layers=st.host_layers, cap_rows=int(bufs["n"]), routing=int(c.routing == "trace"), predictor=pred,
+            host_layers=st.host_layers, cap_rows=cap, routing=int(c.routing == "trace"), predictor=pred,
             counts_preset=int(oracle_table is not None and c.routing == "trace"),
             arena=st.arena.data_ptr(), pool=st.pool.data_ptr() if self.home is None else None,
             router=st.router.data_ptr(),
@@ -533,18 +575,18 @@ class MoEStack:
             trace_routes=trace["routes"].data_ptr() if trace is not None else None,
             trace_gates=trace["gates"].data_ptr() if trace is not None else None,
             trace_tokens=int(trace["routes"].shape[1]) if trace is not None else 0,
-            xn=bufs["xn"].data_ptr(), xp=bufs["xp"].data_ptr(), h1=bufs["h1"].data_ptr(), y=bufs["y"].data_ptr(),
-            out0=bufs["out"].data_ptr(), out1=bufs["out2"].data_ptr(), ids=bufs["ids"].data_ptr(),
-            gates=bufs["gates"].data_ptr(), off=bufs["off"].data_ptr(), src=bufs["src"].data_ptr(),
-            pos=bufs["pos"].data_ptr(), counts=counts.data_ptr(), la_counts=bufs["scratch"].data_ptr(),
+            xn=at("xn", H * 2), xp=at("xp", k * H * 2), h1=at("h1", k * I * 2), y=at("y", k * H * 2),
+            out0=at("out", H * 2), out1=at("out2", H * 2), ids=at("ids", k * 4),
+            gates=at("gates", k * 4), off=bufs[b_off].data_ptr(), src=at("src", k * 4),
+            pos=at("pos", k * 4), counts=counts.data_ptr(), la_counts=bufs["scratch"].data_ptr(),
             y_dev=bufs["y_dev"].data_ptr(), slot_dev=self.slot_dev.data_ptr(),
             counts_host=self.counts_host.data_ptr(), y_host=self.y_host.data_ptr(),
             slot_host=self.slot_host.data_ptr(), shared=c.shared_experts,
             shared_slot_of=st.shared_slot_of.data_ptr() if st.shared_slot_of is not None else None,
-            shared_src=bufs["shared_src"].data_ptr(), shared_off=bufs["shared_off"].data_ptr(),
-            xs=bufs["xs"].data_ptr(), h1s=bufs["h1s"].data_ptr(), ys=bufs["ys"].data_ptr(),
+            shared_src=at("shared_src", max(S, 1) * 4), shared_off=bufs[b_soff].data_ptr(),
+            xs=at("xs", max(S, 1) * H * 2), h1s=at("h1s", max(S, 1) * I * 2), ys=at("ys", max(S, 1) * H * 2),
             need_host=self.need_host.data_ptr(), need_dev=self.need_dev.data_ptr(),
-            ffn_done=bufs["ffn_done"].data_ptr())
+            ffn_done=bufs[b_done].data_ptr())
         h = C.c_void_p()
         check(self._L.vmm_stack_create(C.byref(d), C.byref(h)))
         nl = l1 - l0
@@ -583,11 +625,11 @@ class MoEStack:
             for i in range(nl):
                 ne = c.experts if eng is None else int(n_dem[i])  # pinned prefix: every expert resident
                 nbytes = ne * c.slot_bytes + M * c.hidden * 2 * 2 + M * c.inter * 2 * 2
-                self.profile.append((evs[i], evs[nl + i], nbytes, 6.0 * M * c.hidden * c.inter))
-        res = bufs["out"] if out.x_out == bufs["out"].data_ptr() else bufs["out2"]
+                self.profile.append((evs[i], evs[nl + i], nbytes, 6.0 * M * c.hidden * c.inter, eng is None))
+        res = bufs["out"] if out.x_out == at("out", H * 2) else bufs["out2"]
         self.last_host_us = list(out.host_us)
         self.last_copy_marks = cmarks
-        return res[:n_rows], out.copies, routes_t
+        return res[rb:rb + n_rows], out.copies, routes_t
 
     # ------------------------------------------------------------------
     # decode phase (pipeline.py:723-740): one token per step, the prefill's

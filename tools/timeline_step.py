@@ -35,11 +35,14 @@ for it in range(ITERS):
     prof = stack.profile
     stack.profile = None
 total = e0.elapsed_time(e1)
+pre = [p for p in prof if p[4]]
+prof = [p for p in prof if not p[4]]
 starts = [p[0] for p in prof]
 ffn = [p[0].elapsed_time(p[1]) for p in prof]
-lp = cfg.l_pinned
+lp = 0
 print(f"R={R} step {total:.1f} ms, copies {res.copies}, h2d {res.h2d_bytes / 1e9:.1f} GB")
-print(f"prefix (start -> first cached FFN): {e0.elapsed_time(starts[lp]):.1f} ms; prefix FFN sum {sum(ffn[:lp]):.1f}")
+print(f"prefix (start -> first cached FFN): {e0.elapsed_time(starts[0]):.1f} ms; prefix FFN launches {len(pre)}, "
+      f"sum {sum(p[0].elapsed_time(p[1]) for p in pre):.1f} ms")
 per = [starts[i].elapsed_time(starts[i + 1]) for i in range(lp, len(starts) - 1)]
 print(f"cached layers: period mean {np.mean(per):.2f} ms, FFN(incl. copy waits) mean {np.mean(ffn[lp:]):.2f} ms,"
       f" non-FFN mean {np.mean(per) - np.mean(ffn[lp:-1]):.2f} ms")
