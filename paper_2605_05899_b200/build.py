@@ -17,8 +17,12 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libvismmoe.so")
+# VMM_BUILD_VARIANT=prof: dev build with the FFN wait counters (-DVMM_FFN_PROF) into
+# _build_prof/ and libvismmoe_prof.so (load it with VMM_LIB=...; tools/ffn_prof.py)
+VARIANT = os.environ.get("VMM_BUILD_VARIANT", "")
+OUT = os.path.join(HERE, "_build" + (f"_{VARIANT}" if VARIANT else ""))
+LIB = os.path.join(HERE, "libvismmoe" + (f"_{VARIANT}" if VARIANT else "") + ".so")
+DEFS = {"prof": ["-DVMM_FFN_PROF"]}.get(VARIANT, [])
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CU = {
@@ -63,7 +67,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     for src, extra in CU.items():
         obj = os.path.join(OUT, src + ".o")
         cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-               *extra, *inc, "-c", os.path.join(CSRC, src), "-o", obj]
+               *extra, *DEFS, *inc, "-c", os.path.join(CSRC, src), "-o", obj]
         jobs.append((obj, os.path.join(CSRC, src), cmd))
     for src in CPP:
         obj = os.path.join(OUT, src + ".o")

@@ -21,6 +21,18 @@
 
 #include "sm100.cuh"
 
+// VMM_FFN_PROF (a separate dev build, see tools/ffn_prof.py): per-CTA cycle
+// counters of the pair kernel's waits, read back with vmm_ffn_prof_read.
+#ifdef VMM_FFN_PROF
+__device__ unsigned long long g_ffn_prof[256][24];
+__device__ int g_ffn_prof_mode;  // bit 0: skip the H1 dependency waits, bit 1: skip the epilogue stores (wrong results)
+#define PROF_T0() const long long _pt0 = clock64()
+#define PROF_ADD(slot) (_pacc[slot] += (unsigned long long)(clock64() - _pt0))
+#else
+#define PROF_T0()
+#define PROF_ADD(slot)
+#endif
+
 namespace {
 
 using namespace sm100;
@@ -506,7 +518,18 @@ ffn_fused_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
 constexpr int BM2 = 256, TN2 = 256, kStages2 = 6;
 constexpr uint32_t kHalf2 = 128 * BK * 2;  // 16 KB: 128 rows x 64 K of A or of B
 constexpr uint32_t kStage2 = 2 * kHalf2;
-constexpr size_t kSmem2 = (size_t)kStages2 * kStage2 + 1024 + 256;
+// epilogue staging for the TMA stores: per epilogue warp two 2 KB buffers of
+// 32 rows x 32 bf16 columns (SWIZZLE_64B), after the stage ring
+constexpr uint32_t kStg2 = 4 * 2 * 2048;
+constexpr size_t kSmem2 = (size_t)kStages2 * kStage2 + kStg2 + 1024 + 256;
+
+// Static persistent schedule: wave w hands tiles [w*ncl, (w+1)*ncl) to the ncl
+// clusters, rotated by one cluster per wave.  Without the rotation cluster c
+// would see only the N-tiles j = (c + w*ncl) mod (n1+n2) -- with ncl = 74 and
+// n1+n2 = 14 only 7 of the 14 (one parity) -- so half of every M-tile's GEMM1
+// tiles ran on one group of clusters and the GEMM2 tiles waited on the slower
+// group.  With the rotation every cluster cycles through all N-tiles.
+__device__ __forceinline__ int pair_sched(int w, int cid, int ncl) { return w * ncl + (cid + w) % ncl; }
 
 __device__ __forceinline__ TileInfo pair_tile_info(int m_tile, const int *tile_base, const int *offs, const int *slots,
                                                    int E) {
@@ -537,13 +560,15 @@ template <bool GATHER>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GATHER ? kThreads + 128 : kThreads, 1)
 ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w13,
                 const __grid_constant__ CUtensorMap map_h1, const __grid_constant__ CUtensorMap map_w2,
+                const __grid_constant__ CUtensorMap map_h1s, const __grid_constant__ CUtensorMap map_ys,
                 const int32_t *__restrict__ offsets, const int32_t *__restrict__ slot_of,
                 const uint32_t *__restrict__ need, const uint32_t *ready, int ready_base, uint32_t *done, int E, int H,
                 int I, int lag, const __nv_bfloat16 *__restrict__ xg, const int32_t *__restrict__ src_row,
                 int M_total, __nv_bfloat16 *__restrict__ h1, __nv_bfloat16 *__restrict__ y) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages2 * kStage2);
+  unsigned char *stg = smem + kStages2 * kStage2;
+  uint64_t *full = reinterpret_cast<uint64_t *>(stg + kStg2);
   uint64_t *empty = full + kStages2;
   uint64_t *tmem_full = empty + kStages2;  // [2]
   uint64_t *tmem_empty = tmem_full + 2;    // [2] (the leader's counts 8 epilogue warps of the pair)
@@ -593,24 +618,48 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
   const int total = (MT + lag) * (n1 + n2);
   const int nk1 = H / BK, nk2 = I / BK;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+#ifdef VMM_FFN_PROF
+  unsigned long long _pacc[24] = {};
+  const long long _prof_k0 = clock64();
+  if (threadIdx.x == 0) g_ffn_prof[blockIdx.x][10] = global_ns();
+#endif
 
   if (warp == 0) {
     if (lane == 0) {
       int it = 0;
-      for (int t = cid; t < total; t += ncl) {
+      for (int wv = 0, t = pair_sched(0, cid, ncl); wv * ncl < total; t = pair_sched(++wv, cid, ncl)) {
+        if (t >= total) continue;
         const FusedTile f = fused_tile(t, n1, n2, MT, lag);
         if (!f.valid) continue;
         const TileInfo ti = pair_tile_info(f.m_tile, s_tile_base, s_offs, s_slots, E);
         const uint32_t nd = s_need[ti.expert];
-        if (nd) wait_at_least(ready + (ti.slot - ready_base), nd, 256);
-        if (f.gemm2) wait_at_least(done + f.m_tile, 8u * (uint32_t)n1, 64);
+        {
+          PROF_T0();
+          if (nd) wait_at_least(ready + (ti.slot - ready_base), nd, 256);
+#ifdef VMM_FFN_PROF
+          if (f.gemm2) {
+            const uint32_t v0 = ld_acquire_u32(done + f.m_tile);
+            if ((int)(v0 - 8u * (uint32_t)n1) < 0) _pacc[6] += 1;
+          }
+#endif
+#ifdef VMM_FFN_PROF
+          if (f.gemm2 && !(g_ffn_prof_mode & 1)) wait_at_least(done + f.m_tile, 8u * (uint32_t)n1, 64);
+#else
+          if (f.gemm2) wait_at_least(done + f.m_tile, 8u * (uint32_t)n1, 64);
+#endif
+          PROF_ADD(0);
+        }
         if (nd || f.gemm2) fence_proxy_async_global();
         const CUtensorMap *ma = f.gemm2 ? &map_h1 : &map_x;
         const CUtensorMap *mb = f.gemm2 ? &map_w2 : &map_w13;
         const int nk = f.gemm2 ? nk2 : nk1;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % kStages2;
-          if (it >= kStages2) mbar_wait_watchdog(&empty[s], ((it / kStages2) - 1) & 1);
+          if (it >= kStages2) {
+            PROF_T0();
+            mbar_wait_watchdog(&empty[s], ((it / kStages2) - 1) & 1);
+            PROF_ADD(1);
+          }
           unsigned char *a_dst = smem + s * kStage2;
           const bool a_tma = !GATHER || f.gemm2;
           // both CTAs' TMA bytes land on the leader's barrier
@@ -624,17 +673,29 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
   } else if (warp == 1) {
     if (leader && lane == 0) {
       int it = 0, local = 0;
-      for (int t = cid; t < total; t += ncl) {
+      for (int wv = 0, t = pair_sched(0, cid, ncl); wv * ncl < total; t = pair_sched(++wv, cid, ncl)) {
+        if (t >= total) continue;
         const FusedTile f = fused_tile(t, n1, n2, MT, lag);
         if (!f.valid) continue;
         const int nk = f.gemm2 ? nk2 : nk1;
         const int b = local & 1, use = local >> 1;
-        if (use > 0) mbar_wait_watchdog(&tmem_empty[b], (use - 1) & 1);
+        if (use > 0) {
+          PROF_T0();
+          mbar_wait_watchdog(&tmem_empty[b], (use - 1) & 1);
+          PROF_ADD(2);
+        }
         tc_fence_after();
         const uint32_t acc = tmem + b * TN2;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % kStages2;
-          mbar_wait_watchdog(&full[s], (it / kStages2) & 1);
+          {
+            PROF_T0();
+            mbar_wait_watchdog(&full[s], (it / kStages2) & 1);
+            PROF_ADD(f.gemm2 ? 4 : 3);
+#ifdef VMM_FFN_PROF
+            _pacc[f.gemm2 ? 9 : 8] += 1;
+#endif
+          }
           if (GATHER) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem + s * kStage2);
@@ -675,7 +736,8 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
         --np;
       }
     };
-    for (int tt = cid; tt < total; tt += ncl) {
+    for (int wv = 0, tt = pair_sched(0, cid, ncl); wv * ncl < total; tt = pair_sched(++wv, cid, ncl)) {
+      if (tt >= total) continue;
       const FusedTile f = fused_tile(tt, n1, n2, MT, lag);
       if (!f.valid) continue;
       if (f.gemm2) {  // no gather: publish the stages after their previous round was consumed
@@ -708,77 +770,153 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
     }
     flush_to(0);
   } else if (warp >= 2 && warp < 6) {
+    // epilogue: TMEM -> registers -> bf16 -> swizzled staging -> TMA store (32 rows x 32 columns per
+    // store; a warp's rows that straddle the tile's expert boundary use direct stores instead)
     const int q = warp & 3;
     int local = 0;
+#ifdef VMM_FFN_PROF
+    const bool _nostore = (g_ffn_prof_mode & 2) != 0;
+#else
+    constexpr bool _nostore = false;
+#endif
+    uint32_t nst = 0;  // this warp's TMA stores so far (staging buffer nst & 1)
+    unsigned char *stg_w = stg + q * 4096;
+    auto stage_store = [&](const uint32_t (&w)[16], const CUtensorMap *map, int c0, int r0) {
+      unsigned char *buf = stg_w + (nst & 1) * 2048;
+      if (nst >= 2) {
+        PROF_T0();
+        if (lane == 0) bulk_wait_read<1>();  // the store that last read this buffer is done with it
+        __syncwarp();
+        if (q == 0 && lane == 0) PROF_ADD(14);
+      }
+      PROF_T0();
+      uint4 *rowp = reinterpret_cast<uint4 *>(buf + lane * 64);
+      const int sw = (lane >> 1) & 3;  // SWIZZLE_64B: 16 B chunk ^= address bits 7..8
+#pragma unroll
+      for (int v = 0; v < 4; ++v) rowp[v ^ sw] = make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(map, buf, c0, r0);
+        bulk_commit();
+      }
+      if (q == 0 && lane == 0) PROF_ADD(13);
+      ++nst;
+    };
     const uint32_t te_leader[2] = {mapa_shared(smem_u32(&tmem_empty[0]), 0), mapa_shared(smem_u32(&tmem_empty[1]), 0)};
-    for (int t = cid; t < total; t += ncl) {
+    for (int wv = 0, t = pair_sched(0, cid, ncl); wv * ncl < total; t = pair_sched(++wv, cid, ncl)) {
+      if (t >= total) continue;
       const FusedTile f = fused_tile(t, n1, n2, MT, lag);
       if (!f.valid) continue;
       const TileInfo ti = pair_tile_info(f.m_tile, s_tile_base, s_offs, s_slots, E);
       const int b = local & 1, use = local >> 1;
       ++local;
-      const int row = ti.row0 + 128 * (int)rank + q * 32 + lane;
-      mbar_wait_watchdog(&tmem_full[b], use & 1);
+      const int r_w0 = ti.row0 + 128 * (int)rank + q * 32;
+      const int row = r_w0 + lane;
+      const bool tma_rows = r_w0 + 32 <= ti.row_end;  // all 32 rows of this warp inside the tile's expert
+      {
+        PROF_T0();
+        mbar_wait_watchdog(&tmem_full[b], use & 1);
+        if (q == 0 && lane == 0) PROF_ADD(5);
+      }
       tc_fence_after();
+#ifdef VMM_FFN_PROF
+      const long long _tile_t0 = clock64();
+#endif
       const uint32_t t_base = tmem + b * TN2 + ((uint32_t)(q * 32) << 16);
       if (!f.gemm2) {
 #pragma unroll
         for (int hc = 0; hc < TN2 / 64; ++hc) {
           const int pair = hc >> 1, half = hc & 1;
-          float g[32], u[32];
-          tmem_ld32(t_base + pair * 128 + half * 32, g);
-          tmem_ld32(t_base + pair * 128 + 64 + half * 32, u);
+          uint32_t g[32], u[32];
+          tmem_ld32_nowait(t_base + pair * 128 + half * 32, g);
+          tmem_ld32_nowait(t_base + pair * 128 + 64 + half * 32, u);
+          {
+            PROF_T0();
+            tmem_wait_ld();
+            if (q == 0 && lane == 0) PROF_ADD(15);
+          }
           if (hc == TN2 / 64 - 1) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_relaxed_cluster(te_leader[b]);
           }
-          if (row < ti.row_end) {
-            uint4 *dst = reinterpret_cast<uint4 *>(h1 + (long long)row * I + f.n_tile * (TN2 / 2) + pair * 64 +
-                                                   half * 32);
+          uint32_t w[16];
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              uint4 o;
-              o.x = pack_bf16(silu(g[8 * v + 0]) * u[8 * v + 0], silu(g[8 * v + 1]) * u[8 * v + 1]);
-              o.y = pack_bf16(silu(g[8 * v + 2]) * u[8 * v + 2], silu(g[8 * v + 3]) * u[8 * v + 3]);
-              o.z = pack_bf16(silu(g[8 * v + 4]) * u[8 * v + 4], silu(g[8 * v + 5]) * u[8 * v + 5]);
-              o.w = pack_bf16(silu(g[8 * v + 6]) * u[8 * v + 6], silu(g[8 * v + 7]) * u[8 * v + 7]);
-              dst[v] = o;
-            }
+          for (int e2 = 0; e2 < 16; ++e2) {
+            const float g0 = __uint_as_float(g[2 * e2]), g1 = __uint_as_float(g[2 * e2 + 1]);
+            w[e2] = pack_bf16(silu(g0) * __uint_as_float(u[2 * e2]), silu(g1) * __uint_as_float(u[2 * e2 + 1]));
+          }
+          const int c0 = f.n_tile * (TN2 / 2) + pair * 64 + half * 32;
+          if (_nostore) {
+          } else if (tma_rows) {
+            stage_store(w, &map_h1s, c0, r_w0);
+          } else if (row < ti.row_end) {
+            uint4 *dst = reinterpret_cast<uint4 *>(h1 + (long long)row * I + c0);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) dst[v] = make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
           }
         }
-        fence_proxy_async_global();
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) red_release_add(done + f.m_tile, 1u);
+        // H1 block counter: this warp's rows are written (TMA stores complete, generic stores fenced)
+        {
+          PROF_T0();
+          if (tma_rows && lane == 0) bulk_wait<0>();
+          fence_proxy_async_global();
+          if (!tma_rows) __threadfence();
+          __syncwarp();
+          if (lane == 0) red_release_add(done + f.m_tile, 1u);
+          if (q == 0 && lane == 0) PROF_ADD(12);
+        }
       } else {
 #pragma unroll
-        for (int c = 0; c < TN2 / 32; ++c) {
-          float a[32];
-          tmem_ld32(t_base + c * 32, a);
-          if (c == TN2 / 32 - 1) {
+        for (int c2 = 0; c2 < TN2 / 32; c2 += 2) {  // two 32-column loads per TMEM wait
+          uint32_t a[2][32];
+          tmem_ld32_nowait(t_base + c2 * 32, a[0]);
+          tmem_ld32_nowait(t_base + c2 * 32 + 32, a[1]);
+          {
+            PROF_T0();
+            tmem_wait_ld();
+            if (q == 0 && lane == 0) PROF_ADD(15);
+          }
+          if (c2 == TN2 / 32 - 2) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_relaxed_cluster(te_leader[b]);
           }
-          if (row < ti.row_end) {
-            uint4 *dst = reinterpret_cast<uint4 *>(y + (long long)row * H + f.n_tile * TN2 + c * 32);
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              uint4 o;
-              o.x = pack_bf16(a[8 * v + 0], a[8 * v + 1]);
-              o.y = pack_bf16(a[8 * v + 2], a[8 * v + 3]);
-              o.z = pack_bf16(a[8 * v + 4], a[8 * v + 5]);
-              o.w = pack_bf16(a[8 * v + 6], a[8 * v + 7]);
-              dst[v] = o;
+          for (int h = 0; h < 2; ++h) {
+            uint32_t w[16];
+#pragma unroll
+            for (int e2 = 0; e2 < 16; ++e2)
+              w[e2] = pack_bf16(__uint_as_float(a[h][2 * e2]), __uint_as_float(a[h][2 * e2 + 1]));
+            const int c0 = f.n_tile * TN2 + (c2 + h) * 32;
+            if (_nostore) {
+            } else if (tma_rows) {
+              stage_store(w, &map_ys, c0, r_w0);
+            } else if (row < ti.row_end) {
+              uint4 *dst = reinterpret_cast<uint4 *>(y + (long long)row * H + c0);
+#pragma unroll
+              for (int v = 0; v < 4; ++v) dst[v] = make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
             }
           }
         }
       }
+#ifdef VMM_FFN_PROF
+      if (q == 0 && lane == 0) _pacc[f.gemm2 ? 17 : 16] += (unsigned long long)(clock64() - _tile_t0);
+      if (q == 0 && lane == 0) _pacc[f.gemm2 ? 19 : 18] += 1;
+#endif
     }
+    if (lane == 0) bulk_wait<0>();  // staging reads and Y writes complete before the CTA exits
+    __syncwarp();
   }
   tc_fence_before();
   __syncthreads();
+#ifdef VMM_FFN_PROF
+  if (threadIdx.x == 0) g_ffn_prof[blockIdx.x][7] = (unsigned long long)(clock64() - _prof_k0);
+  if (threadIdx.x == 0) g_ffn_prof[blockIdx.x][11] = global_ns();
+  for (int j = 0; j < 24; ++j)
+    if (_pacc[j] && j != 10 && j != 11) atomicAdd(&g_ffn_prof[blockIdx.x][j], _pacc[j]);
+#endif
   cluster_sync_all();  // every pair MMA into either CTA has been consumed before TMEM is freed
   if (warp == 1) {
     tc_fence_after();
@@ -990,6 +1128,20 @@ __global__ void simt_gemm2_kernel(const __nv_bfloat16 *__restrict__ h1, const in
 
 }  // namespace
 
+#ifdef VMM_FFN_PROF
+extern "C" int vmm_ffn_prof_mode(int mode) {
+  return (int)cudaMemcpyToSymbol(g_ffn_prof_mode, &mode, sizeof(int));
+}
+extern "C" int vmm_ffn_prof_read(unsigned long long *out, int reset) {
+  cudaMemcpyFromSymbol(out, g_ffn_prof, sizeof(unsigned long long) * 256 * 24);
+  if (reset) {
+    static unsigned long long zero[256 * 24];
+    cudaMemcpyToSymbol(g_ffn_prof, zero, sizeof(zero));
+  }
+  return 0;
+}
+#endif
+
 // per-device grid-barrier counter for the persistent decode FFN (monotonic:
 // each launch waits for its own epoch's target, so it is never reset)
 static int skinny_launch(const void *d_xp, const int32_t *d_offsets, int E, int M_total, int H, int I,
@@ -1189,16 +1341,29 @@ extern "C" int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offse
     int gridp = g_num_sms & ~1;
     if (gridp > 2 * max_pair_tiles * (n1 + n2)) gridp = 2 * max_pair_tiles * (n1 + n2);
     const int ncl = gridp / 2;
+    CUtensorMap mh1s, mys;  // epilogue TMA stores: 32 x 32 boxes, SWIZZLE_64B
+    {
+      uint64_t dims[2] = {(uint64_t)I, (uint64_t)M_total};
+      uint64_t str[1] = {(uint64_t)I * 2};
+      uint32_t box[2] = {32, 32};
+      if ((st = make_map_swz(&mh1s, d_h1, 2, dims, str, box, 64))) return st;
+    }
+    {
+      uint64_t dims[2] = {(uint64_t)H, (uint64_t)M_total};
+      uint64_t str[1] = {(uint64_t)H * 2};
+      uint32_t box[2] = {32, 32};
+      if ((st = make_map_swz(&mys, d_y, 2, dims, str, box, 64))) return st;
+    }
     static const int lag_waves = std::getenv("VMM_FFN_LAG") ? std::atoi(std::getenv("VMM_FFN_LAG")) : 4;
     const int lagp = (lag_waves * ncl + n1 + n2 - 1) / (n1 + n2);
     if (d_src_row)
       ffn_pair_kernel<true><<<gridp, kThreads + 128, kSmem2, s>>>(
-          mx, mw13, mh1, mw2, d_offsets, d_slot_of_expert, d_need, d_ready, ready_base, d_done, E, H, I, lagp,
-          (const __nv_bfloat16 *)d_x_rows, d_src_row, M_total, (__nv_bfloat16 *)d_h1, (__nv_bfloat16 *)d_y);
+          mx, mw13, mh1, mw2, mh1s, mys, d_offsets, d_slot_of_expert, d_need, d_ready, ready_base, d_done, E, H, I,
+          lagp, (const __nv_bfloat16 *)d_x_rows, d_src_row, M_total, (__nv_bfloat16 *)d_h1, (__nv_bfloat16 *)d_y);
     else
       ffn_pair_kernel<false><<<gridp, kThreads, kSmem2, s>>>(
-          mx, mw13, mh1, mw2, d_offsets, d_slot_of_expert, d_need, d_ready, ready_base, d_done, E, H, I, lagp,
-          nullptr, nullptr, M_total, (__nv_bfloat16 *)d_h1, (__nv_bfloat16 *)d_y);
+          mx, mw13, mh1, mw2, mh1s, mys, d_offsets, d_slot_of_expert, d_need, d_ready, ready_base, d_done, E, H, I,
+          lagp, nullptr, nullptr, M_total, (__nv_bfloat16 *)d_h1, (__nv_bfloat16 *)d_y);
     VMM_LAUNCH_CHECK("ffn_pair_kernel");
     return VMM_OK;
   }

@@ -24,7 +24,7 @@ EncodeTiledFn encode_fn() {
 }
 
 int make_map_impl(CUtensorMap *m, const void *base, int rank, const uint64_t *dims, const uint64_t *strides_bytes,
-             const uint32_t *box) {
+             const uint32_t *box, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return vmm::fail(VMM_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t d[3], s[2];
@@ -32,7 +32,7 @@ int make_map_impl(CUtensorMap *m, const void *base, int rank, const uint64_t *di
   for (int i = 0; i < rank; ++i) { d[i] = dims[i]; b[i] = box[i]; }
   for (int i = 0; i < rank - 1; ++i) s[i] = strides_bytes[i];
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void *>(base), d, s, b, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return vmm::fail(VMM_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return VMM_OK;
@@ -44,5 +44,13 @@ namespace sm100 {
 int make_map(CUtensorMap *m, const void *base, int rank, const uint64_t *dims, const uint64_t *strides_bytes,
              const uint32_t *box) {
   return make_map_impl(m, base, rank, dims, strides_bytes, box);
+}
+int make_map_swz(CUtensorMap *m, const void *base, int rank, const uint64_t *dims, const uint64_t *strides_bytes,
+                 const uint32_t *box, int swizzle_bytes) {
+  const CUtensorMapSwizzle swz = swizzle_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                                 : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                 : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                       : CU_TENSOR_MAP_SWIZZLE_NONE;
+  return make_map_impl(m, base, rank, dims, strides_bytes, box, swz);
 }
 }  // namespace sm100

@@ -59,3 +59,9 @@ if cm:
           f"gap before next demand {np.mean(idle):.2f} ms (mean)")
 print("per-layer period:", [round(v, 1) for v in per])
 print("per-layer ffn   :", [round(v, 1) for v in ffn])
+if cm and len(cm) // 3 == len(prof):
+    tail = [cm[3 * i + 1].elapsed_time(prof[i][1]) for i in range(len(prof))]
+    lead = [cm[3 * i].elapsed_time(prof[i][0]) for i in range(len(prof))]
+    print(f"FFN end after its demand copies done: mean {np.mean(tail):.2f} ms; FFN start after copies start: "
+          f"mean {np.mean(lead):.2f} ms")
+    print("per-layer tail:", [round(v, 2) for v in tail])
