@@ -152,6 +152,27 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
   // (VMM_FFN_FENCE=1: whole-layer event fence instead, e.g. under a serialising profiler)
   static const bool force_fence = std::getenv("VMM_FFN_FENCE") != nullptr;
   const bool flagged = !force_fence && ready && d.need_host && d.need_dev && d.ffn_done;
+  // Trace routing with preset counts (oracle / no predictor): every layer's demand
+  // set -- and the oracle's scores -- is known before the first layer runs.  Copy
+  // them to the host once and take all the layers' decisions without a per-layer
+  // GPU round trip; the kernels and copies are enqueued ahead of the GPU and the
+  // FFNs wait on the copy stream's ready flags (decode: one sync per token instead
+  // of one per layer).  VMM_NO_PRESYNC=1 restores the per-layer sync.
+  static const bool no_presync = std::getenv("VMM_NO_PRESYNC") != nullptr;
+  const bool presync = !pinned_only && !no_presync && d.routing == 1 && d.counts_preset &&
+                       (d.predictor == 0 || d.predictor == 3);
+  if (presync) {
+    VMM_CUDA(cudaMemcpyAsync(d.counts_host + (size_t)l0 * E, d.counts + (size_t)l0 * E,
+                             sizeof(uint32_t) * E * (l1 - l0), cudaMemcpyDeviceToHost, st),
+             "preset counts D2H");
+    if (d.predictor == 3)
+      VMM_CUDA(cudaMemcpyAsync(d.y_host + (size_t)l0 * E, d.oracle_table + (size_t)l0 * E,
+                               sizeof(double) * E * (l1 - l0), cudaMemcpyDeviceToHost, st),
+               "oracle scores D2H");
+    uint32_t ep = 0;
+    if (host_mark(st, &ep) == 0) VMM_CUDA(host_spin(st, ep), "preset sync");
+    else VMM_CUDA(cudaStreamSynchronize(st), "preset sync");
+  }
   bool have_xn = false;  // the fused combine of the previous layer already produced this layer's xn
   // Early decisions (live routing, large batches): the previous layer's combine ->
   // norm -> this layer's route run on the first n_split rows first; their expert
@@ -252,11 +273,11 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
                                    d.la_counts, d.y_dev, stream));
         ysrc = d.y_dev;
       } else if (d.predictor == 3) {
-        ysrc = d.oracle_table + (size_t)l * E;
+        ysrc = presync ? nullptr : d.oracle_table + (size_t)l * E;  // presync: already in y_host
       } else {
         return vmm::fail(VMM_ECONTRACT, "emitting layer without a predictor");
       }
-      VMM_CUDA(cudaMemcpyAsync(yh, ysrc, sizeof(double) * E, cudaMemcpyDeviceToHost, st), "scores D2H");
+      if (ysrc) VMM_CUDA(cudaMemcpyAsync(yh, ysrc, sizeof(double) * E, cudaMemcpyDeviceToHost, st), "scores D2H");
       if (split_now) VMM_CUDA(cudaEventRecord(ev_y, st), "scores event");
     }
     auto c1 = clk::now(), c2 = c1;
@@ -275,7 +296,11 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
         if (known)
           for (int e = 0; e < E; ++e) demand.push_back(e);
       }
-      if (!known) {
+      if (!known && presync) {  // counts already on the host
+        c1 = c2 = clk::now();
+        for (int e = 0; e < E; ++e)
+          if (ch[e]) demand.push_back(e);
+      } else if (!known) {
         VMM_CUDA(cudaMemcpyAsync(ch, cnt, sizeof(uint32_t) * E, cudaMemcpyDeviceToHost, st), "counts D2H");
         c1 = clk::now();
         uint32_t ep = 0;

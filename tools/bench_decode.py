@@ -62,7 +62,7 @@ for pred in preds:
         e1.record()
         e1.synchronize()
         if stack.profile:
-            ffn = [a.elapsed_time(b) * 1e3 for a, b, _, _ in stack.profile]
+            ffn = [p[0].elapsed_time(p[1]) * 1e3 for p in stack.profile]
         stack.profile = None
         ms.append(e0.elapsed_time(e1))
         copies += r.copies
