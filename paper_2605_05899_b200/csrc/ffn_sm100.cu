@@ -1007,6 +1007,9 @@ skinny_ffn_kernel(const __nv_bfloat16 *__restrict__ xp, const int32_t *__restric
   __shared__ int s_act[kSkinnyRows], s_r0[kSkinnyRows], s_r1[kSkinnyRows];
   __shared__ int s_nact;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef VMM_FFN_PROF
+  if (threadIdx.x == 0) g_ffn_prof[blockIdx.x][20] = global_ns();
+#endif
   if (warp == 0) {  // active experts in ascending id order (at most M_total <= 16 of them)
     int seen = 0;
     for (int c0 = 0; c0 < E; c0 += 32) {
@@ -1052,11 +1055,17 @@ skinny_ffn_kernel(const __nv_bfloat16 *__restrict__ xp, const int32_t *__restric
   // grid-wide barrier (all CTAs co-resident: one per SM): H1 complete before phase 2
   __threadfence();
   __syncthreads();
+#ifdef VMM_FFN_PROF
+  if (threadIdx.x == 0) g_ffn_prof[blockIdx.x][21] = global_ns();
+#endif
   if (threadIdx.x == 0) {
     atomicAdd(grid_bar, 1u);
     wait_at_least(grid_bar, bar_target, 32);
   }
   __syncthreads();
+#ifdef VMM_FFN_PROF
+  if (threadIdx.x == 0) g_ffn_prof[blockIdx.x][22] = global_ns();
+#endif
   // phase 2: down projection, 4 output columns per item
   const int rv2 = I / 8;
   const int ncol4 = H / 4;
@@ -1082,6 +1091,10 @@ skinny_ffn_kernel(const __nv_bfloat16 *__restrict__ xp, const int32_t *__restric
           }
     }
   }
+#ifdef VMM_FFN_PROF
+  __syncthreads();
+  if (threadIdx.x == 0) g_ffn_prof[blockIdx.x][23] = global_ns();
+#endif
 }
 
 // ---- CUDA-core cross-check path -------------------------------------------
