@@ -172,6 +172,17 @@ int vmm_shared_plan(int N, int S, int32_t *d_src, int32_t *d_offsets, void *stre
  * normalised rows, the residual is the raw row): y = x * rsqrt(mean(x^2)+eps) * w
  * (w nullable = ones). */
 int vmm_rmsnorm(const void *d_x, const void *d_w, int n, int H, float eps, void *d_y, void *stream);
+
+/* Decode-token glue in one launch (n <= 4 rows, n*k <= 32 picks, trace routing):
+ * out = resid + sum_j gates_prev[t,j] * y[pos_prev[t,j]] (skipped when d_y is NULL:
+ * the layer input is d_resid), xn = RMSNorm(out) (eps 1e-6, no weight), ids/gates of
+ * this layer from the trace rows (d_tr_l/d_tg_l = layer l's [tokens][k] slices),
+ * the stable plan by expert (offsets[E+1], src_row, pos) and xp[p] = xn[src_row[p]].
+ * Bit-identical to vmm_combine + vmm_rmsnorm + vmm_gather_i32/f32 + vmm_permute. */
+int vmm_decode_glue(const void *d_y, const int32_t *d_pos_prev, const float *d_gates_prev, const void *d_resid,
+                    int n, int k, int H, void *d_out, void *d_xn, const int32_t *d_tr_l, const float *d_tg_l,
+                    const int32_t *d_rows, int E, int32_t *d_ids, float *d_gates, int32_t *d_offsets,
+                    int32_t *d_src_row, int32_t *d_pos, void *d_xp, void *stream);
 /* out[t] = resid[t] + sum_j gates[t,j] * Y[pos[t,j]]  (bf16 rows, fp32 accumulate, j ascending) */
 int vmm_combine(const void *d_y, const int32_t *d_pos, const float *d_gates, const void *d_resid,
                 int N, int k, int H, void *d_out, void *stream);

@@ -92,6 +92,7 @@ _SIGS = {
     "vmm_permute": (I32, [P, I32, I32, I32, P, I32, P, P, P, P, P]),
     "vmm_combine": (I32, [P, P, P, P, I32, I32, I32, P, P]),
     "vmm_rmsnorm": (I32, [P, P, I32, I32, C.c_float, P, P]),
+    "vmm_decode_glue": (I32, [P, P, P, P, I32, I32, I32, P, P, P, P, P, I32, P, P, P, P, P, P, P]),
     "vmm_grouped_swiglu": (I32, [P, P, I32, I32, I32, I32, P, P, I64, I64, P, P, P, P]),
     "vmm_grouped_swiglu_fused": (I32, [P, P, I32, I32, I32, I32, P, P, I64, I64, P, P, P, I32, P, P, P, I32, P, P, P]),
     "vmm_grouped_swiglu_simt": (I32, [P, P, I32, I32, I32, I32, P, P, I64, P, P, P, P]),

@@ -441,7 +441,7 @@ static int permute_impl(const int32_t *d_ids, int N, int k, int E, int32_t *d_of
   if (N * k <= 32) {
     permute_plan_warp_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(d_ids, N * k, k, E, d_offsets, d_src_row, d_pos);
     VMM_LAUNCH_CHECK("permute_plan_warp_kernel");
-    return VMM_OK;
+    return d_xp ? vmm_permute_rows(d_x, d_src_row, N * k, H, d_xp, stream) : VMM_OK;
   }
   const int n_picks = N * k;
   if (n_picks > 2048) {  // multi-CTA stable sort; per-CTA counts in a library scratch (per device)
@@ -623,4 +623,116 @@ extern "C" int vmm_combine_norm(const void *d_y, const int32_t *d_pos, const flo
   int st = vmm_combine_shared(d_y, d_pos, d_gates, d_resid, N, k, H, d_ys, S, d_out, stream);
   if (st) return st;
   return vmm_rmsnorm(d_out, nullptr, N, H, eps, d_xn, stream);
+}
+
+// ---- decode glue: one CTA per decode layer ----------------------------------
+// For a decode token (n <= 2 rows, n*k <= 16 picks) the per-layer glue is six
+// tiny launches (combine, RMSNorm, two trace gathers, plan, row copy), each a
+// few microseconds of launch/dependency latency for a few KB of work.  This
+// kernel does all of it in one CTA with the same arithmetic as those kernels
+// (combine_chunk, warp_row_ss / warp_row_norm_store, the stable (expert, pick)
+// order of the plan), so the results are bit-identical:
+//   A (warp per row): out = resid + sum_j g_j Y[pos_j]  (skipped when y == NULL:
+//                     the layer's input is already `resid`), xn = RMSNorm(out)
+//   B (thread 0):     ids/gates of layer l from the trace rows, stable counting
+//                     sort by expert -> offsets, src_row, pos
+//   C (warp per pick): xp[p] = xn[src_row[p]]
+namespace {
+constexpr int kGlueMaxRows = 4, kGlueMaxPicks = 32;
+
+template <int CH>
+__global__ void __launch_bounds__(256)
+decode_glue_kernel(const uint4 *__restrict__ y, const int32_t *pos_prev, const float *gates_prev,
+                   const uint4 *__restrict__ resid, int n, int k, int row_vec, uint4 *out, uint4 *xn,
+                   const int32_t *tr_l,
+                   const float *tg_l, const int32_t *__restrict__ rows, int E, int32_t *ids, float *gates,
+                   int32_t *offsets, int32_t *src_row, int32_t *pos, uint4 *xp, float eps) {
+  __shared__ uint4 s_xn[kGlueMaxRows][kMaxRowVec];
+  __shared__ int s_src[kGlueMaxPicks];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp < n) {
+    const int t = warp;
+    uint4 v[CH];
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      const int c = lane + 32 * i;
+      if (c >= row_vec) continue;
+      if (y == nullptr) {
+        v[i] = resid[(long long)t * row_vec + c];
+      } else {
+        float acc[8];
+        combine_chunk(y, pos_prev, gates_prev, t, k, row_vec, c, nullptr, 0, n, acc);
+        const uint4 rv = resid[(long long)t * row_vec + c];
+        const __nv_bfloat16 *rh = reinterpret_cast<const __nv_bfloat16 *>(&rv);
+        __nv_bfloat16 *oh = reinterpret_cast<__nv_bfloat16 *>(&v[i]);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) oh[q] = __float2bfloat16(__bfloat162float(rh[q]) + acc[q]);
+        out[(long long)t * row_vec + c] = v[i];
+      }
+    }
+    const float inv = rsqrtf(warp_row_ss<CH>(v, row_vec) / (float)(row_vec * 8) + eps);
+    warp_row_norm_store<CH>(v, row_vec, inv, nullptr, s_xn[t]);
+    __syncwarp();
+    for (int c = lane; c < row_vec; c += 32) xn[(long long)t * row_vec + c] = s_xn[t][c];
+  }
+  __syncthreads();  // phase A has read pos/gates of the previous layer before B overwrites them
+  const int M = n * k;
+  if (threadIdx.x == 0) {
+    int cnt[VMM_MAX_EXPERTS];
+    for (int e = 0; e < E; ++e) cnt[e] = 0;
+    for (int i = 0; i < M; ++i) {
+      const int t = i / k, j = i - t * k;
+      const int e = tr_l[(long long)rows[t] * k + j];
+      ids[i] = e;
+      gates[i] = tg_l[(long long)rows[t] * k + j];
+      cnt[e] += 1;
+    }
+    int run = 0;
+    for (int e = 0; e < E; ++e) {
+      offsets[e] = run;
+      const int c = cnt[e];
+      cnt[e] = run;
+      run += c;
+    }
+    offsets[E] = run;
+    for (int i = 0; i < M; ++i) {
+      const int e = ids[i];
+      const int p = cnt[e]++;
+      pos[i] = p;
+      src_row[p] = i / k;
+      s_src[p] = i / k;
+    }
+  }
+  __syncthreads();
+  for (int p = warp; p < M; p += 8) {
+    const uint4 *s = s_xn[s_src[p]];
+    for (int c = lane; c < row_vec; c += 32) xp[(long long)p * row_vec + c] = s[c];
+  }
+}
+}  // namespace
+
+extern "C" int vmm_decode_glue(const void *d_y, const int32_t *d_pos_prev, const float *d_gates_prev,
+                               const void *d_resid, int n, int k, int H, void *d_out, void *d_xn,
+                               const int32_t *d_tr_l,
+                               const float *d_tg_l, const int32_t *d_rows, int E, int32_t *d_ids, float *d_gates,
+                               int32_t *d_offsets, int32_t *d_src_row, int32_t *d_pos, void *d_xp, void *stream) {
+  if (n <= 0) return VMM_OK;
+  if (n > kGlueMaxRows || n * k > kGlueMaxPicks)
+    return vmm::fail(VMM_EVALIDATION, "decode glue: at most 4 rows and 32 picks");
+  if ((H * 2) % 16) return vmm::fail(VMM_EVALIDATION, "hidden size must be a multiple of 8");
+  const int row_vec = H * 2 / 16;
+  if (row_vec > kMaxRowVec) return vmm::fail(VMM_EVALIDATION, "hidden size above 4096");
+  if (E < 1 || E > VMM_MAX_EXPERTS) return vmm::fail(VMM_EVALIDATION, "experts must lie in [1, 256]");
+  cudaStream_t st = (cudaStream_t)stream;
+#define VMM_GLUE(CH)                                                                                            \
+  decode_glue_kernel<CH><<<1, 256, 0, st>>>((const uint4 *)d_y, d_pos_prev, d_gates_prev, (const uint4 *)d_resid, \
+                                            n, k, row_vec, (uint4 *)d_out, (uint4 *)d_xn, d_tr_l, d_tg_l, d_rows, \
+                                            E, d_ids,                                                             \
+                                            d_gates, d_offsets, d_src_row, d_pos, (uint4 *)d_xp, 1e-6f)
+  if (row_vec <= 64) VMM_GLUE(2);
+  else if (row_vec <= 256) VMM_GLUE(8);
+  else VMM_GLUE(16);
+#undef VMM_GLUE
+  VMM_LAUNCH_CHECK("decode_glue_kernel");
+  return VMM_OK;
 }

@@ -203,10 +203,25 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
   auto us = [](clk::time_point a, clk::time_point b) {
     return std::chrono::duration<double, std::micro>(b - a).count();
   };
+  // Decode-sized layers with trace routing: the previous layer's combine, this
+  // layer's RMSNorm, trace gathers, plan and row copy run as ONE launch
+  // (vmm_decode_glue, bit-identical to the separate kernels) at the layer start.
+  static const bool no_glue = std::getenv("VMM_NO_DECODE_GLUE") != nullptr;
+  static const bool gather_env0 = std::getenv("VMM_FFN_GATHER") != nullptr;
+  const bool glue = !no_glue && !gather_env0 && d.routing == 1 && d.shared == 0 && n_rows <= 4 && n_rows * k <= 16;
+  const void *glue_resid = nullptr;  // pending combine: the previous layer's residual input
   for (int l = l0; l < l1; ++l) {
     auto c0 = clk::now();
     void *xn = d.xn;
-    if (!have_xn) VMM_TRY(vmm_rmsnorm(cur, nullptr, n_rows, H, 1e-6f, xn, stream));
+    if (glue) {
+      const int32_t *tr = d.trace_routes + (size_t)l * d.trace_tokens * k;
+      const float *tg = d.trace_gates + (size_t)l * d.trace_tokens * k;
+      VMM_TRY(vmm_decode_glue(glue_resid ? d.y : nullptr, d.pos, d.gates, glue_resid ? glue_resid : cur, n_rows, k, H,
+                              const_cast<void *>(cur), xn, tr, tg, d_rows, E, d.ids, d.gates, d.off, d.src, d.pos,
+                              d.xp, stream));
+    } else if (!have_xn) {
+      VMM_TRY(vmm_rmsnorm(cur, nullptr, n_rows, H, 1e-6f, xn, stream));
+    }
     const int emits = pinned_only ? 0 : vmm_engine_emits(eng, l, phase);
     uint32_t *cnt = d.counts + (size_t)l * E;
     bool la_done = false;
@@ -247,8 +262,10 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
     } else {
       const int32_t *tr = d.trace_routes + (size_t)l * d.trace_tokens * k;
       const float *tg = d.trace_gates + (size_t)l * d.trace_tokens * k;
-      VMM_TRY(vmm_gather_i32(tr, d_rows, n_rows, k, d.ids, stream));
-      VMM_TRY(vmm_gather_f32(tg, d_rows, n_rows, k, d.gates, stream));
+      if (!glue) {
+        VMM_TRY(vmm_gather_i32(tr, d_rows, n_rows, k, d.ids, stream));
+        VMM_TRY(vmm_gather_f32(tg, d_rows, n_rows, k, d.gates, stream));
+      }
       if (!d.counts_preset) {
         int32_t lay = l;
         (void)lay;
@@ -353,10 +370,13 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
     // at 1.25M rows), so the permuted copy is the default.
     static const bool gather_env = std::getenv("VMM_FFN_GATHER") != nullptr;
     const bool gather = gather_env && d.ffn_done && M > 16;
-    if (gather)
+    if (glue) {
+      // plan and row copy done by the layer's glue launch
+    } else if (gather) {
       VMM_TRY(vmm_permute_plan(d.ids, n_rows, k, E, d.off, d.src, d.pos, stream));
-    else
+    } else {
       VMM_TRY(vmm_permute(d.ids, n_rows, k, E, xn, H, d.off, d.src, d.pos, d.xp, stream));
+    }
     if (out && out->ffn_start)
       VMM_CUDA(cudaEventRecord((cudaEvent_t)out->ffn_start[l - l0], st), "ffn start event");
     VMM_TRY(vmm_grouped_swiglu_fused(d.xp, d.off, E, M, H, I, d.arena, (const char *)d.arena + (size_t)2 * I * H * 2,
@@ -381,7 +401,9 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
     if (out && out->n_demand) out->n_demand[l - l0] = (int)demand.size();
     // the slabs this layer read are free for refills once its FFNs are done
     if (l >= lp && !pinned_only) VMM_TRY(vmm_xfer_layer_done(xf, l, stream));
-    if (l + 1 < l1) {  // combine fused with the next layer's RMSNorm (xn is free again: consumed above)
+    if (l + 1 < l1 && glue) {  // the combine runs in the next layer's glue launch
+      glue_resid = cur;
+    } else if (l + 1 < l1) {  // combine fused with the next layer's RMSNorm (xn is free again: consumed above)
       if (n_split) {  // first chunk only; the rest runs after the next layer's first-chunk route
         VMM_TRY(vmm_combine_norm(d.y, d.pos, d.gates, cur, n_split, k, H, nullptr, 0, 1e-6f, dst, xn, stream));
         pending_rest = true;

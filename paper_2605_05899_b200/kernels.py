@@ -270,6 +270,27 @@ def rmsnorm(x, weight=None, eps: float = 1e-6, stream=None, out=None):
     return out
 
 
+def decode_glue(y, pos_prev, gates_prev, resid, tr_l, tg_l, rows, experts: int, out=None, xn=None, stream=None):
+    """One-launch decode glue (vmm_decode_glue): returns (out, xn, ids, gates,
+    offsets, src_row, pos, xp).  y=None: resid is the layer input (no combine)."""
+    n, H = (int(s) for s in resid.shape)
+    k = int(tr_l.shape[1])
+    dev = resid.device
+    out = torch.empty_like(resid) if out is None else out
+    xn = torch.empty_like(resid) if xn is None else xn
+    ids = torch.empty(n, k, dtype=_i32, device=dev)
+    gates = torch.empty(n, k, dtype=torch.float32, device=dev)
+    offsets = torch.empty(experts + 1, dtype=_i32, device=dev)
+    src = torch.empty(n * k, dtype=_i32, device=dev)
+    pos = torch.empty(n * k, dtype=_i32, device=dev)
+    xp = torch.empty(n * k, H, dtype=resid.dtype, device=dev)
+    _n(1)
+    check(_lib.lib().vmm_decode_glue(ptr(y), ptr(pos_prev), ptr(gates_prev), ptr(resid), n, k, H, ptr(out), ptr(xn),
+                                     ptr(tr_l), ptr(tg_l), ptr(rows), experts, ptr(ids), ptr(gates), ptr(offsets),
+                                     ptr(src), ptr(pos), ptr(xp), stream_ptr(stream)))
+    return out, xn, ids, gates, offsets, src, pos, xp
+
+
 def combine(y, pos, gates, resid, stream=None, out=None):
     N, k = (int(s) for s in gates.shape)
     H = int(y.shape[1])

@@ -203,6 +203,10 @@ def test_permute_plan_small_batches(N, k, E):
     assert torch.equal(off.cpu().long(), roff)
     assert torch.equal(src.cpu().long()[: N * k], rsrc)
     assert torch.equal(pos.cpu().long()[: N * k].reshape(N, k), rpos)
+    # the fused plan + row copy writes every permuted row (also for <= 32 picks)
+    x = torch.randn(N, 64, device="cuda").to(torch.bfloat16)
+    _, src2, _, xp = kernels.permute(ids.cuda(), x, E)
+    assert torch.equal(xp, x[src2[: N * k].long()])
 
 
 @pytest.mark.parametrize("shape", [(1216, 2048, 768, 128, 8), (300, 256, 512, 8, 2), (640, 2048, 1408, 64, 6),
@@ -276,3 +280,38 @@ def test_fused_ffn_waits_for_copy_stream_fills(N):
         assert torch.equal(y, yr)
     finally:
         L.vmm_xfer_destroy(xf)
+
+
+@pytest.mark.parametrize("n,k,E,H,with_y", [(1, 8, 128, 2048, True), (2, 8, 128, 2048, True), (1, 8, 128, 2048, False),
+                                             (2, 2, 8, 256, True), (4, 4, 64, 2560, True)])
+def test_decode_glue_bit_identical_to_separate_kernels(n, k, E, H, with_y):
+    """vmm_decode_glue == combine -> rmsnorm -> trace gathers -> permute (plan + row copy)."""
+    g = torch.Generator(device="cuda").manual_seed(n * 100 + k)
+    T_tr = 50
+    tr = torch.stack([torch.randperm(E, generator=torch.Generator().manual_seed(i))[:k] for i in range(T_tr)]) \
+        .to(torch.int32).cuda()
+    tg = torch.rand(T_tr, k, generator=g, device="cuda")
+    rows = torch.tensor([7, 31, 2, 44][:n], dtype=torch.int32, device="cuda")
+    resid = torch.randn(n, H, generator=g, device="cuda").to(torch.bfloat16)
+    M = n * k
+    y = torch.randn(M, H, generator=g, device="cuda").to(torch.bfloat16)
+    pos_prev = torch.randperm(M, generator=torch.Generator().manual_seed(3)).to(torch.int32).cuda().view(n, k)
+    gates_prev = torch.rand(n, k, generator=g, device="cuda")
+    # separate kernels
+    if with_y:
+        out_ref = kernels.combine(y, pos_prev, gates_prev, resid)
+    else:
+        out_ref = resid
+    xn_ref = kernels.rmsnorm(out_ref)
+    ids_ref = tr[rows.long()].contiguous()
+    gates_ref = tg[rows.long()].contiguous()
+    off_ref, src_ref, pos_ref, xp_ref = kernels.permute(ids_ref, xn_ref, E)
+    # one launch (pos/gates of the previous layer are overwritten in place, as in the executor)
+    out, xn, ids, gates, off, src, pos, xp = kernels.decode_glue(y if with_y else None, pos_prev.clone(),
+                                                                 gates_prev.clone(), resid, tr, tg, rows, E)
+    if with_y:
+        assert torch.equal(out, out_ref)
+    assert torch.equal(xn, xn_ref)
+    assert torch.equal(ids, ids_ref) and torch.equal(gates, gates_ref)
+    assert torch.equal(off, off_ref[: E + 1]) and torch.equal(src, src_ref[:M]) and torch.equal(pos, pos_ref[:M])
+    assert torch.equal(xp, xp_ref)

@@ -390,3 +390,42 @@ def test_chunked_prefix_as_rows_land_is_bit_identical():
     assert np.array_equal(reta, b.retained)
     assert torch.equal(ha, b.hidden)
     assert b.report.to_dict() == repa
+
+
+@pytest.mark.parametrize("routing,pred", [("live", "history"), ("trace", "oracle"), ("trace", "history")])
+def test_decode_step_hidden_matches_resident_layers(routing, pred):
+    """Decode tokens through the cached executor (skinny FFN, one-launch decode glue
+    on trace routing) give bit-identically the hidden state of the same layers run
+    on resident experts with the plain kernels (rmsnorm, route/trace ids, permute,
+    grouped SwiGLU, combine)."""
+    from paper_2605_05899_b200 import kernels
+    from paper_2605_05899_b200.moe import moe_layer_forward
+
+    cfg = tiny_cfg(routing=routing, predictor=pred, num_slabs=20)
+    D = 2
+    tr = generate_trace(TraceGenConfig(n_visual=576, n_text=64, layers=cfg.layers, experts=cfg.experts, k=cfg.k,
+                                       cluster_support=4, visual_noise=0.3, seed=31, decode_steps=D))
+    T = tr.num_tokens - D
+    stack = MoEStack(cfg)
+    x, sal, mod, dtr = request(tr, cfg.hidden, seed=4)
+    stack.forward(x[:T], sal[:T], mod[:T], trace=dtr if routing == "trace" else None, keep_session=True)
+    store, E = stack.store, cfg.experts
+    arena = torch.stack([store.pool[(l % store.host_layers) * E + e] for l in range(cfg.layers)
+                         for e in range(E)]).cuda()
+    g = torch.Generator(device="cuda").manual_seed(9)
+    for s in range(D):
+        xt = torch.randn((1, cfg.hidden), generator=g, device="cuda").to(torch.bfloat16)
+        r = stack.decode_step(xt, tok=T + s if routing == "trace" else None)
+        cur = xt
+        for l in range(cfg.layers):
+            xn = kernels.rmsnorm(cur)
+            if routing == "trace":
+                ids = dtr["routes"][l, T + s].view(1, -1).contiguous()
+                gates = dtr["gates"][l, T + s].view(1, -1).contiguous()
+            else:
+                ids, gates, _ = kernels.route_topk(xn, store.router[l], cfg.k)
+            cur = moe_layer_forward(cur, ids, gates, arena, torch.arange(l * E, (l + 1) * E, dtype=torch.int32,
+                                                                          device="cuda"), cfg.inter, E, xn=xn)
+        torch.cuda.synchronize()
+        assert torch.equal(r.hidden, cur), (routing, pred, s)
+    stack.end_session()
