@@ -145,7 +145,8 @@ def test_skinny_router_decode_sizes_exact(N):
     assert torch.equal(la.cpu().long(), torch.bincount(nid.reshape(-1).long(), minlength=E))
 
 
-@pytest.mark.parametrize("shape", [(1, 2048, 768, 128, 8), (2, 2048, 1408, 64, 6), (1, 2560, 10240, 4, 2)])
+@pytest.mark.parametrize("shape", [(1, 2048, 768, 128, 8), (2, 2048, 768, 128, 8), (2, 1024, 512, 16, 8),
+                                   (2, 2048, 1408, 64, 6), (1, 2560, 10240, 4, 2)])
 def test_decode_sized_swiglu_matches_fp32_restatement(shape):
     """M_total <= 16 rows takes the weight-streaming CUDA-core path."""
     _check_swiglu(shape)
