@@ -52,6 +52,60 @@ def parse():
 
 
 # ---------------------------------------------------------------------------
+def _host_info():
+    """os.cpu_count(), the lscpu model name and the BLAS thread setting."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_count": os.cpu_count(), "model": model,
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS")}
+
+
+def _cpu_restatement(w, T1, n_r):
+    """The builder's torch-CPU fp32 restatement of router + expert FFN + combine
+    (oracle/moe_ref.py) on one post-prefix layer of one request (n_r retained
+    rows), all host threads -- labelled "restatement, not ref".
+    Extrapolated to the stack: l_pinned layers on all T1 tokens plus the rest on
+    n_r rows, at the measured per-row cost."""
+    import torch
+
+    from oracle import moe_ref
+
+    nth = os.cpu_count() or 1
+    torch.set_num_threads(nth)
+    g = torch.Generator().manual_seed(0)
+    H, I, E, k = w.hidden, w.inter, w.experts, w.k
+    x = torch.randn(n_r, H, generator=g).to(torch.bfloat16)
+    wg_r = (torch.randn(E, H, generator=g) / H ** 0.5).to(torch.bfloat16)
+    # one weight set shared by every expert (the FLOPs, not the bytes, are the restatement's cost)
+    w_gate = (torch.randn(I, H, generator=g) / H ** 0.5).to(torch.bfloat16)
+    w_up = (torch.randn(I, H, generator=g) / H ** 0.5).to(torch.bfloat16)
+    w_down = (torch.randn(H, I, generator=g) / I ** 0.5).to(torch.bfloat16)
+    t0 = time.perf_counter()
+    xn = (x.float() * torch.rsqrt(x.float().pow(2).mean(1, keepdim=True) + 1e-6)).to(torch.bfloat16)
+    ids, gates, _ = moe_ref.route(xn, wg_r, k)
+    off, src, pos = moe_ref.permute(ids, E)
+    xr = xn[src]
+    y = torch.empty(n_r * k, H, dtype=torch.bfloat16)
+    for e in range(E):
+        a, b = int(off[e]), int(off[e + 1])
+        if b > a:
+            _, y[a:b] = moe_ref.expert_ffn(xr[a:b], w_gate, w_up, w_down)
+    moe_ref.combine(y, pos, gates, x)
+    layer_s = time.perf_counter() - t0
+    per_row = layer_s / n_r
+    stack_s = per_row * (w.l_pinned * T1 + (w.layers - w.l_pinned) * n_r)
+    return {"label": "restatement, not ref", "value": T1 / stack_s, "unit": "tokens/s", "threads": nth,
+            "layer_ms": layer_s * 1e3, "sample": f"one post-prefix {w.name} layer on {n_r} rows "
+            "(oracle/moe_ref.py: fp64 router, fp32 SwiGLU per expert, combine), extrapolated to the stack"}
+
+
 # reference arm: the reference's CPU path (oracle port: compress + simulate)
 # ---------------------------------------------------------------------------
 def _ref_worker_init(gen_kw, seed):
@@ -430,6 +484,11 @@ def main():
             dt = (time.perf_counter() - t0) / n_req
             cpu = {"value": T1 / dt, "unit": "tokens/s", "cores": 1, "kind": "port",
                    "sample": f"{n_req} x one {w.name} request (compress + simulate, oracle predictor), single thread"}
+            cpu["host"] = _host_info()
+            try:
+                cpu["restatement"] = _cpu_restatement(w, T1, max(1, int(res0.hidden.shape[0]) // R))
+            except Exception as exc:  # noqa: BLE001
+                cpu["restatement"] = {"label": "restatement, not ref", "value": None, "sample": f"failed: {exc}"}
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "unit": "tokens/s", "cores": 1, "kind": "port", "sample": f"failed: {exc}"}
 
