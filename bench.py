@@ -467,6 +467,15 @@ def main():
                                                                           else None)
     h2d_bytes = res0.h2d_bytes
     rep = res0.report
+    # whole-job counters (mode DP: one sum-reduction of the per-rank counters)
+    hits, misses, evictions, copies = rep.hits, rep.misses, rep.evictions, res0.copies
+    retained = int(res0.hidden.shape[0])
+    if world > 1:
+        hits, misses, evictions, copies, h2d_bytes, retained = (v for v in vdist.sum_over_ranks(
+            [hits, misses, evictions, copies, h2d_bytes, retained], dev))
+    hit_rate = hits / (hits + misses) if (hits or misses) and rep.hit_rate is not None else rep.hit_rate
+    if h2d_peak and world > 1 and a.source == "host":
+        h2d_peak = h2d_peak * world  # one host link per GPU: the job's aggregate copy peak
     h2d_gbs = h2d_bytes / (ms * 1e-3) / 1e9
 
     cpu = None
@@ -504,9 +513,9 @@ def main():
                        "miss_source": a.source,
                        "parallelism": f"dp{world} (requests)", "requests_per_gpu_step": R,
                        "l2": "flushed (256 MB write) between timed steps"},
-            "hit_rate": rep.hit_rate, "hits": rep.hits, "misses": rep.misses, "evictions": rep.evictions,
-            "retained_tokens": int(res0.hidden.shape[0]),
-            "h2d": {"gbs": h2d_gbs, "bytes_per_step": h2d_bytes, "copies_per_step": res0.copies,
+            "hit_rate": hit_rate, "hits": int(hits), "misses": int(misses), "evictions": int(evictions),
+            "retained_tokens": int(retained),
+            "h2d": {"gbs": h2d_gbs, "bytes_per_step": h2d_bytes, "copies_per_step": int(copies),
                     "window_ms": res0.h2d_ms,
                     "window_gbs": h2d_bytes / (res0.h2d_ms * 1e-3) / 1e9 if res0.h2d_ms else None,
                     "peak_gbs": h2d_peak, "frac": h2d_gbs / h2d_peak if h2d_peak else None,
