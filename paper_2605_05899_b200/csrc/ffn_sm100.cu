@@ -717,7 +717,7 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
     // the leader's full barrier: 4 warps x 2 CTAs + the producer's expect_tx arrival).  kGD stages
     // stay in flight per thread (kGD < kStages2, so a blocking empty wait never waits on a stage
     // this warp has not published yet).
-    constexpr int kGD = 3;
+    constexpr int kGD = 4;
     const int t = threadIdx.x - 192;
     int it = 0, pend[kGD + 1], np = 0;
     auto publish = [&](int ps) {
@@ -728,7 +728,9 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
     };
     auto flush_to = [&](int keep) {  // publish all but the newest `keep` pending stages
       while (np > keep) {
-        if (keep == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
+        if (keep == 4) asm volatile("cp.async.wait_group 4;" ::: "memory");
+        else if (keep == 3) asm volatile("cp.async.wait_group 3;" ::: "memory");
+        else if (keep == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
         else if (keep == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
         else asm volatile("cp.async.wait_group 0;" ::: "memory");
         publish(pend[0]);
@@ -751,17 +753,30 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
         continue;
       }
       const TileInfo ti = pair_tile_info(f.m_tile, s_tile_base, s_offs, s_slots, E);
-      const int r = ti.row0 + 128 * (int)rank + t;
-      const int tok = src_row[r < M_total ? r : M_total - 1];
-      const char *src = reinterpret_cast<const char *>(xg + (long long)tok * H);
+      // warp gw4 owns local rows [32 gw4, +32); each cp.async instruction covers 4 rows x 128 B
+      // (8 lanes per row: coalesced 128-byte pieces, 4 L1 wavefronts instead of 32)
+      const int gw4 = t >> 5;
+      const int r = ti.row0 + 128 * (int)rank + gw4 * 32 + lane;
+      const int tok_lane = src_row[r < M_total ? r : M_total - 1];
+      const int c = lane & 7;
+      long long src_off[8];
+      uint32_t dst_off[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int rl = gw4 * 32 + 4 * i + (lane >> 3);  // local row 0..127 of this CTA's half
+        const int tok = __shfl_sync(0xffffffffu, tok_lane, 4 * i + (lane >> 3));
+        src_off[i] = (long long)tok * H * 2 + c * 16;
+        dst_off[i] = rl * 128 + ((c ^ (rl & 7)) << 4);
+      }
+      const char *xb = reinterpret_cast<const char *>(xg);
       for (int kb = 0; kb < nk1; ++kb, ++it) {
         const int s = it % kStages2;
         if (it >= kStages2) mbar_wait_watchdog(&empty[s], ((it / kStages2) - 1) & 1);
-        const uint32_t dst = smem_u32(smem + s * kStage2) + t * 128;
+        const uint32_t dst = smem_u32(smem + s * kStage2);
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + ((c ^ (t & 7)) << 4)),
-                       "l"(src + (size_t)kb * BK * 2 + c * 16)
+        for (int i = 0; i < 8; ++i)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + dst_off[i]),
+                       "l"(xb + src_off[i] + (size_t)kb * BK * 2)
                        : "memory");
         asm volatile("cp.async.commit_group;" ::: "memory");
         if (np == kGD) flush_to(kGD - 1);

@@ -40,7 +40,10 @@ for it in range(3):
     lib.vmm_ffn_prof_read(buf, 1)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    kernels.grouped_swiglu(xp, off, arena, slot, I)
+    if os.environ.get("FFN_PROF_GATHER"):
+        kernels.grouped_swiglu(M, off, arena, slot, I, x_rows=x, src_row=src)
+    else:
+        kernels.grouped_swiglu(xp, off, arena, slot, I)
     b.record()
     b.synchronize()
     lib.vmm_ffn_prof_read(buf, 0)
