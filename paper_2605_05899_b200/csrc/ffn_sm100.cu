@@ -1112,6 +1112,238 @@ skinny_ffn_kernel(const __nv_bfloat16 *__restrict__ xp, const int32_t *__restric
 #endif
 }
 
+// ---- decode-sized layers on the tensor cores (swap-AB) -----------------------
+// A decode layer is <= 16 rows spread over <= 16 experts: the FLOPs are nothing,
+// the cost is streaming the active experts' weights (75 MB at C3) from HBM.  The
+// CUDA-core kernel above streams them through the LSUs and tops out near 2 TB/s
+// (each SM's outstanding-load budget).  Here the weights stream by TMA -- an
+// 8-stage ring of 128-row x 64-column tiles per SM -- and tcgen05 does the
+// arithmetic with the roles swapped: D[128 weight rows][16 token slots] =
+// W_tile . X^T, A = the weight tile (K-major, TMA SW128), B = the expert's <= 16
+// token rows staged once per tile in shared memory (zero-padded to 16), the
+// accumulator 16 TMEM columns.
+//   work items: GEMM1 (expert j, 128 W13 rows = 64 gate + 64 up rows of 64
+//   features) -> H1 = SiLU(gate) * up; GEMM2 (expert j, 128 W2 rows = 128 output
+//   columns) after all of expert j's GEMM1 items (per-expert done counters,
+//   release/acquire).  CTAs [0, n1) take one GEMM1 item each when n1 < grid and
+//   the rest share the GEMM2 items (their TMA rings fill with GEMM2 weights while
+//   the GEMM1 CTAs run); otherwise items go round-robin in list order (GEMM1
+//   first), so a CTA never waits on an item queued behind its own.
+// Roles: warp 0 = TMA producer (runs ahead across items), warps 1-4 = B staging,
+// the MMA issuer (warp 1 lane 0) and the epilogue (TMEM lane quarter = warp % 4).
+// a ring stage holds kDecKQ consecutive 64-column k-blocks of the tile's 128 rows, loaded by ONE
+// 4-D TMA box so each weight row's kDecKQ x 128 B are requested together (DRAM page locality)
+#ifndef VMM_DEC_KQ
+#define VMM_DEC_KQ 2
+#endif
+constexpr int kDecKQ = VMM_DEC_KQ;
+constexpr int kDecStages = 8 / kDecKQ, kDecThreads = 160, kDecN = 16;
+constexpr uint32_t kDecTile = 128 * BK * 2 * kDecKQ;  // A stage: kDecKQ x 16 KB
+constexpr int kDecMaxK = 2048;               // B staging: 16 rows x K <= 2048 (64 KB)
+constexpr size_t kDecSmem = (size_t)kDecStages * kDecTile + (size_t)kDecN * kDecMaxK * 2 + 64 * kDecN * 4 + 1024 + 256;
+
+struct DecItem {
+  bool g2;
+  int j, t;
+};
+__device__ __forceinline__ DecItem dec_item(int item, int n1, int per1, int per2) {
+  DecItem d;
+  d.g2 = item >= n1;
+  const int i = d.g2 ? item - n1 : item;
+  const int per = d.g2 ? per2 : per1;
+  d.j = i / per;
+  d.t = i - d.j * per;
+  return d;
+}
+// k-th item of CTA b (-1 when none): split assignment when the GEMM1 items do not fill the grid
+__device__ __forceinline__ int dec_cta_item(int b, int k, int G, int n1, int nt) {
+  if (n1 < G && nt > n1) {
+    if (b < n1) return k == 0 ? b : -1;
+    const int i = n1 + (b - n1) + k * (G - n1);
+    return i < nt ? i : -1;
+  }
+  const int i = b + k * G;
+  return i < nt ? i : -1;
+}
+
+__global__ void __launch_bounds__(kDecThreads, 1)
+decode_tc_kernel(const __grid_constant__ CUtensorMap map_w13, const __grid_constant__ CUtensorMap map_w2,
+                 const __nv_bfloat16 *__restrict__ xp, const int32_t *__restrict__ offsets, int E,
+                 const int32_t *__restrict__ slot_of, int H, int I, const uint32_t *need, const uint32_t *ready,
+                 int ready_base, uint32_t *done, __nv_bfloat16 *h1, __nv_bfloat16 *__restrict__ y,
+                 const __nv_bfloat16 *w13b, const __nv_bfloat16 *w2b, long long stride) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char *ring = smem;
+  unsigned char *bst = ring + kDecStages * kDecTile;                       // B staging (SW128 per k-block)
+  float *s_gate = reinterpret_cast<float *>(bst + (size_t)kDecN * kDecMaxK * 2);  // [64][16]
+  uint64_t *full = reinterpret_cast<uint64_t *>(s_gate + 64 * kDecN);
+  uint64_t *empty = full + kDecStages;
+  uint64_t *tfull = empty + kDecStages;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tfull + 1);
+  __shared__ int s_act[kSkinnyRows], s_r0[kSkinnyRows], s_r1[kSkinnyRows];
+  __shared__ int s_nact;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {  // active experts in ascending id order
+    int seen = 0;
+    for (int c0 = 0; c0 < E; c0 += 32) {
+      const int e = c0 + lane;
+      const bool act = e < E && offsets[e + 1] > offsets[e];
+      const unsigned bal = __ballot_sync(0xffffffffu, act);
+      if (act) {
+        const int j = seen + __popc(bal & ((1u << lane) - 1u));
+        if (j < kSkinnyRows) {
+          s_act[j] = e;
+          s_r0[j] = offsets[e];
+          s_r1[j] = offsets[e + 1];
+        }
+      }
+      seen += __popc(bal);
+    }
+    if (lane == 0) {
+      s_nact = seen < kSkinnyRows ? seen : kSkinnyRows;
+      prefetch_tmap(&map_w13);
+      prefetch_tmap(&map_w2);
+      for (int s = 0; s < kDecStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+      mbar_init(tfull, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(32));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int nact = s_nact;
+  const int per1 = (2 * I) / 128, per2 = H / 128;
+  const int n1 = nact * per1, nt = n1 + nact * per2;
+  const int G = gridDim.x, b = blockIdx.x;
+  if (warp == 0) {
+    if (lane == 0) {  // producer: every item's weight tiles through the ring
+      // first, bulk L2 prefetches of ALL of this CTA's weight tiles (each a contiguous range of
+      // 128 weight rows): DRAM streams them in large contiguous pieces while the ring's strided
+      // 128-byte box rows then mostly hit L2.  Experts still in flight are skipped.
+      for (int k = 0;; ++k) {
+        const int item = dec_cta_item(b, k, G, n1, nt);
+        if (item < 0) break;
+        const DecItem d = dec_item(item, n1, per1, per2);
+        const int e = s_act[d.j];
+        if (need && need[e]) continue;
+        const long long K = d.g2 ? I : H;
+        const char *base = reinterpret_cast<const char *>(d.g2 ? w2b : w13b) + (long long)slot_of[e] * stride * 2 +
+                           (long long)d.t * 128 * K * 2;
+        const long long bytes = 128 * K * 2;
+        for (long long off = 0; off < bytes; off += 65536) {
+          const unsigned n = (unsigned)(bytes - off < 65536 ? bytes - off : 65536);
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + off), "r"(n) : "memory");
+        }
+      }
+      int it = 0;
+      for (int k = 0;; ++k) {
+        const int item = dec_cta_item(b, k, G, n1, nt);
+        if (item < 0) break;
+        const DecItem d = dec_item(item, n1, per1, per2);
+        const int e = s_act[d.j];
+        if (need && need[e]) {
+          wait_at_least(ready + (slot_of[e] - ready_base), need[e], 128);
+          fence_proxy_async_global();
+        }
+        const CUtensorMap *map = d.g2 ? &map_w2 : &map_w13;
+        const int nk = (d.g2 ? I : H) / (BK * kDecKQ);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % kDecStages;
+          if (it >= kDecStages) mbar_wait_watchdog(&empty[s], ((it / kDecStages) - 1) & 1);
+          mbar_expect_tx(&full[s], kDecTile);
+          tma_load_4d(map, &full[s], ring + s * kDecTile, 0, d.t * 128, kb * kDecKQ, slot_of[e]);
+        }
+      }
+    }
+  } else {
+    const int gt = threadIdx.x - 32;  // 0..127
+    const int wq = warp & 3;          // TMEM lane quarter this warp may read
+    int it = 0;
+    for (int k = 0;; ++k) {
+      const int item = dec_cta_item(b, k, G, n1, nt);
+      if (item < 0) break;
+      const DecItem d = dec_item(item, n1, per1, per2);
+      const int r0 = s_r0[d.j], ne = s_r1[d.j] - s_r0[d.j];
+      const int K = d.g2 ? I : H, nkb = K / BK;
+      if (d.g2) {  // every GEMM1 item of this expert has published its H1 columns
+        if (gt == 0) wait_at_least(done + d.j, (uint32_t)per1, 64);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+      // B: the expert's rows (zero-padded to 16), one SW128 K-major 16 x 64 block per k-block
+      const uint4 *src = reinterpret_cast<const uint4 *>(d.g2 ? h1 : xp);
+      const int rv = K / 8;
+      for (int idx = gt; idx < kDecN * rv; idx += 128) {
+        const int r = idx / rv, cc = idx - r * rv;  // row, 16-byte chunk along K
+        const int kb = cc >> 3, c = cc & 7;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (r < ne) v = d.g2 ? __ldcg(src + (long long)(r0 + r) * rv + cc) : __ldg(src + (long long)(r0 + r) * rv + cc);
+        *reinterpret_cast<uint4 *>(bst + kb * (kDecN * 128) + r * 128 + ((c ^ (r & 7)) << 4)) = v;
+      }
+      fence_proxy_async_smem();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (gt == 0) {  // MMA issuer
+        tc_fence_after();
+        for (int ks = 0; ks < nkb / kDecKQ; ++ks, ++it) {
+          const int s = it % kDecStages;
+          mbar_wait_watchdog(&full[s], (it / kDecStages) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int q = 0; q < kDecKQ; ++q) {
+            const int kb = ks * kDecKQ + q;
+            const uint32_t a_addr = smem_u32(ring + s * kDecTile + q * (128 * BK * 2));
+            const uint32_t b_addr = smem_u32(bst + kb * (kDecN * 128));
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk)
+              umma_bf16(tmem, sw128_desc(a_addr + kk * 32), sw128_desc(b_addr + kk * 32), idesc_bf16(128, kDecN),
+                        (kb | kk) != 0);
+          }
+          umma_commit(&empty[s]);
+        }
+        umma_commit(tfull);
+      }
+      mbar_wait_watchdog(tfull, k & 1);
+      tc_fence_after();
+      uint32_t v[16];
+      tmem_ld16_nowait(tmem + ((uint32_t)(32 * wq) << 16), v);
+      tmem_wait_ld();
+      const int row = 32 * wq + lane;  // weight row within the tile
+      if (!d.g2) {
+        if (row < 64)
+#pragma unroll
+          for (int n = 0; n < kDecN; ++n) s_gate[row * kDecN + n] = __uint_as_float(v[n]);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (row >= 64) {
+          const int f = d.t * 64 + row - 64;
+          for (int n = 0; n < ne; ++n)
+            h1[(long long)(r0 + n) * I + f] =
+                __float2bfloat16(silu(s_gate[(row - 64) * kDecN + n]) * __uint_as_float(v[n]));
+        }
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (gt == 0) red_release_add(done + d.j, 1u);
+      } else {
+        const int col = d.t * 128 + row;
+        for (int n = 0; n < ne; ++n) y[(long long)(r0 + n) * H + col] = __float2bfloat16(__uint_as_float(v[n]));
+      }
+      tc_fence_before();
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // TMEM, B staging and s_gate free for the next item
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(32));
+  }
+}
+
 // ---- CUDA-core cross-check path -------------------------------------------
 __device__ __forceinline__ int expert_of_row(const int32_t *offsets, int E, int row) {
   int lo = 0, hi = E - 1;
@@ -1199,6 +1431,59 @@ static int skinny_launch(const void *d_xp, const int32_t *d_offsets, int E, int 
   return VMM_OK;
 }
 
+// decode-sized layer on the tensor cores; returns 1 (nothing launched) when the shape does not fit
+static int decode_tc_launch(const void *d_xp, const int32_t *d_offsets, int E, int M_total, int H, int I,
+                            const void *d_w13, const void *d_w2, long long stride, long long n_slots,
+                            const int32_t *d_slot_of, const uint32_t *d_need, const uint32_t *d_ready, int ready_base,
+                            void *d_h1, void *d_y, void *stream) {
+  // opt-in (VMM_DECODE_TC=1, read per call): measured slower than the CUDA-core kernel at C3
+  // decode sizes (43 vs 39 us for 8 experts): per-SM TMA streaming of 128-byte box rows tops
+  // out near 30-40 GB/s and only the GEMM1 items' SMs stream during GEMM1
+  const bool tc = std::getenv("VMM_DECODE_TC") != nullptr;
+  if (!tc || H % 128 || I % 64 || H > kDecMaxK || I > kDecMaxK || M_total > kSkinnyRows || stride % 8) return 1;
+  static uint32_t *done_tab[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return vmm::fail(VMM_ECUDA, "device index out of range");
+  if (!done_tab[dev]) {
+    cudaError_t e = cudaMalloc(&done_tab[dev], sizeof(uint32_t) * kSkinnyRows);
+    if (e != cudaSuccess) return vmm::cuda_status(e, "decode FFN counters");
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(decode_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDecSmem);
+    if (e != cudaSuccess) return vmm::cuda_status(e, "decode FFN attr");
+    attr = true;
+  }
+  CUtensorMap mw13, mw2;
+  int st;
+  // 4-D views {64 columns, rows, K / 64 column blocks, slots}: a box {64, 128, kDecKQ, 1} lands as
+  // kDecKQ SW128 k-block tiles of 128 rows, one after the other
+  if ((H / BK) % kDecKQ || (I / BK) % kDecKQ) return 1;
+  {
+    uint64_t dims[4] = {(uint64_t)BK, (uint64_t)2 * I, (uint64_t)H / BK, (uint64_t)n_slots};
+    uint64_t str[3] = {(uint64_t)H * 2, (uint64_t)BK * 2, (uint64_t)stride * 2};
+    uint32_t box[4] = {BK, 128, (uint32_t)kDecKQ, 1};
+    if ((st = make_map(&mw13, d_w13, 4, dims, str, box))) return st;
+  }
+  {
+    uint64_t dims[4] = {(uint64_t)BK, (uint64_t)H, (uint64_t)I / BK, (uint64_t)n_slots};
+    uint64_t str[3] = {(uint64_t)I * 2, (uint64_t)BK * 2, (uint64_t)stride * 2};
+    uint32_t box[4] = {BK, 128, (uint32_t)kDecKQ, 1};
+    if ((st = make_map(&mw2, d_w2, 4, dims, str, box))) return st;
+  }
+  if (!g_num_sms) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t ce = cudaMemsetAsync(done_tab[dev], 0, sizeof(uint32_t) * kSkinnyRows, s);
+  if (ce != cudaSuccess) return vmm::cuda_status(ce, "decode FFN counters memset");
+  decode_tc_kernel<<<g_num_sms, kDecThreads, kDecSmem, s>>>(
+      mw13, mw2, (const __nv_bfloat16 *)d_xp, d_offsets, E, d_slot_of, H, I, d_need, d_ready, ready_base,
+      done_tab[dev], (__nv_bfloat16 *)d_h1, (__nv_bfloat16 *)d_y, (const __nv_bfloat16 *)d_w13,
+      (const __nv_bfloat16 *)d_w2, stride);
+  VMM_LAUNCH_CHECK("decode_tc_kernel");
+  return VMM_OK;
+}
+
 extern "C" int vmm_grouped_swiglu(const void *d_xp, const int32_t *d_offsets, int E, int M_total, int H, int I,
                                   const void *d_w13_arena, const void *d_w2_arena, long long slot_stride,
                                   long long n_slots, const int32_t *d_slot_of_expert, void *d_h1, void *d_y,
@@ -1209,6 +1494,9 @@ extern "C" int vmm_grouped_swiglu(const void *d_xp, const int32_t *d_offsets, in
   if (E < 1 || E > VMM_MAX_EXPERTS) return vmm::fail(VMM_EVALIDATION, "experts must lie in [1, 256]");
   if (slot_stride % 8) return vmm::fail(VMM_EVALIDATION, "slot stride must be a multiple of 8 elements");
   if (M_total <= kSkinnyRows) {  // decode-sized layer: every expert has <= 16 rows
+    const int r = decode_tc_launch(d_xp, d_offsets, E, M_total, H, I, d_w13_arena, d_w2_arena, slot_stride, n_slots,
+                                   d_slot_of_expert, nullptr, nullptr, 0, d_h1, d_y, stream);
+    if (r != 1) return r;
     return skinny_launch(d_xp, d_offsets, E, M_total, H, I, d_w13_arena, d_w2_arena, slot_stride, d_slot_of_expert,
                          nullptr, nullptr, 0, d_h1, d_y, stream);
   }
@@ -1278,6 +1566,9 @@ extern "C" int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offse
   if (M_total <= kSkinnyRows) {  // decode-sized: persistent weight-streaming kernel (waits on flags too)
     if (d_src_row) return vmm::fail(VMM_ECONTRACT, "row gather needs the tensor-core path (M > 16)");
     if (d_need && !d_ready) return vmm::fail(VMM_ECONTRACT, "need[] without ready flags");
+    const int r = decode_tc_launch(d_xp, d_offsets, E, M_total, H, I, d_w13_arena, d_w2_arena, slot_stride, n_slots,
+                                   d_slot_of_expert, d_need, d_ready, ready_base, d_h1, d_y, stream);
+    if (r != 1) return r;
     return skinny_launch(d_xp, d_offsets, E, M_total, H, I, d_w13_arena, d_w2_arena, slot_stride, d_slot_of_expert,
                          d_need, d_ready, ready_base, d_h1, d_y, stream);
   }

@@ -152,6 +152,14 @@ def test_decode_sized_swiglu_matches_fp32_restatement(shape):
     _check_swiglu(shape)
 
 
+@pytest.mark.parametrize("shape", [(1, 2048, 768, 128, 8), (2, 2048, 768, 128, 8), (2, 1024, 512, 16, 8),
+                                   (1, 2048, 1408, 64, 6)])
+def test_decode_sized_tensor_core_swiglu_matches_fp32_restatement(shape, monkeypatch):
+    """Opt-in swap-AB tcgen05 decode FFN (TMA weight ring, per-expert H1 counters)."""
+    monkeypatch.setenv("VMM_DECODE_TC", "1")
+    _check_swiglu(shape)
+
+
 def _check_swiglu(shape):
     N, H, I, E, k = shape
     n_slots = E + 3
