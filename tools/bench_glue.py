@@ -27,6 +27,8 @@ xn = torch.empty_like(x)
 bufs = (torch.empty(E + 1, dtype=torch.int32, device=dev), torch.empty(N * k, dtype=torch.int32, device=dev),
         torch.empty(N * k, dtype=torch.int32, device=dev))
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+wr = (torch.randn(E, H, device=dev) / H ** 0.5).to(torch.bfloat16)
+cnt = torch.zeros(E, dtype=torch.int32, device=dev)
 
 
 def cuda_ms(fn, reps=10):
@@ -53,6 +55,7 @@ cases = {
     "permute_rows": (lambda: kernels.permute_rows(x, src, M, out=xp), 2 * M * row),
     "combine": (lambda: kernels.combine(y, pos.view(N, k), gates, x, out=out), M * row + 2 * N * row),
     "rmsnorm": (lambda: kernels.rmsnorm(out, out=xn), 2 * N * row),
+    "route": (lambda: kernels.route_topk(xn, wr, k, counts=cnt), N * row + E * row + N * k * 8),
 }
 only = os.environ.get("GLUE_ONLY")
 for name, (fn, bytes_) in cases.items():
