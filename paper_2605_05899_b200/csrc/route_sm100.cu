@@ -22,12 +22,15 @@ namespace {
 using namespace sm100;
 
 constexpr int BM = 128, BK = 64;
-// plain router (NG = 1): 3 x 32 KB stages so two CTAs share an SM (one's epilogue overlaps the
-// other's loads: 0.44 -> 0.32 ms at 311k rows); the fused lookahead variant (NG = 2, 48 KB stages)
-// keeps 4 stages at one CTA per SM
+// Stages sized so two CTAs share an SM (one's epilogue overlaps the other's loads): plain
+// router (NG = 1) 3 x 32 KB, 0.44 -> 0.32 ms at 311k rows; fused lookahead (NG = 2) 2 x 48 KB,
+// 0.43 -> 0.39 ms (4 stages at one CTA per SM before)
+#ifndef VMM_ROUTE_LA_STAGES
+#define VMM_ROUTE_LA_STAGES 2
+#endif
 template <int NG>
 struct RouteStages {
-  static constexpr int value = NG == 1 ? 3 : 4;
+  static constexpr int value = NG == 1 ? 3 : VMM_ROUTE_LA_STAGES;
 };
 constexpr int kMaxK = 8;
 
@@ -101,7 +104,7 @@ __device__ __forceinline__ void epilogue(uint32_t t_base, int gate, int row, boo
 }
 
 template <int EG, int NG, int K>
-__global__ void __launch_bounds__(RouteCfg<EG, NG>::kThreads, NG == 1 ? 2 : 1)
+__global__ void __launch_bounds__(RouteCfg<EG, NG>::kThreads, RouteCfg<EG, NG>::kStages <= 2 || NG == 1 ? 2 : 1)
 route_sm100_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w, int w_row0,
                    int N, int Kdim, int E, int32_t *__restrict__ ids, float *__restrict__ gates,
                    float *__restrict__ logits_out, uint32_t *__restrict__ counts, uint32_t *__restrict__ la_counts) {

@@ -29,6 +29,8 @@ bufs = (torch.empty(E + 1, dtype=torch.int32, device=dev), torch.empty(N * k, dt
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 wr = (torch.randn(E, H, device=dev) / H ** 0.5).to(torch.bfloat16)
 cnt = torch.zeros(E, dtype=torch.int32, device=dev)
+cnt2 = torch.zeros(E, dtype=torch.int32, device=dev)
+wr2 = (torch.randn(2, E, H, device=dev) / H ** 0.5).to(torch.bfloat16)
 
 
 def cuda_ms(fn, reps=10):
@@ -56,6 +58,7 @@ cases = {
     "combine": (lambda: kernels.combine(y, pos.view(N, k), gates, x, out=out), M * row + 2 * N * row),
     "rmsnorm": (lambda: kernels.rmsnorm(out, out=xn), 2 * N * row),
     "route": (lambda: kernels.route_topk(xn, wr, k, counts=cnt), N * row + E * row + N * k * 8),
+    "route_lookahead": (lambda: kernels.route_lookahead(xn, wr2, 0, k, cnt, cnt2), N * row + 2 * E * row + N * k * 8),
 }
 only = os.environ.get("GLUE_ONLY")
 for name, (fn, bytes_) in cases.items():
