@@ -111,21 +111,22 @@ __device__ __forceinline__ void combine_chunk(const uint4 *__restrict__ y, const
                                               const uint4 *__restrict__ ys, int S, int N, float (&acc)[8]) {
 #pragma unroll
   for (int q = 0; q < 8; ++q) acc[q] = 0.f;
-  for (int j0 = 0; j0 < k; j0 += 8) {
-    int pj[8];
-    float gj[8];
-    uint4 v[8];
+  constexpr int kJ = 4;  // picks per pass (4 rows x 16 B in flight; keeps the kernel at <= 64 registers)
+  for (int j0 = 0; j0 < k; j0 += kJ) {
+    int pj[kJ];
+    float gj[kJ];
+    uint4 v[kJ];
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
+    for (int j = 0; j < kJ; ++j)
       if (j0 + j < k) {
         pj[j] = __ldg(pos + (long long)t * k + j0 + j);
         gj[j] = __ldg(gates + (long long)t * k + j0 + j);
       }
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
+    for (int j = 0; j < kJ; ++j)
       if (j0 + j < k) v[j] = __ldg(y + (long long)pj[j] * row_vec + c);
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
+    for (int j = 0; j < kJ; ++j)
       if (j0 + j < k) {
         const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&v[j]);
 #pragma unroll
@@ -141,7 +142,7 @@ __device__ __forceinline__ void combine_chunk(const uint4 *__restrict__ y, const
 }
 
 // out[t] = resid[t] + sum_j gates[t,j] * Y[pos[t,j]]; each thread owns 8 columns
-__global__ void combine_kernel(const uint4 *__restrict__ y, const int32_t *__restrict__ pos,
+__global__ void __launch_bounds__(256, 4) combine_kernel(const uint4 *__restrict__ y, const int32_t *__restrict__ pos,
                                const float *__restrict__ gates, const uint4 *__restrict__ resid, int N, int k,
                                int row_vec, uint4 *__restrict__ out, const uint4 *__restrict__ ys, int S) {
   long long total = (long long)N * row_vec;
