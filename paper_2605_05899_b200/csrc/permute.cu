@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(kPT) plan_scatter_kernel(const int32_t *__rest
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const int c = c0v + lane + 32 * u;
-            if (c < row_vec) xp[(long long)pj * row_vec + c] = v[u];
+            if (c < row_vec) __stcs(xp + (long long)pj * row_vec + c, v[u]);  // streaming: the FFN reads it once, much later
           }
         }
         cur_t = t;
