@@ -30,6 +30,8 @@ import ctypes as C
 import math
 from dataclasses import dataclass, field, replace
 
+import os
+
 import numpy as np
 import torch
 
@@ -451,7 +453,7 @@ class MoEStack:
         x_ctx = None
         cur = x
         offs_req = [0, T] if req_off is None else [int(v) for v in req_off]
-        if lp and not x_ready and len(offs_req) > 2 and T >= 16384:
+        if lp and not x_ready and len(offs_req) > 2 and T >= 16384 and not os.environ.get("VMM_PREFIX_ONE_STREAM"):
             # two request-aligned halves on two streams: one half's memory-bound kernels
             # (combine, permute, route) overlap the other half's tensor-core FFN
             mid = min(offs_req[1:-1], key=lambda v: abs(2 * v - T))
