@@ -367,8 +367,12 @@ ffn_fused_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
       const TileInfo ti = tile_info(f.m_tile * n1, n1, s_tile_base, s_offs, s_slots, E);
       if (lane == 0) {
         const uint32_t nd = s_need[ti.expert];
-        // the expert's slot fill must have landed (copy stream -> ready flag)
-        if (nd) wait_at_least(ready + (ti.slot - ready_base), nd, 256);
+        // the expert's slot fill must have landed (copy stream -> ready flag); once seen, the
+        // expert's later tiles skip the flag load (only this thread reads s_need)
+        if (nd) {
+          wait_at_least(ready + (ti.slot - ready_base), nd, 256);
+          s_need[ti.expert] = 0u;
+        }
         // GEMM2: H1 rows of this m-tile complete (all GEMM1 n-tiles stored)
         if (f.gemm2) wait_at_least(done + f.m_tile, 4u * (uint32_t)n1, 64);
         if (nd || f.gemm2) fence_proxy_async_global();
@@ -635,7 +639,10 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
         const uint32_t nd = s_need[ti.expert];
         {
           PROF_T0();
-          if (nd) wait_at_least(ready + (ti.slot - ready_base), nd, 256);
+          if (nd) {  // once seen, the expert's later tiles skip the flag load (only this thread reads s_need)
+            wait_at_least(ready + (ti.slot - ready_base), nd, 256);
+            s_need[ti.expert] = 0u;
+          }
 #ifdef VMM_FFN_PROF
           if (f.gemm2) {
             const uint32_t v0 = ld_acquire_u32(done + f.m_tile);

@@ -65,3 +65,7 @@ if cm and len(cm) // 3 == len(prof):
     print(f"FFN end after its demand copies done: mean {np.mean(tail):.2f} ms; FFN start after copies start: "
           f"mean {np.mean(lead):.2f} ms")
     print("per-layer tail:", [round(v, 2) for v in tail])
+if cm and len(cm) // 3 == len(prof):
+    post = [prof[i][1].elapsed_time(cm[3 * (i + 1)]) for i in range(len(prof) - 1)]
+    print(f"FFN(l) end -> layer l+1 copies start: mean {np.mean(post):.2f} ms (first-chunk combine/norm/route, "
+          f"D2H, host decision, issue)")
