@@ -54,6 +54,7 @@ int vmm_gather_i32(const int32_t *d_src, const int32_t *d_rows, int n, int width
 int vmm_gather_f32(const float *d_src, const int32_t *d_rows, int n, int width, float *d_dst, void *stream);
 const uint32_t *vmm_xfer_ready(vmm_xfer *x);
 void *vmm_xfer_stream(vmm_xfer *x);
+int vmm_xfer_mark(vmm_xfer *x, void *ev);
 int vmm_xfer_need(vmm_xfer *x, const int32_t *h_slabs, int n, uint32_t *h_need);
 }
 
@@ -333,13 +334,11 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
       }
       VMM_TRY(vmm_engine_layer(eng, l, demand.data(), (int)demand.size(), phase, step, nullptr));
       if (out && out->copy_marks)
-        VMM_CUDA(cudaEventRecord((cudaEvent_t)out->copy_marks[3 * (l - l0)], (cudaStream_t)vmm_xfer_stream(xf)),
-                 "copy mark");
+        VMM_TRY(vmm_xfer_mark(xf, out->copy_marks[3 * (l - l0)]));
       VMM_TRY(vmm_xfer_issue_engine(xf, eng, d.pool, d.host_layers, E, d.arena, d.n_pinned_slots, d.slot_bytes, &n));
       copies += n;
       if (out && out->copy_marks)
-        VMM_CUDA(cudaEventRecord((cudaEvent_t)out->copy_marks[3 * (l - l0) + 1], (cudaStream_t)vmm_xfer_stream(xf)),
-                 "copy mark");
+        VMM_TRY(vmm_xfer_mark(xf, out->copy_marks[3 * (l - l0) + 1]));
     }
     const int32_t *slot_of;
     const uint32_t *need_of = nullptr;
@@ -437,8 +436,7 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
       copies += n;
     }
     if (out && out->copy_marks && !pinned_only)
-      VMM_CUDA(cudaEventRecord((cudaEvent_t)out->copy_marks[3 * (l - l0) + 2], (cudaStream_t)vmm_xfer_stream(xf)),
-               "copy mark");
+      VMM_TRY(vmm_xfer_mark(xf, out->copy_marks[3 * (l - l0) + 2]));
   }
   if (out) {
     out->host_us[0] = t_pre;
