@@ -446,6 +446,13 @@ class MoEStack:
         L, E, k, lp = c.layers, c.experts, c.k, c.l_pinned
         dev = self.device
         T = int(x.shape[0])
+        # The last prefix layer's FFN only matters for the tokens the prune keeps: route it on
+        # every token (its routes feed the prune), run its experts on the retained rows only
+        # (row-independent GEMMs: the retained rows come out bit-identical).  Live routing
+        # without shared experts; VMM_PREFIX_FULL_LAST=1 runs it on every token.
+        skip_last = lp >= 1 and c.routing == "live" and c.shared_experts == 0 and \
+            not os.environ.get("VMM_PREFIX_FULL_LAST")
+        lpe = lp - 1 if skip_last else lp  # prefix layers run in full on all tokens
         # --- pinned prefix: all prefill tokens, resident experts, no cache decisions:
         # the native executor in engine-less mode (no host sync inside the prefix)
         prefix = torch.empty((max(lp, 1), T, k), dtype=torch.int32, device=dev)
@@ -453,12 +460,12 @@ class MoEStack:
         x_ctx = None
         cur = x
         offs_req = [0, T] if req_off is None else [int(v) for v in req_off]
-        if lp and not x_ready and len(offs_req) > 2 and T >= 16384 and not os.environ.get("VMM_PREFIX_ONE_STREAM"):
+        if lpe and not x_ready and len(offs_req) > 2 and T >= 16384 and not os.environ.get("VMM_PREFIX_ONE_STREAM"):
             # two request-aligned halves on two streams: one half's memory-bound kernels
             # (combine, permute, route) overlap the other half's tensor-core FFN
             mid = min(offs_req[1:-1], key=lambda v: abs(2 * v - T))
             x_ready = [(mid, None), (T, None)]
-        if lp and x_ready:
+        if lpe and x_ready:
             # chunk by chunk (as the rows land, or the two halves), alternating over two streams
             if self._pbufs.get("n", 0) < T:
                 self._pbufs = dict(n=T, cur=torch.empty_like(x), xn=torch.empty_like(x))
@@ -477,7 +484,7 @@ class MoEStack:
             if not two:
                 caps = [max(b - a for a, b, _ in bounds), 0]
             base = [0, caps[0]]
-            counts_lane = [torch.zeros((lp, E), dtype=torch.int32, device=dev) for _ in range(2)]
+            counts_lane = [torch.zeros((lpe, E), dtype=torch.int32, device=dev) for _ in range(2)]
             for sp_ in self._pstreams:
                 sp_.wait_stream(main)
             for i, (r0, r1, ev) in enumerate(bounds):
@@ -489,26 +496,41 @@ class MoEStack:
                 with torch.cuda.stream(side):
                     if ev is not None:
                         side.wait_event(ev)
-                    routes_c = torch.empty((lp, n, k), dtype=torch.int32, device=dev)
-                    counts_c = torch.zeros((lp, E), dtype=torch.int32, device=dev)
+                    routes_c = torch.empty((lpe, n, k), dtype=torch.int32, device=dev)
+                    counts_c = torch.zeros((lpe, E), dtype=torch.int32, device=dev)
                     rows_c = torch.arange(r0, r1, dtype=torch.int32, device=dev) if c.routing == "trace" else None
-                    out_c, _, _ = self._native_layers(None, x[r0:r1], n, 0, lp, 0, -1, rows=rows_c, counts=counts_c,
+                    out_c, _, _ = self._native_layers(None, x[r0:r1], n, 0, lpe, 0, -1, rows=rows_c, counts=counts_c,
                                                       trace=trace, record_into=routes_c,
                                                       region=(base[lane], caps[lane], lane))
                     cur_full[r0:r1].copy_(out_c)
                     if c.predictor == "gate":  # the boot emission's context rows (layer lp-1 input)
                         xn_full[r0:r1].copy_(bufs["xn"][base[lane]:base[lane] + n])
-                    prefix[:lp, r0:r1].copy_(routes_c)
+                    prefix[:lpe, r0:r1].copy_(routes_c)
                     counts_lane[lane] += counts_c
             for sp_ in self._pstreams:
                 main.wait_stream(sp_)
-            counts_pre[:lp] += counts_lane[0] + counts_lane[1]
+            counts_pre[:lpe] += counts_lane[0] + counts_lane[1]
             cur, x_ctx = cur_full, xn_full
-        elif lp:
+        elif lpe:
             rows_all = torch.arange(T, dtype=torch.int32, device=dev) if c.routing == "trace" else None
-            cur, _, _ = self._native_layers(None, x, T, 0, lp, 0, -1, rows=rows_all, counts=counts_pre, trace=trace,
-                                            record_into=prefix[:lp])
+            cur, _, _ = self._native_layers(None, x, T, 0, lpe, 0, -1, rows=rows_all, counts=counts_pre, trace=trace,
+                                            record_into=prefix[:lpe])
             x_ctx = bufs["xn"][:T]  # normalised input of layer lp-1: context of the boot emission (gate predictor)
+        if x_ready and not lpe:  # no full prefix layer ran: the rows must have landed before layer lp-1
+            main = torch.cuda.current_stream()
+            for _, ev in x_ready:
+                if ev is not None:
+                    main.wait_event(ev)
+        last = None
+        if skip_last:  # layer lp-1: RMSNorm + router on every token (the prune needs its routes)
+            l = lp - 1
+            xn_l = kernels.rmsnorm(cur, out=bufs["xn"][:T])
+            ids_l, gates_l, _ = kernels.route_topk(xn_l, self.store.router[l], k, counts=counts_pre[l],
+                                                   ids=bufs["ids"][:T], gates=bufs["gates"][:T])
+            prefix[l].copy_(ids_l)
+            x_ctx = xn_l  # normalised input of layer lp-1: context of the boot emission (gate predictor)
+            last = (cur, xn_l, ids_l, gates_l)
+
 
         # --- prune (token compression) on the prefix routes, one CTA per request
         offs = [0, T] if req_off is None else [int(v) for v in req_off]
@@ -534,8 +556,22 @@ class MoEStack:
             ret = (pr["retained"][:T] + starts[seg])[valid]
         n_r = int(ret.shape[0])
         ret_off = np.concatenate([[0], np.cumsum(n_ret)]).astype(np.int64)
-        xr = kernels.gather_rows(cur, ret, out=bufs["xp"][:n_r])  # scratch until permute of layer lp
-        xr = xr.clone()
+        if last is None:
+            xr = kernels.gather_rows(cur, ret, out=bufs["xp"][:n_r])  # scratch until permute of layer lp
+            xr = xr.clone()
+        else:  # layer lp-1's experts on the retained rows only
+            cur_l, xn_l, ids_l, gates_l = last
+            rl = ret.long()
+            x_ret = kernels.gather_rows(cur_l, ret)
+            xn_ret = kernels.gather_rows(xn_l, ret)
+            ids_ret, gates_ret = ids_l[rl].contiguous(), gates_l[rl].contiguous()
+            M = n_r * k
+            off, src, pos, xp = kernels.permute(ids_ret, xn_ret, E, bufs=(bufs["off"], bufs["src"][:M], bufs["pos"][:M]),
+                                                out=bufs["xp"][:M])
+            _, y = kernels.grouped_swiglu(xp, off, self.store.arena, self.store.pinned_slot_of[lp - 1], c.inter,
+                                          h1=bufs["h1"][:M], y=bufs["y"][:M])
+            xr = kernels.combine(y, pos.view(n_r, k), gates_ret, x_ret)
+            cur = xr
         return cur, x_ctx, prefix, counts_pre, ret, n_r, ret_off, xr
 
 
