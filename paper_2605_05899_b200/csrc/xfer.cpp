@@ -128,6 +128,13 @@ int vmm_xfer_copy(vmm_xfer *x, int slab, const void *h_src, void *d_dst, size_t 
   const int k = x->stream2 ? (int)(x->fill_seq & 1) : 0;  // alternate the copy streams
   cudaStream_t st = k ? x->stream2 : x->stream;
   long long &waited = k ? x->copy_waited_read2 : x->copy_waited_read;
+  // write-after-write: a previous fill of this slab still in flight on the OTHER copy stream
+  // (a fill can be evicted and refilled before any layer reads it) must land first
+  const long long pf = x->slab_fill_seq[slab];
+  if (x->stream2 && pf > 0 && (int)((pf - 1) & 1) != k) {
+    if ((e = cudaStreamWaitEvent(st, x->fill_ev[(pf - 1) % kRing], 0)) != cudaSuccess)
+      return cuda_status(e, "copy wait previous fill");
+  }
   long long r = x->slab_read_seq[slab];
   if (r > waited) {  // write-after-read: the last layer that read this slab has finished
     if ((e = cudaStreamWaitEvent(st, x->read_ev[(r - 1) % kRing], 0)) != cudaSuccess)
