@@ -324,3 +324,30 @@ def test_decode_glue_bit_identical_to_separate_kernels(n, k, E, H, with_y):
     assert torch.equal(ids, ids_ref) and torch.equal(gates, gates_ref)
     assert torch.equal(off, off_ref[: E + 1]) and torch.equal(src, src_ref[:M]) and torch.equal(pos, pos_ref[:M])
     assert torch.equal(xp, xp_ref)
+
+
+def test_refill_of_a_slab_lands_last_across_copy_streams():
+    """Fills alternate over two copy streams; a slab filled twice with no reader in
+    between (evict + refill) must end with the second fill's bytes (write-after-write)."""
+    import ctypes as C
+
+    from paper_2605_05899_b200 import _lib
+
+    L = _lib.lib()
+    nbytes = 64 << 20
+    a = torch.full((nbytes,), 1, dtype=torch.uint8).pin_memory()
+    b = torch.full((nbytes,), 2, dtype=torch.uint8).pin_memory()
+    dst = torch.zeros(2, nbytes, dtype=torch.uint8, device="cuda")
+    xf = C.c_void_p()
+    _lib.check(L.vmm_xfer_create(2, nbytes, 1, C.byref(xf)))
+    try:
+        for _ in range(4):
+            # fill 2k+1 -> stream 0 (slab 0, bytes of a), fill 2k+2 -> stream 1 (slab 0 again, bytes of b)
+            _lib.check(L.vmm_xfer_copy(xf, 0, a.data_ptr(), dst[0].data_ptr(), nbytes, 0))
+            _lib.check(L.vmm_xfer_copy(xf, 0, b.data_ptr(), dst[0].data_ptr(), nbytes, 0))
+            _lib.check(L.vmm_xfer_sync(xf))
+            assert int(dst[0].min()) == 2 and int(dst[0].max()) == 2
+            dst.zero_()
+            torch.cuda.synchronize()
+    finally:
+        L.vmm_xfer_destroy(xf)
