@@ -3,10 +3,13 @@
 // Makes the reference's logical transfer channel (pkg/src/moesim/pipeline.py:
 // 440-494: one serial channel, issue order decided by the policy) real: every
 // decided issue becomes a cudaMemcpyAsync on a dedicated copy stream, followed
-// by an event and a ready-flag write.  Issues alternate over TWO copy streams
-// (VMM_COPY_STREAMS=1: one): the flag write's memory barrier stalls a stream
-// between copies, and a second stream keeps the PCIe link busy through the
-// stall (measured 52.6 -> 53.6 GB/s for back-to-back 9.44 MB copies).
+// by an event and a ready-flag write.  Issues go round-robin over several copy
+// streams -- 2 for the pinned host pool, 4 once HBM / NVLink sources are set
+// (VMM_COPY_STREAMS=N forces N): the flag write's memory barrier stalls a
+// stream between copies, and the other streams keep the link busy through the
+// stall (PCIe: 52.6 -> 53.6 GB/s for back-to-back 9.44 MB copies).  Per-slab
+// write-after-read and write-after-write waits keep every slab's fills and
+// readers ordered across the streams.
 //   * compute never reads a slab before its fill lands: vmm_xfer_fence makes
 //     the compute stream wait for the newest fill among the slabs a layer
 //     reads (FIFO => one wait covers all older fills);
@@ -54,13 +57,16 @@ WriteValue32Fn write_value_fn() {
 }  // namespace
 
 struct vmm_xfer {
-  cudaStream_t stream = nullptr;   // copy stream 0 (also the timing / marks stream)
-  cudaStream_t stream2 = nullptr;  // copy stream 1 (null: one stream)
-  long long copy_waited_read2 = 0;
-  long long last_fill[2] = {0, 0};  // fill sequence of the newest copy on each stream
+  cudaStream_t stream = nullptr;       // copy stream 0 (also the timing / marks stream)
+  static constexpr int kMaxCS = 4;
+  cudaStream_t cs[kMaxCS] = {};        // copy streams (cs[0] == stream)
+  int ncs = 1, nact = 1;               // created / in use (2 for the host pool, 4 for HBM/NVLink sources)
+  long long waited[kMaxCS] = {};       // newest reader event each copy stream already waits for
+  long long last_fill[kMaxCS] = {};    // fill sequence of the newest copy on each stream
+  std::vector<int8_t> slab_fill_stream;  // copy stream of each slab's newest fill
   std::vector<cudaEvent_t> fill_ev, read_ev;
   std::vector<long long> slab_fill_seq, slab_read_seq;
-  long long fill_seq = 0, read_seq = 0, copy_waited_read = 0;
+  long long fill_seq = 0, read_seq = 0;
   std::vector<int> pending_readers;
   double bytes = 0.0;
   long long copies = 0;
@@ -80,10 +86,14 @@ int vmm_xfer_create(int num_slabs, size_t slab_bytes, int max_layers, vmm_xfer *
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   cudaError_t e = cudaStreamCreateWithPriority(&x->stream, cudaStreamNonBlocking, prio_hi);
   if (e != cudaSuccess) { delete x; return cuda_status(e, "copy stream"); }
+  x->cs[0] = x->stream;
   const char *ns = std::getenv("VMM_COPY_STREAMS");
-  if (!(ns && std::atoi(ns) == 1)) {
-    e = cudaStreamCreateWithPriority(&x->stream2, cudaStreamNonBlocking, prio_hi);
-    if (e != cudaSuccess) { vmm_xfer_destroy(x); return cuda_status(e, "copy stream 2"); }
+  const int want = ns ? std::atoi(ns) : 0;  // 0: automatic (2, or 4 once peer/HBM sources are set)
+  x->ncs = want >= 1 ? (want > vmm_xfer::kMaxCS ? vmm_xfer::kMaxCS : want) : vmm_xfer::kMaxCS;
+  x->nact = want >= 1 ? x->ncs : 2;
+  for (int i = 1; i < x->ncs; ++i) {
+    e = cudaStreamCreateWithPriority(&x->cs[i], cudaStreamNonBlocking, prio_hi);
+    if (e != cudaSuccess) { vmm_xfer_destroy(x); return cuda_status(e, "copy stream"); }
   }
   x->fill_ev.resize(kRing);
   x->read_ev.resize(kRing);
@@ -95,6 +105,7 @@ int vmm_xfer_create(int num_slabs, size_t slab_bytes, int max_layers, vmm_xfer *
   if (e == cudaSuccess) e = cudaEventCreate(&x->t_last);
   if (e != cudaSuccess) { vmm_xfer_destroy(x); return cuda_status(e, "copy events"); }
   x->slab_fill_seq.assign(num_slabs, 0);
+  x->slab_fill_stream.assign(num_slabs, 0);
   x->slab_read_seq.assign(num_slabs, 0);
   if (write_value_fn() && num_slabs > 0) {
     if ((e = cudaMalloc(&x->ready, sizeof(uint32_t) * num_slabs)) != cudaSuccess ||
@@ -109,14 +120,14 @@ int vmm_xfer_create(int num_slabs, size_t slab_bytes, int max_layers, vmm_xfer *
 
 void vmm_xfer_destroy(vmm_xfer *x) {
   if (!x) return;
-  if (x->stream) cudaStreamSynchronize(x->stream);
-  if (x->stream2) cudaStreamSynchronize(x->stream2);
+  for (int i = 0; i < vmm_xfer::kMaxCS; ++i)
+    if (x->cs[i]) cudaStreamSynchronize(x->cs[i]);
   for (auto ev : x->fill_ev) if (ev) cudaEventDestroy(ev);
   for (auto ev : x->read_ev) if (ev) cudaEventDestroy(ev);
   if (x->t_first) cudaEventDestroy(x->t_first);
   if (x->t_last) cudaEventDestroy(x->t_last);
-  if (x->stream) cudaStreamDestroy(x->stream);
-  if (x->stream2) cudaStreamDestroy(x->stream2);
+  for (int i = 0; i < vmm_xfer::kMaxCS; ++i)
+    if (x->cs[i]) cudaStreamDestroy(x->cs[i]);
   if (x->ready) cudaFree(x->ready);
   delete x;
 }
@@ -125,13 +136,13 @@ int vmm_xfer_copy(vmm_xfer *x, int slab, const void *h_src, void *d_dst, size_t 
   (void)wait_layer;
   if (slab < 0 || slab >= (int)x->slab_fill_seq.size()) return vmm::fail(VMM_ECONTRACT, "slab out of range");
   cudaError_t e;
-  const int k = x->stream2 ? (int)(x->fill_seq & 1) : 0;  // alternate the copy streams
-  cudaStream_t st = k ? x->stream2 : x->stream;
-  long long &waited = k ? x->copy_waited_read2 : x->copy_waited_read;
+  const int k = (int)(x->fill_seq % x->nact);  // round-robin over the copy streams
+  cudaStream_t st = x->cs[k];
+  long long &waited = x->waited[k];
   // write-after-write: a previous fill of this slab still in flight on the OTHER copy stream
   // (a fill can be evicted and refilled before any layer reads it) must land first
   const long long pf = x->slab_fill_seq[slab];
-  if (x->stream2 && pf > 0 && (int)((pf - 1) & 1) != k) {
+  if (pf > 0 && x->slab_fill_stream[slab] != k) {
     if ((e = cudaStreamWaitEvent(st, x->fill_ev[(pf - 1) % kRing], 0)) != cudaSuccess)
       return cuda_status(e, "copy wait previous fill");
   }
@@ -154,6 +165,7 @@ int vmm_xfer_copy(vmm_xfer *x, int slab, const void *h_src, void *d_dst, size_t 
     return cuda_status(e, "fill event");
   x->last_fill[k] = x->fill_seq;
   x->slab_fill_seq[slab] = x->fill_seq;
+  x->slab_fill_stream[slab] = (int8_t)k;
   if (x->ready) {  // ordered after the copy, with a memory barrier: readers polling ready[] see the data
     CUresult r = write_value_fn()((CUstream)st, (CUdeviceptr)(x->ready + slab), (cuuint32_t)x->fill_seq, 0);
     if (r != CUDA_SUCCESS) return vmm::fail(VMM_ECUDA, "cuStreamWriteValue32 failed (" + std::to_string((int)r) + ")");
@@ -176,7 +188,7 @@ int vmm_xfer_fence(vmm_xfer *x, const int32_t *slabs, int n, void *compute_strea
     if (e != cudaSuccess) return cuda_status(e, "fence wait");
     // two copy streams: older fills may sit on the other stream -- also wait for its newest fill
     // (conservative: it may be younger than needed)
-    for (int k = 0; k < 2 && x->stream2; ++k) {
+    for (int k = 0; k < vmm_xfer::kMaxCS; ++k) {
       const long long f = x->last_fill[k];
       if (f > 0 && f != need) {
         e = cudaStreamWaitEvent((cudaStream_t)compute_stream, x->fill_ev[(f - 1) % kRing], 0);
@@ -213,7 +225,7 @@ int vmm_xfer_layer_done(vmm_xfer *x, int layer, void *compute_stream) {
 
 int vmm_xfer_join(vmm_xfer *x, void *compute_stream) {
   if (x->fill_seq == 0) return VMM_OK;
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < vmm_xfer::kMaxCS; ++k) {
     const long long f = x->last_fill[k];
     if (f <= 0) continue;
     cudaError_t e = cudaStreamWaitEvent((cudaStream_t)compute_stream, x->fill_ev[(f - 1) % kRing], 0);
@@ -223,8 +235,9 @@ int vmm_xfer_join(vmm_xfer *x, void *compute_stream) {
 }
 
 int vmm_xfer_sync(vmm_xfer *x) {
-  cudaError_t e = cudaStreamSynchronize(x->stream);
-  if (e == cudaSuccess && x->stream2) e = cudaStreamSynchronize(x->stream2);
+  cudaError_t e = cudaSuccess;
+  for (int i = 0; i < vmm_xfer::kMaxCS && e == cudaSuccess; ++i)
+    if (x->cs[i]) e = cudaStreamSynchronize(x->cs[i]);
   return cuda_status(e, "copy sync");
 }
 
@@ -233,8 +246,8 @@ int vmm_xfer_stats(vmm_xfer *x, double *bytes, double *busy_ms, long long *copie
   *copies = x->copies;
   *busy_ms = 0.0;
   if (x->timing_started) {
-    if (x->stream2 && x->last_fill[1] > 0)  // the window ends when both copy streams are done
-      cudaStreamWaitEvent(x->stream, x->fill_ev[(x->last_fill[1] - 1) % kRing], 0);
+    for (int i = 1; i < vmm_xfer::kMaxCS; ++i)  // the window ends when every copy stream is done
+      if (x->last_fill[i] > 0) cudaStreamWaitEvent(x->stream, x->fill_ev[(x->last_fill[i] - 1) % kRing], 0);
     cudaEventRecord(x->t_last, x->stream);
     cudaEventSynchronize(x->t_last);
     float ms = 0.f;
@@ -255,8 +268,9 @@ void *vmm_xfer_stream(vmm_xfer *x) { return (void *)x->stream; }
 
 // record `ev` once every copy issued so far has landed (diagnostic marks; joins stream 1 into stream 0)
 int vmm_xfer_mark(vmm_xfer *x, void *ev) {
-  if (x->stream2 && x->last_fill[1] > 0) {
-    cudaError_t e = cudaStreamWaitEvent(x->stream, x->fill_ev[(x->last_fill[1] - 1) % kRing], 0);
+  for (int i = 1; i < vmm_xfer::kMaxCS; ++i) {
+    if (x->last_fill[i] <= 0) continue;
+    cudaError_t e = cudaStreamWaitEvent(x->stream, x->fill_ev[(x->last_fill[i] - 1) % kRing], 0);
     if (e != cudaSuccess) return cuda_status(e, "mark join");
   }
   return cuda_status(cudaEventRecord((cudaEvent_t)ev, x->stream), "copy mark");
@@ -264,6 +278,8 @@ int vmm_xfer_mark(vmm_xfer *x, void *ev) {
 
 int vmm_xfer_set_sources(vmm_xfer *x, const void *const *h_table, long long n) {
   x->sources.assign(h_table, h_table + n);
+  // HBM / NVLink sources: the per-copy flag stall is a larger share of a ~10 us copy -> 4 streams
+  if (!std::getenv("VMM_COPY_STREAMS")) x->nact = x->ncs;
   return VMM_OK;
 }
 
