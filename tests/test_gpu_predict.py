@@ -61,3 +61,26 @@ def test_gate_lookahead_exact_on_integer_inputs():
     y = kernels.gate_lookahead(x.cuda(), w.cuda(), 6).cpu().numpy()
     ref = predictor_ref.gate_lookahead(x.float().numpy(), w.float().numpy(), 6)
     assert y.tolist() == ref.tolist()
+
+
+def test_a4_oracle_recall_perfect():
+    """Reference acceptance A4 (pkg/tests/test_acceptance.py:153-178): the device oracle's
+    top-B reaches hot recall exactly 1.0 whenever the budget covers the next layer's set."""
+    from paper_2605_05899_b200.predictor import OraclePredictor
+
+    checked = 0
+    for seed in range(12):
+        tr = generate_trace(TraceGenConfig(n_visual=10, n_text=4, layers=8, experts=24, k=2, clusters=3,
+                                           cluster_support=6, rho=[0.0, 0.5, 0.9, 1.0][seed % 4],
+                                           visual_noise=[0.0, 0.3][seed % 2], seed=seed))
+        ids = tr.prefill_ids()
+        o = OraclePredictor(tr, ids, window=5, gamma=0.8)
+        for layer in range(tr.layers - 1):
+            actual = tr.active_union(layer + 1, ids)
+            for budget in (len(actual), len(actual) + 3, tr.experts):
+                if budget > tr.experts:
+                    continue
+                picks = set(o.predict(layer, budget))
+                assert actual <= picks
+                checked += 1
+    assert checked > 100
