@@ -73,3 +73,29 @@ def test_core_always_kept_for_every_lambda():
         p = compress(tr, CompressionConfig(alpha=0.1, beta=0.5, lam=lam, prefix_layers=(0, 1)))
         assert set(p.core) <= set(p.keep)
         assert len(p.keep) == 48
+
+
+def test_a8_working_set_compaction():
+    """Reference acceptance A8 (pkg/tests/test_acceptance.py:282-320) on the device prune:
+    at beta=0.5, lambda=2 the retained tokens' mean per-layer working set is >= 15% smaller
+    than uniform-random retention at equal budget, and the inactive-expert count exceeds the
+    uncompressed set's at every layer (50 seeds)."""
+    comp_ws, rand_ws, inactive_kept, inactive_all = [], [], [], []
+    rng = np.random.default_rng(777)
+    layers = 6
+    for seed in range(50):
+        tr = generate_trace(TraceGenConfig(n_visual=48, n_text=0, layers=layers, experts=128, k=8, clusters=4,
+                                           cluster_support=16, rho=0.9, visual_noise=0.05, seed=seed))
+        p = compress(tr, CompressionConfig(alpha=0.07, beta=0.5, lam=2.0, prefix_layers=(0, 1)))
+        kept = p.retained_ids(tr)
+        rand_keep = sorted(int(i) for i in rng.choice(tr.visual_ids(), size=len(p.keep), replace=False))
+        allp = tr.prefill_ids()
+        ws_kept = [len(tr.active_union(l, kept)) for l in range(layers)]
+        ws_rand = [len(tr.active_union(l, rand_keep)) for l in range(layers)]
+        ws_all = [len(tr.active_union(l, allp)) for l in range(layers)]
+        comp_ws.append(np.mean(ws_kept))
+        rand_ws.append(np.mean(ws_rand))
+        inactive_kept.append([tr.experts - w for w in ws_kept])
+        inactive_all.append([tr.experts - w for w in ws_all])
+    assert float(np.mean(comp_ws)) <= 0.85 * float(np.mean(rand_ws))
+    assert np.all(np.mean(np.array(inactive_kept), axis=0) > np.mean(np.array(inactive_all), axis=0))
