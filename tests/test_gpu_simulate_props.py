@@ -68,3 +68,33 @@ def test_lower_bounds_and_overlap_identity():
                 assert r.makespan >= cfg.transfer_ms
             assert r.exposed_transfer + r.overlapped_transfer == r.total_transfer
             assert 0.0 <= r.exposed_transfer <= r.total_transfer
+
+
+def test_a6_ablation_ordering():
+    """Reference acceptance A6 (pkg/tests/test_acceptance.py:209-246), with the four stacked
+    configurations of pipeline.py:793-829 built from simulate()/simulate_reactive(): on 20
+    clustered 48x128x8 traces in a bandwidth-bound config, makespans are monotone
+    base >= +compression >= +prediction >= full and the full mean is <= 0.7x the base mean."""
+    from dataclasses import replace
+
+    base_spans, full_spans = [], []
+    for seed in range(20):
+        tr = generate_trace(TraceGenConfig(n_visual=64, n_text=16, layers=48, experts=128, k=8, clusters=4,
+                                           cluster_support=16, rho=0.85, visual_noise=0.3, seed=seed,
+                                           decode_steps=4))
+        cfg = SimConfig(bandwidth_mb_per_ms=17.3 / 8.0, expert_size_mb=17.3, gpu_ms_per_expert=2.0, l_pinned=4,
+                        num_slabs=256, decode_steps=4, predictor=PredictorSpec(kind="oracle", budget=20, window=5))
+        ccfg = CompressionConfig(alpha=0.1, beta=0.5, lam=2.0, prefix_layers=(0, 1, 2, 3))
+        base_cfg = replace(cfg, compress_latency_ms=0.0, predictor_bootstrap_ms=0.0)
+        b = simulate_reactive(tr, build_plan(tr, replace(base_cfg, predictor=PredictorSpec(kind="none"))),
+                              base_cfg).makespan
+        comp_cfg = replace(cfg, predictor_bootstrap_ms=0.0)
+        c = simulate_reactive(tr, build_plan(tr, replace(comp_cfg, predictor=PredictorSpec(kind="none")), ccfg),
+                              comp_cfg).makespan
+        pred_cfg = replace(cfg, speculative_grace=0, victim_policy="fifo")
+        p = simulate(tr, build_plan(tr, pred_cfg, ccfg), pred_cfg).makespan
+        f = simulate(tr, build_plan(tr, cfg, ccfg), cfg).makespan
+        assert b >= c >= p >= f, (seed, b, c, p, f)
+        base_spans.append(b)
+        full_spans.append(f)
+    assert sum(full_spans) / len(full_spans) <= 0.7 * sum(base_spans) / len(base_spans)
