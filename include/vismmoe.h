@@ -336,9 +336,9 @@ void vmm_xfer_destroy(vmm_xfer *x);
  * fenced on this slab (so a slab is never overwritten while being read).
  * `reserved` must be 0. */
 int vmm_xfer_copy(vmm_xfer *x, int slab, const void *h_src, void *d_dst, size_t bytes, int reserved);
-/* make `compute_stream` wait for the newest fill among the given slabs
- * (FIFO copy stream => covers all older fills) and register them as read by
- * the next layer */
+/* make `compute_stream` wait for the newest fill among the given slabs and the
+ * newest fill of every other copy stream (each stream is FIFO => covers all
+ * older fills) and register them as read by the next layer */
 int vmm_xfer_fence(vmm_xfer *x, const int32_t *h_slabs, int n, void *compute_stream);
 /* device u32 [num_slabs] fill flags: after each fill of slab s the copy stream
  * writes that fill's sequence number to ready[s] (stream memory op, ordered

@@ -10,9 +10,10 @@
 // stall (PCIe: 52.6 -> 53.6 GB/s for back-to-back 9.44 MB copies).  Per-slab
 // write-after-read and write-after-write waits keep every slab's fills and
 // readers ordered across the streams.
-//   * compute never reads a slab before its fill lands: vmm_xfer_fence makes
-//     the compute stream wait for the newest fill among the slabs a layer
-//     reads (FIFO => one wait covers all older fills);
+//   * compute never reads a slab before its fill lands: per-expert ready
+//     flags (the FFN spins on them), or vmm_xfer_fence, which makes the
+//     compute stream wait for the newest fill among the slabs a layer reads
+//     plus the newest fill of every other copy stream (FIFO per stream);
 //   * a slab is never overwritten while a layer may still read it: the copy
 //     into slab s first waits for the compute event of the last layer fenced
 //     on s (again one wait per newer reader, FIFO on the compute stream).

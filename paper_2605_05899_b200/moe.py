@@ -10,9 +10,11 @@ reference's `simulate` on the routes the run produced); execution follows the
 decided schedule on real streams:
 
   compute stream : route / predictor / permute / FFN / combine kernels
-  copy stream    : one cudaMemcpyAsync per decided expert transfer (pinned
-                   host pool -> HBM slab), FIFO in decision order, fenced by
-                   events both ways (vmm_xfer_*).
+  copy streams   : one cudaMemcpyAsync per decided expert transfer (pinned
+                   host pool -> HBM slab), issued in decision order round-robin
+                   over two copy streams, each followed by a ready-flag write;
+                   per-slab write-after-read / write-after-write events
+                   (vmm_xfer_*).
 
 HBM layout (SURVEY §8(d), C3 numbers):
   arena   bf16 [l_pinned*E + num_slabs, 3*I*H]  -- slot = [W13 (2I x H,
