@@ -9,7 +9,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
-from paper_2605_05899_b200 import kernels
+from paper_2605_05899_b200 import _lib, kernels
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 150000
 H = int(sys.argv[2]) if len(sys.argv) > 2 else 2048
@@ -57,6 +57,10 @@ cases = {
     "permute_rows": (lambda: kernels.permute_rows(x, src, M, out=xp), 2 * M * row),
     "combine": (lambda: kernels.combine(y, pos.view(N, k), gates, x, out=out), M * row + 2 * N * row),
     "rmsnorm": (lambda: kernels.rmsnorm(out, out=xn), 2 * N * row),
+    "combine_norm": (lambda: _lib.check(_lib.lib().vmm_combine_norm(y.data_ptr(), pos.data_ptr(), gates.data_ptr(),
+                                                                     x.data_ptr(), N, k, H, None, 0, 1e-6,
+                                                                     out.data_ptr(), xn.data_ptr(), 0)),
+                     M * row + 3 * N * row),
     "route": (lambda: kernels.route_topk(xn, wr, k, counts=cnt), N * row + E * row + N * k * 8),
     "route_lookahead": (lambda: kernels.route_lookahead(xn, wr2, 0, k, cnt, cnt2), N * row + 2 * E * row + N * k * 8),
 }
