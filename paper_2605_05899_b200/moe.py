@@ -505,7 +505,7 @@ class MoEStack:
                                                       trace=trace, record_into=routes_c,
                                                       region=(base[lane], caps[lane], lane))
                     cur_full[r0:r1].copy_(out_c)
-                    if c.predictor == "gate":  # the boot emission's context rows (layer lp-1 input)
+                    if c.predictor == "gate" and not skip_last:  # boot emission context (layer lp-1 input)
                         xn_full[r0:r1].copy_(bufs["xn"][base[lane]:base[lane] + n])
                     prefix[:lpe, r0:r1].copy_(routes_c)
                     counts_lane[lane] += counts_c
