@@ -322,6 +322,13 @@ int vmm_cache_select_victim(vmm_cache *c);
 int vmm_cache_info(const vmm_cache *c, long long *evictions, int *occupancy, int *step);
 int vmm_cache_slab(const vmm_cache *c, int slab, int *layer, int *expert, int *state, int *cls,
                    double *priority, double *ready, int *last_window_step, int *executed, int *seq);
+/* every slab in one call: ints [n][7] = layer, expert, state, cls, last_window_step,
+ * executed, seq; doubles [n][2] = priority, ready (NaN if none).  Returns n (>= 0)
+ * or -status.  Backs the `slabs` attribute the reference engine iterates
+ * (pkg/src/moesim/pipeline.py:520-524, cache.py:91). */
+int vmm_cache_slabs(const vmm_cache *c, int32_t *h_ints, double *h_dbls, int cap);
+/* slab holding (layer, expert), or -1 (ExpertCache.entry, cache.py:112-114) */
+int vmm_cache_find(const vmm_cache *c, int layer, int expert);
 
 /* ------------------------------------------------------------------------
  * Expert transfer runtime: pinned host pool -> HBM slab arena on a dedicated

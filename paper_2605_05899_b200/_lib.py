@@ -124,6 +124,8 @@ _SIGS = {
     "vmm_cache_select_victim": (I32, [P]),
     "vmm_cache_info": (I32, [P, C.POINTER(I64), PI32, PI32]),
     "vmm_cache_slab": (I32, [P, I32, PI32, PI32, PI32, PI32, PF64, PF64, PI32, PI32, PI32]),
+    "vmm_cache_slabs": (I32, [P, P, P, I32]),
+    "vmm_cache_find": (I32, [P, I32, I32]),
     "vmm_xfer_create": (I32, [I32, SZ, I32, C.POINTER(P)]),
     "vmm_xfer_destroy": (None, [P]),
     "vmm_xfer_copy": (I32, [P, I32, P, P, SZ, I32]),

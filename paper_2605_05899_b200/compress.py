@@ -105,7 +105,12 @@ def compress(trace, cfg: CompressionConfig) -> CompressionPlan:
     """Run the full selection policy over the trace's visual tokens (on the GPU)."""
     cfg.validate(trace.layers)
     visual = trace.visual_ids()
-    k_core, k_keep = cfg.budgets(len(visual))
+    # budgets inline (compress.py:151-154): `cfg` may be the reference's own
+    # CompressionConfig, which has only alpha/beta/lam/prefix_layers + validate()
+    k_core = math.floor(cfg.alpha * len(visual))
+    k_keep = math.floor(cfg.beta * len(visual))
+    if k_keep < k_core:
+        raise ValidationError("beta budget smaller than alpha budget")
     dt = device_trace(trace)
     dev = dt.device
     layers = torch.tensor(list(cfg.prefix_layers), dtype=torch.long, device=dev)

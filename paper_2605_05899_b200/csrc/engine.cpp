@@ -710,4 +710,26 @@ int vmm_cache_slab(const vmm_cache *c, int slab, int *layer, int *expert, int *s
   return VMM_OK;
 }
 
+/* slab holding (layer, expert), or -1 (ExpertCache.entry, cache.py:112-114) */
+int vmm_cache_find(const vmm_cache *c, int layer, int expert) {
+  return c->c.find(ckey(layer, expert));
+}
+
+/* all slabs at once (one call per `slabs` snapshot): ints [n][7] = layer,
+ * expert, state, cls, last_window_step, executed, seq; doubles [n][2] =
+ * priority, ready (NaN if none).  Returns n. */
+int vmm_cache_slabs(const vmm_cache *c, int32_t *h_ints, double *h_dbls, int cap) {
+  if (cap < c->c.n) return -vmm::fail(VMM_ECONTRACT, "slab snapshot buffer too small");
+  for (int i = 0; i < c->c.n; ++i) {
+    const Slab &s = c->c.slabs[i];
+    int32_t *o = h_ints + 7 * (size_t)i;
+    o[0] = s.key < 0 ? -1 : (int32_t)(s.key / (1 << 20));
+    o[1] = s.key < 0 ? -1 : (int32_t)(s.key % (1 << 20));
+    o[2] = s.state; o[3] = s.cls; o[4] = (int32_t)s.last_step; o[5] = s.executed ? 1 : 0; o[6] = (int32_t)s.seq;
+    h_dbls[2 * (size_t)i] = s.pri;
+    h_dbls[2 * (size_t)i + 1] = s.has_ready ? s.ready : kNaN;
+  }
+  return c->c.n;
+}
+
 }  // extern "C"
