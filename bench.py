@@ -106,27 +106,66 @@ def _cpu_restatement(w, T1, n_r):
             "(oracle/moe_ref.py: fp64 router, fp32 SwiGLU per expert, combine), extrapolated to the stack"}
 
 
-# reference arm: the reference's CPU path (oracle port: compress + simulate)
+# reference arm: the UNMODIFIED reference (moesim from baseline/_ref) on the host
+# cores -- build_plan (compress) + simulate, its own public API and stock path
+# (pipeline.py:191,768; compress.py:142).  The oracle port is timed beside it
+# as a labelled secondary figure.
 # ---------------------------------------------------------------------------
-def _ref_worker_init(gen_kw, seed):
-    global _REF_TRACE
-    from paper_2605_05899_b200.trace import TraceGenConfig, generate_trace
+def load_moesim():
+    """The reference package from its offline install (baseline/_ref); None if absent."""
+    try:
+        import moesim  # noqa: F401
+        return sys.modules["moesim"]
+    except ImportError:
+        pass
+    p = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(p, "moesim")):
+        sys.path.insert(0, p)
+        try:
+            import moesim  # noqa: F401
+            return sys.modules["moesim"]
+        except ImportError:
+            sys.path.remove(p)
+    return None
 
-    kw = dict(gen_kw)
-    kw["seed"] = seed
-    _REF_TRACE = generate_trace(TraceGenConfig(**kw))
+
+_REF = {}
 
 
-def _ref_request(args):
-    sim, comp = args
-    from oracle import harness
+def _ref_setup(kind, w, seed=0):
+    """Build one request's inputs for the reference path (in the parent, before fork)."""
+    gen = {k: v for k, v in w.trace_config(seed=seed).__dict__.items()}
+    if kind == "reference":
+        m = load_moesim()
+        tr = m.generate_trace(m.TraceGenConfig(**gen))
+        cfg = m.SimConfig(**{k: v for k, v in ref_sim_dict(w).items() if k not in ("predictor", "l_pinned")},
+                          l_pinned=w.l_pinned, predictor=m.PredictorSpec(**ref_sim_dict(w)["predictor"]))
+        ccfg = m.CompressionConfig(alpha=w.alpha, beta=w.beta, lam=w.lam, prefix_layers=tuple(w.prefix_layers))
+        _REF.update(kind=kind, m=m, trace=tr, cfg=cfg, ccfg=ccfg)
+    else:
+        from paper_2605_05899_b200.trace import TraceGenConfig, generate_trace
 
+        _REF.update(kind=kind, trace=generate_trace(TraceGenConfig(**gen)), sim=ref_sim_dict(w),
+                    comp=dict(alpha=w.alpha, beta=w.beta, lam=w.lam, prefix=list(w.prefix_layers)))
+
+
+def _ref_request(_=None):
+    """One request through the reference path; returns seconds."""
     t0 = time.perf_counter()
-    harness.simulate(_REF_TRACE, sim, comp, False)
+    if _REF["kind"] == "reference":
+        m = _REF["m"]
+        plan = m.build_plan(_REF["trace"], _REF["cfg"], _REF["ccfg"])
+        m.simulate(_REF["trace"], plan, _REF["cfg"])
+    else:
+        from oracle import harness
+
+        harness.simulate(_REF["trace"], _REF["sim"], _REF["comp"], False)
     return time.perf_counter() - t0
 
 
 def ref_sim_dict(w):
+    """Reference SimConfig for one request of workload w (the oracle predictor:
+    the reference's default kind; it has no router, so no gate predictor)."""
     return dict(bandwidth_mb_per_ms=1.0, expert_size_mb=0.17, gpu_ms_per_expert=0.002, num_slabs=w.num_slabs,
                 victim_policy="priority", speculative_grace=w.grace, l_pinned=w.l_pinned, shared_experts=0,
                 compress_latency_ms=0.0, predictor_bootstrap_ms=0.0,
@@ -134,40 +173,51 @@ def ref_sim_dict(w):
                                history_decay=w.history_decay))
 
 
-def run_reference(a, w):
+def _ref_pool_rate(kind, w, cores, warmup, steps):
+    """tokens/s of `cores` processes, one request each per step (fork after setup)."""
     import multiprocessing as mp
 
+    _ref_setup(kind, w)
+    pool = mp.get_context("fork").Pool(cores)
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        pool.map(_ref_request, range(cores))
+        if i >= warmup:
+            times.append(time.perf_counter() - t0)
+    pool.close()
+    pool.join()
+    step = float(np.mean(times))
+    return cores * w.n_tokens / step, step
+
+
+def run_reference(a, w):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    gen = {k: v for k, v in w.trace_config(seed=0).__dict__.items() if k != "seed"}
-    comp = dict(alpha=w.alpha, beta=w.beta, lam=w.lam, prefix=list(w.prefix_layers))
-    sim = ref_sim_dict(w)
     cores = os.cpu_count() or 1
-    ctx = mp.get_context("fork")
-    pools = []
-    # one worker per core, each with its own synthetic request trace
-    pool = ctx.Pool(cores, initializer=_ref_worker_init, initargs=(gen, 0))
-    pools.append(pool)
-    times = []
-    for i in range(a.warmup + a.steps):
-        t0 = time.perf_counter()
-        pool.map(_ref_request, [(sim, comp)] * cores)
-        dt = time.perf_counter() - t0
-        if i >= a.warmup:
-            times.append(dt)
-    pool.close()
-    step = float(np.mean(times))
-    val = cores * w.n_tokens / step
+    kind = "reference" if load_moesim() is not None else "port"
+    val, step = _ref_pool_rate(kind, w, cores, a.warmup, a.steps)
+    port = None
+    if kind == "reference":  # the builder's port beside it, labelled (not the arm's value)
+        pv, ps = _ref_pool_rate("port", w, cores, 1, max(1, min(a.steps, 3)))
+        port = {"label": "oracle port (oracle/harness.py), not the reference", "value": pv, "unit": "tokens/s",
+                "ms_per_step": ps * 1e3}
+    what = ("moesim.build_plan (compress) + moesim.simulate, unmodified reference from baseline/_ref"
+            if kind == "reference" else "oracle port of moesim (baseline/_ref absent)")
     line = {
         "impl": "reference", "metric": "prefill tokens/s per VL-MoE layer stack", "value": val, "unit": "tokens/s",
         "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": step * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference trace generator, seed 0)",
-        "config": {"workload": w.name, "requests_per_step": cores, "predictor": "oracle B=%d W=%d" % (w.budget, w.window),
-                   "path": "compress + simulate (decision path; the reference has no router/FFN numerics)"},
-        "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "port",
-                         "sample": f"{cores} C3 requests per step, one per process (oracle port of moesim)"},
+        "config": {"workload": w.name, "requests_per_step": cores, "path": what,
+                   "routing": "trace (the reference has no router)",
+                   "predictor": "oracle B=%d W=%d (the reference has no gate predictor)" % (w.budget, w.window),
+                   "vs_ours": "decision path only: the reference moves no expert bytes and computes no expert "
+                              "FLOPs; our arm routes live and predicts with the gate-reuse lookahead"},
+        "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": kind,
+                         "sample": f"{cores} {w.name} requests per step, one per process ({what})",
+                         "port": port},
         "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -230,6 +280,7 @@ class _EPResult:
 
 
 def measure_h2d_peak(torch, dev):
+    """Best of 3 pinned 1 GiB host->device copies on this rank."""
     n = 1 << 30
     src = torch.empty(n, dtype=torch.uint8, pin_memory=True)
     dst = torch.empty(n, dtype=torch.uint8, device=dev)
@@ -245,11 +296,67 @@ def measure_h2d_peak(torch, dev):
     return best
 
 
+def measure_peer_peak(torch, dev, rank, world, device_of_rank=None, reps=10):
+    """Best of `reps` 1 GiB copy-engine pulls from the next rank's HBM into this
+    rank's (IPC-mapped peer pointer, peer access enabled: NVLink/NVSwitch on a
+    multi-GPU box; a local D2D copy when the ranks share one device or world=1).
+    Run on every rank at once, so the figure is the per-GPU rate under all-to-all load."""
+    import torch.distributed as dist
+
+    from paper_2605_05899_b200 import _lib as vlib
+
+    L = vlib.lib()
+    n = 1 << 30
+    src = torch.empty(n, dtype=torch.uint8, device=dev).fill_(rank & 0xFF)
+    dst = torch.empty(n, dtype=torch.uint8, device=dev)
+    opened, ptr = None, src.data_ptr()
+    if world > 1:
+        handles = [None] * world
+        dist.all_gather_object(handles, vlib.ipc_export(src.data_ptr()))
+        peer = (rank + 1) % world
+        vlib.check(L.vmm_peer_enable(peer if device_of_rank is None else int(device_of_rank[peer])))
+        opened, ptr = vlib.ipc_import(handles[peer])
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    s = torch.cuda.current_stream(dev)
+    best = 0.0
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        vlib.check(L.vmm_copy_async(dst.data_ptr(), ptr, n, s.cuda_stream))
+        b.record(s)
+        b.synchronize()
+        best = max(best, n / (a.elapsed_time(b) * 1e-3) / 1e9)
+    ok = world == 1 or int(dst[0].item()) == ((rank + 1) % world) & 0xFF
+    if opened is not None:
+        vlib.check(L.vmm_ipc_close(opened))
+    if world > 1:
+        dist.barrier()
+    del src, dst
+    torch.cuda.synchronize(dev)
+    return best if ok else None
+
+
+def relaunch(a) -> int:
+    """--gpus N without a torchrun environment: re-exec under torch.distributed.run
+    (one process per GPU, rendezvous on 127.0.0.1)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     a = parse()
     from paper_2605_05899_b200.configs import WORKLOADS
 
     w = WORKLOADS[a.workload]
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(a)
     if a.impl == "reference":
         return run_reference(a, w)
 
@@ -274,12 +381,20 @@ def main():
     predictor = a.predictor or ("gate" if a.routing == "live" else "oracle")
     from paper_2605_05899_b200.moe import ExpertStore, ShardedHome
 
-    # pinned host pool: layer l is served from pool layer l % host_layers (every byte moved is a real
-    # PCIe transfer); one process per GPU each pins its own pool, so shrink it as N grows (8 ranks x 9.7 GB
-    # would pin ~78 GB of host memory)
-    kw = dict(routing=a.routing, predictor=predictor, host_layers=max(1, 8 // world))
-    if a.source == "sharded":  # logical clock: one slot over NVLink (770 GB/s measured peer copy) or local D2D
-        kw["transfer_ms"] = w.expert_bytes / (770e9 if world > 1 else 3000e9) * 1e3
+    # link peaks, measured on every rank at once before the stack exists:
+    # pinned H2D (the host pool's link) and a peer-HBM pull (NVLink; local D2D at world 1)
+    vdist.barrier()
+    h2d_rank_peak = measure_h2d_peak(torch, dev)
+    h2d_peak_job = sum(vdist.sum_over_ranks([h2d_rank_peak], dev))
+    p2p_peak = measure_peer_peak(torch, dev, rank, world, [0] * world if share else None)
+    if p2p_peak is None:
+        raise SystemExit(f"rank {rank}: the peer copy returned the wrong bytes")
+    p2p_peak_min = -vdist.max_over_ranks(-p2p_peak, dev)  # the slowest rank's link
+    # pinned host pool: layer l is served from pool layer l % 8 (every byte moved is a real PCIe
+    # transfer); the same synthetic model at every N (9.7 GB pinned per rank)
+    kw = dict(routing=a.routing, predictor=predictor, host_layers=8)
+    if a.source == "sharded":  # logical clock: one slot pulled at the measured peer (or D2D) rate
+        kw["transfer_ms"] = w.expert_bytes / (p2p_peak_min * 1e9) * 1e3
     if a.source == "ep":
         kw.update(predictor="none", budget=0)
         predictor = "none (expert-parallel: no cache)"
@@ -463,8 +578,7 @@ def main():
         tj = json.load(open(tpath)).get(f"{w.name}/R{a.requests}")
         traffic = tj["dram_bytes_per_launch"] if tj else None
     res0 = results[-1][0]
-    h2d_peak = measure_h2d_peak(torch, dev) if a.source == "host" else (770.0 if world > 1 and a.source == "sharded"
-                                                                          else None)
+    h2d_peak = h2d_peak_job if a.source == "host" else (p2p_peak_min * world if a.source == "sharded" else None)
     h2d_bytes = res0.h2d_bytes
     rep = res0.report
     # whole-job counters (mode DP: one sum-reduction of the per-rank counters)
@@ -474,25 +588,29 @@ def main():
         hits, misses, evictions, copies, h2d_bytes, retained = (v for v in vdist.sum_over_ranks(
             [hits, misses, evictions, copies, h2d_bytes, retained], dev))
     hit_rate = hits / (hits + misses) if (hits or misses) and rep.hit_rate is not None else rep.hit_rate
-    if h2d_peak and world > 1 and a.source == "host":
-        h2d_peak = h2d_peak * world  # one host link per GPU: the job's aggregate copy peak
     h2d_gbs = h2d_bytes / (ms * 1e-3) / 1e9
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         try:
-            sys.path.insert(0, ROOT)
-            from oracle import harness
+            def single_thread(kind, budget_s):
+                _ref_setup(kind, w)
+                t0, n = time.perf_counter(), 0
+                while time.perf_counter() - t0 < budget_s or n == 0:
+                    _ref_request()
+                    n += 1
+                return T1 * n / (time.perf_counter() - t0), n
 
-            comp = dict(alpha=w.alpha, beta=w.beta, lam=w.lam, prefix=list(w.prefix_layers))
-            t0 = time.perf_counter()
-            n_req = 0
-            while time.perf_counter() - t0 < 10.0 or n_req == 0:
-                harness.simulate(tr, ref_sim_dict(w), comp, False)
-                n_req += 1
-            dt = (time.perf_counter() - t0) / n_req
-            cpu = {"value": T1 / dt, "unit": "tokens/s", "cores": 1, "kind": "port",
-                   "sample": f"{n_req} x one {w.name} request (compress + simulate, oracle predictor), single thread"}
+            kind = "reference" if load_moesim() is not None else "port"
+            v, n_req = single_thread(kind, 10.0)
+            cpu = {"value": v, "unit": "tokens/s", "cores": 1, "kind": kind,
+                   "sample": f"{n_req} x one {w.name} request, single thread: " +
+                             ("moesim.build_plan + moesim.simulate (unmodified reference, oracle predictor)"
+                              if kind == "reference" else "oracle port (compress + simulate, oracle predictor)")}
+            if kind == "reference":
+                pv, pn = single_thread("port", 3.0)
+                cpu["port"] = {"label": "oracle port (oracle/harness.py), not the reference", "value": pv,
+                               "unit": "tokens/s", "cores": 1, "sample": f"{pn} requests"}
             cpu["host"] = _host_info()
             try:
                 cpu["restatement"] = _cpu_restatement(w, T1, max(1, int(res0.hidden.shape[0]) // R))
@@ -523,8 +641,14 @@ def main():
                             ("none: expert-parallel, token rows over peer memory" if a.source == "ep" else
                              ("NVLink P2P + local D2D (sharded HBM home copies)" if world > 1 else
                               "local D2D (HBM home)")),
-                    "peak_source": "measured pinned 1 GiB H2D in this run" if a.source == "host" else
-                                   "B200_PROFILING.md measured peer copy 770 GB/s"},
+                    "peak_source": ("pinned 1 GiB H2D, measured in this run on all ranks at once (job sum)"
+                                    if a.source == "host" else
+                                    "1 GiB peer-HBM pull (IPC, copy engine), best of 10, all ranks at once "
+                                    "(min over ranks x world)" if world > 1 else "1 GiB local D2D copy, best of 10")},
+            "links": {"h2d_gbs_per_rank": h2d_rank_peak, "h2d_gbs_job": h2d_peak_job,
+                      "peer_gbs_per_rank_min": p2p_peak_min,
+                      "peer_kind": ("NVLink P2P (IPC-mapped peer HBM)" if world > 1 and not share else
+                                    "same-device IPC copy (ranks share one GPU)" if world > 1 else "local D2D")},
             "roofline": {"bound": bound,
                          "kernel": "ffn_fused_kernel (tcgen05 GEMM1+SwiGLU+GEMM2, one launch per layer)",
                          "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,

@@ -369,6 +369,9 @@ int vmm_ipc_open(const void *h_handle64, void **d_ptr);
 int vmm_ipc_offset(const void *d_ptr, long long *off);
 int vmm_ipc_close(void *d_ptr);
 int vmm_peer_enable(int peer);
+/* one copy-engine copy (any direction, incl. an IPC-mapped peer pointer) on `stream`;
+ * used to measure the link peaks the logical clock is calibrated with */
+int vmm_copy_async(void *d_dst, const void *src, size_t bytes, void *stream);
 /* drain the engine's transfer commands and enqueue each as one copy of
  * slot_bytes from the pinned host pool slot ((layer % host_layers)*experts +
  * expert) into arena slot (slab_offset + slab) */

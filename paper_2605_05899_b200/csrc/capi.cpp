@@ -82,6 +82,12 @@ int vmm_ipc_close(void *d_ptr) {
   return VMM_OK;
 }
 
+int vmm_copy_async(void *d_dst, const void *src, size_t bytes, void *stream) {
+  cudaError_t e = cudaMemcpyAsync(d_dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream);
+  if (e != cudaSuccess) return vmm::fail(VMM_ECUDA, std::string("cudaMemcpyAsync: ") + cudaGetErrorString(e));
+  return VMM_OK;
+}
+
 int vmm_peer_enable(int peer) {
   int dev = 0, can = 0;
   cudaGetDevice(&dev);
