@@ -337,6 +337,46 @@ def measure_peer_peak(torch, dev, rank, world, device_of_rank=None, reps=10):
     return best if ok else None
 
 
+def ffn_kernel_name(M: int, E: int, H: int, I: int) -> str:
+    """The grouped-SwiGLU kernel libvismmoe launches for M picks (csrc/ffn_sm100.cu dispatch)."""
+    wide = H % 256 == 0 and (2 * I) % 256 == 0
+    if M <= 16:
+        return "skinny_ffn_kernel (decode-sized, CUDA cores)"
+    if wide and M >= 256 * E:
+        return "ffn_pair_kernel (tcgen05 cta_group::2, 256x256 tiles, GEMM1+SwiGLU+GEMM2 in one launch)"
+    return f"ffn_fused_kernel<{256 if wide else 128}> (tcgen05, 128x{256 if wide else 128} tiles, one launch)"
+
+
+def step_roofline(w, T, n_r, report, ms, tc_tflops, hbm_gbs, link_gbs, skip_last, slot_bytes):
+    """SURVEY 8(d) stack roofline: sum over layers of max(FLOP / tensor peak,
+    HBM bytes / HBM peak, miss bytes / link peak) against the measured step.
+    Per layer: FLOP = router 2*N_route*H*E + FFN 6*N_ffn*k*H*I; HBM bytes = the
+    demanded experts' weights + one read of the layer input + one write of its
+    output + the router weights (the minimum any implementation moves); miss
+    bytes = the layer's transfers (report.per_layer) x the expert slot."""
+    H, I, E, k, L, lp = w.hidden, w.inter, w.experts, w.k, w.layers, w.l_pinned
+    stats = {s.layer: s for s in report.per_layer if s.phase == "prefill"}
+    floor_s, parts = 0.0, {"tensor": 0.0, "hbm": 0.0, "link": 0.0}
+    for l in range(L):
+        n_route = T if l < lp else n_r
+        n_ffn = n_route if (l < lp - 1 or (l == lp - 1 and not skip_last)) else n_r
+        st = stats.get(l)
+        ne = E if l < lp or st is None else int(st.hits + st.transfers)
+        miss = 0 if l < lp or st is None else int(st.transfers)
+        fl = 2.0 * n_route * H * E + 6.0 * n_ffn * k * H * I
+        by = ne * slot_bytes + E * H * 2 + n_route * H * 2 + n_ffn * H * 2
+        t = {"tensor": fl / (tc_tflops * 1e12), "hbm": by / (hbm_gbs * 1e9),
+             "link": miss * slot_bytes / (link_gbs * 1e9) if link_gbs else 0.0}
+        b = max(t, key=t.get)
+        parts[b] += t[b]
+        floor_s += t[b]
+    return {"step_frac": floor_s * 1e3 / ms, "floor_ms": floor_s * 1e3,
+            "floor_by_bound_ms": {k_: v * 1e3 for k_, v in parts.items()},
+            "peaks": {"tensor_tflops": tc_tflops, "hbm_gbs": hbm_gbs, "link_gbs": link_gbs},
+            "definition": "sum_layer max(FLOP/tensor, bytes/HBM, miss bytes/link) / ms_per_step; "
+                          "sustained peaks (MEASURED_PEAKS.json) and the link peak measured in this run"}
+
+
 def relaunch(a) -> int:
     """--gpus N without a torchrun environment: re-exec under torch.distributed.run
     (one process per GPU, rendezvous on 127.0.0.1)."""
@@ -393,7 +433,21 @@ def main():
     # pinned host pool: layer l is served from pool layer l % 8 (every byte moved is a real PCIe
     # transfer); the same synthetic model at every N (9.7 GB pinned per rank)
     kw = dict(routing=a.routing, predictor=predictor, host_layers=8)
-    if a.source == "sharded":  # logical clock: one slot pulled at the measured peer (or D2D) rate
+    # Calibrated logical clock (hard part 2: decide on a logical clock, execute on
+    # real streams): one transfer = the expert slot at the link rate measured above; one
+    # expert's compute = the roofline time of the average expert at this batch (retained
+    # rows x k / E picks), at the sustained peaks.  Decisions stay exactly replayable: the
+    # values are in the JSON line and in cfg.sim_config().
+    pk_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peaks = json.load(open(pk_path)) if os.path.exists(pk_path) else {}
+    hbm_sus = float(peaks.get("hbm_gbs", 6650.0))
+    tc_sus = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0)))
+    rows_per_req = math.floor(w.beta * w.n_visual) + w.n_text
+    picks_per_expert = a.requests * rows_per_req * w.k / w.experts
+    kw["gpu_ms"] = max(w.expert_bytes / (hbm_sus * 1e9),
+                       6.0 * picks_per_expert * w.hidden * w.inter / (tc_sus * 1e12)) * 1e3
+    kw["transfer_ms"] = w.expert_bytes / (h2d_rank_peak * 1e9) * 1e3
+    if a.source == "sharded":  # one slot pulled at the measured peer (or D2D) rate
         kw["transfer_ms"] = w.expert_bytes / (p2p_peak_min * 1e9) * 1e3
     if a.source == "ep":
         kw.update(predictor="none", budget=0)
@@ -572,11 +626,14 @@ def main():
         bound, ach, peak, unit = "hbm", sum(nbytes) / t_act / 1e9, hbm_peak, "GB/s"
         peak_src = "of measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else \
             "of fallback (B200_PROFILING.md: 6.65 TB/s)"
-    traffic = None
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         tj = json.load(open(tpath)).get(f"{w.name}/R{a.requests}")
-        traffic = tj["dram_bytes_per_launch"] if tj else None
+        if tj:
+            traffic = tj["dram_bytes_per_launch"]
+            traffic_src = f"from profiles/ncu_traffic.json ({tj.get('source', 'ncu --set full capture')}), " \
+                          "not measured in this run"
     res0 = results[-1][0]
     h2d_peak = h2d_peak_job if a.source == "host" else (p2p_peak_min * world if a.source == "sharded" else None)
     h2d_bytes = res0.h2d_bytes
@@ -619,6 +676,12 @@ def main():
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "unit": "tokens/s", "cores": 1, "kind": "port", "sample": f"failed: {exc}"}
 
+    step_rl = None
+    if a.source != "ep":
+        skip_last = a.routing == "live" and w.shared_experts == 0 and not os.environ.get("VMM_PREFIX_FULL_LAST")
+        link = h2d_rank_peak if a.source == "host" else p2p_peak_min
+        step_rl = step_roofline(w, T, int(res0.hidden.shape[0]), rep, ms, tc_sus, hbm_sus, link, skip_last,
+                                cfg.slot_bytes)
     if rank == 0:
         line = {
             "metric": "prefill tokens/s per VL-MoE layer stack", "value": value, "unit": "tokens/s",
@@ -650,20 +713,24 @@ def main():
                       "peer_kind": ("NVLink P2P (IPC-mapped peer HBM)" if world > 1 and not share else
                                     "same-device IPC copy (ranks share one GPU)" if world > 1 else "local D2D")},
             "roofline": {"bound": bound,
-                         "kernel": "ffn_fused_kernel (tcgen05 GEMM1+SwiGLU+GEMM2, one launch per layer)",
+                         "kernel": ffn_kernel_name(M, w.experts, w.hidden, w.inter),
                          "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
-                         "traffic": traffic, "launch_ms": float(np.mean(durs)),
+                         "traffic": traffic, "traffic_source": traffic_src, "launch_ms": float(np.mean(durs)),
                          "timing": "last layer's FFN replayed on its real inputs, experts resident, L2 flushed",
                          "live_launch_ms_incl_copy_waits": live_ms,
                          "bytes_per_launch": float(np.mean(nbytes)), "flops_per_launch": float(np.mean(nflops)),
                          "hbm_frac": (sum(nbytes) / t_act / 1e9) / hbm_peak,
                          "tensor_frac": (sum(nflops) / t_act / 1e12) / tc_peak,
-                         "peak_source": peak_src},
+                         "peak_source": peak_src,
+                         "step": step_rl},
             "clocks": clk.summary(local),
             "gpu_launches": int(launches),
             "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": int(T * w.hidden * 2 + T * 9),
                     "d2h_bytes_per_step": int(res0.hidden.numel() * 2), "ms_per_step": ms_e2e},
             "cpu_baseline": cpu,
+            "config_clock": {"transfer_ms": cfg.transfer_ms, "gpu_ms": cfg.gpu_ms,
+                             "basis": "transfer = expert slot / measured link peak; gpu = roofline time of the "
+                                      "average expert's picks at sustained peaks"},
         }
         print(json.dumps(line), flush=True)
         if a.out:

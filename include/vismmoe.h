@@ -50,23 +50,32 @@ int vmm_device_check(int dev);
  * Replaces compress() pkg/src/moesim/compress.py:142-185 (normalize_saliency
  * :104-114, salient core :156-157, active_experts :125-132,
  * marginal_expansion :135-139, extras order :174) and
- * CompressionPlan.retained_ids :63-65.
+ * CompressionPlan.retained_ids :63-65.  Selections are threshold searches over
+ * order-preserving fp64 keys + an id-ordered tie scan (no sort, no size cap).
  *   d_saliency [T] f64, d_modality [T] u8 (0 visual, 1 text, 2 decode),
  *   d_routes [P][T][k] i32: routes of the prefix layers for all T tokens,
- *   d_req_off [R+1] i32 token offsets, d_k_core/d_k_keep [R] i32 budgets
- *   (host: floor(alpha*n_visual), floor(beta*n_visual), exactly as :151-152).
+ *   d_req_off [R+1] i32 token offsets.  Budgets: d_k_core/d_k_keep [R] i32, or
+ *   both NULL -> floor(alpha*n_visual), floor(beta*n_visual) of each request on
+ *   the device, exactly as :151-152 (one correctly rounded product each).
  * Outputs (token-indexed, per request segment): s_norm/delta/score f64 (NaN
  * where undefined), flags u8 (bit0 core, bit1 keep, bit2 retained),
  * d_retained i32 (request-local ids, ascending, packed at d_req_off[r]),
  * d_n_retained [R] i32, d_target [R][4] u64 expert bitmask, d_status [R] i32
- * (0 ok, 1 invalid saliency, 2 too many visual tokens).
+ * (0 ok, 1 invalid saliency [ValidationError], 3 beta budget smaller than the
+ * alpha budget [ValidationError], 4 expert id outside [0, experts) [TraceError]).
  * ------------------------------------------------------------------------ */
 int vmm_prune(const double *d_saliency, const uint8_t *d_modality, const int32_t *d_routes,
               const int32_t *d_req_off, const int32_t *d_k_core, const int32_t *d_k_keep,
-              int R, int T, int P, int k, int experts, double lam,
+              double alpha, double beta, int R, int T, int P, int k, int experts, double lam,
               double *d_s_norm, double *d_delta, double *d_score, uint8_t *d_flags,
               int32_t *d_retained, int32_t *d_n_retained, uint64_t *d_target, int32_t *d_status,
               void *stream);
+
+/* Pack the per-request retained lists of vmm_prune into one ascending list of
+ * global row ids (request r's ids + req_off[r]) and the offsets of each
+ * request's rows in it: d_out [sum n_retained], d_out_off [R+1]. */
+int vmm_retained_pack(const int32_t *d_req_off, const int32_t *d_retained, const int32_t *d_n_retained, int R,
+                      int32_t *d_out, int32_t *d_out_off, void *stream);
 
 /* Row gather (stream compaction of hidden states): dst[i] = src[idx[i]], bf16 rows of H. */
 int vmm_gather_rows(const void *d_src, const int32_t *d_idx, int n, int H, void *d_dst, void *stream);

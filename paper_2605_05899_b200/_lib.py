@@ -72,7 +72,8 @@ _SIGS = {
     "vmm_abi_version": (I32, []),
     "vmm_launch_count": (I64, []),
     "vmm_device_check": (I32, [I32]),
-    "vmm_prune": (I32, [P, P, P, P, P, P, I32, I32, I32, I32, I32, F64, P, P, P, P, P, P, P, P, P]),
+    "vmm_prune": (I32, [P, P, P, P, P, P, F64, F64, I32, I32, I32, I32, I32, F64, P, P, P, P, P, P, P, P, P]),
+    "vmm_retained_pack": (I32, [P, P, P, I32, P, P, P]),
     "vmm_gather_rows": (I32, [P, P, I32, I32, P, P]),
     "vmm_route_topk": (I32, [P, P, I32, I32, I32, I32, P, P, P, P, P]),
     "vmm_route_lookahead": (I32, [P, P, I32, I32, I32, I32, I32, I32, P, P, P, P, P]),

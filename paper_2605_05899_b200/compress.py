@@ -21,7 +21,7 @@ import torch
 
 from . import kernels
 from .device_trace import device_trace
-from .errors import ValidationError
+from .errors import TraceError, ValidationError
 
 DEFAULT_TRADEOFF = 2.0  # compress.py:21
 
@@ -98,7 +98,16 @@ def compress_device(saliency, modality, prefix_routes, req_off, k_core, k_keep, 
     return kernels.prune(saliency, modality, prefix_routes, req_off, k_core, k_keep, experts, lam, stream)
 
 
-_STATUS_MSG = {1: "saliency entries must be finite and >= 0", 2: "too many visual tokens for one CTA (max 8192)"}
+_STATUS = {1: (ValidationError, "saliency entries must be finite and >= 0"),
+           3: (ValidationError, "beta budget smaller than alpha budget"),
+           4: (TraceError, "prefix route expert id outside [0, experts)")}
+
+
+def raise_prune_status(status: int) -> None:
+    """Map a vmm_prune status to the reference's exception (compress.py:104-154)."""
+    if status:
+        cls, msg = _STATUS.get(status, (ValidationError, f"prune failed with status {status}"))
+        raise cls(msg)
 
 
 def compress(trace, cfg: CompressionConfig) -> CompressionPlan:
@@ -119,10 +128,8 @@ def compress(trace, cfg: CompressionConfig) -> CompressionPlan:
     kc = torch.tensor([k_core], dtype=torch.int32, device=dev)
     kk = torch.tensor([k_keep], dtype=torch.int32, device=dev)
     out = kernels.prune(dt.saliency, dt.modality, prefix, req_off, kc, kk, trace.experts, cfg.lam)
+    raise_prune_status(int(out["status"].cpu()[0]))
     flags = out["flags"].cpu().numpy()
-    status = int(out["status"].cpu()[0])
-    if status != 0:
-        raise ValidationError(_STATUS_MSG.get(status, f"prune failed with status {status}"))
     s_norm = out["s_norm"].cpu().numpy()
     delta = out["delta"].cpu().numpy()
     score = out["score"].cpu().numpy()

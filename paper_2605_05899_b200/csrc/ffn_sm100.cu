@@ -17,6 +17,7 @@
 #include <math.h>
 
 #include <cstdlib>
+#include <atomic>
 #include <mutex>
 
 #include "sm100.cuh"
@@ -1409,32 +1410,48 @@ extern "C" int vmm_ffn_prof_read(unsigned long long *out, int reset) {
 }
 #endif
 
-// per-device grid-barrier counter for the persistent decode FFN (monotonic:
-// each launch waits for its own epoch's target, so it is never reset)
+// Grid barrier of the persistent decode FFN: a ring of per-device counters; each
+// launch takes the next one, zeroes it on ITS stream (cudaMemsetAsync, stream-
+// ordered before the kernel) and waits for target = grid.  Launches on different
+// streams therefore never share a live counter (unless > kBarRing are in flight),
+// a failed launch leaves no state behind, and the cooperative launch guarantees
+// that all `grid` CTAs are co-resident.
 static int skinny_launch(const void *d_xp, const int32_t *d_offsets, int E, int M_total, int H, int I,
                          const void *d_w13, const void *d_w2, long long stride, const int32_t *d_slot_of,
                          const uint32_t *d_need, const uint32_t *d_ready, int ready_base, void *d_h1, void *d_y,
                          void *stream) {
   if (H % 8 || I % 8 || H % 4) return vmm::fail(VMM_EVALIDATION, "decode FFN: hidden/inter must be multiples of 8");
+  constexpr int kBarRing = 64;
   static unsigned int *bar[64] = {nullptr};
-  static unsigned long long epoch[64] = {0};
+  static std::atomic<unsigned int> next[64];
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) return vmm::fail(VMM_ECUDA, "device index out of range");
-  if (!bar[dev]) {
-    cudaError_t e = cudaMalloc(&bar[dev], sizeof(unsigned int));
-    if (e == cudaSuccess) e = cudaMemset(bar[dev], 0, sizeof(unsigned int));
-    if (e != cudaSuccess) return vmm::cuda_status(e, "decode FFN barrier");
+  {
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!bar[dev]) {
+      cudaError_t e = cudaMalloc(&bar[dev], sizeof(unsigned int) * kBarRing);
+      if (e == cudaSuccess) e = cudaMemset(bar[dev], 0, sizeof(unsigned int) * kBarRing);
+      if (e != cudaSuccess) return vmm::cuda_status(e, "decode FFN barrier");
+    }
   }
   if (!g_num_sms) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = g_num_sms;
-  epoch[dev] += 1;
-  const unsigned int target = (unsigned int)(epoch[dev] * (unsigned long long)grid);  // wraps consistently
-  skinny_ffn_kernel<<<grid, kSkinnyThreads, 0, (cudaStream_t)stream>>>(
-      (const __nv_bfloat16 *)d_xp, d_offsets, E, d_slot_of, (const __nv_bfloat16 *)d_w13,
-      (const __nv_bfloat16 *)d_w2, stride, H, I, d_need, d_ready, ready_base, bar[dev], target,
-      (__nv_bfloat16 *)d_h1, (__nv_bfloat16 *)d_y);
-  VMM_LAUNCH_CHECK("skinny_ffn_kernel");
+  int grid = g_num_sms;
+  unsigned int *counter = bar[dev] + (next[dev].fetch_add(1u) % kBarRing);
+  cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(unsigned int), (cudaStream_t)stream);
+  if (e != cudaSuccess) return vmm::cuda_status(e, "decode FFN barrier reset");
+  const __nv_bfloat16 *xp = (const __nv_bfloat16 *)d_xp, *w13 = (const __nv_bfloat16 *)d_w13,
+                      *w2 = (const __nv_bfloat16 *)d_w2;
+  __nv_bfloat16 *h1 = (__nv_bfloat16 *)d_h1, *y = (__nv_bfloat16 *)d_y;
+  unsigned int target = (unsigned int)grid;
+  void *args[] = {(void *)&xp, (void *)&d_offsets, (void *)&E, (void *)&d_slot_of, (void *)&w13, (void *)&w2,
+                  (void *)&stride, (void *)&H, (void *)&I, (void *)&d_need, (void *)&d_ready, (void *)&ready_base,
+                  (void *)&counter, (void *)&target, (void *)&h1, (void *)&y};
+  e = cudaLaunchCooperativeKernel((const void *)skinny_ffn_kernel, dim3(grid), dim3(kSkinnyThreads), args, 0,
+                                  (cudaStream_t)stream);
+  if (e != cudaSuccess) return vmm::cuda_status(e, "skinny_ffn_kernel (cooperative launch)");
+  vmm::count_launch();
   return VMM_OK;
 }
 

@@ -9,265 +9,410 @@
 //   score  = s_norm - lam * delta   (separately rounded)    compress.py:172
 //   extras = top (k_keep - k_core) by (-score, -s_norm, id) compress.py:174
 //   retained = keep U text ids, ascending                   compress.py:63-65
-// Both selections are a shared-memory bitonic sort of (key1, key2, id) with
-// exact lexicographic tie keys; stream compaction uses block-wide ballot scans.
+//
+// Selection without sorting.  Both selections only need the SET of winners
+// (the outputs are id-sorted), so each is a threshold search: an 8-ary
+// bisection over the 64-bit order-preserving keys of the doubles (7 pivots
+// per step, counts reduced with warp `redux` + one smem pass, ~21 steps for
+// any double range), then the tie at the threshold is broken by id with one
+// block-wide ordered ballot scan.  The composite extras key (-score, -s_norm,
+// id) is two nested searches (score, then s_norm among the score ties) and
+// the id scan.  No per-token state is kept on chip: the keys are re-read
+// from the s_norm/score outputs the CTA itself wrote (L1/L2-resident), so
+// there is no cap on the tokens per request.  Routes are read exactly once:
+// the core tokens' masks for the target set, then every other visual
+// token's mask for its marginal expansion.
 #include <math.h>
 
 #include "common.cuh"
 
 namespace {
 
-constexpr int kThreads = 1024;
-constexpr int kMaxVisual = 8192;
 constexpr int kWords = VMM_MAX_EXPERTS / 64;
+constexpr int kPiv = 7;  // 8-ary search
 
-struct SortBuf {
-  uint64_t *k1;
-  uint64_t *k2;
-  uint32_t *id;
+struct Shared {
+  int warp_tot[64];
+  int red[32][kPiv + 1];
+  int tot[kPiv + 1];
+  unsigned long long kmin[32], kmax[32];
+  double dlo[32], dhi[32];
+  unsigned long long target[kWords];
+  int total, nvis, bad;
 };
 
-__device__ __forceinline__ bool before(uint64_t a1, uint64_t a2, uint32_t ai, uint64_t b1, uint64_t b2,
-                                       uint32_t bi) {
-  if (a1 != b1) return a1 < b1;
-  if (a2 != b2) return a2 < b2;
-  return ai < bi;
-}
-
-// ascending bitonic sort of npad (power of two) entries
-__device__ void bitonic_sort(SortBuf s, int npad) {
-  for (int size = 2; size <= npad; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < (npad >> 1); i += blockDim.x) {
-        int lo = 2 * i - (i & (stride - 1));
-        int hi = lo + stride;
-        bool up = ((lo & size) == 0);
-        uint64_t a1 = s.k1[lo], a2 = s.k2[lo], b1 = s.k1[hi], b2 = s.k2[hi];
-        uint32_t ai = s.id[lo], bi = s.id[hi];
-        bool swap = up ? before(b1, b2, bi, a1, a2, ai) : before(a1, a2, ai, b1, b2, bi);
-        if (swap) {
-          s.k1[lo] = b1; s.k2[lo] = b2; s.id[lo] = bi;
-          s.k1[hi] = a1; s.k2[hi] = a2; s.id[hi] = ai;
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
-
-// block-wide exclusive scan of a 0/1 flag; returns prefix, writes total to *total
-__device__ __forceinline__ int block_scan_flag(int flag, int *warp_tot, int *total) {
+// block-wide exclusive scan of a 0/1 flag; returns prefix, writes total to sh.total
+__device__ __forceinline__ int block_scan_flag(int flag, Shared &sh) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned bal = __ballot_sync(0xffffffffu, flag);
   int in_warp = __popc(bal & ((1u << lane) - 1u));
-  if (lane == 0) warp_tot[warp] = __popc(bal);
+  if (lane == 0) sh.warp_tot[warp] = __popc(bal);
   __syncthreads();
   if (warp == 0) {
-    int v = (lane < (blockDim.x >> 5)) ? warp_tot[lane] : 0;
+    int v = (lane < (int)(blockDim.x >> 5)) ? sh.warp_tot[lane] : 0;
     int x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       int y = __shfl_up_sync(0xffffffffu, x, o);
       if (lane >= o) x += y;
     }
-    warp_tot[32 + lane] = x - v;  // exclusive
-    if (lane == 31) *total = x;
+    sh.warp_tot[32 + lane] = x - v;  // exclusive
+    if (lane == 31) sh.total = x;
   }
   __syncthreads();
-  int r = warp_tot[32 + warp] + in_warp;
+  int r = sh.warp_tot[32 + warp] + in_warp;
   __syncthreads();
   return r;
 }
 
-__device__ __forceinline__ void token_mask(const int32_t *routes, int P, long long T, int k, long long tok,
-                                           uint64_t m[kWords]) {
+// block-wide sums of kPiv+1 per-thread counters (result in sh.tot)
+__device__ __forceinline__ void block_sum(int (&c)[kPiv + 1], Shared &sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int w = 0; w < kWords; ++w) m[w] = 0;
-  for (int p = 0; p < P; ++p) {
-    const int32_t *r = routes + ((long long)p * T + tok) * k;
-    for (int j = 0; j < k; ++j) {
-      int e = r[j];
-      m[e >> 6] |= 1ull << (e & 63);
+  for (int j = 0; j <= kPiv; ++j) {
+    int v = __reduce_add_sync(0xffffffffu, c[j]);
+    if (lane == 0) sh.red[warp][j] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x <= kPiv) {
+    int s = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh.red[w][threadIdx.x];
+    sh.tot[threadIdx.x] = s;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void block_minmax(unsigned long long lo, unsigned long long hi, Shared &sh,
+                                             unsigned long long *out_lo, unsigned long long *out_hi) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, o), b = __shfl_xor_sync(0xffffffffu, hi, o);
+    lo = a < lo ? a : lo;
+    hi = b > hi ? b : hi;
+  }
+  if (lane == 0) { sh.kmin[warp] = lo; sh.kmax[warp] = hi; }
+  __syncthreads();
+  lo = ~0ull;
+  hi = 0ull;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+    lo = sh.kmin[w] < lo ? sh.kmin[w] : lo;
+    hi = sh.kmax[w] > hi ? sh.kmax[w] : hi;
+  }
+  *out_lo = lo;
+  *out_hi = hi;
+  __syncthreads();
+}
+
+// Threshold search: among candidate tokens (cand(t) true) with keys key(t), the
+// largest T with count(key >= T) >= need (need >= 1 and <= #candidates).
+// Returns T and count(key > T).  All threads of the block must call it.
+template <class Cand, class Key>
+__device__ void block_threshold(int n_tok, int need, Cand cand, Key key, Shared &sh, unsigned long long *T_out,
+                                int *gt_out) {
+  unsigned long long lo = ~0ull, hi = 0ull;
+  for (int t = threadIdx.x; t < n_tok; t += blockDim.x)
+    if (cand(t)) {
+      unsigned long long k = key(t);
+      lo = k < lo ? k : lo;
+      hi = k > hi ? k : hi;
     }
+  block_minmax(lo, hi, sh, &lo, &hi);
+  // invariant: count(key >= lo) >= need ; count(key > hi) == above < need
+  int above = 0;
+  while (lo < hi) {
+    const unsigned long long w = hi - lo;  // span - 1
+    unsigned long long off[kPiv + 1];
+    bool valid[kPiv + 1];
+#pragma unroll
+    for (int j = 1; j <= kPiv; ++j) {
+      // floor((w + 1) * j / 8) without overflow; strictly increasing when w >= 7
+      unsigned long long o = (w / 8) * j + ((w % 8 + 1) * (unsigned long long)j) / 8;
+      if (w < 7) o = (unsigned long long)j;
+      off[j] = o;
+      valid[j] = o <= w;
+    }
+    unsigned long long q[kPiv + 1];
+#pragma unroll
+    for (int j = 1; j <= kPiv; ++j) q[j] = valid[j] ? lo + off[j] : ~0ull;  // <= hi: no overflow
+    int c[kPiv + 1];
+#pragma unroll
+    for (int j = 0; j <= kPiv; ++j) c[j] = 0;
+    for (int t = threadIdx.x; t < n_tok; t += blockDim.x)
+      if (cand(t)) {
+        const unsigned long long k = key(t);  // count(key >= q_j) over ALL candidates
+#pragma unroll
+        for (int j = 1; j <= kPiv; ++j) c[j] += (valid[j] && k >= q[j]) ? 1 : 0;
+      }
+    block_sum(c, sh);
+    int js = 0;
+#pragma unroll
+    for (int j = 1; j <= kPiv; ++j)
+      if (valid[j] && sh.tot[j] >= need) js = j;
+    unsigned long long nlo = lo + (js ? off[js] : 0ull), nhi = hi;
+    if (js < kPiv && valid[js + 1]) {
+      nhi = lo + off[js + 1] - 1;
+      above = sh.tot[js + 1];
+    }
+    lo = nlo;
+    hi = nhi;
+    __syncthreads();  // sh.tot is rewritten by the next step
+  }
+  *T_out = lo;
+  *gt_out = above;
+}
+
+// Mark, in id order, the first r candidates with key == T (ties at the threshold).
+template <class Tie, class Mark>
+__device__ void block_mark_first(int n_tok, int r, Tie tie, Mark mark, Shared &sh) {
+  int done = 0;
+  for (int c0 = 0; c0 < n_tok && done < r; c0 += blockDim.x) {
+    const int t = c0 + threadIdx.x;
+    const int f = (t < n_tok) && tie(t);
+    const int pre = block_scan_flag(f, sh);
+    if (f && done + pre < r) mark(t);
+    done += sh.total;
+    __syncthreads();
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+__device__ __forceinline__ int token_mask(const int32_t *__restrict__ routes, int P, long long T, int k, int E,
+                                          long long tok, uint64_t (&m)[kWords]) {
+#pragma unroll
+  for (int w = 0; w < kWords; ++w) m[w] = 0;
+  int bad = 0;
+  for (int p = 0; p < P; ++p) {
+    const int32_t *r = routes + ((long long)p * T + tok) * k;
+    for (int j = 0; j < k; ++j) {
+      const int e = __ldg(r + j);
+      if ((unsigned)e >= (unsigned)E) {
+        bad = 1;
+        continue;
+      }
+      m[e >> 6] |= 1ull << (e & 63);
+    }
+  }
+  return bad;
+}
+
+template <int kT>
+__global__ void __launch_bounds__(kT)
 prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, const int32_t *__restrict__ routes,
              const int32_t *__restrict__ req_off, const int32_t *__restrict__ kcore_arr,
-             const int32_t *__restrict__ kkeep_arr, long long T, int P, int k, double lam, int npad,
-             double *__restrict__ s_norm_out, double *__restrict__ delta_out, double *__restrict__ score_out,
-             uint8_t *__restrict__ flags_out, int32_t *__restrict__ retained, int32_t *__restrict__ n_retained,
-             uint64_t *__restrict__ target_out, int32_t *__restrict__ status) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  SortBuf sb;
-  sb.k1 = reinterpret_cast<uint64_t *>(smem);
-  sb.k2 = sb.k1 + npad;
-  sb.id = reinterpret_cast<uint32_t *>(sb.k2 + npad);
-  int32_t *vis_tok = reinterpret_cast<int32_t *>(sb.id + npad);  // [npad]
-  uint8_t *vflag = reinterpret_cast<uint8_t *>(vis_tok + npad);  // [npad] bit0 core bit1 keep
-  __shared__ int warp_tot[64];
-  __shared__ int s_total, s_nvis, s_bad;
-  __shared__ double s_lo[32], s_hi[32];
-  __shared__ unsigned long long s_target[kWords];
-
+             const int32_t *__restrict__ kkeep_arr, double alpha, double beta, long long T, int P, int k, int E,
+             double lam, double *s_norm_out, double *delta_out, double *score_out, uint8_t *flags_out,
+             int32_t *__restrict__ retained, int32_t *__restrict__ n_retained, uint64_t *__restrict__ target_out,
+             int32_t *__restrict__ status) {
+  __shared__ Shared sh;
   const int r = blockIdx.x;
   const long long base = req_off[r];
   const int n_tok = req_off[r + 1] - req_off[r];
-  const int k_core = kcore_arr[r], k_keep = kkeep_arr[r];
   const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  const double *s_req = sal + base;
+  const uint8_t *m_req = mod + base;
+  double *sn = s_norm_out + base, *dl = delta_out + base, *sc = score_out + base;
+  uint8_t *fl = flags_out + base;
 
-  if (threadIdx.x == 0) { s_nvis = 0; s_bad = 0; }
-  if (threadIdx.x < kWords) s_target[threadIdx.x] = 0ull;
-  for (int t = threadIdx.x; t < n_tok; t += blockDim.x) {
-    s_norm_out[base + t] = qnan;
-    delta_out[base + t] = qnan;
-    score_out[base + t] = qnan;
-    flags_out[base + t] = 0;
-  }
-  __syncthreads();
+  if (threadIdx.x < kWords) sh.target[threadIdx.x] = 0ull;
 
-  // 1. visual positions in id order
-  for (int c0 = 0; c0 < n_tok; c0 += blockDim.x) {
-    int t = c0 + threadIdx.x;
-    int f = (t < n_tok) && mod[base + t] == 0;
-    int pre = block_scan_flag(f, warp_tot, &s_total);
-    int nv = s_nvis;
-    if (f && nv + pre < npad) vis_tok[nv + pre] = t;
-    __syncthreads();
-    if (threadIdx.x == 0) s_nvis = nv + s_total;
-    __syncthreads();
-  }
-  const int n = s_nvis;
-  if (n > kMaxVisual || n > npad) {
-    if (threadIdx.x == 0) status[r] = 2;
-    return;
-  }
-
-  // 2. validation + min/max
+  // 1. outputs reset, visual count, saliency validation and min/max (compress.py:104-114)
   double lo = INFINITY, hi = -INFINITY;
-  int bad = 0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    double v = sal[base + vis_tok[i]];
-    if (!isfinite(v) || v < 0.0) bad = 1;
-    lo = fmin(lo, v);
-    hi = fmax(hi, v);
+  int nv = 0, bad = 0;
+  for (int t = threadIdx.x; t < n_tok; t += kT) {
+    sn[t] = qnan;
+    dl[t] = qnan;
+    sc[t] = qnan;
+    fl[t] = 0;
+    if (m_req[t] == 0) {
+      const double v = s_req[t];
+      if (!isfinite(v) || v < 0.0) bad = 1;
+      lo = fmin(lo, v);
+      hi = fmax(hi, v);
+      ++nv;
+    }
   }
-  if (__syncthreads_or(bad)) {
-    if (threadIdx.x == 0) status[r] = 1;
-    return;
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-  }
-  if ((threadIdx.x & 31) == 0) { s_lo[threadIdx.x >> 5] = lo; s_hi[threadIdx.x >> 5] = hi; }
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    lo = threadIdx.x < (blockDim.x >> 5) ? s_lo[threadIdx.x] : INFINITY;
-    hi = threadIdx.x < (blockDim.x >> 5) ? s_hi[threadIdx.x] : -INFINITY;
+  {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
       hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
     }
-    if (threadIdx.x == 0) { s_lo[0] = lo; s_hi[0] = hi; }
+    nv = __reduce_add_sync(0xffffffffu, nv);
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if (lane == 0) { sh.dlo[warp] = lo; sh.dhi[warp] = hi; sh.red[warp][0] = nv; sh.red[warp][1] = bad; }
+    __syncthreads();
+    lo = INFINITY;
+    hi = -INFINITY;
+    nv = 0;
+    bad = 0;
+    for (int w = 0; w < kT / 32; ++w) {
+      lo = fmin(lo, sh.dlo[w]);
+      hi = fmax(hi, sh.dhi[w]);
+      nv += sh.red[w][0];
+      bad |= sh.red[w][1];
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  lo = s_lo[0];
-  hi = s_hi[0];
+  if (bad) {
+    if (threadIdx.x == 0) { status[r] = 1; n_retained[r] = 0; }
+    return;
+  }
+  int k_core, k_keep;
+  if (kcore_arr) {
+    k_core = kcore_arr[r];
+    k_keep = kkeep_arr[r];
+  } else {  // compress.py:151-152: floor(alpha * n_visual) -- one correctly rounded product
+    k_core = (int)floor(__dmul_rn(alpha, (double)nv));
+    k_keep = (int)floor(__dmul_rn(beta, (double)nv));
+  }
+  if (k_keep < k_core || k_core < 0) {  // compress.py:153-154
+    if (threadIdx.x == 0) { status[r] = 3; n_retained[r] = 0; }
+    return;
+  }
+  if (k_keep > nv) k_keep = nv;
+  if (k_core > nv) k_core = nv;
+
+  // 2. normalised saliency
   const double span = __dsub_rn(hi, lo);
+  for (int t = threadIdx.x; t < n_tok; t += kT)
+    if (m_req[t] == 0) sn[t] = (hi == lo) ? 0.5 : __ddiv_rn(__dsub_rn(s_req[t], lo), span);
+  __syncthreads();
 
-  // 3. normalised saliency + core sort keys
-  for (int i = threadIdx.x; i < npad; i += blockDim.x) {
-    if (i < n) {
-      double v = sal[base + vis_tok[i]];
-      double s = (hi == lo) ? 0.5 : __ddiv_rn(__dsub_rn(v, lo), span);
-      s_norm_out[base + vis_tok[i]] = s;
-      sb.k1[i] = ~vmm::ord_key(s);
-      sb.k2[i] = 0;
-      sb.id[i] = (uint32_t)i;
-      vflag[i] = 0;
+  auto is_vis = [&](int t) { return m_req[t] == 0; };
+  auto key_s = [&](int t) { return vmm::ord_key(sn[t]); };
+
+  // 3. salient core: top k_core by (-s_norm, id)
+  if (k_core > 0) {
+    if (k_core >= nv) {
+      for (int t = threadIdx.x; t < n_tok; t += kT)
+        if (m_req[t] == 0) fl[t] = 1;
     } else {
-      sb.k1[i] = ~0ull; sb.k2[i] = ~0ull; sb.id[i] = 0xffffffffu;
+      unsigned long long Ts;
+      int gt;
+      block_threshold(n_tok, k_core, is_vis, key_s, sh, &Ts, &gt);
+      for (int t = threadIdx.x; t < n_tok; t += kT)
+        if (m_req[t] == 0 && key_s(t) > Ts) fl[t] = 1;
+      __syncthreads();
+      block_mark_first(n_tok, k_core - gt, [&](int t) { return m_req[t] == 0 && key_s(t) == Ts; },
+                       [&](int t) { fl[t] = 1; }, sh);
     }
   }
-  __syncthreads();
-  bitonic_sort(sb, npad);
-  for (int i = threadIdx.x; i < k_core; i += blockDim.x) vflag[sb.id[i]] = 1;
   __syncthreads();
 
-  // 4. target expert set of the core
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    if (vflag[i] & 1) {
-      uint64_t m[kWords];
-      token_mask(routes, P, T, k, base + vis_tok[i], m);
+  // 4. target expert set = OR of the core tokens' prefix masks
+  {
+    uint64_t acc[kWords] = {};
+    int ebad = 0;
+    for (int t = threadIdx.x; t < n_tok; t += kT)
+      if (fl[t] & 1) {
+        uint64_t m[kWords];
+        ebad |= token_mask(routes, P, T, k, E, base + t, m);
 #pragma unroll
-      for (int w = 0; w < kWords; ++w)
-        if (m[w]) atomicOr(&s_target[w], (unsigned long long)m[w]);
+        for (int w = 0; w < kWords; ++w) acc[w] |= m[w];
+      }
+#pragma unroll
+    for (int w = 0; w < kWords; ++w) {
+      unsigned lo32 = __reduce_or_sync(0xffffffffu, (unsigned)acc[w]);
+      unsigned hi32 = __reduce_or_sync(0xffffffffu, (unsigned)(acc[w] >> 32));
+      if ((threadIdx.x & 31) == 0 && (lo32 | hi32))
+        atomicOr(&sh.target[w], ((unsigned long long)hi32 << 32) | lo32);
     }
+    bad = __syncthreads_or(ebad);
   }
-  __syncthreads();
   uint64_t tg[kWords];
 #pragma unroll
-  for (int w = 0; w < kWords; ++w) tg[w] = s_target[w];
+  for (int w = 0; w < kWords; ++w) tg[w] = sh.target[w];
 
-  // 5. marginal expansion + score; extras sort keys
-  for (int i = threadIdx.x; i < npad; i += blockDim.x) {
-    if (i < n && !(vflag[i] & 1)) {
-      long long tok = base + vis_tok[i];
-      uint64_t m[kWords];
-      token_mask(routes, P, T, k, tok, m);
-      int sz = 0, out = 0;
+  // 5. marginal expansion + score for the non-core visual tokens (compress.py:163-172)
+  {
+    int ebad = 0;
+    for (int t = threadIdx.x; t < n_tok; t += kT)
+      if (m_req[t] == 0 && !(fl[t] & 1)) {
+        uint64_t m[kWords];
+        ebad |= token_mask(routes, P, T, k, E, base + t, m);
+        int sz = 0, out = 0;
 #pragma unroll
-      for (int w = 0; w < kWords; ++w) { sz += __popcll(m[w]); out += __popcll(m[w] & ~tg[w]); }
-      double d = __ddiv_rn((double)out, (double)sz);
-      double s = s_norm_out[tok];
-      double p = __dsub_rn(s, __dmul_rn(lam, d));
-      delta_out[tok] = d;
-      score_out[tok] = p;
-      sb.k1[i] = ~vmm::ord_key(p);
-      sb.k2[i] = ~vmm::ord_key(s);
-      sb.id[i] = (uint32_t)i;
+        for (int w = 0; w < kWords; ++w) { sz += __popcll(m[w]); out += __popcll(m[w] & ~tg[w]); }
+        const double d = __ddiv_rn((double)out, (double)sz);
+        dl[t] = d;
+        sc[t] = __dsub_rn(sn[t], __dmul_rn(lam, d));
+      }
+    bad |= __syncthreads_or(ebad);
+  }
+  if (bad) {  // an expert id outside [0, E) in the prefix routes (TraceError)
+    if (threadIdx.x == 0) { status[r] = 4; n_retained[r] = 0; }
+    return;
+  }
+
+  // 6. extras: top (k_keep - k_core) non-core visual tokens by (-score, -s_norm, id)
+  const int need = k_keep - k_core;
+  auto is_rest = [&](int t) { return m_req[t] == 0 && !(fl[t] & 1); };
+  if (need > 0) {
+    if (need >= nv - k_core) {
+      for (int t = threadIdx.x; t < n_tok; t += kT)
+        if (is_rest(t)) fl[t] |= 2;
     } else {
-      sb.k1[i] = ~0ull; sb.k2[i] = ~0ull; sb.id[i] = 0xffffffffu;
+      auto key_p = [&](int t) { return vmm::ord_key(sc[t]); };
+      unsigned long long Tp, Ts;
+      int gtp, gts;
+      block_threshold(n_tok, need, is_rest, key_p, sh, &Tp, &gtp);
+      const int r1 = need - gtp;  // from the score ties, by s_norm
+      auto tie_p = [&](int t) { return is_rest(t) && key_p(t) == Tp; };
+      block_threshold(n_tok, r1, tie_p, key_s, sh, &Ts, &gts);
+      const int r2 = r1 - gts;  // from the (score, s_norm) ties, by id
+      for (int t = threadIdx.x; t < n_tok; t += kT)
+        if (is_rest(t)) {
+          const unsigned long long kp = key_p(t);
+          if (kp > Tp || (kp == Tp && key_s(t) > Ts)) fl[t] |= 2;
+        }
+      __syncthreads();
+      block_mark_first(n_tok, r2, [&](int t) { return tie_p(t) && key_s(t) == Ts; }, [&](int t) { fl[t] |= 2; },
+                       sh);
     }
   }
   __syncthreads();
-  bitonic_sort(sb, npad);
-  for (int i = threadIdx.x; i < k_keep - k_core; i += blockDim.x) vflag[sb.id[i]] |= 2;
-  __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x)
-    if (vflag[i] & 1) vflag[i] |= 2;
+  for (int t = threadIdx.x; t < n_tok; t += kT)
+    if (fl[t] & 1) fl[t] |= 2;
   if (threadIdx.x < kWords) target_out[(long long)r * kWords + threadIdx.x] = tg[threadIdx.x];
   __syncthreads();
 
-  // 6. retained = keep U text, ascending ids (recompute visual positions in the same order)
-  if (threadIdx.x == 0) { s_nvis = 0; s_bad = 0; }
-  __syncthreads();
+  // 7. retained = keep U text, ascending request-local ids (compress.py:63-65)
   int n_ret = 0;
-  for (int c0 = 0; c0 < n_tok; c0 += blockDim.x) {
-    int t = c0 + threadIdx.x;
-    int m = (t < n_tok) ? mod[base + t] : 3;
-    int isv = (m == 0);
-    int vpre = block_scan_flag(isv, warp_tot, &s_total);
-    int vbase = s_nvis;
-    int vt = s_total;
-    int keepv = isv ? ((vflag[vbase + vpre] >> 1) & 1) : 0;
-    int f = (m == 1) || keepv;
-    int pre = block_scan_flag(f, warp_tot, &s_total);
-    if (f) retained[base + n_ret + pre] = t;
-    if (t < n_tok) {
-      uint8_t fl = 0;
-      if (isv) fl = vflag[vbase + vpre] & 3;
-      if (f) fl |= 4;
-      flags_out[base + t] = fl;
+  for (int c0 = 0; c0 < n_tok; c0 += kT) {
+    const int t = c0 + threadIdx.x;
+    int f = 0;
+    if (t < n_tok) f = (m_req[t] == 1) || (fl[t] & 2);
+    const int pre = block_scan_flag(f, sh);
+    if (f) {
+      retained[base + n_ret + pre] = t;
+      fl[t] |= 4;
     }
-    n_ret += s_total;
-    __syncthreads();
-    if (threadIdx.x == 0) s_nvis = vbase + vt;
-    __syncthreads();
+    n_ret += sh.total;
   }
   if (threadIdx.x == 0) { n_retained[r] = n_ret; status[r] = 0; }
+}
+
+// Pack the per-request retained lists into one ascending list of GLOBAL row ids
+// (request r's ids + req_off[r]) and the per-request offsets into it.
+__global__ void retained_pack_kernel(const int32_t *__restrict__ req_off, const int32_t *__restrict__ retained,
+                                     const int32_t *__restrict__ n_retained, int R, int32_t *__restrict__ out,
+                                     int32_t *__restrict__ out_off) {
+  __shared__ int s_off;
+  const int r = blockIdx.x;
+  int acc = 0;
+  for (int i = threadIdx.x; i < r; i += blockDim.x) acc += n_retained[i];
+  acc = __reduce_add_sync(0xffffffffu, acc);
+  if (threadIdx.x == 0) s_off = 0;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(&s_off, acc);
+  __syncthreads();
+  const int off = s_off, n = n_retained[r], b = req_off[r];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) out[off + i] = retained[b + i] + b;
+  if (threadIdx.x == 0) {
+    out_off[r] = off;
+    if (r == R - 1) out_off[R] = off + n;
+  }
 }
 
 __global__ void gather_rows_kernel(const uint4 *__restrict__ src, const int32_t *__restrict__ idx, int n,
@@ -286,27 +431,36 @@ __global__ void gather_rows_kernel(const uint4 *__restrict__ src, const int32_t 
 }  // namespace
 
 extern "C" int vmm_prune(const double *d_saliency, const uint8_t *d_modality, const int32_t *d_routes,
-                         const int32_t *d_req_off, const int32_t *d_k_core, const int32_t *d_k_keep, int R,
-                         int T, int P, int k, int experts, double lam, double *d_s_norm, double *d_delta,
-                         double *d_score, uint8_t *d_flags, int32_t *d_retained, int32_t *d_n_retained,
-                         uint64_t *d_target, int32_t *d_status, void *stream) {
+                         const int32_t *d_req_off, const int32_t *d_k_core, const int32_t *d_k_keep, double alpha,
+                         double beta, int R, int T, int P, int k, int experts, double lam, double *d_s_norm,
+                         double *d_delta, double *d_score, uint8_t *d_flags, int32_t *d_retained,
+                         int32_t *d_n_retained, uint64_t *d_target, int32_t *d_status, void *stream) {
   if (R <= 0) return VMM_OK;
   if (experts < 1 || experts > VMM_MAX_EXPERTS) return vmm::fail(VMM_EVALIDATION, "experts must lie in [1, 256]");
   if (P < 1 || k < 1) return vmm::fail(VMM_EVALIDATION, "prefix_layers must be non-empty and k >= 1");
-  int npad = 2;
-  while (npad < kMaxVisual && npad < T) npad <<= 1;
-  size_t smem = (size_t)npad * (8 + 8 + 4 + 4 + 1);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(prune_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)((size_t)kMaxVisual * 25));
-    if (e != cudaSuccess) return vmm::cuda_status(e, "prune attr");
-    attr_set = true;
+  if ((d_k_core == nullptr) != (d_k_keep == nullptr))
+    return vmm::fail(VMM_ECONTRACT, "k_core and k_keep must both be given or both be NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  // a few requests: 1024 threads each (latency); a batch: 256 threads, up to 8 CTAs per SM (throughput)
+  if (R >= 64) {
+    prune_kernel<256><<<R, 256, 0, st>>>(d_saliency, d_modality, d_routes, d_req_off, d_k_core, d_k_keep, alpha,
+                                         beta, (long long)T, P, k, experts, lam, d_s_norm, d_delta, d_score,
+                                         d_flags, d_retained, d_n_retained, d_target, d_status);
+  } else {
+    prune_kernel<1024><<<R, 1024, 0, st>>>(d_saliency, d_modality, d_routes, d_req_off, d_k_core, d_k_keep, alpha,
+                                           beta, (long long)T, P, k, experts, lam, d_s_norm, d_delta, d_score,
+                                           d_flags, d_retained, d_n_retained, d_target, d_status);
   }
-  prune_kernel<<<R, kThreads, smem, (cudaStream_t)stream>>>(
-      d_saliency, d_modality, d_routes, d_req_off, d_k_core, d_k_keep, (long long)T, P, k, lam, npad, d_s_norm,
-      d_delta, d_score, d_flags, d_retained, d_n_retained, d_target, d_status);
   VMM_LAUNCH_CHECK("prune_kernel");
+  return VMM_OK;
+}
+
+extern "C" int vmm_retained_pack(const int32_t *d_req_off, const int32_t *d_retained, const int32_t *d_n_retained,
+                                 int R, int32_t *d_out, int32_t *d_out_off, void *stream) {
+  if (R <= 0) return VMM_OK;
+  retained_pack_kernel<<<R, 256, 0, (cudaStream_t)stream>>>(d_req_off, d_retained, d_n_retained, R, d_out,
+                                                            d_out_off);
+  VMM_LAUNCH_CHECK("retained_pack_kernel");
   return VMM_OK;
 }
 

@@ -162,15 +162,18 @@ int vmm_xfer_copy(vmm_xfer *x, int slab, const void *h_src, void *d_dst, size_t 
   if ((e = cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyDefault, st)) != cudaSuccess)
     return cuda_status(e, "expert copy");
   x->fill_seq++;
+  if (x->ready) {  // ordered after the copy, with a memory barrier: readers polling ready[] see the data
+    CUresult r = write_value_fn()((CUstream)st, (CUdeviceptr)(x->ready + slab), (cuuint32_t)x->fill_seq, 0);
+    if (r != CUDA_SUCCESS) return vmm::fail(VMM_ECUDA, "cuStreamWriteValue32 failed (" + std::to_string((int)r) + ")");
+  }
+  // the fill event is recorded AFTER the flag write: a refill of this slab on another copy
+  // stream waits on it (write-after-write above), so the newer fill's flag can never be
+  // overwritten by this older one -- ready[slab] only moves forward
   if ((e = cudaEventRecord(x->fill_ev[(x->fill_seq - 1) % kRing], st)) != cudaSuccess)
     return cuda_status(e, "fill event");
   x->last_fill[k] = x->fill_seq;
   x->slab_fill_seq[slab] = x->fill_seq;
   x->slab_fill_stream[slab] = (int8_t)k;
-  if (x->ready) {  // ordered after the copy, with a memory barrier: readers polling ready[] see the data
-    CUresult r = write_value_fn()((CUstream)st, (CUdeviceptr)(x->ready + slab), (cuuint32_t)x->fill_seq, 0);
-    if (r != CUDA_SUCCESS) return vmm::fail(VMM_ECUDA, "cuStreamWriteValue32 failed (" + std::to_string((int)r) + ")");
-  }
   x->bytes += (double)bytes;
   x->copies++;
   return VMM_OK;

@@ -31,10 +31,13 @@ def _dev():
 # ---------------------------------------------------------------------------
 # prune
 # ---------------------------------------------------------------------------
-def prune(saliency, modality, prefix_routes, req_off, k_core, k_keep, experts: int, lam: float, stream=None):
+def prune(saliency, modality, prefix_routes, req_off, k_core, k_keep, experts: int, lam: float, stream=None,
+          alpha: float = 0.0, beta: float = 0.0):
     """Batched compression.  Shapes: saliency f64 [T], modality u8 [T],
-    prefix_routes i32 [P, T, k], req_off i32 [R+1], k_core/k_keep i32 [R].
-    Returns dict of device tensors (see include/vismmoe.h vmm_prune)."""
+    prefix_routes i32 [P, T, k], req_off i32 [R+1], k_core/k_keep i32 [R]
+    (or both None: budgets floor(alpha*n_visual), floor(beta*n_visual) per
+    request on the device).  Returns dict of device tensors (include/vismmoe.h
+    vmm_prune)."""
     L = _lib.lib()
     T = int(saliency.shape[0])
     P, _, k = (int(x) for x in prefix_routes.shape)
@@ -46,16 +49,30 @@ def prune(saliency, modality, prefix_routes, req_off, k_core, k_keep, experts: i
         score=torch.empty(T, dtype=torch.float64, device=dev),
         flags=torch.empty(T, dtype=torch.uint8, device=dev),
         retained=torch.empty(max(T, 1), dtype=_i32, device=dev),
-        n_retained=torch.empty(R, dtype=_i32, device=dev),
+        # n_retained and status side by side: one D2H reads both
+        ns=torch.full((2, R), -1, dtype=_i32, device=dev),
         target=torch.zeros(R, 4, dtype=torch.int64, device=dev),
-        status=torch.full((R,), -1, dtype=_i32, device=dev),
     )
+    out["n_retained"], out["status"] = out["ns"][0], out["ns"][1]
     _n(1)
-    check(L.vmm_prune(ptr(saliency), ptr(modality), ptr(prefix_routes), ptr(req_off), ptr(k_core), ptr(k_keep),
-                      R, T, P, k, experts, float(lam), ptr(out["s_norm"]), ptr(out["delta"]), ptr(out["score"]),
-                      ptr(out["flags"]), ptr(out["retained"]), ptr(out["n_retained"]), ptr(out["target"]),
-                      ptr(out["status"]), stream_ptr(stream)))
+    check(L.vmm_prune(ptr(saliency), ptr(modality), ptr(prefix_routes), ptr(req_off),
+                      None if k_core is None else ptr(k_core), None if k_keep is None else ptr(k_keep),
+                      float(alpha), float(beta), R, T, P, k, experts, float(lam), ptr(out["s_norm"]),
+                      ptr(out["delta"]), ptr(out["score"]), ptr(out["flags"]), ptr(out["retained"]),
+                      ptr(out["n_retained"]), ptr(out["target"]), ptr(out["status"]), stream_ptr(stream)))
     return out
+
+
+def retained_pack(req_off, retained, n_retained, stream=None, out=None, out_off=None):
+    """Per-request retained lists -> (global ascending row ids [T cap], offsets [R+1])."""
+    R = int(req_off.shape[0]) - 1
+    dev = retained.device
+    out = torch.empty(int(retained.shape[0]), dtype=_i32, device=dev) if out is None else out
+    out_off = torch.empty(R + 1, dtype=_i32, device=dev) if out_off is None else out_off
+    _n(1)
+    check(_lib.lib().vmm_retained_pack(ptr(req_off), ptr(retained), ptr(n_retained), R, ptr(out), ptr(out_off),
+                                       stream_ptr(stream)))
+    return out, out_off
 
 
 def gather_rows(src, idx, stream=None, out=None):
@@ -64,6 +81,16 @@ def gather_rows(src, idx, stream=None, out=None):
     out = torch.empty(n, H, dtype=src.dtype, device=src.device) if out is None else out
     _n(1)
     check(_lib.lib().vmm_gather_rows(ptr(src), ptr(idx), n, H, ptr(out), stream_ptr(stream)))
+    return out
+
+
+def gather_cols(src, idx, stream=None, out=None):
+    """Rows of an i32 or f32 [N, width] table by index (vmm_gather_i32/f32)."""
+    n, width = int(idx.shape[0]), int(src.shape[1])
+    out = torch.empty(n, width, dtype=src.dtype, device=src.device) if out is None else out
+    fn = {torch.int32: _lib.lib().vmm_gather_i32, torch.float32: _lib.lib().vmm_gather_f32}[src.dtype]
+    _n(1)
+    check(fn(ptr(src), ptr(idx), n, width, ptr(out), stream_ptr(stream)))
     return out
 
 

@@ -39,7 +39,6 @@ import torch
 
 from . import _lib, kernels
 from ._lib import check
-from .compress import CompressionConfig
 from .configs import Workload
 from .errors import ContractError, ValidationError
 from .pipeline import Engine, PredictorSpec, SimConfig, SimReport
@@ -272,6 +271,9 @@ class MoEStack:
         home=ShardedHome(...): from the sharded HBM home copies (D2D / NVLink)."""
         if cfg.predictor == "oracle" and cfg.routing != "trace":
             raise ValidationError("the oracle predictor needs trace routing (future routes)")
+        if not 1 <= cfg.l_pinned <= cfg.layers:
+            # the prune reads the pinned prefix's routes (prefix_layers non-empty, compress.py:41-42)
+            raise ValidationError("the stack needs 1 <= l_pinned <= layers")
         self.cfg = cfg
         self.store = store or ExpertStore(cfg, seed)
         self.device = self.store.device
@@ -534,39 +536,40 @@ class MoEStack:
             last = (cur, xn_l, ids_l, gates_l)
 
 
-        # --- prune (token compression) on the prefix routes, one CTA per request
+        # --- prune (token compression) on the prefix routes, one CTA per request; budgets
+        # floor(alpha n_vis) / floor(beta n_vis) on the device, then the per-request lists are
+        # packed into one ascending list of global rows.  One small D2H (retained counts +
+        # status) is the only host sync: the row count sizes every later launch.
         offs = [0, T] if req_off is None else [int(v) for v in req_off]
         R = len(offs) - 1
-        mod_h = modality.cpu().numpy() if isinstance(modality, torch.Tensor) else np.asarray(modality)
-        ccfg = CompressionConfig(c.alpha, c.beta, c.lam, tuple(range(lp)) if lp else (0,))
-        budgets = [ccfg.budgets(int((mod_h[offs[r]:offs[r + 1]] == 0).sum())) for r in range(R)]
-        pr = kernels.prune(saliency, modality, prefix[:max(lp, 1)],
-                           torch.tensor(offs, dtype=torch.int32, device=dev),
-                           torch.tensor([b[0] for b in budgets], dtype=torch.int32, device=dev),
-                           torch.tensor([b[1] for b in budgets], dtype=torch.int32, device=dev), E, c.lam)
-        n_ret = pr["n_retained"].cpu().numpy()
-        if (pr["status"].cpu().numpy() != 0).any():
-            raise ValidationError("saliency entries must be finite and >= 0")
-        if R == 1:
-            ret = pr["retained"][: int(n_ret[0])]
-        else:  # request-local ids -> global row ids, requests in order (constant launch count in R)
-            starts = torch.tensor(offs[:-1], dtype=torch.int32, device=dev)
-            lens = torch.tensor([offs[r + 1] - offs[r] for r in range(R)], dtype=torch.int64, device=dev)
-            seg = torch.repeat_interleave(torch.arange(R, device=dev), lens, output_size=T)
-            local = torch.arange(T, dtype=torch.int32, device=dev) - starts[seg]
-            valid = local < torch.from_numpy(n_ret.astype(np.int32)).to(dev)[seg]
-            ret = (pr["retained"][:T] + starts[seg])[valid]
-        n_r = int(ret.shape[0])
+        offs_d = torch.tensor(offs, dtype=torch.int32).pin_memory().to(dev, non_blocking=True)
+        pr = kernels.prune(saliency, modality, prefix[:max(lp, 1)], offs_d, None, None, E, c.lam,
+                           alpha=c.alpha, beta=c.beta)
+        ret_all, ret_off_d = kernels.retained_pack(offs_d, pr["retained"], pr["n_retained"])
+        ns = self._ns_host[:, :R] if getattr(self, "_ns_host", None) is not None and \
+            self._ns_host.shape[1] >= R else None
+        if ns is None:
+            self._ns_host = torch.empty((2, max(R, 1)), dtype=torch.int32, pin_memory=True)
+            ns = self._ns_host[:, :R]
+        ns.copy_(pr["ns"], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        n_ret = ns[0].numpy().astype(np.int64)
+        st = ns[1].numpy()
+        if (st != 0).any():
+            from .compress import raise_prune_status
+
+            raise_prune_status(int(st[st != 0][0]))
         ret_off = np.concatenate([[0], np.cumsum(n_ret)]).astype(np.int64)
+        n_r = int(ret_off[-1])
+        ret = ret_all[:n_r]
         if last is None:
             xr = kernels.gather_rows(cur, ret, out=bufs["xp"][:n_r])  # scratch until permute of layer lp
             xr = xr.clone()
         else:  # layer lp-1's experts on the retained rows only
             cur_l, xn_l, ids_l, gates_l = last
-            rl = ret.long()
             x_ret = kernels.gather_rows(cur_l, ret)
             xn_ret = kernels.gather_rows(xn_l, ret)
-            ids_ret, gates_ret = ids_l[rl].contiguous(), gates_l[rl].contiguous()
+            ids_ret, gates_ret = kernels.gather_cols(ids_l, ret), kernels.gather_cols(gates_l, ret)
             M = n_r * k
             off, src, pos, xp = kernels.permute(ids_ret, xn_ret, E, bufs=(bufs["off"], bufs["src"][:M], bufs["pos"][:M]),
                                                 out=bufs["xp"][:M])

@@ -121,3 +121,84 @@ def test_gather_rows_compacts_hidden_states():
     idx = torch.tensor([0, 5, 7, 99, 42], dtype=torch.int32, device="cuda")
     y = kernels.gather_rows(x, idx)
     assert torch.equal(y, x[idx.long()])
+
+
+def _batch(rng, specs, P, k, E, ties=True):
+    sal, mod, routes, offs = [], [], [], [0]
+    for nv, nt in specs:
+        n = nv + nt
+        s = rng.integers(0, 6, size=n).astype(float) if ties else rng.gamma(2.0, 1.0, size=n)
+        m = np.r_[np.zeros(nv, np.uint8), np.ones(nt, np.uint8)]
+        rng.shuffle(m)
+        r = np.stack([np.stack([rng.choice(E, size=k, replace=False) for _ in range(n)]) if n else
+                      np.zeros((0, k), int) for _ in range(P)])
+        sal.append(s); mod.append(m); routes.append(r); offs.append(offs[-1] + n)
+    dev = torch.device("cuda")
+    d = dict(sal=torch.from_numpy(np.concatenate(sal)).to(dev), mod=torch.from_numpy(np.concatenate(mod)).to(dev),
+             routes=torch.from_numpy(np.concatenate(routes, axis=1).astype(np.int32)).to(dev),
+             offs=torch.tensor(offs, dtype=torch.int32, device=dev))
+    return d, sal, mod, routes, offs
+
+
+@pytest.mark.parametrize("lam", [0.0, 0.5, 1.0, 2.0, 5.0])
+def test_batched_device_budgets_both_cta_sizes_match_oracle(lam):
+    """R=70 requests (the 256-thread batch variant) and R=5 (the 1024-thread variant),
+    budgets floor(alpha n_vis)/floor(beta n_vis) computed on the device, heavy ties
+    (integer saliencies, A1 style, pkg/tests/test_acceptance.py:47-78), every lambda of A1;
+    the packed global retained list equals the concatenation of the oracle's."""
+    rng = np.random.default_rng(int(lam * 10) + 17)
+    P, k, E = 2, 3, 40
+    for R in (70, 5):
+        specs = [(int(rng.integers(0, 400)), int(rng.integers(0, 30))) for _ in range(R)]
+        d, sal, mod, routes, offs = _batch(rng, specs, P, k, E, ties=R == 70)
+        out = kernels.prune(d["sal"], d["mod"], d["routes"], d["offs"], None, None, E, lam, alpha=0.13, beta=0.55)
+        assert (out["status"].cpu().numpy() == 0).all()
+        packed, poff = kernels.retained_pack(d["offs"], out["retained"], out["n_retained"])
+        flags = out["flags"].cpu().numpy()
+        sc, dl = out["score"].cpu().numpy(), out["delta"].cpu().numpy()
+        packed, poff = packed.cpu().numpy(), poff.cpu().numpy()
+        for r in range(R):
+            o = compress_ref.compress(sal[r], mod[r], [], routes[r], E, 0.13, 0.55, lam, list(range(P)))
+            a, b = offs[r], offs[r + 1]
+            assert np.flatnonzero(flags[a:b] & 1).tolist() == o["core"], (R, r)
+            assert np.flatnonzero(flags[a:b] & 2).tolist() == o["keep"], (R, r)
+            assert packed[poff[r]:poff[r + 1]].tolist() == (np.asarray(o["retained"]) + a).tolist(), (R, r)
+            for pos, tok in enumerate(o["visual"]):
+                if not math.isnan(o["score"][pos]):
+                    assert sc[a + tok] == o["score"][pos] and dl[a + tok] == o["delta"][pos]
+
+
+def test_large_request_beyond_old_cap_matches_oracle():
+    """20 000 visual tokens in one request (the round-1 kernel refused > 8192) and a
+    C3-shaped request (2304 + 64, 8 prefix layers, E=128), both against the oracle."""
+    rng = np.random.default_rng(3)
+    for nv, nt, P, k, E in ((20000, 100, 2, 4, 64), (2304, 64, 8, 8, 128)):
+        d, sal, mod, routes, offs = _batch(rng, [(nv, nt)], P, k, E, ties=False)
+        out = kernels.prune(d["sal"], d["mod"], d["routes"], d["offs"], None, None, E, 2.0, alpha=0.1, beta=0.5)
+        assert int(out["status"].cpu()[0]) == 0
+        o = compress_ref.compress(sal[0], mod[0], [], routes[0], E, 0.1, 0.5, 2.0, list(range(P)))
+        flags = out["flags"].cpu().numpy()
+        assert np.flatnonzero(flags & 1).tolist() == o["core"]
+        assert np.flatnonzero(flags & 2).tolist() == o["keep"]
+        n = int(out["n_retained"].cpu()[0])
+        assert out["retained"][:n].cpu().numpy().tolist() == list(o["retained"])
+
+
+def test_prune_status_codes():
+    """alpha > beta -> status 3 (ValidationError); an expert id outside [0, E) -> status 4
+    (TraceError) instead of an out-of-bounds mask write."""
+    from paper_2605_05899_b200.compress import raise_prune_status
+    from paper_2605_05899_b200.errors import TraceError
+
+    rng = np.random.default_rng(9)
+    d, *_ = _batch(rng, [(50, 5)], 1, 2, 8)
+    out = kernels.prune(d["sal"], d["mod"], d["routes"], d["offs"], None, None, 8, 2.0, alpha=0.6, beta=0.3)
+    assert int(out["status"].cpu()[0]) == 3
+    with pytest.raises(ValidationError):
+        raise_prune_status(3)
+    bad = d["routes"].clone()
+    bad[0, 7, 1] = 200
+    out = kernels.prune(d["sal"], d["mod"], bad, d["offs"], None, None, 8, 2.0, alpha=0.1, beta=0.5)
+    assert int(out["status"].cpu()[0]) == 4
+    with pytest.raises(TraceError):
+        raise_prune_status(4)

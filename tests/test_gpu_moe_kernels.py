@@ -341,12 +341,18 @@ def test_refill_of_a_slab_lands_last_across_copy_streams():
     xf = C.c_void_p()
     _lib.check(L.vmm_xfer_create(2, nbytes, 1, C.byref(xf)))
     try:
-        for _ in range(4):
+        for i in range(4):
             # fill 2k+1 -> stream 0 (slab 0, bytes of a), fill 2k+2 -> stream 1 (slab 0 again, bytes of b)
             _lib.check(L.vmm_xfer_copy(xf, 0, a.data_ptr(), dst[0].data_ptr(), nbytes, 0))
             _lib.check(L.vmm_xfer_copy(xf, 0, b.data_ptr(), dst[0].data_ptr(), nbytes, 0))
             _lib.check(L.vmm_xfer_sync(xf))
             assert int(dst[0].min()) == 2 and int(dst[0].max()) == 2
+            # the slab's ready flag ends at the LAST fill's sequence (never moves backwards)
+            flags = torch.zeros(2, dtype=torch.int32, device="cuda")
+            _lib.check(L.vmm_copy_async(flags.data_ptr(), L.vmm_xfer_ready(xf), 8,
+                                        torch.cuda.current_stream().cuda_stream))
+            torch.cuda.synchronize()
+            assert int(flags[0]) == 2 * i + 2, (int(flags[0]), 2 * i + 2)
             dst.zero_()
             torch.cuda.synchronize()
     finally:
