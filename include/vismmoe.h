@@ -126,6 +126,11 @@ int vmm_mlp_predict(const double *d_hist /* [n_ctx][E] */, const double *d_emb, 
                     const double *d_w2, const double *d_b2, int d_bottleneck,
                     const double *d_wo, const double *d_bo,
                     double *d_feat /* nullable [n_ctx][E+2D] */, double *d_y, void *stream);
+/* Column means of emb[ids[i]] (rows with d_mod[row] != 0 skipped when d_mod is
+ * given) in numpy's axis-0 order, zeros when none: the MLP's static visual
+ * summary over the kept visual tokens (visual_summary, predictor.py:78-83). */
+int vmm_row_mean(const double *d_emb, int D, const int32_t *d_ids, int n, const uint8_t *d_mod, double *d_out,
+                 void *stream);
 /* Gate-reuse lookahead: counts of experts in the top-k of W_next applied to
  * layer-l hidden states, normalised by N*k -> y f64 [E]. */
 int vmm_normalize_counts(const uint32_t *d_counts, int E, double denom, double *d_y, void *stream);
@@ -461,6 +466,15 @@ typedef struct {
   uint32_t *need_host;                  /* nullable h pinned [L][E]: fill seq each expert's FFN waits for */
   uint32_t *need_dev;                   /* nullable d [L][E] (with need_host: flag-based copy overlap) */
   uint32_t *ffn_done;                   /* nullable d [cap*k/128 + E + 1] fused-FFN scratch (NULL: 2 launches) */
+  /* predictor 4 = MLP (predictor.py:521-550): features from the stack's own routes
+   * (history over counts[0..ctx]) + the request tokens' embeddings; fp64 weights row-major */
+  const double *mlp_emb;                /* d [tokens][mlp_dim] token embeddings (rows indexed by mlp_ids) */
+  const double *mlp_drift;              /* d [L][mlp_dim] cumulative layer drift (predictor.py:36-44) */
+  const double *mlp_hv;                 /* d [mlp_dim] kept-visual embedding mean (predictor.py:78-83) */
+  const int32_t *mlp_ids;               /* d [mlp_n_ids] retained token rows of mlp_emb */
+  int mlp_dim, mlp_n_ids, mlp_hidden, mlp_bottleneck;
+  const double *mlp_w1, *mlp_b1, *mlp_w2, *mlp_b2, *mlp_wo, *mlp_bo;
+  double *mlp_hist;                     /* d [E] scratch: the history feature of the context layer */
 } vmm_stack_desc;
 
 typedef struct {

@@ -59,6 +59,10 @@ class StackDesc(C.Structure):
         ("shared", I32), ("shared_slot_of", P), ("shared_src", P), ("shared_off", P),
         ("xs", P), ("h1s", P), ("ys", P),
         ("need_host", P), ("need_dev", P), ("ffn_done", P),
+        ("mlp_emb", P), ("mlp_drift", P), ("mlp_hv", P), ("mlp_ids", P),
+        ("mlp_dim", I32), ("mlp_n_ids", I32), ("mlp_hidden", I32), ("mlp_bottleneck", I32),
+        ("mlp_w1", P), ("mlp_b1", P), ("mlp_w2", P), ("mlp_b2", P), ("mlp_wo", P), ("mlp_bo", P),
+        ("mlp_hist", P),
     ]
 
 
@@ -82,6 +86,7 @@ _SIGS = {
     "vmm_oracle_targets": (I32, [P, I32, I32, P, I32, I32, P, P, P]),
     "vmm_history": (I32, [P, I32, I32, P, I32, P, P, P]),
     "vmm_mlp_predict": (I32, [P, P, I32, P, P, I32, P, P, I32, I32, P, P, I32, P, P, I32, P, P, P, P, P]),
+    "vmm_row_mean": (I32, [P, I32, P, I32, P, P, P]),
     "vmm_gate_lookahead": (I32, [P, P, I32, I32, I32, I32, P, P, P]),
     "vmm_permute_plan": (I32, [P, I32, I32, I32, P, P, P, P]),
     "vmm_permute_rows": (I32, [P, P, I32, I32, P, P]),

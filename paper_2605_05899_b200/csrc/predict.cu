@@ -147,6 +147,24 @@ __global__ void mlp_kernel(const double *__restrict__ hist, const double *__rest
   }
 }
 
+// column means of the selected rows (ids in the given order, rows with mod != 0
+// skipped when mod is given), accumulated row by row then divided by the count:
+// numpy's `emb[rows].mean(axis=0)` order (visual_summary, predictor.py:78-83)
+__global__ void row_mean_kernel(const double *__restrict__ emb, int D, const int32_t *__restrict__ ids, int n,
+                                const uint8_t *__restrict__ mod, double *__restrict__ out) {
+  for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < D; d += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    int cnt = 0;
+    for (int i = 0; i < n; ++i) {
+      const int r = ids[i];
+      if (mod && mod[r] != 0) continue;
+      s = __dadd_rn(s, emb[(long long)r * D + d]);
+      ++cnt;
+    }
+    out[d] = cnt ? __ddiv_rn(s, (double)cnt) : 0.0;
+  }
+}
+
 __global__ void normalize_counts_kernel(const uint32_t *__restrict__ counts, int E, double denom,
                                         double *__restrict__ y) {
   for (int e = threadIdx.x; e < E; e += blockDim.x) y[e] = denom > 0 ? (double)counts[e] / denom : 0.0;
@@ -208,6 +226,14 @@ extern "C" int vmm_mlp_predict(const double *d_hist, const double *d_emb, int D,
                                                          d_w1, d_b1, d_hidden, d_w2, d_b2, d_bottleneck, d_wo,
                                                          d_bo, d_feat, d_y);
   VMM_LAUNCH_CHECK("mlp_kernel");
+  return VMM_OK;
+}
+
+extern "C" int vmm_row_mean(const double *d_emb, int D, const int32_t *d_ids, int n, const uint8_t *d_mod,
+                            double *d_out, void *stream) {
+  if (D <= 0) return VMM_OK;
+  row_mean_kernel<<<(D + 127) / 128, 128, 0, (cudaStream_t)stream>>>(d_emb, D, d_ids, n, d_mod, d_out);
+  VMM_LAUNCH_CHECK("row_mean_kernel");
   return VMM_OK;
 }
 

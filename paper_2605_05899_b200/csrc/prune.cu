@@ -74,10 +74,10 @@ __device__ __forceinline__ void block_sum(int (&c)[kPiv + 1], Shared &sh) {
     if (lane == 0) sh.red[warp][j] = v;
   }
   __syncthreads();
-  if (threadIdx.x <= kPiv) {
-    int s = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh.red[w][threadIdx.x];
-    sh.tot[threadIdx.x] = s;
+  if (warp <= kPiv) {  // warp j sums counter j over the warps (blockDim >= 256: >= 8 warps)
+    int v = lane < (int)(blockDim.x >> 5) ? sh.red[lane][warp] : 0;
+    v = __reduce_add_sync(0xffffffffu, v);
+    if (lane == 0) sh.tot[warp] = v;
   }
   __syncthreads();
 }
@@ -122,40 +122,38 @@ __device__ void block_threshold(int n_tok, int need, Cand cand, Key key, Shared 
   int above = 0;
   while (lo < hi) {
     const unsigned long long w = hi - lo;  // span - 1
-    unsigned long long off[kPiv + 1];
-    bool valid[kPiv + 1];
-#pragma unroll
-    for (int j = 1; j <= kPiv; ++j) {
-      // floor((w + 1) * j / 8) without overflow; strictly increasing when w >= 7
-      unsigned long long o = (w / 8) * j + ((w % 8 + 1) * (unsigned long long)j) / 8;
-      if (w < 7) o = (unsigned long long)j;
-      off[j] = o;
-      valid[j] = o <= w;
-    }
-    unsigned long long q[kPiv + 1];
-#pragma unroll
-    for (int j = 1; j <= kPiv; ++j) q[j] = valid[j] ? lo + off[j] : ~0ull;  // <= hi: no overflow
+    // pivot offsets floor((w + 1) j / 8) without overflow (strictly increasing when w >= 7);
+    // for w < 7 the offsets are 1..w.  Computed, not indexed, so everything stays in registers.
+    auto off = [w](int j) -> unsigned long long {
+      return w < 7 ? (unsigned long long)j : (w / 8) * j + ((w % 8 + 1) * (unsigned long long)j) / 8;
+    };
+    const int nvalid = w < 7 ? (int)w : kPiv;
     int c[kPiv + 1];
 #pragma unroll
     for (int j = 0; j <= kPiv; ++j) c[j] = 0;
     for (int t = threadIdx.x; t < n_tok; t += blockDim.x)
       if (cand(t)) {
-        const unsigned long long k = key(t);  // count(key >= q_j) over ALL candidates
+        const unsigned long long kk = key(t);
+        // count(key >= lo + off(j)) over ALL candidates (keys outside [lo, hi] included)
+        const unsigned long long rel = kk < lo ? 0ull : (kk > hi ? ~0ull : kk - lo);
+        const bool in = kk >= lo;
 #pragma unroll
-        for (int j = 1; j <= kPiv; ++j) c[j] += (valid[j] && k >= q[j]) ? 1 : 0;
+        for (int j = 1; j <= kPiv; ++j) c[j] += (j <= nvalid && in && rel >= off(j)) ? 1 : 0;
       }
     block_sum(c, sh);
-    int js = 0;
+    int js = 0, tot_next = 0;
 #pragma unroll
     for (int j = 1; j <= kPiv; ++j)
-      if (valid[j] && sh.tot[j] >= need) js = j;
-    unsigned long long nlo = lo + (js ? off[js] : 0ull), nhi = hi;
-    if (js < kPiv && valid[js + 1]) {
-      nhi = lo + off[js + 1] - 1;
-      above = sh.tot[js + 1];
+      if (j <= nvalid && sh.tot[j] >= need) js = j;
+#pragma unroll
+    for (int j = 1; j <= kPiv; ++j)
+      if (j == js + 1) tot_next = sh.tot[j];
+    const unsigned long long nlo = lo + (js ? off(js) : 0ull);
+    if (js < nvalid) {
+      hi = lo + off(js + 1) - 1;
+      above = tot_next;
     }
     lo = nlo;
-    hi = nhi;
     __syncthreads();  // sh.tot is rewritten by the next step
   }
   *T_out = lo;
@@ -176,34 +174,90 @@ __device__ void block_mark_first(int n_tok, int r, Tie tie, Mark mark, Shared &s
   }
 }
 
+__device__ __forceinline__ void mask_set(uint64_t (&m)[kWords], int e) {
+  const uint64_t bit = 1ull << (e & 63);
+  const int w = e >> 6;
+#pragma unroll
+  for (int i = 0; i < kWords; ++i) m[i] |= (i == w) ? bit : 0ull;  // no dynamic register indexing
+}
+
+// expert mask of one token over the P prefix layers; loads for 4 layers are issued
+// before any is consumed (k == 8: two 16-byte loads per layer row)
 __device__ __forceinline__ int token_mask(const int32_t *__restrict__ routes, int P, long long T, int k, int E,
                                           long long tok, uint64_t (&m)[kWords]) {
 #pragma unroll
   for (int w = 0; w < kWords; ++w) m[w] = 0;
   int bad = 0;
-  for (int p = 0; p < P; ++p) {
-    const int32_t *r = routes + ((long long)p * T + tok) * k;
-    for (int j = 0; j < k; ++j) {
-      const int e = __ldg(r + j);
-      if ((unsigned)e >= (unsigned)E) {
-        bad = 1;
-        continue;
+  constexpr int kG = 4, kK = 8;
+  for (int p0 = 0; p0 < P; p0 += kG) {
+    int v[kG][kK];
+#pragma unroll
+    for (int q = 0; q < kG; ++q) {
+      const int32_t *r = routes + ((long long)(p0 + q) * T + tok) * k;
+      if (p0 + q >= P) {
+#pragma unroll
+        for (int j = 0; j < kK; ++j) v[q][j] = -1;
+      } else if (k == 8) {
+        const int4 a = __ldg(reinterpret_cast<const int4 *>(r)), b = __ldg(reinterpret_cast<const int4 *>(r) + 1);
+        v[q][0] = a.x; v[q][1] = a.y; v[q][2] = a.z; v[q][3] = a.w;
+        v[q][4] = b.x; v[q][5] = b.y; v[q][6] = b.z; v[q][7] = b.w;
+      } else {
+#pragma unroll
+        for (int j = 0; j < kK; ++j) v[q][j] = j < k ? __ldg(r + j) : -1;
       }
-      m[e >> 6] |= 1ull << (e & 63);
     }
+#pragma unroll
+    for (int q = 0; q < kG; ++q)
+#pragma unroll
+      for (int j = 0; j < kK; ++j) {
+        const int e = v[q][j];
+        if (p0 + q < P && j < k) {
+          if ((unsigned)e >= (unsigned)E) bad = 1;
+          else mask_set(m, e);
+        }
+      }
+    if (k > kK)  // wide top-k: the rest of each row, scalar
+      for (int q = 0; q < kG && p0 + q < P; ++q) {
+        const int32_t *r = routes + ((long long)(p0 + q) * T + tok) * k;
+        for (int j = kK; j < k; ++j) {
+          const int e = __ldg(r + j);
+          if ((unsigned)e >= (unsigned)E) bad = 1;
+          else mask_set(m, e);
+        }
+      }
   }
   return bad;
 }
 
+// Per-token working state: 64-bit order keys of s_norm and score plus flags
+// (bit0 core, bit1 keep, bit7 visual).  On chip (dynamic smem, 17 B/token)
+// when the request fits `cap` tokens, else re-derived from the global outputs.
+struct TokState {
+  bool onchip;
+  unsigned long long *ks, *kp;
+  uint8_t *f;
+  const double *sn, *sc;
+  const uint8_t *mod;
+  uint8_t *fl;
+  __device__ __forceinline__ bool vis(int t) const { return onchip ? (f[t] & 0x80) != 0 : mod[t] == 0; }
+  __device__ __forceinline__ uint8_t flags(int t) const { return onchip ? f[t] : fl[t]; }
+  __device__ __forceinline__ void set_flags(int t, uint8_t v) {
+    if (onchip) f[t] = v; else fl[t] = v;
+  }
+  __device__ __forceinline__ unsigned long long key_s(int t) const { return onchip ? ks[t] : vmm::ord_key(sn[t]); }
+  __device__ __forceinline__ unsigned long long key_p(int t) const { return onchip ? kp[t] : vmm::ord_key(sc[t]); }
+};
+
 template <int kT>
-__global__ void __launch_bounds__(kT)
+__global__ void __launch_bounds__(kT, kT == 256 ? 3 : 1)
 prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, const int32_t *__restrict__ routes,
              const int32_t *__restrict__ req_off, const int32_t *__restrict__ kcore_arr,
              const int32_t *__restrict__ kkeep_arr, double alpha, double beta, long long T, int P, int k, int E,
-             double lam, double *s_norm_out, double *delta_out, double *score_out, uint8_t *flags_out,
+             double lam, int cap, double *s_norm_out, double *delta_out, double *score_out, uint8_t *flags_out,
              int32_t *__restrict__ retained, int32_t *__restrict__ n_retained, uint64_t *__restrict__ target_out,
              int32_t *__restrict__ status) {
   __shared__ Shared sh;
+  extern __shared__ __align__(16) unsigned char dyn[];
   const int r = blockIdx.x;
   const long long base = req_off[r];
   const int n_tok = req_off[r + 1] - req_off[r];
@@ -212,6 +266,15 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
   const uint8_t *m_req = mod + base;
   double *sn = s_norm_out + base, *dl = delta_out + base, *sc = score_out + base;
   uint8_t *fl = flags_out + base;
+  TokState S;
+  S.onchip = n_tok <= cap;
+  S.ks = reinterpret_cast<unsigned long long *>(dyn);
+  S.kp = S.ks + (S.onchip ? n_tok : 0);
+  S.f = reinterpret_cast<uint8_t *>(S.kp + (S.onchip ? n_tok : 0));
+  S.sn = sn;
+  S.sc = sc;
+  S.mod = m_req;
+  S.fl = fl;
 
   if (threadIdx.x < kWords) sh.target[threadIdx.x] = 0ull;
 
@@ -219,15 +282,17 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
   double lo = INFINITY, hi = -INFINITY;
   int nv = 0, bad = 0;
   for (int t = threadIdx.x; t < n_tok; t += kT) {
-    sn[t] = qnan;
     dl[t] = qnan;
     sc[t] = qnan;
-    fl[t] = 0;
-    if (m_req[t] == 0) {
-      const double v = s_req[t];
-      if (!isfinite(v) || v < 0.0) bad = 1;
-      lo = fmin(lo, v);
-      hi = fmax(hi, v);
+    const bool v = m_req[t] == 0;
+    if (!v) sn[t] = qnan;
+    if (S.onchip) S.f[t] = v ? 0x80 : 0;
+    else fl[t] = 0;
+    if (v) {
+      const double x = s_req[t];
+      if (!isfinite(x) || x < 0.0) bad = 1;
+      lo = fmin(lo, x);
+      hi = fmax(hi, x);
       ++nv;
     }
   }
@@ -246,6 +311,7 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
     hi = -INFINITY;
     nv = 0;
     bad = 0;
+#pragma unroll 8
     for (int w = 0; w < kT / 32; ++w) {
       lo = fmin(lo, sh.dlo[w]);
       hi = fmax(hi, sh.dhi[w]);
@@ -255,6 +321,7 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
     __syncthreads();
   }
   if (bad) {
+    for (int t = threadIdx.x; t < n_tok; t += kT) { sn[t] = qnan; fl[t] = 0; }
     if (threadIdx.x == 0) { status[r] = 1; n_retained[r] = 0; }
     return;
   }
@@ -267,6 +334,7 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
     k_keep = (int)floor(__dmul_rn(beta, (double)nv));
   }
   if (k_keep < k_core || k_core < 0) {  // compress.py:153-154
+    for (int t = threadIdx.x; t < n_tok; t += kT) { sn[t] = qnan; fl[t] = 0; }
     if (threadIdx.x == 0) { status[r] = 3; n_retained[r] = 0; }
     return;
   }
@@ -276,26 +344,30 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
   // 2. normalised saliency
   const double span = __dsub_rn(hi, lo);
   for (int t = threadIdx.x; t < n_tok; t += kT)
-    if (m_req[t] == 0) sn[t] = (hi == lo) ? 0.5 : __ddiv_rn(__dsub_rn(s_req[t], lo), span);
+    if (m_req[t] == 0) {
+      const double v = (hi == lo) ? 0.5 : __ddiv_rn(__dsub_rn(s_req[t], lo), span);
+      sn[t] = v;
+      if (S.onchip) S.ks[t] = vmm::ord_key(v);
+    }
   __syncthreads();
 
-  auto is_vis = [&](int t) { return m_req[t] == 0; };
-  auto key_s = [&](int t) { return vmm::ord_key(sn[t]); };
+  auto is_vis = [&](int t) { return S.vis(t); };
+  auto key_s = [&](int t) { return S.key_s(t); };
 
   // 3. salient core: top k_core by (-s_norm, id)
   if (k_core > 0) {
     if (k_core >= nv) {
       for (int t = threadIdx.x; t < n_tok; t += kT)
-        if (m_req[t] == 0) fl[t] = 1;
+        if (S.vis(t)) S.set_flags(t, S.flags(t) | 1);
     } else {
       unsigned long long Ts;
       int gt;
       block_threshold(n_tok, k_core, is_vis, key_s, sh, &Ts, &gt);
       for (int t = threadIdx.x; t < n_tok; t += kT)
-        if (m_req[t] == 0 && key_s(t) > Ts) fl[t] = 1;
+        if (S.vis(t) && S.key_s(t) > Ts) S.set_flags(t, S.flags(t) | 1);
       __syncthreads();
-      block_mark_first(n_tok, k_core - gt, [&](int t) { return m_req[t] == 0 && key_s(t) == Ts; },
-                       [&](int t) { fl[t] = 1; }, sh);
+      block_mark_first(n_tok, k_core - gt, [&](int t) { return S.vis(t) && S.key_s(t) == Ts; },
+                       [&](int t) { S.set_flags(t, S.flags(t) | 1); }, sh);
     }
   }
   __syncthreads();
@@ -305,7 +377,7 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
     uint64_t acc[kWords] = {};
     int ebad = 0;
     for (int t = threadIdx.x; t < n_tok; t += kT)
-      if (fl[t] & 1) {
+      if (S.flags(t) & 1) {
         uint64_t m[kWords];
         ebad |= token_mask(routes, P, T, k, E, base + t, m);
 #pragma unroll
@@ -328,66 +400,69 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
   {
     int ebad = 0;
     for (int t = threadIdx.x; t < n_tok; t += kT)
-      if (m_req[t] == 0 && !(fl[t] & 1)) {
+      if (S.vis(t) && !(S.flags(t) & 1)) {
         uint64_t m[kWords];
         ebad |= token_mask(routes, P, T, k, E, base + t, m);
         int sz = 0, out = 0;
 #pragma unroll
         for (int w = 0; w < kWords; ++w) { sz += __popcll(m[w]); out += __popcll(m[w] & ~tg[w]); }
         const double d = __ddiv_rn((double)out, (double)sz);
+        const double p = __dsub_rn(sn[t], __dmul_rn(lam, d));
         dl[t] = d;
-        sc[t] = __dsub_rn(sn[t], __dmul_rn(lam, d));
+        sc[t] = p;
+        if (S.onchip) S.kp[t] = vmm::ord_key(p);
       }
     bad |= __syncthreads_or(ebad);
   }
   if (bad) {  // an expert id outside [0, E) in the prefix routes (TraceError)
+    for (int t = threadIdx.x; t < n_tok; t += kT) fl[t] = 0;
     if (threadIdx.x == 0) { status[r] = 4; n_retained[r] = 0; }
     return;
   }
 
   // 6. extras: top (k_keep - k_core) non-core visual tokens by (-score, -s_norm, id)
   const int need = k_keep - k_core;
-  auto is_rest = [&](int t) { return m_req[t] == 0 && !(fl[t] & 1); };
+  auto is_rest = [&](int t) { return S.vis(t) && !(S.flags(t) & 1); };
   if (need > 0) {
     if (need >= nv - k_core) {
       for (int t = threadIdx.x; t < n_tok; t += kT)
-        if (is_rest(t)) fl[t] |= 2;
+        if (is_rest(t)) S.set_flags(t, S.flags(t) | 2);
     } else {
-      auto key_p = [&](int t) { return vmm::ord_key(sc[t]); };
+      auto key_p = [&](int t) { return S.key_p(t); };
       unsigned long long Tp, Ts;
       int gtp, gts;
       block_threshold(n_tok, need, is_rest, key_p, sh, &Tp, &gtp);
       const int r1 = need - gtp;  // from the score ties, by s_norm
-      auto tie_p = [&](int t) { return is_rest(t) && key_p(t) == Tp; };
+      auto tie_p = [&](int t) { return is_rest(t) && S.key_p(t) == Tp; };
       block_threshold(n_tok, r1, tie_p, key_s, sh, &Ts, &gts);
       const int r2 = r1 - gts;  // from the (score, s_norm) ties, by id
       for (int t = threadIdx.x; t < n_tok; t += kT)
         if (is_rest(t)) {
-          const unsigned long long kp = key_p(t);
-          if (kp > Tp || (kp == Tp && key_s(t) > Ts)) fl[t] |= 2;
+          const unsigned long long kp = S.key_p(t);
+          if (kp > Tp || (kp == Tp && S.key_s(t) > Ts)) S.set_flags(t, S.flags(t) | 2);
         }
       __syncthreads();
-      block_mark_first(n_tok, r2, [&](int t) { return tie_p(t) && key_s(t) == Ts; }, [&](int t) { fl[t] |= 2; },
-                       sh);
+      block_mark_first(n_tok, r2, [&](int t) { return tie_p(t) && S.key_s(t) == Ts; },
+                       [&](int t) { S.set_flags(t, S.flags(t) | 2); }, sh);
     }
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < n_tok; t += kT)
-    if (fl[t] & 1) fl[t] |= 2;
   if (threadIdx.x < kWords) target_out[(long long)r * kWords + threadIdx.x] = tg[threadIdx.x];
-  __syncthreads();
 
-  // 7. retained = keep U text, ascending request-local ids (compress.py:63-65)
+  // 7. retained = keep U text, ascending request-local ids (compress.py:63-65); final flags
   int n_ret = 0;
   for (int c0 = 0; c0 < n_tok; c0 += kT) {
     const int t = c0 + threadIdx.x;
     int f = 0;
-    if (t < n_tok) f = (m_req[t] == 1) || (fl[t] & 2);
-    const int pre = block_scan_flag(f, sh);
-    if (f) {
-      retained[base + n_ret + pre] = t;
-      fl[t] |= 4;
+    uint8_t fo = 0;
+    if (t < n_tok) {
+      const uint8_t fs = S.flags(t);
+      fo = (fs & 1) ? 3 : (fs & 2);  // core tokens are kept
+      f = (m_req[t] == 1) || (fo & 2);
     }
+    const int pre = block_scan_flag(f, sh);
+    if (f) retained[base + n_ret + pre] = t;
+    if (t < n_tok) fl[t] = fo | (f ? 4 : 0);
     n_ret += sh.total;
   }
   if (threadIdx.x == 0) { n_retained[r] = n_ret; status[r] = 0; }
@@ -441,15 +516,29 @@ extern "C" int vmm_prune(const double *d_saliency, const uint8_t *d_modality, co
   if ((d_k_core == nullptr) != (d_k_keep == nullptr))
     return vmm::fail(VMM_ECONTRACT, "k_core and k_keep must both be given or both be NULL");
   cudaStream_t st = (cudaStream_t)stream;
-  // a few requests: 1024 threads each (latency); a batch: 256 threads, up to 8 CTAs per SM (throughput)
-  if (R >= 64) {
-    prune_kernel<256><<<R, 256, 0, st>>>(d_saliency, d_modality, d_routes, d_req_off, d_k_core, d_k_keep, alpha,
-                                         beta, (long long)T, P, k, experts, lam, d_s_norm, d_delta, d_score,
-                                         d_flags, d_retained, d_n_retained, d_target, d_status);
+  // per-token state on chip (17 B/token) for requests up to `cap` tokens; larger ones
+  // run from the global outputs.  A few requests: 1024 threads each (latency), up to
+  // 8192 tokens on chip; a batch: 256 threads, up to 4096 tokens (~68 KB: 3 CTAs/SM)
+  const bool batch = R >= 64;
+  const int cap = batch ? 4096 : (T < 8192 ? T : 8192);
+  const size_t smem = (size_t)cap * 17;
+  static bool attr[2] = {false, false};
+  if (!attr[batch]) {
+    cudaError_t e = batch ? cudaFuncSetAttribute(prune_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 4096 * 17)
+                          : cudaFuncSetAttribute(prune_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 8192 * 17);
+    if (e != cudaSuccess) return vmm::cuda_status(e, "prune attr");
+    attr[batch] = true;
+  }
+  if (batch) {
+    prune_kernel<256><<<R, 256, smem, st>>>(d_saliency, d_modality, d_routes, d_req_off, d_k_core, d_k_keep, alpha,
+                                            beta, (long long)T, P, k, experts, lam, cap, d_s_norm, d_delta, d_score,
+                                            d_flags, d_retained, d_n_retained, d_target, d_status);
   } else {
-    prune_kernel<1024><<<R, 1024, 0, st>>>(d_saliency, d_modality, d_routes, d_req_off, d_k_core, d_k_keep, alpha,
-                                           beta, (long long)T, P, k, experts, lam, d_s_norm, d_delta, d_score,
-                                           d_flags, d_retained, d_n_retained, d_target, d_status);
+    prune_kernel<1024><<<R, 1024, smem, st>>>(d_saliency, d_modality, d_routes, d_req_off, d_k_core, d_k_keep,
+                                              alpha, beta, (long long)T, P, k, experts, lam, cap, d_s_norm, d_delta,
+                                              d_score, d_flags, d_retained, d_n_retained, d_target, d_status);
   }
   VMM_LAUNCH_CHECK("prune_kernel");
   return VMM_OK;

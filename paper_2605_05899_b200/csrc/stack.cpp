@@ -296,6 +296,14 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
         ysrc = d.y_dev;
       } else if (d.predictor == 3) {
         ysrc = presync ? nullptr : d.oracle_table + (size_t)l * E;  // presync: already in y_host
+      } else if (d.predictor == 4) {  // MLP: history feature of context l, then the bottleneck MLP
+        if (!d.mlp_w1 || !d.mlp_hist || !d.mlp_emb || !d.mlp_ids)
+          return vmm::fail(VMM_ECONTRACT, "MLP predictor without weights / features");
+        VMM_TRY(vmm_history(d.counts, L, E, d.layer_ids + l, 1, d.pow_table, d.mlp_hist, stream));
+        VMM_TRY(vmm_mlp_predict(d.mlp_hist, d.mlp_emb, d.mlp_dim, d.mlp_drift, d.mlp_ids, d.mlp_n_ids, d.mlp_hv,
+                                d.layer_ids + l, 1, E, d.mlp_w1, d.mlp_b1, d.mlp_hidden, d.mlp_w2, d.mlp_b2,
+                                d.mlp_bottleneck, d.mlp_wo, d.mlp_bo, nullptr, d.y_dev, stream));
+        ysrc = d.y_dev;
       } else {
         return vmm::fail(VMM_ECONTRACT, "emitting layer without a predictor");
       }

@@ -84,6 +84,16 @@ def gather_rows(src, idx, stream=None, out=None):
     return out
 
 
+def row_mean(emb, ids, modality=None, stream=None, out=None):
+    """Column means of emb[ids] (numpy axis-0 order), skipping rows whose modality != 0."""
+    D = int(emb.shape[1])
+    out = torch.empty(D, dtype=torch.float64, device=emb.device) if out is None else out
+    _n(1)
+    check(_lib.lib().vmm_row_mean(ptr(emb), D, ptr(ids), int(ids.shape[0]),
+                                  None if modality is None else ptr(modality), ptr(out), stream_ptr(stream)))
+    return out
+
+
 def gather_cols(src, idx, stream=None, out=None):
     """Rows of an i32 or f32 [N, width] table by index (vmm_gather_i32/f32)."""
     n, width = int(idx.shape[0]), int(src.shape[1])

@@ -57,7 +57,7 @@ class StackConfig:
     alpha: float = 0.1
     beta: float = 0.5
     lam: float = 2.0
-    predictor: str = "history"  # history | gate | oracle | none
+    predictor: str = "history"  # history | gate | oracle | mlp | none
     budget: int = 20
     window: int = 5
     gamma: float = 0.8
@@ -266,14 +266,24 @@ class MoEStack:
     """One-request-at-a-time VL-MoE layer stack with the offloaded expert cache."""
 
     def __init__(self, cfg: StackConfig, store: ExpertStore | None = None, seed: int = 0,
-                 home: ShardedHome | None = None):
+                 home: ShardedHome | None = None, mlp_model=None):
         """home=None: misses are served from the pinned host pool over PCIe;
-        home=ShardedHome(...): from the sharded HBM home copies (D2D / NVLink)."""
+        home=ShardedHome(...): from the sharded HBM home copies (D2D / NVLink).
+        mlp_model: the reference's MLPModel (or this package's; JSON-compatible)
+        for predictor="mlp" (predictor.py:521-550): its features are the
+        decayed routing histogram of the stack's OWN routes over the retained
+        tokens, the mean of those tokens' embeddings plus the layer drift, and
+        the kept-visual embedding mean (build_features, predictor.py:86-112);
+        the token embeddings are a side input of forward()."""
         if cfg.predictor == "oracle" and cfg.routing != "trace":
             raise ValidationError("the oracle predictor needs trace routing (future routes)")
         if not 1 <= cfg.l_pinned <= cfg.layers:
             # the prune reads the pinned prefix's routes (prefix_layers non-empty, compress.py:41-42)
             raise ValidationError("the stack needs 1 <= l_pinned <= layers")
+        if cfg.predictor not in ("history", "gate", "oracle", "mlp", "none"):
+            raise ValidationError(f"unknown predictor kind '{cfg.predictor}'")
+        if cfg.predictor == "mlp" and mlp_model is None:
+            raise ValidationError("mlp predictor requires a trained model")  # pipeline.py:185-186
         self.cfg = cfg
         self.store = store or ExpertStore(cfg, seed)
         self.device = self.store.device
@@ -297,6 +307,19 @@ class MoEStack:
         self.step_counts = torch.zeros((L, E), dtype=torch.int32, device=self.device)
         self._bufs = {}
         self._pbufs = {}  # chunked-prefix outputs (x_ready)
+        self._mlp = None
+        if mlp_model is not None:
+            from .predictor import MLPModel, drift_table
+
+            m = mlp_model if isinstance(mlp_model, MLPModel) else MLPModel.from_reference(mlp_model)
+            d_in, d_h, d_b, n_out = m.dims
+            D = (d_in - E) // 2
+            if n_out != E or d_in != E + 2 * D:
+                raise ValidationError(f"MLP dims {m.dims} do not fit {E} experts")
+            self._mlp = dict(w=m.to_device(self.device), D=D, dh=d_h, db=d_b,
+                             drift=torch.from_numpy(drift_table(L, D)).to(self.device),
+                             hist=torch.empty(E, dtype=torch.float64, device=self.device),
+                             hv=torch.zeros(D, dtype=torch.float64, device=self.device), emb=None, ids=None)
         self.profile = None  # list -> (start_ev, end_ev, bytes, flops, is_prefix) per FFN launch
 
     def __del__(self):
@@ -340,7 +363,7 @@ class MoEStack:
         return self._bufs
 
     def forward(self, x, saliency, modality, trace=None, record: bool = False, req_off=None,
-                keep_session: bool = False, attn_qk=None, x_ready=None) -> StackResult:
+                keep_session: bool = False, attn_qk=None, x_ready=None, embeddings=None) -> StackResult:
         """Prefill a batch of requests through the whole stack.
 
         x bf16 [T, H] (device), saliency f64 [T], modality u8 [T] (0 visual,
@@ -355,7 +378,9 @@ class MoEStack:
         x_ready: optional [(row_end, cuda.Event)] -- rows [prev_end, row_end) of x
         are valid once the event fires (a host->device copy in flight on another
         stream): the pinned prefix then runs chunk by chunk as the rows land
-        (rows are independent in the prefix, so the result is identical)."""
+        (rows are independent in the prefix, so the result is identical).
+        embeddings: f64 [>= T, D] token embeddings (device), required by the
+        MLP predictor (rows beyond T may hold decode tokens, see decode_step)."""
         c = self.cfg
         L, E, k, lp = c.layers, c.experts, c.k, c.l_pinned
         dev = self.device
@@ -375,8 +400,14 @@ class MoEStack:
             raise ContractError("routing='trace' needs the trace's device routes")
         check(self._L.vmm_xfer_reset_stats(self._x))
 
+        if c.predictor == "mlp" and (embeddings is None or int(embeddings.shape[0]) < T):
+            raise ContractError("the MLP predictor needs the tokens' embeddings (f64 [T, D])")
         cur, x_ctx, prefix, counts_pre, ret, n_r, ret_off, xr = self._prefix_and_prune(
             x, saliency, modality, trace, req_off, bufs, x_ready=x_ready)
+        if self._mlp is not None and c.predictor == "mlp":
+            mp = self._mlp
+            mp["emb"], mp["ids"] = embeddings.contiguous(), ret
+            kernels.row_mean(mp["emb"], ret, modality, out=mp["hv"])  # visual_summary over the kept visual rows
 
         # --- per-layer demand counts over the retained tokens
         counts_ret = torch.zeros((L, E), dtype=torch.int32, device=dev)
@@ -403,6 +434,11 @@ class MoEStack:
             elif c.predictor == "gate":
                 yt = kernels.gate_lookahead(x_in, self.store.router[ctx + 1], k, scratch=bufs["scratch"],
                                             out=bufs["y_dev"])
+            elif c.predictor == "mlp":
+                mp = self._mlp
+                cx = torch.tensor([ctx], dtype=torch.int32, device=dev)
+                hist = kernels.history(counts_ret, cx, self.pow)
+                yt = kernels.mlp_predict(hist, mp["emb"], mp["drift"], mp["ids"], mp["hv"], cx, mp["w"])[0][0]
             else:
                 yt = oracle_table[ctx]
             self.y_host[ctx].copy_(yt, non_blocking=True)
@@ -581,7 +617,7 @@ class MoEStack:
 
 
     def _native_layers(self, eng, x, n_rows, l0, l1, phase, step, rows=None, counts=None, oracle_table=None,
-                       trace=None, record=False, record_into=None, region=None):
+                       trace=None, record=False, record_into=None, region=None, mlp_ids=None):
         """Run layers [l0, l1) through the native executor (csrc/stack.cpp).
         eng=None: pinned-prefix mode (no decisions / copies / host syncs).
         region=(row_base, cap, lane): run in rows [row_base, row_base+cap) of the
@@ -591,7 +627,7 @@ class MoEStack:
         L, E, k = c.layers, c.experts, c.k
         bufs = self._buffers(n_rows)
         st = self.store
-        pred = {"none": 0, "history": 1, "gate": 2, "oracle": 3}[c.predictor]
+        pred = {"none": 0, "history": 1, "gate": 2, "oracle": 3, "mlp": 4}[c.predictor]
         rb, cap, lane = (0, int(bufs["n"]), 0) if region is None else region
         if region is not None:
             if eng is not None or rb + cap > int(bufs["n"]) or n_rows > cap:
@@ -630,6 +666,16 @@ class MoEStack:
             xs=at("xs", max(S, 1) * H * 2), h1s=at("h1s", max(S, 1) * I * 2), ys=at("ys", max(S, 1) * H * 2),
             need_host=self.need_host.data_ptr(), need_dev=self.need_dev.data_ptr(),
             ffn_done=bufs[b_done].data_ptr())
+        mp = self._mlp
+        if pred == 4 and eng is not None:
+            ids_t = mp["ids"] if mlp_ids is None else mlp_ids
+            d.mlp_emb, d.mlp_drift, d.mlp_hv = mp["emb"].data_ptr(), mp["drift"].data_ptr(), mp["hv"].data_ptr()
+            d.mlp_ids, d.mlp_n_ids = ids_t.data_ptr(), int(ids_t.shape[0])
+            d.mlp_dim, d.mlp_hidden, d.mlp_bottleneck = mp["D"], mp["dh"], mp["db"]
+            w = mp["w"]
+            d.mlp_w1, d.mlp_b1, d.mlp_w2 = w["w1"].data_ptr(), w["b1"].data_ptr(), w["w2"].data_ptr()
+            d.mlp_b2, d.mlp_wo, d.mlp_bo = w["b2"].data_ptr(), w["wo"].data_ptr(), w["bo"].data_ptr()
+            d.mlp_hist = mp["hist"].data_ptr()
         h = C.c_void_p()
         check(self._L.vmm_stack_create(C.byref(d), C.byref(h)))
         nl = l1 - l0
