@@ -11,10 +11,10 @@
 //   retained = keep U text ids, ascending                   compress.py:63-65
 //
 // Selection without sorting.  Both selections only need the SET of winners
-// (the outputs are id-sorted), so each is a threshold search: an 8-ary
-// bisection over the 64-bit order-preserving keys of the doubles (7 pivots
-// per step, counts reduced with warp `redux` + one smem pass, ~21 steps for
-// any double range), then the tie at the threshold is broken by id with one
+// (the outputs are id-sorted), so each is a threshold search: a radix select
+// over the 64-bit order-preserving keys of the doubles (eight 8-bit digit
+// passes, shared-memory histograms with warp-aggregated adds for the skewed
+// top digits), then the tie at the threshold is broken by id with one
 // block-wide ordered ballot scan.  The composite extras key (-score, -s_norm,
 // id) is two nested searches (score, then s_norm among the score ties) and
 // the id scan.  No per-token state is kept on chip: the keys are re-read
@@ -29,13 +29,12 @@
 namespace {
 
 constexpr int kWords = VMM_MAX_EXPERTS / 64;
-constexpr int kPiv = 7;  // 8-ary search
 
 struct Shared {
   int warp_tot[64];
-  int red[32][kPiv + 1];
-  int tot[kPiv + 1];
-  unsigned long long kmin[32], kmax[32];
+  int red[32][2];
+  int hist[256];
+  int sel_digit, sel_above;
   double dlo[32], dhi[32];
   unsigned long long target[kWords];
   int total, nvis, bad;
@@ -65,98 +64,72 @@ __device__ __forceinline__ int block_scan_flag(int flag, Shared &sh) {
   return r;
 }
 
-// block-wide sums of kPiv+1 per-thread counters (result in sh.tot)
-__device__ __forceinline__ void block_sum(int (&c)[kPiv + 1], Shared &sh) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int j = 0; j <= kPiv; ++j) {
-    int v = __reduce_add_sync(0xffffffffu, c[j]);
-    if (lane == 0) sh.red[warp][j] = v;
-  }
-  __syncthreads();
-  if (warp <= kPiv) {  // warp j sums counter j over the warps (blockDim >= 256: >= 8 warps)
-    int v = lane < (int)(blockDim.x >> 5) ? sh.red[lane][warp] : 0;
-    v = __reduce_add_sync(0xffffffffu, v);
-    if (lane == 0) sh.tot[warp] = v;
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ void block_minmax(unsigned long long lo, unsigned long long hi, Shared &sh,
-                                             unsigned long long *out_lo, unsigned long long *out_hi) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, o), b = __shfl_xor_sync(0xffffffffu, hi, o);
-    lo = a < lo ? a : lo;
-    hi = b > hi ? b : hi;
-  }
-  if (lane == 0) { sh.kmin[warp] = lo; sh.kmax[warp] = hi; }
-  __syncthreads();
-  lo = ~0ull;
-  hi = 0ull;
-  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-    lo = sh.kmin[w] < lo ? sh.kmin[w] : lo;
-    hi = sh.kmax[w] > hi ? sh.kmax[w] : hi;
-  }
-  *out_lo = lo;
-  *out_hi = hi;
-  __syncthreads();
-}
-
-// Threshold search: among candidate tokens (cand(t) true) with keys key(t), the
-// largest T with count(key >= T) >= need (need >= 1 and <= #candidates).
+// Threshold search (radix select): among candidate tokens (cand(t) true) with
+// 64-bit keys key(t), the largest T with count(key >= T) >= need (1 <= need <=
+// #candidates).  Eight passes over 8-bit digits, most significant first: a
+// shared-memory histogram of the candidates matching the digits fixed so far,
+// then a suffix scan picks the digit holding the need-th largest key.
 // Returns T and count(key > T).  All threads of the block must call it.
 template <class Cand, class Key>
 __device__ void block_threshold(int n_tok, int need, Cand cand, Key key, Shared &sh, unsigned long long *T_out,
                                 int *gt_out) {
-  unsigned long long lo = ~0ull, hi = 0ull;
-  for (int t = threadIdx.x; t < n_tok; t += blockDim.x)
-    if (cand(t)) {
-      unsigned long long k = key(t);
-      lo = k < lo ? k : lo;
-      hi = k > hi ? k : hi;
-    }
-  block_minmax(lo, hi, sh, &lo, &hi);
-  // invariant: count(key >= lo) >= need ; count(key > hi) == above < need
-  int above = 0;
-  while (lo < hi) {
-    const unsigned long long w = hi - lo;  // span - 1
-    // pivot offsets floor((w + 1) j / 8) without overflow (strictly increasing when w >= 7);
-    // for w < 7 the offsets are 1..w.  Computed, not indexed, so everything stays in registers.
-    auto off = [w](int j) -> unsigned long long {
-      return w < 7 ? (unsigned long long)j : (w / 8) * j + ((w % 8 + 1) * (unsigned long long)j) / 8;
-    };
-    const int nvalid = w < 7 ? (int)w : kPiv;
-    int c[kPiv + 1];
-#pragma unroll
-    for (int j = 0; j <= kPiv; ++j) c[j] = 0;
-    for (int t = threadIdx.x; t < n_tok; t += blockDim.x)
-      if (cand(t)) {
-        const unsigned long long kk = key(t);
-        // count(key >= lo + off(j)) over ALL candidates (keys outside [lo, hi] included)
-        const unsigned long long rel = kk < lo ? 0ull : (kk > hi ? ~0ull : kk - lo);
-        const bool in = kk >= lo;
-#pragma unroll
-        for (int j = 1; j <= kPiv; ++j) c[j] += (j <= nvalid && in && rel >= off(j)) ? 1 : 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long prefix = 0ull, pmask = 0ull;
+  int remaining = need, above = 0;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) sh.hist[b] = 0;
+    __syncthreads();
+    for (int t0 = 0; t0 < n_tok; t0 += blockDim.x) {  // warp-uniform trip count
+      const int t = t0 + threadIdx.x;
+      int dig = -1;
+      if (t < n_tok && cand(t)) {
+        const unsigned long long k = key(t);
+        if ((k & pmask) == prefix) dig = (int)((k >> shift) & 255ull);
       }
-    block_sum(c, sh);
-    int js = 0, tot_next = 0;
-#pragma unroll
-    for (int j = 1; j <= kPiv; ++j)
-      if (j <= nvalid && sh.tot[j] >= need) js = j;
-#pragma unroll
-    for (int j = 1; j <= kPiv; ++j)
-      if (j == js + 1) tot_next = sh.tot[j];
-    const unsigned long long nlo = lo + (js ? off(js) : 0ull);
-    if (js < nvalid) {
-      hi = lo + off(js + 1) - 1;
-      above = tot_next;
+      // skewed digits are the common case (the top bytes of doubles in one binade):
+      // a warp whose valid lanes agree adds once
+      const unsigned act = __ballot_sync(0xffffffffu, dig >= 0);
+      if (act) {
+        const int d0 = __shfl_sync(0xffffffffu, dig, __ffs(act) - 1);
+        if (__all_sync(0xffffffffu, dig < 0 || dig == d0)) {
+          if (lane == __ffs(act) - 1) atomicAdd(&sh.hist[d0], __popc(act));
+        } else if (dig >= 0) {
+          atomicAdd(&sh.hist[dig], 1);
+        }
+      }
     }
-    lo = nlo;
-    __syncthreads();  // sh.tot is rewritten by the next step
+    __syncthreads();
+    if (warp == 0) {  // lane l owns bins [8l, 8l + 8); suffix sums from the top bin down
+      int c[8], own = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { c[i] = sh.hist[lane * 8 + i]; own += c[i]; }
+      int suf = own;  // inclusive suffix sum over lanes >= lane
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_down_sync(0xffffffffu, suf, o);
+        if (lane + o < 32) suf += v;
+      }
+      const int beyond = suf - own;  // keys in bins of higher lanes
+      if (beyond < remaining && remaining <= suf) {  // exactly one lane
+        int acc = beyond, d = lane * 8 + 7;
+#pragma unroll
+        for (int i = 7; i >= 0; --i) {
+          if (acc + c[i] >= remaining) { d = lane * 8 + i; break; }
+          acc += c[i];
+        }
+        sh.sel_digit = d;
+        sh.sel_above = acc;  // candidates above the chosen digit at this level
+      }
+    }
+    __syncthreads();
+    const int d = sh.sel_digit, ab = sh.sel_above;
+    above += ab;
+    remaining -= ab;
+    prefix |= (unsigned long long)d << shift;
+    pmask |= 255ull << shift;
+    __syncthreads();  // sel_* and hist are rewritten by the next pass
   }
-  *T_out = lo;
+  *T_out = prefix;
   *gt_out = above;
 }
 

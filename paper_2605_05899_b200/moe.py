@@ -727,7 +727,8 @@ class MoEStack:
     # ------------------------------------------------------------------
     def decode_step(self, x_tok, tok: int | None = None, record: bool = False) -> "DecodeResult":
         """x_tok bf16 [1, H]: the decode token's hidden state entering layer 0.
-        With routing="trace", `tok` is the token's row in the session trace."""
+        With routing="trace", `tok` is the token's row in the session trace; with
+        predictor="mlp", its row in forward()'s embeddings."""
         sess = getattr(self, "_sess", None)
         if sess is None:
             raise ContractError("decode_step needs forward(..., keep_session=True) first")
@@ -738,6 +739,11 @@ class MoEStack:
         trace = sess["trace"]
         if c.routing == "trace" and tok is None:
             raise ContractError("routing='trace' decode needs the token's trace row")
+        mlp_ids = None
+        if c.predictor == "mlp":  # decode emissions pool the decode token alone (pipeline.py:723-740)
+            if tok is None or self._mlp["emb"] is None or tok >= int(self._mlp["emb"].shape[0]):
+                raise ContractError("mlp decode needs the token's row in forward()'s embeddings")
+            mlp_ids = torch.tensor([tok], dtype=torch.int32, device=dev)
         check(self._L.vmm_xfer_reset_stats(self._x))
         counts = self.step_counts
         rows, otab = None, None
@@ -748,7 +754,7 @@ class MoEStack:
                 dec = torch.tensor(decay_table(c.gamma, c.window), dtype=torch.float64, device=dev)
                 otab = kernels.oracle_targets(counts, self.layer_ids, c.window, dec)
         cur, n_cp, routes_t = self._native_layers(eng, x_tok, 1, 0, L, 1, s, rows=rows, counts=counts,
-                                                  oracle_table=otab, trace=trace, record=record)
+                                                  oracle_table=otab, trace=trace, record=record, mlp_ids=mlp_ids)
         scores = {l: self.y_host[l].numpy().copy() for l in range(L) if eng.emits(l, 1)}
         eng.end_step()
         sess["step"] = s + 1

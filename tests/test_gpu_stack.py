@@ -429,3 +429,43 @@ def test_decode_step_hidden_matches_resident_layers(routing, pred):
         torch.cuda.synchronize()
         assert torch.equal(r.hidden, cur), (routing, pred, s)
     stack.end_session()
+
+
+@pytest.mark.parametrize("routing", ["trace", "live"])
+def test_mlp_predictor_in_the_stack(routing):
+    """predictor="mlp" (predictor.py:521-550) inside MoEStack: every emission's scores
+    equal the MLP predictor evaluated on the routes the run used (rtol 1e-12: the
+    reference's BLAS order is not bit-reproducible), and the whole
+    decision stream replays exactly through the oracle engine with those scores."""
+    from paper_2605_05899_b200 import CompressionConfig, MLPPredictor, compress
+    from paper_2605_05899_b200.predictor import MLPModel
+
+    cfg = tiny_cfg(routing=routing, predictor="mlp")
+    tr = small_trace(cfg, seed=41)
+    D = tr.embed_dim
+    rng = np.random.default_rng(3)
+    d_in, E = cfg.experts + 2 * D, cfg.experts
+
+    def uni(r, c):
+        return rng.uniform(-1 / np.sqrt(c), 1 / np.sqrt(c), size=(r, c))
+    model = MLPModel(uni(32, d_in), np.zeros(32), uni(16, 32), np.zeros(16), uni(E, 16), np.zeros(E))
+    stack = MoEStack(cfg, mlp_model=model)
+    x, sal, mod, dtr = request(tr, cfg.hidden, seed=7)
+    emb = torch.from_numpy(np.ascontiguousarray(tr.embedding)).cuda()
+    res = stack.forward(x, sal, mod, trace=dtr if routing == "trace" else None, record=True, embeddings=emb)
+    tr_run = tr if routing == "trace" else _trace_from_run(cfg, tr, res)
+    plan = compress(tr_run, CompressionConfig(cfg.alpha, cfg.beta, cfg.lam, tuple(range(cfg.l_pinned))))
+    ret = plan.retained_ids(tr_run)
+    assert res.retained.tolist() == ret
+    pred = MLPPredictor(model, tr_run, plan, cfg.history_decay)
+    assert len(res.scores) >= cfg.layers - cfg.l_pinned
+    for ctx, y in res.scores.items():
+        np.testing.assert_allclose(y, pred.priorities(ctx, ret), rtol=1e-12, atol=0)
+    sd = _sim_dict(cfg)
+    sd["predictor"]["kind"] = "history"  # placeholder kind; scores come from y_override
+    comp = dict(alpha=cfg.alpha, beta=cfg.beta, lam=cfg.lam, prefix=list(range(cfg.l_pinned)))
+    exp = harness.simulate(tr_run, sd, comp, False, y_override=lambda ctx, ids: res.scores[ctx])
+    got = res.report.to_dict()
+    for key in _F:
+        assert got[key] == exp[key], key
+    assert got["per_layer"] == exp["per_layer"]
