@@ -1,4 +1,6 @@
-// Affinity-aware visual-token compression ("prune") -- one CTA per request.
+// Affinity-aware visual-token compression ("prune") -- one thread-block
+// CLUSTER per request: a single CTA for batches of requests, up to 16 CTAs
+// (one token slice each, distributed shared memory) for a single request.
 //
 // Restates compress() (pkg/src/moesim/compress.py:142-185) on the device,
 // bit-exact in fp64:
@@ -13,32 +15,49 @@
 // Selection without sorting.  Both selections only need the SET of winners
 // (the outputs are id-sorted), so each is a threshold search: a radix select
 // over the 64-bit order-preserving keys of the doubles (eight 8-bit digit
-// passes, shared-memory histograms with warp-aggregated adds for the skewed
-// top digits), then the tie at the threshold is broken by id with one
-// block-wide ordered ballot scan.  The composite extras key (-score, -s_norm,
-// id) is two nested searches (score, then s_norm among the score ties) and
-// the id scan.  No per-token state is kept on chip: the keys are re-read
-// from the s_norm/score outputs the CTA itself wrote (L1/L2-resident), so
-// there is no cap on the tokens per request.  Routes are read exactly once:
-// the core tokens' masks for the target set, then every other visual
-// token's mask for its marginal expansion.
+// passes; each CTA histograms its slice, warp-aggregated for the skewed top
+// digits, and every CTA sums the cluster's histograms over DSMEM and takes
+// the same digit), then the tie at the threshold is broken by id: each CTA
+// counts its slice's ties, takes its quota after the lower-ranked slices
+// (DSMEM prefix) and marks it with an ordered ballot scan.  The composite
+// extras key (-score, -s_norm, id) is a select on score, a select on s_norm
+// among the score ties (skipped when all of them fit) and the id quota.
+// Per-token state (order keys of s_norm / score + flags, 17 B) lives in the
+// slice's shared memory when it fits, else it is re-derived from the global
+// outputs: no cap on the tokens per request.  Routes are read exactly once:
+// the core tokens' masks for the target set, every other visual token's mask
+// for its marginal expansion.
+#include <cooperative_groups.h>
 #include <math.h>
 
 #include "common.cuh"
 
+namespace cg = cooperative_groups;
+
 namespace {
 
-constexpr int kWords = VMM_MAX_EXPERTS / 64;
+constexpr int kMaxCluster = 16;
 
 struct Shared {
   int warp_tot[64];
-  int red[32][2];
-  int hist[256];
-  int sel_digit, sel_above;
+  int hist[2][256];  // double-buffered: remote CTAs read pass p while this CTA fills pass p+1
+  int tot[256];
   double dlo[32], dhi[32];
-  unsigned long long target[kWords];
-  int total, nvis, bad;
+  int wred[32][2];
+  int sel_digit, sel_above, total;
+  // cluster-visible per-CTA partials (one field per exchange: no reuse races)
+  int part_nv, part_bad, part_tie0, part_tie1, part_ret, part_bad2;
+  double part_lo, part_hi;
+  unsigned long long part_mask[4];
+  unsigned long long target[4];
+  int g_nv, g_bad, g_prefix;
+  double g_lo, g_hi;
 };
+
+template <class T>
+__device__ __forceinline__ T *remote(cg::cluster_group &cl, T *p, int rank) {
+  return cl.map_shared_rank(p, rank);
+}
 
 // block-wide exclusive scan of a 0/1 flag; returns prefix, writes total to sh.total
 __device__ __forceinline__ int block_scan_flag(int flag, Shared &sh) {
@@ -64,25 +83,42 @@ __device__ __forceinline__ int block_scan_flag(int flag, Shared &sh) {
   return r;
 }
 
-// Threshold search (radix select): among candidate tokens (cand(t) true) with
-// 64-bit keys key(t), the largest T with count(key >= T) >= need (1 <= need <=
-// #candidates).  Eight passes over 8-bit digits, most significant first: a
-// shared-memory histogram of the candidates matching the digits fixed so far,
-// then a suffix scan picks the digit holding the need-th largest key.
-// Returns T and count(key > T).  All threads of the block must call it.
-template <class Cand, class Key>
-__device__ void block_threshold(int n_tok, int need, Cand cand, Key key, Shared &sh, unsigned long long *T_out,
-                                int *gt_out) {
+// sum over the cluster of an int partial (every thread gets the same value);
+// `before` = sum over ranks < this CTA's rank
+__device__ __forceinline__ int cluster_sum(cg::cluster_group &cl, Shared &sh, int *field, int *before) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int C = (int)cl.num_blocks(), me = (int)cl.block_rank();
+  if (warp == 0) {
+    const int v = lane < C ? *remote(cl, field, lane) : 0;
+    const int tot = __reduce_add_sync(0xffffffffu, v);
+    const int pre = __reduce_add_sync(0xffffffffu, lane < me ? v : 0);
+    if (lane == 0) { sh.total = tot; sh.g_prefix = pre; }
+  }
+  __syncthreads();
+  const int tot = sh.total;
+  if (before) *before = sh.g_prefix;
+  __syncthreads();
+  return tot;
+}
+
+// Radix select over the cluster: among candidate tokens of every slice, the
+// largest key T with count(key >= T) >= need (1 <= need <= #candidates).
+// Returns T, count(key > T) and count(key == T).  All threads of all CTAs call it.
+template <class Cand, class Key>
+__device__ void cluster_threshold(cg::cluster_group &cl, int t0s, int t1s, int need, Cand cand, Key key,
+                                  Shared &sh, unsigned long long *T_out, int *gt_out, int *eq_out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int C = (int)cl.num_blocks();
   unsigned long long prefix = 0ull, pmask = 0ull;
-  int remaining = need, above = 0;
-  for (int shift = 56; shift >= 0; shift -= 8) {
-    for (int b = threadIdx.x; b < 256; b += blockDim.x) sh.hist[b] = 0;
+  int remaining = need, above = 0, eq = 0;
+  for (int pass = 0, shift = 56; shift >= 0; ++pass, shift -= 8) {
+    int *hist = sh.hist[pass & 1];
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0;
     __syncthreads();
-    for (int t0 = 0; t0 < n_tok; t0 += blockDim.x) {  // warp-uniform trip count
-      const int t = t0 + threadIdx.x;
+    for (int b0 = t0s; b0 < t1s; b0 += blockDim.x) {  // warp-uniform trip count
+      const int t = b0 + threadIdx.x;
       int dig = -1;
-      if (t < n_tok && cand(t)) {
+      if (t < t1s && cand(t)) {
         const unsigned long long k = key(t);
         if ((k & pmask) == prefix) dig = (int)((k >> shift) & 255ull);
       }
@@ -92,24 +128,30 @@ __device__ void block_threshold(int n_tok, int need, Cand cand, Key key, Shared 
       if (act) {
         const int d0 = __shfl_sync(0xffffffffu, dig, __ffs(act) - 1);
         if (__all_sync(0xffffffffu, dig < 0 || dig == d0)) {
-          if (lane == __ffs(act) - 1) atomicAdd(&sh.hist[d0], __popc(act));
+          if (lane == __ffs(act) - 1) atomicAdd(&hist[d0], __popc(act));
         } else if (dig >= 0) {
-          atomicAdd(&sh.hist[dig], 1);
+          atomicAdd(&hist[dig], 1);
         }
       }
+    }
+    cl.sync();  // every slice's histogram of this pass is complete
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) {
+      int v = 0;
+      for (int r = 0; r < C; ++r) v += *remote(cl, hist + b, r);
+      sh.tot[b] = v;
     }
     __syncthreads();
     if (warp == 0) {  // lane l owns bins [8l, 8l + 8); suffix sums from the top bin down
       int c[8], own = 0;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) { c[i] = sh.hist[lane * 8 + i]; own += c[i]; }
+      for (int i = 0; i < 8; ++i) { c[i] = sh.tot[lane * 8 + i]; own += c[i]; }
       int suf = own;  // inclusive suffix sum over lanes >= lane
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int v = __shfl_down_sync(0xffffffffu, suf, o);
         if (lane + o < 32) suf += v;
       }
-      const int beyond = suf - own;  // keys in bins of higher lanes
+      const int beyond = suf - own;
       if (beyond < remaining && remaining <= suf) {  // exactly one lane
         int acc = beyond, d = lane * 8 + 7;
 #pragma unroll
@@ -118,48 +160,68 @@ __device__ void block_threshold(int n_tok, int need, Cand cand, Key key, Shared 
           acc += c[i];
         }
         sh.sel_digit = d;
-        sh.sel_above = acc;  // candidates above the chosen digit at this level
+        sh.sel_above = acc;
       }
     }
     __syncthreads();
     const int d = sh.sel_digit, ab = sh.sel_above;
+    eq = sh.tot[d];
     above += ab;
     remaining -= ab;
     prefix |= (unsigned long long)d << shift;
     pmask |= 255ull << shift;
-    __syncthreads();  // sel_* and hist are rewritten by the next pass
+    __syncthreads();  // sel_* / tot are rewritten by the next pass
   }
   *T_out = prefix;
   *gt_out = above;
+  *eq_out = eq;
 }
 
-// Mark, in id order, the first r candidates with key == T (ties at the threshold).
+// Mark, in global id order over the cluster, the first r candidates with tie(t):
+// this slice's quota is r minus the ties of the lower-ranked slices.
 template <class Tie, class Mark>
-__device__ void block_mark_first(int n_tok, int r, Tie tie, Mark mark, Shared &sh) {
+__device__ void cluster_mark_first(cg::cluster_group &cl, int t0s, int t1s, int r, int *part, Tie tie, Mark mark,
+                                   Shared &sh) {
+  int cnt = 0;
+  for (int t = t0s + threadIdx.x; t < t1s; t += blockDim.x) cnt += tie(t) ? 1 : 0;
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if ((threadIdx.x & 31) == 0) sh.wred[threadIdx.x >> 5][0] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh.wred[w][0];
+    *part = s;
+  }
+  cl.sync();
+  int before = 0;
+  cluster_sum(cl, sh, part, &before);
+  const int quota = r - before;
   int done = 0;
-  for (int c0 = 0; c0 < n_tok && done < r; c0 += blockDim.x) {
+  for (int c0 = t0s; c0 < t1s && done < quota; c0 += blockDim.x) {
     const int t = c0 + threadIdx.x;
-    const int f = (t < n_tok) && tie(t);
+    const int f = (t < t1s) && tie(t);
     const int pre = block_scan_flag(f, sh);
-    if (f && done + pre < r) mark(t);
+    if (f && done + pre < quota) mark(t);
     done += sh.total;
     __syncthreads();
   }
 }
 
-__device__ __forceinline__ void mask_set(uint64_t (&m)[kWords], int e) {
+template <int NW>
+__device__ __forceinline__ void mask_set(uint64_t (&m)[NW], int e) {
   const uint64_t bit = 1ull << (e & 63);
   const int w = e >> 6;
 #pragma unroll
-  for (int i = 0; i < kWords; ++i) m[i] |= (i == w) ? bit : 0ull;  // no dynamic register indexing
+  for (int i = 0; i < NW; ++i) m[i] |= (i == w) ? bit : 0ull;  // no dynamic register indexing
 }
 
 // expert mask of one token over the P prefix layers; loads for 4 layers are issued
 // before any is consumed (k == 8: two 16-byte loads per layer row)
+template <int NW>
 __device__ __forceinline__ int token_mask(const int32_t *__restrict__ routes, int P, long long T, int k, int E,
-                                          long long tok, uint64_t (&m)[kWords]) {
+                                          long long tok, uint64_t (&m)[NW]) {
 #pragma unroll
-  for (int w = 0; w < kWords; ++w) m[w] = 0;
+  for (int w = 0; w < NW; ++w) m[w] = 0;
   int bad = 0;
   constexpr int kG = 4, kK = 8;
   for (int p0 = 0; p0 < P; p0 += kG) {
@@ -186,7 +248,7 @@ __device__ __forceinline__ int token_mask(const int32_t *__restrict__ routes, in
         const int e = v[q][j];
         if (p0 + q < P && j < k) {
           if ((unsigned)e >= (unsigned)E) bad = 1;
-          else mask_set(m, e);
+          else mask_set<NW>(m, e);
         }
       }
     if (k > kK)  // wide top-k: the rest of each row, scalar
@@ -195,34 +257,40 @@ __device__ __forceinline__ int token_mask(const int32_t *__restrict__ routes, in
         for (int j = kK; j < k; ++j) {
           const int e = __ldg(r + j);
           if ((unsigned)e >= (unsigned)E) bad = 1;
-          else mask_set(m, e);
+          else mask_set<NW>(m, e);
         }
       }
   }
   return bad;
 }
 
-// Per-token working state: 64-bit order keys of s_norm and score plus flags
-// (bit0 core, bit1 keep, bit7 visual).  On chip (dynamic smem, 17 B/token)
-// when the request fits `cap` tokens, else re-derived from the global outputs.
+// Per-token working state of the CTA's slice: 64-bit order keys of s_norm and
+// score plus flags (bit0 core, bit1 keep, bit7 visual).  On chip (dynamic smem,
+// 17 B/token, indexed t - t0) when the slice fits, else re-derived from the
+// global outputs.
 struct TokState {
   bool onchip;
+  int t0;
   unsigned long long *ks, *kp;
   uint8_t *f;
   const double *sn, *sc;
   const uint8_t *mod;
   uint8_t *fl;
-  __device__ __forceinline__ bool vis(int t) const { return onchip ? (f[t] & 0x80) != 0 : mod[t] == 0; }
-  __device__ __forceinline__ uint8_t flags(int t) const { return onchip ? f[t] : fl[t]; }
+  __device__ __forceinline__ bool vis(int t) const { return onchip ? (f[t - t0] & 0x80) != 0 : mod[t] == 0; }
+  __device__ __forceinline__ uint8_t flags(int t) const { return onchip ? f[t - t0] : fl[t]; }
   __device__ __forceinline__ void set_flags(int t, uint8_t v) {
-    if (onchip) f[t] = v; else fl[t] = v;
+    if (onchip) f[t - t0] = v; else fl[t] = v;
   }
-  __device__ __forceinline__ unsigned long long key_s(int t) const { return onchip ? ks[t] : vmm::ord_key(sn[t]); }
-  __device__ __forceinline__ unsigned long long key_p(int t) const { return onchip ? kp[t] : vmm::ord_key(sc[t]); }
+  __device__ __forceinline__ unsigned long long key_s(int t) const {
+    return onchip ? ks[t - t0] : vmm::ord_key(sn[t]);
+  }
+  __device__ __forceinline__ unsigned long long key_p(int t) const {
+    return onchip ? kp[t - t0] : vmm::ord_key(sc[t]);
+  }
 };
 
-template <int kT>
-__global__ void __launch_bounds__(kT, kT == 256 ? 3 : 1)
+template <int NW>
+__global__ void __launch_bounds__(256, 2)
 prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, const int32_t *__restrict__ routes,
              const int32_t *__restrict__ req_off, const int32_t *__restrict__ kcore_arr,
              const int32_t *__restrict__ kkeep_arr, double alpha, double beta, long long T, int P, int k, int E,
@@ -231,35 +299,39 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
              int32_t *__restrict__ status) {
   __shared__ Shared sh;
   extern __shared__ __align__(16) unsigned char dyn[];
-  const int r = blockIdx.x;
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = (int)cl.num_blocks(), me = (int)cl.block_rank();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = blockIdx.x / C;
   const long long base = req_off[r];
   const int n_tok = req_off[r + 1] - req_off[r];
+  const int slice = (n_tok + C - 1) / C;
+  const int t0 = min(n_tok, me * slice), t1 = min(n_tok, t0 + slice);
   const double qnan = __longlong_as_double(0x7ff8000000000000ll);
   const double *s_req = sal + base;
   const uint8_t *m_req = mod + base;
   double *sn = s_norm_out + base, *dl = delta_out + base, *sc = score_out + base;
   uint8_t *fl = flags_out + base;
   TokState S;
-  S.onchip = n_tok <= cap;
+  S.onchip = t1 - t0 <= cap;
+  S.t0 = t0;
   S.ks = reinterpret_cast<unsigned long long *>(dyn);
-  S.kp = S.ks + (S.onchip ? n_tok : 0);
-  S.f = reinterpret_cast<uint8_t *>(S.kp + (S.onchip ? n_tok : 0));
+  S.kp = S.ks + (S.onchip ? t1 - t0 : 0);
+  S.f = reinterpret_cast<uint8_t *>(S.kp + (S.onchip ? t1 - t0 : 0));
   S.sn = sn;
   S.sc = sc;
   S.mod = m_req;
   S.fl = fl;
 
-  if (threadIdx.x < kWords) sh.target[threadIdx.x] = 0ull;
-
   // 1. outputs reset, visual count, saliency validation and min/max (compress.py:104-114)
   double lo = INFINITY, hi = -INFINITY;
   int nv = 0, bad = 0;
-  for (int t = threadIdx.x; t < n_tok; t += kT) {
+  for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
     dl[t] = qnan;
     sc[t] = qnan;
     const bool v = m_req[t] == 0;
     if (!v) sn[t] = qnan;
-    if (S.onchip) S.f[t] = v ? 0x80 : 0;
+    if (S.onchip) S.f[t - t0] = v ? 0x80 : 0;
     else fl[t] = 0;
     if (v) {
       const double x = s_req[t];
@@ -269,46 +341,66 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
       ++nv;
     }
   }
-  {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  nv = __reduce_add_sync(0xffffffffu, nv);
+  bad = __reduce_or_sync(0xffffffffu, bad);
+  if (lane == 0) { sh.dlo[warp] = lo; sh.dhi[warp] = hi; sh.wred[warp][0] = nv; sh.wred[warp][1] = bad; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double l = INFINITY, h = -INFINITY;
+    int n = 0, b = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      l = fmin(l, sh.dlo[w]);
+      h = fmax(h, sh.dhi[w]);
+      n += sh.wred[w][0];
+      b |= sh.wred[w][1];
+    }
+    sh.part_lo = l; sh.part_hi = h; sh.part_nv = n; sh.part_bad = b;
+    for (int w = 0; w < 4; ++w) sh.target[w] = 0ull;
+  }
+  cl.sync();
+  if (warp == 0) {  // cluster totals (fmin/fmax and integer sums: order-independent, exact)
+    double l = INFINITY, h = -INFINITY;
+    int n = 0, b = 0;
+    if (lane < C) {
+      l = *remote(cl, &sh.part_lo, lane);
+      h = *remote(cl, &sh.part_hi, lane);
+      n = *remote(cl, &sh.part_nv, lane);
+      b = *remote(cl, &sh.part_bad, lane);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      l = fmin(l, __shfl_xor_sync(0xffffffffu, l, o));
+      h = fmax(h, __shfl_xor_sync(0xffffffffu, h, o));
     }
-    nv = __reduce_add_sync(0xffffffffu, nv);
-    bad = __reduce_or_sync(0xffffffffu, bad);
-    if (lane == 0) { sh.dlo[warp] = lo; sh.dhi[warp] = hi; sh.red[warp][0] = nv; sh.red[warp][1] = bad; }
-    __syncthreads();
-    lo = INFINITY;
-    hi = -INFINITY;
-    nv = 0;
-    bad = 0;
-#pragma unroll 8
-    for (int w = 0; w < kT / 32; ++w) {
-      lo = fmin(lo, sh.dlo[w]);
-      hi = fmax(hi, sh.dhi[w]);
-      nv += sh.red[w][0];
-      bad |= sh.red[w][1];
+    n = __reduce_add_sync(0xffffffffu, n);
+    b = __reduce_or_sync(0xffffffffu, b);
+    if (lane == 0) { sh.g_lo = l; sh.g_hi = h; sh.g_nv = n; sh.g_bad = b; }
+  }
+  __syncthreads();
+  lo = sh.g_lo;
+  hi = sh.g_hi;
+  nv = sh.g_nv;
+  bad = sh.g_bad;
+  int k_core = 0, k_keep = 0, st = bad ? 1 : 0;
+  if (!st) {
+    if (kcore_arr) {
+      k_core = kcore_arr[r];
+      k_keep = kkeep_arr[r];
+    } else {  // compress.py:151-152: floor(alpha * n_visual) -- one correctly rounded product
+      k_core = (int)floor(__dmul_rn(alpha, (double)nv));
+      k_keep = (int)floor(__dmul_rn(beta, (double)nv));
     }
-    __syncthreads();
+    if (k_keep < k_core || k_core < 0) st = 3;  // compress.py:153-154
   }
-  if (bad) {
-    for (int t = threadIdx.x; t < n_tok; t += kT) { sn[t] = qnan; fl[t] = 0; }
-    if (threadIdx.x == 0) { status[r] = 1; n_retained[r] = 0; }
-    return;
-  }
-  int k_core, k_keep;
-  if (kcore_arr) {
-    k_core = kcore_arr[r];
-    k_keep = kkeep_arr[r];
-  } else {  // compress.py:151-152: floor(alpha * n_visual) -- one correctly rounded product
-    k_core = (int)floor(__dmul_rn(alpha, (double)nv));
-    k_keep = (int)floor(__dmul_rn(beta, (double)nv));
-  }
-  if (k_keep < k_core || k_core < 0) {  // compress.py:153-154
-    for (int t = threadIdx.x; t < n_tok; t += kT) { sn[t] = qnan; fl[t] = 0; }
-    if (threadIdx.x == 0) { status[r] = 3; n_retained[r] = 0; }
+  if (st) {
+    for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) { sn[t] = qnan; fl[t] = 0; }
+    if (me == 0 && threadIdx.x == 0) { status[r] = st; n_retained[r] = 0; }
+    cl.sync();  // no CTA leaves while another may still read its shared memory
     return;
   }
   if (k_keep > nv) k_keep = nv;
@@ -316,11 +408,11 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
 
   // 2. normalised saliency
   const double span = __dsub_rn(hi, lo);
-  for (int t = threadIdx.x; t < n_tok; t += kT)
+  for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x)
     if (m_req[t] == 0) {
       const double v = (hi == lo) ? 0.5 : __ddiv_rn(__dsub_rn(s_req[t], lo), span);
       sn[t] = v;
-      if (S.onchip) S.ks[t] = vmm::ord_key(v);
+      if (S.onchip) S.ks[t - t0] = vmm::ord_key(v);
     }
   __syncthreads();
 
@@ -330,66 +422,86 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
   // 3. salient core: top k_core by (-s_norm, id)
   if (k_core > 0) {
     if (k_core >= nv) {
-      for (int t = threadIdx.x; t < n_tok; t += kT)
+      for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x)
         if (S.vis(t)) S.set_flags(t, S.flags(t) | 1);
     } else {
       unsigned long long Ts;
-      int gt;
-      block_threshold(n_tok, k_core, is_vis, key_s, sh, &Ts, &gt);
-      for (int t = threadIdx.x; t < n_tok; t += kT)
+      int gt, eq;
+      cluster_threshold(cl, t0, t1, k_core, is_vis, key_s, sh, &Ts, &gt, &eq);
+      for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x)
         if (S.vis(t) && S.key_s(t) > Ts) S.set_flags(t, S.flags(t) | 1);
       __syncthreads();
-      block_mark_first(n_tok, k_core - gt, [&](int t) { return S.vis(t) && S.key_s(t) == Ts; },
-                       [&](int t) { S.set_flags(t, S.flags(t) | 1); }, sh);
+      auto tie = [&](int t) { return S.vis(t) && S.key_s(t) == Ts; };
+      auto mark = [&](int t) { S.set_flags(t, S.flags(t) | 1); };
+      if (k_core - gt == eq) {  // every tie fits
+        for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x)
+          if (tie(t)) mark(t);
+      } else {
+        cluster_mark_first(cl, t0, t1, k_core - gt, &sh.part_tie0, tie, mark, sh);
+      }
     }
   }
   __syncthreads();
 
-  // 4. target expert set = OR of the core tokens' prefix masks
+  // 4. target expert set = OR of the core tokens' prefix masks, over the cluster
+  int ebad = 0;
   {
-    uint64_t acc[kWords] = {};
-    int ebad = 0;
-    for (int t = threadIdx.x; t < n_tok; t += kT)
+    uint64_t acc[NW] = {};
+    for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x)
       if (S.flags(t) & 1) {
-        uint64_t m[kWords];
-        ebad |= token_mask(routes, P, T, k, E, base + t, m);
+        uint64_t m[NW];
+        ebad |= token_mask<NW>(routes, P, T, k, E, base + t, m);
 #pragma unroll
-        for (int w = 0; w < kWords; ++w) acc[w] |= m[w];
+        for (int w = 0; w < NW; ++w) acc[w] |= m[w];
       }
 #pragma unroll
-    for (int w = 0; w < kWords; ++w) {
+    for (int w = 0; w < NW; ++w) {
       unsigned lo32 = __reduce_or_sync(0xffffffffu, (unsigned)acc[w]);
       unsigned hi32 = __reduce_or_sync(0xffffffffu, (unsigned)(acc[w] >> 32));
-      if ((threadIdx.x & 31) == 0 && (lo32 | hi32))
-        atomicOr(&sh.target[w], ((unsigned long long)hi32 << 32) | lo32);
+      if (lane == 0 && (lo32 | hi32)) atomicOr(&sh.target[w], ((unsigned long long)hi32 << 32) | lo32);
     }
-    bad = __syncthreads_or(ebad);
-  }
-  uint64_t tg[kWords];
+    __syncthreads();
+    if (threadIdx.x < 4) sh.part_mask[threadIdx.x] = sh.target[threadIdx.x];
+    cl.sync();
+    if (warp == 0) {
+      uint64_t m[4] = {0, 0, 0, 0};
+      if (lane < C)
 #pragma unroll
-  for (int w = 0; w < kWords; ++w) tg[w] = sh.target[w];
+        for (int w = 0; w < NW; ++w) m[w] = *remote(cl, &sh.part_mask[w], lane);
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        unsigned lo32 = __reduce_or_sync(0xffffffffu, (unsigned)m[w]);
+        unsigned hi32 = __reduce_or_sync(0xffffffffu, (unsigned)(m[w] >> 32));
+        if (lane == 0) sh.target[w] = ((unsigned long long)hi32 << 32) | lo32;
+      }
+    }
+    __syncthreads();
+  }
+  uint64_t tg[NW];
+#pragma unroll
+  for (int w = 0; w < NW; ++w) tg[w] = sh.target[w];
 
   // 5. marginal expansion + score for the non-core visual tokens (compress.py:163-172)
-  {
-    int ebad = 0;
-    for (int t = threadIdx.x; t < n_tok; t += kT)
-      if (S.vis(t) && !(S.flags(t) & 1)) {
-        uint64_t m[kWords];
-        ebad |= token_mask(routes, P, T, k, E, base + t, m);
-        int sz = 0, out = 0;
+  for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x)
+    if (S.vis(t) && !(S.flags(t) & 1)) {
+      uint64_t m[NW];
+      ebad |= token_mask<NW>(routes, P, T, k, E, base + t, m);
+      int sz = 0, out = 0;
 #pragma unroll
-        for (int w = 0; w < kWords; ++w) { sz += __popcll(m[w]); out += __popcll(m[w] & ~tg[w]); }
-        const double d = __ddiv_rn((double)out, (double)sz);
-        const double p = __dsub_rn(sn[t], __dmul_rn(lam, d));
-        dl[t] = d;
-        sc[t] = p;
-        if (S.onchip) S.kp[t] = vmm::ord_key(p);
-      }
-    bad |= __syncthreads_or(ebad);
-  }
-  if (bad) {  // an expert id outside [0, E) in the prefix routes (TraceError)
-    for (int t = threadIdx.x; t < n_tok; t += kT) fl[t] = 0;
-    if (threadIdx.x == 0) { status[r] = 4; n_retained[r] = 0; }
+      for (int w = 0; w < NW; ++w) { sz += __popcll(m[w]); out += __popcll(m[w] & ~tg[w]); }
+      const double d = __ddiv_rn((double)out, (double)sz);
+      const double p = __dsub_rn(sn[t], __dmul_rn(lam, d));
+      dl[t] = d;
+      sc[t] = p;
+      if (S.onchip) S.kp[t - t0] = vmm::ord_key(p);
+    }
+  ebad = __syncthreads_or(ebad);
+  if (threadIdx.x == 0) sh.part_bad2 = ebad;
+  cl.sync();
+  if (cluster_sum(cl, sh, &sh.part_bad2, nullptr)) {  // an expert id outside [0, E) (TraceError)
+    for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) fl[t] = 0;
+    if (me == 0 && threadIdx.x == 0) { status[r] = 4; n_retained[r] = 0; }
+    cl.sync();
     return;
   }
 
@@ -398,47 +510,77 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
   auto is_rest = [&](int t) { return S.vis(t) && !(S.flags(t) & 1); };
   if (need > 0) {
     if (need >= nv - k_core) {
-      for (int t = threadIdx.x; t < n_tok; t += kT)
+      for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x)
         if (is_rest(t)) S.set_flags(t, S.flags(t) | 2);
     } else {
       auto key_p = [&](int t) { return S.key_p(t); };
-      unsigned long long Tp, Ts;
-      int gtp, gts;
-      block_threshold(n_tok, need, is_rest, key_p, sh, &Tp, &gtp);
+      auto mark = [&](int t) { S.set_flags(t, S.flags(t) | 2); };
+      unsigned long long Tp, Ts = 0ull;
+      int gtp, eqp, gts = 0, eqs = 0;
+      cluster_threshold(cl, t0, t1, need, is_rest, key_p, sh, &Tp, &gtp, &eqp);
       const int r1 = need - gtp;  // from the score ties, by s_norm
       auto tie_p = [&](int t) { return is_rest(t) && S.key_p(t) == Tp; };
-      block_threshold(n_tok, r1, tie_p, key_s, sh, &Ts, &gts);
-      const int r2 = r1 - gts;  // from the (score, s_norm) ties, by id
-      for (int t = threadIdx.x; t < n_tok; t += kT)
+      const bool all_p = r1 == eqp;
+      if (!all_p) {
+        cluster_threshold(cl, t0, t1, r1, tie_p, key_s, sh, &Ts, &gts, &eqs);
+      }
+      for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x)
         if (is_rest(t)) {
           const unsigned long long kp = S.key_p(t);
-          if (kp > Tp || (kp == Tp && S.key_s(t) > Ts)) S.set_flags(t, S.flags(t) | 2);
+          if (kp > Tp || (kp == Tp && (all_p || S.key_s(t) > Ts))) mark(t);
         }
       __syncthreads();
-      block_mark_first(n_tok, r2, [&](int t) { return tie_p(t) && S.key_s(t) == Ts; },
-                       [&](int t) { S.set_flags(t, S.flags(t) | 2); }, sh);
+      if (!all_p) {
+        const int r2 = r1 - gts;  // from the (score, s_norm) ties, by id
+        auto tie_ps = [&](int t) { return tie_p(t) && S.key_s(t) == Ts; };
+        if (r2 == eqs) {
+          for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x)
+            if (tie_ps(t)) mark(t);
+        } else {
+          cluster_mark_first(cl, t0, t1, r2, &sh.part_tie1, tie_ps, mark, sh);
+        }
+      }
     }
   }
   __syncthreads();
-  if (threadIdx.x < kWords) target_out[(long long)r * kWords + threadIdx.x] = tg[threadIdx.x];
+  if (me == 0 && threadIdx.x < NW) target_out[(long long)r * 4 + threadIdx.x] = tg[threadIdx.x];
+  if (me == 0 && threadIdx.x >= NW && threadIdx.x < 4) target_out[(long long)r * 4 + threadIdx.x] = 0ull;
 
-  // 7. retained = keep U text, ascending request-local ids (compress.py:63-65); final flags
-  int n_ret = 0;
-  for (int c0 = 0; c0 < n_tok; c0 += kT) {
+  // 7. retained = keep U text, ascending request-local ids (compress.py:63-65); final flags.
+  // Slice counts first, then each slice writes at its cluster prefix.
+  int cnt = 0;
+  for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+    const uint8_t fs = S.flags(t);
+    cnt += (m_req[t] == 1) || (fs & 3);
+  }
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if (lane == 0) sh.wred[warp][0] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh.wred[w][0];
+    sh.part_ret = s;
+  }
+  cl.sync();
+  int before = 0;
+  const int n_ret_all = cluster_sum(cl, sh, &sh.part_ret, &before);
+  int n_ret = before;
+  for (int c0 = t0; c0 < t1; c0 += blockDim.x) {
     const int t = c0 + threadIdx.x;
     int f = 0;
     uint8_t fo = 0;
-    if (t < n_tok) {
+    if (t < t1) {
       const uint8_t fs = S.flags(t);
       fo = (fs & 1) ? 3 : (fs & 2);  // core tokens are kept
       f = (m_req[t] == 1) || (fo & 2);
     }
     const int pre = block_scan_flag(f, sh);
     if (f) retained[base + n_ret + pre] = t;
-    if (t < n_tok) fl[t] = fo | (f ? 4 : 0);
+    if (t < t1) fl[t] = fo | (f ? 4 : 0);
     n_ret += sh.total;
   }
-  if (threadIdx.x == 0) { n_retained[r] = n_ret; status[r] = 0; }
+  if (me == 0 && threadIdx.x == 0) { n_retained[r] = n_ret_all; status[r] = 0; }
+  cl.sync();  // DSMEM lifetime: every remote read of this CTA's partials is done
 }
 
 // Pack the per-request retained lists into one ascending list of GLOBAL row ids
@@ -488,31 +630,47 @@ extern "C" int vmm_prune(const double *d_saliency, const uint8_t *d_modality, co
   if (P < 1 || k < 1) return vmm::fail(VMM_EVALIDATION, "prefix_layers must be non-empty and k >= 1");
   if ((d_k_core == nullptr) != (d_k_keep == nullptr))
     return vmm::fail(VMM_ECONTRACT, "k_core and k_keep must both be given or both be NULL");
-  cudaStream_t st = (cudaStream_t)stream;
-  // per-token state on chip (17 B/token) for requests up to `cap` tokens; larger ones
-  // run from the global outputs.  A few requests: 1024 threads each (latency), up to
-  // 8192 tokens on chip; a batch: 256 threads, up to 4096 tokens (~68 KB: 3 CTAs/SM)
-  const bool batch = R >= 64;
-  const int cap = batch ? 4096 : (T < 8192 ? T : 8192);
+  // one cluster per request: as many CTAs per request as keep ~148 SMs busy (16 for one
+  // request, 1 for a batch of >= 148); each CTA keeps up to 4096 tokens' state on chip
+  static int num_sms = 0;
+  if (!num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int C = 1;
+  while (C < kMaxCluster && (long long)R * C * 2 <= num_sms) C <<= 1;
+  const int cap = 4096;
   const size_t smem = (size_t)cap * 17;
   static bool attr[2] = {false, false};
-  if (!attr[batch]) {
-    cudaError_t e = batch ? cudaFuncSetAttribute(prune_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 4096 * 17)
-                          : cudaFuncSetAttribute(prune_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 8192 * 17);
+  const bool wide = experts > 128;
+  if (!attr[wide]) {
+    const void *fn = wide ? (const void *)prune_kernel<4> : (const void *)prune_kernel<2>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return vmm::cuda_status(e, "prune attr");
-    attr[batch] = true;
+    attr[wide] = true;
   }
-  if (batch) {
-    prune_kernel<256><<<R, 256, smem, st>>>(d_saliency, d_modality, d_routes, d_req_off, d_k_core, d_k_keep, alpha,
-                                            beta, (long long)T, P, k, experts, lam, cap, d_s_norm, d_delta, d_score,
-                                            d_flags, d_retained, d_n_retained, d_target, d_status);
-  } else {
-    prune_kernel<1024><<<R, 1024, smem, st>>>(d_saliency, d_modality, d_routes, d_req_off, d_k_core, d_k_keep,
-                                              alpha, beta, (long long)T, P, k, experts, lam, cap, d_s_norm, d_delta,
-                                              d_score, d_flags, d_retained, d_n_retained, d_target, d_status);
-  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(R * C);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = (cudaStream_t)stream;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const long long TT = T;
+  cudaError_t e = wide ? cudaLaunchKernelEx(&cfg, prune_kernel<4>, d_saliency, d_modality, d_routes, d_req_off,
+                                            d_k_core, d_k_keep, alpha, beta, TT, P, k, experts, lam, cap, d_s_norm,
+                                            d_delta, d_score, d_flags, d_retained, d_n_retained, d_target, d_status)
+                       : cudaLaunchKernelEx(&cfg, prune_kernel<2>, d_saliency, d_modality, d_routes, d_req_off,
+                                            d_k_core, d_k_keep, alpha, beta, TT, P, k, experts, lam, cap, d_s_norm,
+                                            d_delta, d_score, d_flags, d_retained, d_n_retained, d_target, d_status);
+  if (e != cudaSuccess) return vmm::cuda_status(e, "prune_kernel launch");
   VMM_LAUNCH_CHECK("prune_kernel");
   return VMM_OK;
 }
