@@ -59,6 +59,13 @@ __device__ __forceinline__ T *remote(cg::cluster_group &cl, T *p, int rank) {
   return cl.map_shared_rank(p, rank);
 }
 
+// cluster barrier; a one-CTA cluster (batches) only needs the block barrier, which
+// also keeps L1 warm (barrier.cluster invalidates L1D)
+__device__ __forceinline__ void csync(cg::cluster_group &cl) {
+  if (cl.num_blocks() > 1) cl.sync();
+  else __syncthreads();
+}
+
 // block-wide exclusive scan of a 0/1 flag; returns prefix, writes total to sh.total
 __device__ __forceinline__ int block_scan_flag(int flag, Shared &sh) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -134,11 +141,16 @@ __device__ void cluster_threshold(cg::cluster_group &cl, int t0s, int t1s, int n
         }
       }
     }
-    cl.sync();  // every slice's histogram of this pass is complete
+    csync(cl);  // every slice's histogram of this pass is complete
     for (int b = threadIdx.x; b < 256; b += blockDim.x) {
-      int v = 0;
-      for (int r = 0; r < C; ++r) v += *remote(cl, hist + b, r);
-      sh.tot[b] = v;
+      // all C remote loads issued before any is consumed (one DSMEM round trip, not C)
+      int v[kMaxCluster];
+#pragma unroll
+      for (int r = 0; r < kMaxCluster; ++r) v[r] = r < C ? *remote(cl, hist + b, r) : 0;
+      int sum = 0;
+#pragma unroll
+      for (int r = 0; r < kMaxCluster; ++r) sum += v[r];
+      sh.tot[b] = sum;
     }
     __syncthreads();
     if (warp == 0) {  // lane l owns bins [8l, 8l + 8); suffix sums from the top bin down
@@ -192,7 +204,7 @@ __device__ void cluster_mark_first(cg::cluster_group &cl, int t0s, int t1s, int 
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh.wred[w][0];
     *part = s;
   }
-  cl.sync();
+  csync(cl);
   int before = 0;
   cluster_sum(cl, sh, part, &before);
   const int quota = r - before;
@@ -362,7 +374,7 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
     sh.part_lo = l; sh.part_hi = h; sh.part_nv = n; sh.part_bad = b;
     for (int w = 0; w < 4; ++w) sh.target[w] = 0ull;
   }
-  cl.sync();
+  csync(cl);
   if (warp == 0) {  // cluster totals (fmin/fmax and integer sums: order-independent, exact)
     double l = INFINITY, h = -INFINITY;
     int n = 0, b = 0;
@@ -400,7 +412,7 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
   if (st) {
     for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) { sn[t] = qnan; fl[t] = 0; }
     if (me == 0 && threadIdx.x == 0) { status[r] = st; n_retained[r] = 0; }
-    cl.sync();  // no CTA leaves while another may still read its shared memory
+    csync(cl);  // no CTA leaves while another may still read its shared memory
     return;
   }
   if (k_keep > nv) k_keep = nv;
@@ -462,7 +474,7 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
     }
     __syncthreads();
     if (threadIdx.x < 4) sh.part_mask[threadIdx.x] = sh.target[threadIdx.x];
-    cl.sync();
+    csync(cl);
     if (warp == 0) {
       uint64_t m[4] = {0, 0, 0, 0};
       if (lane < C)
@@ -497,11 +509,11 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
     }
   ebad = __syncthreads_or(ebad);
   if (threadIdx.x == 0) sh.part_bad2 = ebad;
-  cl.sync();
+  csync(cl);
   if (cluster_sum(cl, sh, &sh.part_bad2, nullptr)) {  // an expert id outside [0, E) (TraceError)
     for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) fl[t] = 0;
     if (me == 0 && threadIdx.x == 0) { status[r] = 4; n_retained[r] = 0; }
-    cl.sync();
+    csync(cl);
     return;
   }
 
@@ -561,7 +573,7 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh.wred[w][0];
     sh.part_ret = s;
   }
-  cl.sync();
+  csync(cl);
   int before = 0;
   const int n_ret_all = cluster_sum(cl, sh, &sh.part_ret, &before);
   int n_ret = before;
@@ -580,7 +592,7 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
     n_ret += sh.total;
   }
   if (me == 0 && threadIdx.x == 0) { n_retained[r] = n_ret_all; status[r] = 0; }
-  cl.sync();  // DSMEM lifetime: every remote read of this CTA's partials is done
+  csync(cl);  // DSMEM lifetime: every remote read of this CTA's partials is done
 }
 
 // Pack the per-request retained lists into one ascending list of GLOBAL row ids
