@@ -45,6 +45,7 @@ struct Shared {
   double dlo[32], dhi[32];
   int wred[32][2];
   int sel_digit, sel_above, total;
+  int hpass;  // radix passes run so far (histogram double-buffer parity)
   // cluster-visible per-CTA partials (one field per exchange: no reuse races)
   int part_nv, part_bad, part_tie0, part_tie1, part_ret, part_bad2;
   double part_lo, part_hi;
@@ -111,15 +112,22 @@ __device__ __forceinline__ int cluster_sum(cg::cluster_group &cl, Shared &sh, in
 // Radix select over the cluster: among candidate tokens of every slice, the
 // largest key T with count(key >= T) >= need (1 <= need <= #candidates).
 // Returns T, count(key > T) and count(key == T).  All threads of all CTAs call it.
+// Early exit: once every key of the selected bucket is needed (the common case
+// after 2-4 digits for continuous keys), the winners are exactly the
+// candidates with key >= T, T = the bucket's lowest key; *ge_out = 1 then and
+// the caller marks key >= T with no tie step.
 template <class Cand, class Key>
 __device__ void cluster_threshold(cg::cluster_group &cl, int t0s, int t1s, int need, Cand cand, Key key,
-                                  Shared &sh, unsigned long long *T_out, int *gt_out, int *eq_out) {
+                                  Shared &sh, unsigned long long *T_out, int *gt_out, int *eq_out, int *ge_out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int C = (int)cl.num_blocks();
   unsigned long long prefix = 0ull, pmask = 0ull;
-  int remaining = need, above = 0, eq = 0;
-  for (int pass = 0, shift = 56; shift >= 0; ++pass, shift -= 8) {
-    int *hist = sh.hist[pass & 1];
+  int remaining = need, above = 0, eq = 0, ge = 0;
+  // histogram buffers alternate over every pass of every call (the pass count is the
+  // same sequence in every CTA): a remote CTA may still read this CTA's previous pass
+  int hp = sh.hpass;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    int *hist = sh.hist[hp & 1];
     for (int b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0;
     __syncthreads();
     for (int b0 = t0s; b0 < t1s; b0 += blockDim.x) {  // warp-uniform trip count
@@ -183,10 +191,18 @@ __device__ void cluster_threshold(cg::cluster_group &cl, int t0s, int t1s, int n
     prefix |= (unsigned long long)d << shift;
     pmask |= 255ull << shift;
     __syncthreads();  // sel_* / tot are rewritten by the next pass
+    ++hp;
+    if (shift > 0 && remaining == eq) {  // the whole bucket is needed: done
+      ge = 1;
+      break;
+    }
   }
+  if (threadIdx.x == 0) sh.hpass = hp;
+  __syncthreads();
   *T_out = prefix;
   *gt_out = above;
   *eq_out = eq;
+  *ge_out = ge;
 }
 
 // Mark, in global id order over the cluster, the first r candidates with tie(t):
@@ -219,61 +235,70 @@ __device__ void cluster_mark_first(cg::cluster_group &cl, int t0s, int t1s, int 
   }
 }
 
-template <int NW>
-__device__ __forceinline__ void mask_set(uint64_t (&m)[NW], int e) {
-  const uint64_t bit = 1ull << (e & 63);
-  const int w = e >> 6;
+// 1 << s with PTX clamping: any s >= 32 (including the wrapped "negative" e - 32 i of a
+// lower word) gives 0, so setting bit e of word i is branch- and select-free
+__device__ __forceinline__ uint32_t bit_clamped(uint32_t s) {
+  uint32_t r;
+  asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(1u), "r"(s));
+  return r;
+}
+
+template <int NW32>
+__device__ __forceinline__ void mask_add(uint32_t (&m)[NW32], uint32_t e) {
 #pragma unroll
-  for (int i = 0; i < NW; ++i) m[i] |= (i == w) ? bit : 0ull;  // no dynamic register indexing
+  for (int i = 0; i < NW32; ++i) m[i] |= bit_clamped(e - 32u * i);
 }
 
 // expert mask of one token over the P prefix layers; loads for 4 layers are issued
-// before any is consumed (k == 8: two 16-byte loads per layer row)
+// before any is consumed (k == 8: two 16-byte loads per layer row).  Built in 32-bit
+// words (about 2.5 instructions per id and word); an id outside [0, E) sets *bad
+// (the caller reports it; its bit, if any, never reaches an output).
 template <int NW>
 __device__ __forceinline__ int token_mask(const int32_t *__restrict__ routes, int P, long long T, int k, int E,
                                           long long tok, uint64_t (&m)[NW]) {
+  constexpr int NW32 = 2 * NW;
+  uint32_t w[NW32];
 #pragma unroll
-  for (int w = 0; w < NW; ++w) m[w] = 0;
-  int bad = 0;
+  for (int i = 0; i < NW32; ++i) w[i] = 0u;
+  uint32_t emax = 0u;  // unsigned max: a negative id wraps above E
   constexpr int kG = 4, kK = 8;
-  for (int p0 = 0; p0 < P; p0 += kG) {
-    int v[kG][kK];
+  if (k == kK) {
+    for (int p0 = 0; p0 < P; p0 += kG) {
+      int4 a[kG], b[kG];
 #pragma unroll
-    for (int q = 0; q < kG; ++q) {
-      const int32_t *r = routes + ((long long)(p0 + q) * T + tok) * k;
-      if (p0 + q >= P) {
+      for (int q = 0; q < kG; ++q) {
+        if (p0 + q < P) {
+          const int4 *r = reinterpret_cast<const int4 *>(routes + ((long long)(p0 + q) * T + tok) * kK);
+          a[q] = __ldg(r);
+          b[q] = __ldg(r + 1);
+        }
+      }
 #pragma unroll
-        for (int j = 0; j < kK; ++j) v[q][j] = -1;
-      } else if (k == 8) {
-        const int4 a = __ldg(reinterpret_cast<const int4 *>(r)), b = __ldg(reinterpret_cast<const int4 *>(r) + 1);
-        v[q][0] = a.x; v[q][1] = a.y; v[q][2] = a.z; v[q][3] = a.w;
-        v[q][4] = b.x; v[q][5] = b.y; v[q][6] = b.z; v[q][7] = b.w;
-      } else {
+      for (int q = 0; q < kG; ++q) {
+        if (p0 + q < P) {
+          const uint32_t v[8] = {(uint32_t)a[q].x, (uint32_t)a[q].y, (uint32_t)a[q].z, (uint32_t)a[q].w,
+                                 (uint32_t)b[q].x, (uint32_t)b[q].y, (uint32_t)b[q].z, (uint32_t)b[q].w};
 #pragma unroll
-        for (int j = 0; j < kK; ++j) v[q][j] = j < k ? __ldg(r + j) : -1;
+          for (int j = 0; j < kK; ++j) {
+            emax = max(emax, v[j]);
+            mask_add<NW32>(w, v[j]);
+          }
+        }
       }
     }
-#pragma unroll
-    for (int q = 0; q < kG; ++q)
-#pragma unroll
-      for (int j = 0; j < kK; ++j) {
-        const int e = v[q][j];
-        if (p0 + q < P && j < k) {
-          if ((unsigned)e >= (unsigned)E) bad = 1;
-          else mask_set<NW>(m, e);
-        }
+  } else {
+    for (int p = 0; p < P; ++p) {
+      const int32_t *r = routes + ((long long)p * T + tok) * k;
+      for (int j = 0; j < k; ++j) {
+        const uint32_t e = (uint32_t)__ldg(r + j);
+        emax = max(emax, e);
+        mask_add<NW32>(w, e);
       }
-    if (k > kK)  // wide top-k: the rest of each row, scalar
-      for (int q = 0; q < kG && p0 + q < P; ++q) {
-        const int32_t *r = routes + ((long long)(p0 + q) * T + tok) * k;
-        for (int j = kK; j < k; ++j) {
-          const int e = __ldg(r + j);
-          if ((unsigned)e >= (unsigned)E) bad = 1;
-          else mask_set<NW>(m, e);
-        }
-      }
+    }
   }
-  return bad;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) m[i] = ((uint64_t)w[2 * i + 1] << 32) | w[2 * i];
+  return emax >= (uint32_t)E;
 }
 
 // Per-token working state of the CTA's slice: 64-bit order keys of s_norm and
@@ -373,6 +398,7 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
     }
     sh.part_lo = l; sh.part_hi = h; sh.part_nv = n; sh.part_bad = b;
     for (int w = 0; w < 4; ++w) sh.target[w] = 0ull;
+    sh.hpass = 0;
   }
   csync(cl);
   if (warp == 0) {  // cluster totals (fmin/fmax and integer sums: order-independent, exact)
@@ -438,14 +464,16 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
         if (S.vis(t)) S.set_flags(t, S.flags(t) | 1);
     } else {
       unsigned long long Ts;
-      int gt, eq;
-      cluster_threshold(cl, t0, t1, k_core, is_vis, key_s, sh, &Ts, &gt, &eq);
+      int gt, eq, ge;
+      cluster_threshold(cl, t0, t1, k_core, is_vis, key_s, sh, &Ts, &gt, &eq, &ge);
       for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x)
-        if (S.vis(t) && S.key_s(t) > Ts) S.set_flags(t, S.flags(t) | 1);
+        if (S.vis(t) && (S.key_s(t) > Ts || (ge && S.key_s(t) == Ts))) S.set_flags(t, S.flags(t) | 1);
       __syncthreads();
       auto tie = [&](int t) { return S.vis(t) && S.key_s(t) == Ts; };
       auto mark = [&](int t) { S.set_flags(t, S.flags(t) | 1); };
-      if (k_core - gt == eq) {  // every tie fits
+      if (ge) {
+        // key >= Ts marked above
+      } else if (k_core - gt == eq) {  // every tie fits
         for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x)
           if (tie(t)) mark(t);
       } else {
@@ -528,21 +556,21 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
       auto key_p = [&](int t) { return S.key_p(t); };
       auto mark = [&](int t) { S.set_flags(t, S.flags(t) | 2); };
       unsigned long long Tp, Ts = 0ull;
-      int gtp, eqp, gts = 0, eqs = 0;
-      cluster_threshold(cl, t0, t1, need, is_rest, key_p, sh, &Tp, &gtp, &eqp);
+      int gtp, eqp, gep, gts = 0, eqs = 0, ges = 0;
+      cluster_threshold(cl, t0, t1, need, is_rest, key_p, sh, &Tp, &gtp, &eqp, &gep);
       const int r1 = need - gtp;  // from the score ties, by s_norm
       auto tie_p = [&](int t) { return is_rest(t) && S.key_p(t) == Tp; };
-      const bool all_p = r1 == eqp;
+      const bool all_p = gep || r1 == eqp;  // gep: every key >= Tp wins (Tp is a bucket bound)
       if (!all_p) {
-        cluster_threshold(cl, t0, t1, r1, tie_p, key_s, sh, &Ts, &gts, &eqs);
+        cluster_threshold(cl, t0, t1, r1, tie_p, key_s, sh, &Ts, &gts, &eqs, &ges);
       }
       for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x)
         if (is_rest(t)) {
           const unsigned long long kp = S.key_p(t);
-          if (kp > Tp || (kp == Tp && (all_p || S.key_s(t) > Ts))) mark(t);
+          if (kp > Tp || (kp == Tp && (all_p || S.key_s(t) > Ts || (ges && S.key_s(t) == Ts)))) mark(t);
         }
       __syncthreads();
-      if (!all_p) {
+      if (!all_p && !ges) {
         const int r2 = r1 - gts;  // from the (score, s_norm) ties, by id
         auto tie_ps = [&](int t) { return tie_p(t) && S.key_s(t) == Ts; };
         if (r2 == eqs) {
