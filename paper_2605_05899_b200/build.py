@@ -22,7 +22,7 @@ CSRC = os.path.join(HERE, "csrc")
 VARIANT = os.environ.get("VMM_BUILD_VARIANT", "")
 OUT = os.path.join(HERE, "_build" + (f"_{VARIANT}" if VARIANT else ""))
 LIB = os.path.join(HERE, "libvismmoe" + (f"_{VARIANT}" if VARIANT else "") + ".so")
-DEFS = {"prof": ["-DVMM_FFN_PROF"]}.get(VARIANT, [])
+DEFS = {"prof": ["-DVMM_FFN_PROF", "-DVMM_PRUNE_PROF"]}.get(VARIANT, [])
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CU = {

@@ -22,13 +22,16 @@
 // (DSMEM prefix) and marks it with an ordered ballot scan.  The composite
 // extras key (-score, -s_norm, id) is a select on score, a select on s_norm
 // among the score ties (skipped when all of them fit) and the id quota.
-// Per-token state (order keys of s_norm / score + flags, 17 B) lives in the
-// slice's shared memory when it fits, else it is re-derived from the global
-// outputs: no cap on the tokens per request.  Routes are read exactly once:
-// the core tokens' masks for the target set, every other visual token's mask
-// for its marginal expansion.
+// Per-token state (prefix expert mask, order keys of s_norm / score, flags:
+// 33 B at E <= 128) lives in the slice's shared memory when it fits: the
+// routes are read once, in the first pass, with every prefix layer's loads in
+// flight, and the selections, target OR and marginal expansion run on chip.
+// A slice that does not fit re-derives its state from the global outputs and
+// the routes (core masks for the target set, the rest for their expansion):
+// no cap on the tokens per request.
 #include <cooperative_groups.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -37,6 +40,24 @@ namespace cg = cooperative_groups;
 namespace {
 
 constexpr int kMaxCluster = 16;
+
+// VMM_PRUNE_PROF (the prof dev build, tools/prune_prof.py): %globaltimer at the phase
+// boundaries of CTA 0, thread 0
+#ifdef VMM_PRUNE_PROF
+__device__ unsigned long long g_prune_ts[16];
+#define PRUNE_TS(i)                                                                     \
+  do {                                                                                  \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                                          \
+      unsigned long long t_;                                                            \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
+      g_prune_ts[i] = t_;                                                               \
+    }                                                                                   \
+  } while (0)
+#else
+#define PRUNE_TS(i) \
+  do {              \
+  } while (0)
+#endif
 
 struct Shared {
   int warp_tot[64];
@@ -261,7 +282,7 @@ __device__ __forceinline__ int token_mask(const int32_t *__restrict__ routes, in
 #pragma unroll
   for (int i = 0; i < NW32; ++i) w[i] = 0u;
   uint32_t emax = 0u;  // unsigned max: a negative id wraps above E
-  constexpr int kG = 4, kK = 8;
+  constexpr int kG = 8, kK = 8;
   if (k == kK) {
     for (int p0 = 0; p0 < P; p0 += kG) {
       int4 a[kG], b[kG];
@@ -308,6 +329,7 @@ __device__ __forceinline__ int token_mask(const int32_t *__restrict__ routes, in
 struct TokState {
   bool onchip;
   int t0;
+  unsigned long long *mk;  // on chip: the token's prefix expert mask (NW words), built in phase 1
   unsigned long long *ks, *kp;
   uint8_t *f;
   const double *sn, *sc;
@@ -352,7 +374,8 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
   TokState S;
   S.onchip = t1 - t0 <= cap;
   S.t0 = t0;
-  S.ks = reinterpret_cast<unsigned long long *>(dyn);
+  S.mk = reinterpret_cast<unsigned long long *>(dyn);
+  S.ks = S.mk + (S.onchip ? (t1 - t0) * NW : 0);
   S.kp = S.ks + (S.onchip ? t1 - t0 : 0);
   S.f = reinterpret_cast<uint8_t *>(S.kp + (S.onchip ? t1 - t0 : 0));
   S.sn = sn;
@@ -360,9 +383,13 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
   S.mod = m_req;
   S.fl = fl;
 
+  PRUNE_TS(0);
   // 1. outputs reset, visual count, saliency validation and min/max (compress.py:104-114)
+  // On chip, every visual token's prefix expert mask is built here too, once: its route
+  // loads (all P layers in flight, P <= 8) overlap the min/max and the core selection, and
+  // the target OR / marginal expansion then read shared memory only.
   double lo = INFINITY, hi = -INFINITY;
-  int nv = 0, bad = 0;
+  int nv = 0, bad = 0, ebad = 0;
   for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
     dl[t] = qnan;
     sc[t] = qnan;
@@ -376,6 +403,12 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
       lo = fmin(lo, x);
       hi = fmax(hi, x);
       ++nv;
+      if (S.onchip) {
+        uint64_t m[NW];
+        ebad |= token_mask<NW>(routes, P, T, k, E, base + t, m);
+#pragma unroll
+        for (int w = 0; w < NW; ++w) S.mk[(t - t0) * NW + w] = m[w];
+      }
     }
   }
 #pragma unroll
@@ -444,6 +477,7 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
   if (k_keep > nv) k_keep = nv;
   if (k_core > nv) k_core = nv;
 
+  PRUNE_TS(1);
   // 2. normalised saliency
   const double span = __dsub_rn(hi, lo);
   for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x)
@@ -457,6 +491,7 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
   auto is_vis = [&](int t) { return S.vis(t); };
   auto key_s = [&](int t) { return S.key_s(t); };
 
+  PRUNE_TS(2);
   // 3. salient core: top k_core by (-s_norm, id)
   if (k_core > 0) {
     if (k_core >= nv) {
@@ -483,14 +518,19 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
   }
   __syncthreads();
 
+  PRUNE_TS(3);
   // 4. target expert set = OR of the core tokens' prefix masks, over the cluster
-  int ebad = 0;
   {
     uint64_t acc[NW] = {};
     for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x)
       if (S.flags(t) & 1) {
         uint64_t m[NW];
-        ebad |= token_mask<NW>(routes, P, T, k, E, base + t, m);
+        if (S.onchip) {
+#pragma unroll
+          for (int w = 0; w < NW; ++w) m[w] = S.mk[(t - t0) * NW + w];
+        } else {
+          ebad |= token_mask<NW>(routes, P, T, k, E, base + t, m);
+        }
 #pragma unroll
         for (int w = 0; w < NW; ++w) acc[w] |= m[w];
       }
@@ -521,11 +561,17 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
 #pragma unroll
   for (int w = 0; w < NW; ++w) tg[w] = sh.target[w];
 
+  PRUNE_TS(4);
   // 5. marginal expansion + score for the non-core visual tokens (compress.py:163-172)
   for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x)
     if (S.vis(t) && !(S.flags(t) & 1)) {
       uint64_t m[NW];
-      ebad |= token_mask<NW>(routes, P, T, k, E, base + t, m);
+      if (S.onchip) {
+#pragma unroll
+        for (int w = 0; w < NW; ++w) m[w] = S.mk[(t - t0) * NW + w];
+      } else {
+        ebad |= token_mask<NW>(routes, P, T, k, E, base + t, m);
+      }
       int sz = 0, out = 0;
 #pragma unroll
       for (int w = 0; w < NW; ++w) { sz += __popcll(m[w]); out += __popcll(m[w] & ~tg[w]); }
@@ -545,6 +591,7 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
     return;
   }
 
+  PRUNE_TS(5);
   // 6. extras: top (k_keep - k_core) non-core visual tokens by (-score, -s_norm, id)
   const int need = k_keep - k_core;
   auto is_rest = [&](int t) { return S.vis(t) && !(S.flags(t) & 1); };
@@ -586,6 +633,7 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
   if (me == 0 && threadIdx.x < NW) target_out[(long long)r * 4 + threadIdx.x] = tg[threadIdx.x];
   if (me == 0 && threadIdx.x >= NW && threadIdx.x < 4) target_out[(long long)r * 4 + threadIdx.x] = 0ull;
 
+  PRUNE_TS(6);
   // 7. retained = keep U text, ascending request-local ids (compress.py:63-65); final flags.
   // Slice counts first, then each slice writes at its cluster prefix.
   int cnt = 0;
@@ -620,7 +668,9 @@ prune_kernel(const double *__restrict__ sal, const uint8_t *__restrict__ mod, co
     n_ret += sh.total;
   }
   if (me == 0 && threadIdx.x == 0) { n_retained[r] = n_ret_all; status[r] = 0; }
+  PRUNE_TS(7);
   csync(cl);  // DSMEM lifetime: every remote read of this CTA's partials is done
+  PRUNE_TS(8);
 }
 
 // Pack the per-request retained lists into one ascending list of GLOBAL row ids
@@ -678,12 +728,20 @@ extern "C" int vmm_prune(const double *d_saliency, const uint8_t *d_modality, co
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
+  static int c_max = -1;  // VMM_PRUNE_CLUSTER: cap on the CTAs per request (tuning knob)
+  if (c_max < 0) {
+    const char *v = getenv("VMM_PRUNE_CLUSTER");
+    c_max = v ? atoi(v) : kMaxCluster;
+    if (c_max < 1 || c_max > kMaxCluster) c_max = kMaxCluster;
+  }
   int C = 1;
-  while (C < kMaxCluster && (long long)R * C * 2 <= num_sms) C <<= 1;
-  const int cap = 4096;
-  const size_t smem = (size_t)cap * 17;
-  static bool attr[2] = {false, false};
+  while (C < c_max && (long long)R * C * 2 <= num_sms) C <<= 1;
+  // on-chip token state per slice: NW mask words + two order keys + flags (33 B/token at
+  // E <= 128); a C3 request (2368 tokens) fits one CTA with two CTAs per SM
   const bool wide = experts > 128;
+  const int cap = 2560;
+  const size_t smem = (size_t)cap * (8 * (wide ? 4 : 2) + 17);
+  static bool attr[2] = {false, false};
   if (!attr[wide]) {
     const void *fn = wide ? (const void *)prune_kernel<4> : (const void *)prune_kernel<2>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -735,3 +793,9 @@ extern "C" int vmm_gather_rows(const void *d_src, const int32_t *d_idx, int n, i
   VMM_LAUNCH_CHECK("gather_rows_kernel");
   return VMM_OK;
 }
+
+#ifdef VMM_PRUNE_PROF
+extern "C" int vmm_prune_prof_read(unsigned long long *out16) {
+  return cudaMemcpyFromSymbol(out16, g_prune_ts, sizeof(g_prune_ts)) == cudaSuccess ? VMM_OK : VMM_ECUDA;
+}
+#endif
