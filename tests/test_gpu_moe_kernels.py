@@ -125,6 +125,34 @@ def test_fused_route_and_lookahead_exact_on_integer_inputs():
         assert torch.equal(counts.cpu().long(), torch.bincount(rid.reshape(-1).long(), minlength=E))
 
 
+@pytest.mark.parametrize("N,E,k", [(130, 128, 8), (1216, 128, 8), (2368, 64, 6), (4000, 128, 8), (700, 16, 2)])
+def test_split_k_router_exact_on_integer_inputs(N, E, k):
+    """Few row tiles: the cluster split-K router (partials over K summed across the
+    cluster in rank order).  Integer inputs keep every partial sum exact, so logits,
+    ids, gates and both count vectors must equal the restatement exactly."""
+    g = torch.Generator().manual_seed(N + E)
+    L, H = 3, 2048
+    x = torch.randint(-4, 5, (N, H), generator=g).to(torch.bfloat16)
+    router = torch.randint(-1, 2, (L, E, H), generator=g).to(torch.bfloat16)
+    counts = torch.zeros(E, dtype=torch.int32, device="cuda")
+    ids, gates, logits = kernels.route_topk(x.cuda(), router[0].cuda(), k, counts=counts, want_logits=True)
+    rid, rg, rl = moe_ref.route(x, router[0], k)
+    assert torch.equal(logits.cpu().double(), rl)
+    assert torch.equal(ids.cpu(), rid)
+    assert (gates.cpu() - rg).abs().max().item() <= 1e-6
+    assert torch.equal(counts.cpu().long(), torch.bincount(rid.reshape(-1).long(), minlength=E))
+    if E % 16 == 0:
+        c2 = torch.zeros(E, dtype=torch.int32, device="cuda")
+        la = torch.zeros(E, dtype=torch.int32, device="cuda")
+        ids2, gates2 = kernels.route_lookahead(x.cuda(), router.cuda(), 1, k, c2, la)
+        rid1, rg1, _ = moe_ref.route(x, router[1], k)
+        nid, _, _ = moe_ref.route(x, router[2], k)
+        assert torch.equal(ids2.cpu(), rid1)
+        assert (gates2.cpu() - rg1).abs().max().item() <= 1e-6
+        assert torch.equal(la.cpu().long(), torch.bincount(nid.reshape(-1).long(), minlength=E))
+        assert torch.equal(c2.cpu().long(), torch.bincount(rid1.reshape(-1).long(), minlength=E))
+
+
 @pytest.mark.parametrize("N", [1, 5, 32])
 def test_skinny_router_decode_sizes_exact(N):
     g = torch.Generator().manual_seed(N)
