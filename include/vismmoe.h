@@ -99,6 +99,18 @@ int vmm_route_topk(const void *d_x, const void *d_wg, int N, int H, int E, int k
 int vmm_route_lookahead(const void *d_x, const void *d_router, int layer, int L, int N, int H, int E, int k,
                         int32_t *d_ids, float *d_gates, uint32_t *d_counts, uint32_t *d_la_counts, void *stream);
 
+/* Batch-invariant forms: the N rows are a chunk of a logical batch of batch_rows
+ * (>= N) rows.  The kernel choice and the K-split count (so the fp32 summation
+ * order of every logit) follow batch_rows, not N, so routing a batch in chunks
+ * gives bit-for-bit the ids and gates of one launch over the whole batch.  The
+ * plain entry points are the _ex forms with batch_rows = N. */
+int vmm_route_topk_ex(const void *d_x, const void *d_wg, int N, int H, int E, int k,
+                      int32_t *d_ids, float *d_gates, float *d_logits, uint32_t *d_counts, int batch_rows,
+                      void *stream);
+int vmm_route_lookahead_ex(const void *d_x, const void *d_router, int layer, int L, int N, int H, int E, int k,
+                           int32_t *d_ids, float *d_gates, uint32_t *d_counts, uint32_t *d_la_counts,
+                           int batch_rows, void *stream);
+
 /* ------------------------------------------------------------------------
  * Demand / predictor kernels (pkg/src/moesim/predictor.py)
  * ------------------------------------------------------------------------ */
@@ -237,6 +249,11 @@ int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offsets, int E, 
                              const uint32_t *d_ready, int ready_base, uint32_t *d_done,
                              const void *d_x_rows, const int32_t *d_src_row, int n_x_rows, void *d_h1, void *d_y,
                              void *stream);
+/* H1 is scratch.  On the CTA-pair path (tensor-bound batches) the last GEMM2 tile
+ * that consumes an H1 block drops it from L2 without a write-back
+ * (discard.global.L2), so d_h1's contents after the call are undefined; keep != 0
+ * (process-wide) keeps them, e.g. to compare H1 bit for bit. */
+int vmm_ffn_keep_h1(int keep);
 /* Reference (CUDA-core, fp32) version of the same contraction for cross-checks. */
 int vmm_grouped_swiglu_simt(const void *d_xp, const int32_t *d_offsets, int E, int M_total,
                             int H, int I, const void *d_w13_arena, const void *d_w2_arena, long long slot_stride,
@@ -475,6 +492,8 @@ typedef struct {
   int mlp_dim, mlp_n_ids, mlp_hidden, mlp_bottleneck;
   const double *mlp_w1, *mlp_b1, *mlp_w2, *mlp_b2, *mlp_wo, *mlp_bo;
   double *mlp_hist;                     /* d [E] scratch: the history feature of the context layer */
+  int route_batch_rows;                 /* rows of the logical batch these rows belong to (0: n_rows); the
+                                           router's split count follows it (vmm_route_topk_ex) */
 } vmm_stack_desc;
 
 typedef struct {

@@ -62,7 +62,7 @@ class StackDesc(C.Structure):
         ("mlp_emb", P), ("mlp_drift", P), ("mlp_hv", P), ("mlp_ids", P),
         ("mlp_dim", I32), ("mlp_n_ids", I32), ("mlp_hidden", I32), ("mlp_bottleneck", I32),
         ("mlp_w1", P), ("mlp_b1", P), ("mlp_w2", P), ("mlp_b2", P), ("mlp_wo", P), ("mlp_bo", P),
-        ("mlp_hist", P),
+        ("mlp_hist", P), ("route_batch_rows", I32),
     ]
 
 
@@ -81,6 +81,9 @@ _SIGS = {
     "vmm_gather_rows": (I32, [P, P, I32, I32, P, P]),
     "vmm_route_topk": (I32, [P, P, I32, I32, I32, I32, P, P, P, P, P]),
     "vmm_route_lookahead": (I32, [P, P, I32, I32, I32, I32, I32, I32, P, P, P, P, P]),
+    "vmm_ffn_keep_h1": (I32, [I32]),
+    "vmm_route_topk_ex": (I32, [P, P, I32, I32, I32, I32, P, P, P, P, I32, P]),
+    "vmm_route_lookahead_ex": (I32, [P, P, I32, I32, I32, I32, I32, I32, P, P, P, P, I32, P]),
     "vmm_normalize_counts": (I32, [P, I32, F64, P, P]),
     "vmm_demand_counts": (I32, [P, I32, I32, I32, I32, P, I32, P, I32, P, P]),
     "vmm_oracle_targets": (I32, [P, I32, I32, P, I32, I32, P, P, P]),

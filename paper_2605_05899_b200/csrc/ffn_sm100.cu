@@ -252,6 +252,11 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
 __device__ __forceinline__ void red_release_add(uint32_t *p, uint32_t v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ uint32_t atom_acq_rel_add(uint32_t *p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ uint64_t global_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -569,7 +574,7 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
                 const int32_t *__restrict__ offsets, const int32_t *__restrict__ slot_of,
                 const uint32_t *__restrict__ need, const uint32_t *ready, int ready_base, uint32_t *done, int E, int H,
                 int I, int lag, const __nv_bfloat16 *__restrict__ xg, const int32_t *__restrict__ src_row,
-                int M_total, __nv_bfloat16 *__restrict__ h1, __nv_bfloat16 *__restrict__ y) {
+                int M_total, __nv_bfloat16 *__restrict__ h1, __nv_bfloat16 *__restrict__ y, int discard_h1) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char *stg = smem + kStages2 * kStage2;
@@ -921,6 +926,25 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
 #pragma unroll
               for (int v = 0; v < 4; ++v) dst[v] = make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
             }
+          }
+        }
+        // H1 is dead once every GEMM2 tile of this m-tile has consumed it (its accumulator is
+        // complete, so its TMA loads of H1 landed): the last of the 8 * n2 epilogue warps drops
+        // the m-tile's H1 rows from L2 without a write-back (discard.global.L2), so the dirty
+        // H1 lines never reach DRAM.  The arrivals share the m-tile's GEMM1 counter in its high
+        // half (GEMM2 tiles only run once the low half reached 8 * n1).  Only the tile's own
+        // rows [row0, row_end) are dropped: rows past row_end belong to the next expert.
+        if (discard_h1) {
+          __syncwarp();
+          uint32_t old = 0;
+          if (lane == 0) old = atom_acq_rel_add(done + f.m_tile, 1u << 16);
+          old = __shfl_sync(0xffffffffu, old, 0);
+          if ((old >> 16) == 8u * (uint32_t)n2 - 1u) {
+            const int r_end = ti.row_end < ti.row0 + BM2 ? ti.row_end : ti.row0 + BM2;
+            const char *b0 = reinterpret_cast<const char *>(h1 + (long long)ti.row0 * I);
+            const long long n_lines = (long long)(r_end - ti.row0) * I * 2 / 128;
+            for (long long i = lane; i < n_lines; i += 32)
+              asm volatile("discard.global.L2 [%0], 128;" ::"l"(b0 + i * 128) : "memory");
           }
         }
       }
@@ -1580,6 +1604,15 @@ extern "C" int vmm_grouped_swiglu(const void *d_xp, const int32_t *d_offsets, in
   return VMM_OK;
 }
 
+// H1 is scratch: by default the CTA-pair path drops consumed H1 rows from L2 without
+// writing them back, so its contents after the call are undefined.  keep != 0 keeps them
+// (tests compare H1 bit for bit).
+static std::atomic<int> g_keep_h1{0};
+extern "C" int vmm_ffn_keep_h1(int keep) {
+  g_keep_h1.store(keep ? 1 : 0, std::memory_order_relaxed);
+  return VMM_OK;
+}
+
 extern "C" int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offsets, int E, int M_total, int H, int I,
                                         const void *d_w13_arena, const void *d_w2_arena, long long slot_stride,
                                         long long n_slots, const int32_t *d_slot_of_expert, const uint32_t *d_need,
@@ -1699,14 +1732,19 @@ extern "C" int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offse
     }
     static const int lag_waves = std::getenv("VMM_FFN_LAG") ? std::atoi(std::getenv("VMM_FFN_LAG")) : 4;
     const int lagp = (lag_waves * ncl + n1 + n2 - 1) / (n1 + n2);
+    // drop consumed H1 rows from L2 without write-back unless the caller keeps H1 (vmm_ffn_keep_h1;
+    // VMM_FFN_NO_DISCARD=1 keeps it for the whole process, for A/B runs)
+    static const bool no_discard_env = std::getenv("VMM_FFN_NO_DISCARD") != nullptr;
+    const int discard = (no_discard_env || g_keep_h1.load(std::memory_order_relaxed)) ? 0 : 1;
     if (d_src_row)
       ffn_pair_kernel<true><<<gridp, kThreads + 128, kSmem2, s>>>(
           mx, mw13, mh1, mw2, mh1s, mys, d_offsets, d_slot_of_expert, d_need, d_ready, ready_base, d_done, E, H, I,
-          lagp, (const __nv_bfloat16 *)d_x_rows, d_src_row, M_total, (__nv_bfloat16 *)d_h1, (__nv_bfloat16 *)d_y);
+          lagp, (const __nv_bfloat16 *)d_x_rows, d_src_row, M_total, (__nv_bfloat16 *)d_h1, (__nv_bfloat16 *)d_y,
+          discard);
     else
       ffn_pair_kernel<false><<<gridp, kThreads, kSmem2, s>>>(
           mx, mw13, mh1, mw2, mh1s, mys, d_offsets, d_slot_of_expert, d_need, d_ready, ready_base, d_done, E, H, I,
-          lagp, nullptr, nullptr, M_total, (__nv_bfloat16 *)d_h1, (__nv_bfloat16 *)d_y);
+          lagp, nullptr, nullptr, M_total, (__nv_bfloat16 *)d_h1, (__nv_bfloat16 *)d_y, discard);
     VMM_LAUNCH_CHECK("ffn_pair_kernel");
     return VMM_OK;
   }

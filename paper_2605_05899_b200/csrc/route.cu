@@ -240,32 +240,41 @@ int route_skinny(const void *x, const void *w, int N, int H, int E, int NG, int 
 namespace vmm {
 int route_sm100(const void *x, const void *wg_base, int w_row0, long long w_rows, int N, int H, int E, int k,
                 int32_t *ids, float *gates, float *logits, uint32_t *counts, uint32_t *la_counts, bool fused,
-                cudaStream_t s);
+                int batch_rows, cudaStream_t s);
+}
+
+extern "C" int vmm_route_lookahead_ex(const void *d_x, const void *d_router, int layer, int L, int N, int H, int E,
+                                      int k, int32_t *d_ids, float *d_gates, uint32_t *d_counts, uint32_t *d_la_counts,
+                                      int batch_rows, void *stream) {
+  if (N <= 0) return VMM_OK;
+  if (layer < 0 || layer + 1 >= L) return vmm::fail(VMM_ECONTRACT, "lookahead needs a next layer");
+  if (batch_rows < N) batch_rows = N;
+  if (batch_rows <= kSkinnyMaxN && H % 8 == 0 && E <= kMaxE && k <= kMaxK)  // decode-sized: gate rows over many CTAs
+    return route_skinny(d_x, (const __nv_bfloat16 *)d_router + (long long)layer * E * H, N, H, E, 2, k, d_ids,
+                        d_gates, nullptr, d_counts, d_la_counts, (cudaStream_t)stream);
+  int st = vmm::route_sm100(d_x, d_router, layer * E, (long long)L * E, N, H, E, k, d_ids, d_gates, nullptr,
+                            d_counts, d_la_counts, true, batch_rows, (cudaStream_t)stream);
+  if (st == -1) return vmm::fail(VMM_EVALIDATION, "fused route+lookahead needs E in {16,32,64,128}, H % 64 == 0");
+  return st;
 }
 
 extern "C" int vmm_route_lookahead(const void *d_x, const void *d_router, int layer, int L, int N, int H, int E, int k,
                                    int32_t *d_ids, float *d_gates, uint32_t *d_counts, uint32_t *d_la_counts,
                                    void *stream) {
-  if (N <= 0) return VMM_OK;
-  if (layer < 0 || layer + 1 >= L) return vmm::fail(VMM_ECONTRACT, "lookahead needs a next layer");
-  if (N <= kSkinnyMaxN && H % 8 == 0 && E <= kMaxE && k <= kMaxK)  // decode-sized: gate rows over many CTAs
-    return route_skinny(d_x, (const __nv_bfloat16 *)d_router + (long long)layer * E * H, N, H, E, 2, k, d_ids,
-                        d_gates, nullptr, d_counts, d_la_counts, (cudaStream_t)stream);
-  int st = vmm::route_sm100(d_x, d_router, layer * E, (long long)L * E, N, H, E, k, d_ids, d_gates, nullptr,
-                            d_counts, d_la_counts, true, (cudaStream_t)stream);
-  if (st == -1) return vmm::fail(VMM_EVALIDATION, "fused route+lookahead needs E in {16,32,64,128}, H % 64 == 0");
-  return st;
+  return vmm_route_lookahead_ex(d_x, d_router, layer, L, N, H, E, k, d_ids, d_gates, d_counts, d_la_counts, N,
+                                stream);
 }
 
-extern "C" int vmm_route_topk(const void *d_x, const void *d_wg, int N, int H, int E, int k, int32_t *d_ids,
-                              float *d_gates, float *d_logits, uint32_t *d_counts, void *stream) {
+extern "C" int vmm_route_topk_ex(const void *d_x, const void *d_wg, int N, int H, int E, int k, int32_t *d_ids,
+                                 float *d_gates, float *d_logits, uint32_t *d_counts, int batch_rows, void *stream) {
   if (N <= 0) return VMM_OK;
   if (E < 1 || E > kMaxE) return vmm::fail(VMM_EVALIDATION, "router: experts must lie in [1, 256]");
   if (k < 1 || k > kMaxK || k > E) return vmm::fail(VMM_EVALIDATION, "router: k must lie in [1, min(16, E)]");
-  if (N <= kSkinnyMaxN && H % 8 == 0)  // decode-sized: gate rows over many CTAs
+  if (batch_rows < N) batch_rows = N;
+  if (batch_rows <= kSkinnyMaxN && H % 8 == 0)  // decode-sized: gate rows over many CTAs
     return route_skinny(d_x, d_wg, N, H, E, 1, k, d_ids, d_gates, d_logits, d_counts, nullptr, (cudaStream_t)stream);
   int st = vmm::route_sm100(d_x, d_wg, 0, E, N, H, E, k, d_ids, d_gates, d_logits, d_counts, nullptr, false,
-                            (cudaStream_t)stream);
+                            batch_rows, (cudaStream_t)stream);
   if (st != -1) return st;
   // shapes the tcgen05 tile does not cover (E > 128 or H % 64): CUDA-core kernel
   size_t smem = sizeof(float) * ((size_t)kTok * (kKc + 1) + (size_t)E * (kKc + 1) + (size_t)kTok * E);
@@ -281,4 +290,9 @@ extern "C" int vmm_route_topk(const void *d_x, const void *d_wg, int N, int H, i
                                                               d_gates, d_logits, d_counts);
   VMM_LAUNCH_CHECK("route_kernel");
   return VMM_OK;
+}
+
+extern "C" int vmm_route_topk(const void *d_x, const void *d_wg, int N, int H, int E, int k, int32_t *d_ids,
+                              float *d_gates, float *d_logits, uint32_t *d_counts, void *stream) {
+  return vmm_route_topk_ex(d_x, d_wg, N, H, E, k, d_ids, d_gates, d_logits, d_counts, N, stream);
 }

@@ -483,6 +483,9 @@ inline int split_k(int N, int H) {
   static int off = -1;  // VMM_ROUTE_NO_SPLITK=1: always the one-CTA kernel
   if (off < 0) off = getenv("VMM_ROUTE_NO_SPLITK") ? 1 : 0;
   if (off) return 1;
+  static int forced = -1;  // VMM_ROUTE_SPLIT=S: S splits at every N (measurement knob)
+  if (forced < 0) forced = getenv("VMM_ROUTE_SPLIT") ? atoi(getenv("VMM_ROUTE_SPLIT")) : 0;
+  if (forced > 0) return forced;
   const int tiles = (N + BM - 1) / BM, nk = H / BK;
   int S = 1;
   while (S < kMaxSplit && tiles * S * 2 <= num_sms && nk >= 4 * S) S <<= 1;
@@ -491,9 +494,11 @@ inline int split_k(int N, int H) {
 
 template <int EG, int NG, int K>
 int launch(const void *x, const void *wg, int w_row0, long long w_rows, int N, int H, int E, int32_t *ids,
-           float *gates, float *logits, uint32_t *counts, uint32_t *la_counts, cudaStream_t s) {
+           float *gates, float *logits, uint32_t *counts, uint32_t *la_counts, int batch_rows, cudaStream_t s) {
   using Cfg = RouteCfg<EG, NG>;
-  const int S = split_k(N, H);
+  // the split count (and so the fp32 summation order of every logit) follows the logical
+  // batch, not this launch: rows routed in chunks get the bits of one launch over the batch
+  const int S = split_k(batch_rows > N ? batch_rows : N, H);
   if (S > 1)
     return launch_splitk<EG, NG, K>(S, x, wg, w_row0, w_rows, N, H, E, ids, gates, logits, counts, la_counts, s);
   static bool attr = false;
@@ -526,10 +531,11 @@ int launch(const void *x, const void *wg, int w_row0, long long w_rows, int N, i
 
 template <int EG, int NG>
 int launch_k(int k, const void *x, const void *wg, int w_row0, long long w_rows, int N, int H, int E, int32_t *ids,
-             float *gates, float *logits, uint32_t *counts, uint32_t *la_counts, cudaStream_t s) {
+             float *gates, float *logits, uint32_t *counts, uint32_t *la_counts, int batch_rows, cudaStream_t s) {
   switch (k) {
 #define VMM_K(KK) \
-  case KK: return launch<EG, NG, KK>(x, wg, w_row0, w_rows, N, H, E, ids, gates, logits, counts, la_counts, s);
+  case KK: \
+    return launch<EG, NG, KK>(x, wg, w_row0, w_rows, N, H, E, ids, gates, logits, counts, la_counts, batch_rows, s);
     VMM_K(1) VMM_K(2) VMM_K(3) VMM_K(4) VMM_K(5) VMM_K(6) VMM_K(7) VMM_K(8)
 #undef VMM_K
     default: return -1;
@@ -542,22 +548,30 @@ namespace vmm {
 // tcgen05 router; returns -1 if the shape is not tileable (caller uses the SIMT kernel)
 int route_sm100(const void *x, const void *wg_base, int w_row0, long long w_rows, int N, int H, int E, int k,
                 int32_t *ids, float *gates, float *logits, uint32_t *counts, uint32_t *la_counts, bool fused,
-                cudaStream_t s) {
+                int batch_rows, cudaStream_t s) {
   if (H % BK || k > kMaxK || k < 1 || E > 128 || N <= 0) return -1;
   if (fused) {
     switch (E) {
-      case 16: return launch_k<16, 2>(k, x, wg_base, w_row0, w_rows, N, H, E, ids, gates, logits, counts, la_counts, s);
-      case 32: return launch_k<32, 2>(k, x, wg_base, w_row0, w_rows, N, H, E, ids, gates, logits, counts, la_counts, s);
-      case 64: return launch_k<64, 2>(k, x, wg_base, w_row0, w_rows, N, H, E, ids, gates, logits, counts, la_counts, s);
+      case 16: return launch_k<16, 2>(
+          k, x, wg_base, w_row0, w_rows, N, H, E, ids, gates, logits, counts, la_counts, batch_rows, s);
+      case 32: return launch_k<32, 2>(
+          k, x, wg_base, w_row0, w_rows, N, H, E, ids, gates, logits, counts, la_counts, batch_rows, s);
+      case 64: return launch_k<64, 2>(
+          k, x, wg_base, w_row0, w_rows, N, H, E, ids, gates, logits, counts, la_counts, batch_rows, s);
       case 128:
-        return launch_k<128, 2>(k, x, wg_base, w_row0, w_rows, N, H, E, ids, gates, logits, counts, la_counts, s);
+        return launch_k<128, 2>(
+          k, x, wg_base, w_row0, w_rows, N, H, E, ids, gates, logits, counts, la_counts, batch_rows, s);
       default: return -1;
     }
   }
-  if (E <= 16) return launch_k<16, 1>(k, x, wg_base, w_row0, w_rows, N, H, E, ids, gates, logits, counts, nullptr, s);
-  if (E <= 32) return launch_k<32, 1>(k, x, wg_base, w_row0, w_rows, N, H, E, ids, gates, logits, counts, nullptr, s);
-  if (E <= 64) return launch_k<64, 1>(k, x, wg_base, w_row0, w_rows, N, H, E, ids, gates, logits, counts, nullptr, s);
-  return launch_k<128, 1>(k, x, wg_base, w_row0, w_rows, N, H, E, ids, gates, logits, counts, nullptr, s);
+  if (E <= 16) return launch_k<16, 1>(
+          k, x, wg_base, w_row0, w_rows, N, H, E, ids, gates, logits, counts, nullptr, batch_rows, s);
+  if (E <= 32) return launch_k<32, 1>(
+          k, x, wg_base, w_row0, w_rows, N, H, E, ids, gates, logits, counts, nullptr, batch_rows, s);
+  if (E <= 64) return launch_k<64, 1>(
+          k, x, wg_base, w_row0, w_rows, N, H, E, ids, gates, logits, counts, nullptr, batch_rows, s);
+  return launch_k<128, 1>(
+          k, x, wg_base, w_row0, w_rows, N, H, E, ids, gates, logits, counts, nullptr, batch_rows, s);
 }
 }  // namespace vmm
 

@@ -241,11 +241,13 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
       // rows [r0, r1) of this layer's router (counts accumulate over the launches)
       auto route_rows = [&](int r0, int r1) -> int {
         const char *x0 = (const char *)xn + (size_t)r0 * H * 2;
+        // the split router's numerics follow the whole batch, not the chunk (vmm_route_topk_ex)
+        const int br = d.route_batch_rows > n_rows ? d.route_batch_rows : n_rows;
         if (fused_la)
-          return vmm_route_lookahead(x0, d.router, l, L, r1 - r0, H, E, k, d.ids + (size_t)r0 * k,
-                                     d.gates + (size_t)r0 * k, cnt, d.la_counts, stream);
-        return vmm_route_topk(x0, (const char *)d.router + (size_t)l * E * H * 2, r1 - r0, H, E, k,
-                              d.ids + (size_t)r0 * k, d.gates + (size_t)r0 * k, nullptr, cnt, stream);
+          return vmm_route_lookahead_ex(x0, d.router, l, L, r1 - r0, H, E, k, d.ids + (size_t)r0 * k,
+                                        d.gates + (size_t)r0 * k, cnt, d.la_counts, br, stream);
+        return vmm_route_topk_ex(x0, (const char *)d.router + (size_t)l * E * H * 2, r1 - r0, H, E, k,
+                                 d.ids + (size_t)r0 * k, d.gates + (size_t)r0 * k, nullptr, cnt, br, stream);
       };
       if (split_now) {
         VMM_TRY(route_rows(0, n_split));

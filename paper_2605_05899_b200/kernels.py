@@ -107,28 +107,34 @@ def gather_cols(src, idx, stream=None, out=None):
 # ---------------------------------------------------------------------------
 # router / predictors
 # ---------------------------------------------------------------------------
-def route_topk(x, w_gate, k: int, counts=None, want_logits=False, stream=None, ids=None, gates=None):
-    """x bf16 [N, H], w_gate bf16 [E, H] -> (ids i32 [N,k], gates f32 [N,k], logits|None)."""
+def route_topk(x, w_gate, k: int, counts=None, want_logits=False, stream=None, ids=None, gates=None,
+               batch_rows=None):
+    """x bf16 [N, H], w_gate bf16 [E, H] -> (ids i32 [N,k], gates f32 [N,k], logits|None).
+    batch_rows: the rows are a chunk of a batch of that many rows -- the result is
+    bit-identical to routing the whole batch in one call (vmm_route_topk_ex)."""
     N, H = (int(s) for s in x.shape)
     E = int(w_gate.shape[0])
     ids = torch.empty(N, k, dtype=_i32, device=x.device) if ids is None else ids
     gates = torch.empty(N, k, dtype=torch.float32, device=x.device) if gates is None else gates
     logits = torch.empty(N, E, dtype=torch.float32, device=x.device) if want_logits else None
     _n(1)
-    check(_lib.lib().vmm_route_topk(ptr(x), ptr(w_gate), N, H, E, k, ptr(ids), ptr(gates), ptr(logits),
-                                    ptr(counts), stream_ptr(stream)))
+    check(_lib.lib().vmm_route_topk_ex(ptr(x), ptr(w_gate), N, H, E, k, ptr(ids), ptr(gates), ptr(logits),
+                                       ptr(counts), max(N, batch_rows or 0), stream_ptr(stream)))
     return ids, gates, logits
 
 
-def route_lookahead(x, router, layer: int, k: int, counts, la_counts, stream=None, ids=None, gates=None):
-    """Fused router (layer) + gate lookahead (layer+1) on the same rows; router bf16 [L, E, H]."""
+def route_lookahead(x, router, layer: int, k: int, counts, la_counts, stream=None, ids=None, gates=None,
+                    batch_rows=None):
+    """Fused router (layer) + gate lookahead (layer+1) on the same rows; router bf16 [L, E, H].
+    batch_rows: as for route_topk."""
     N, H = (int(s) for s in x.shape)
     L_, E = int(router.shape[0]), int(router.shape[1])
     ids = torch.empty(N, k, dtype=_i32, device=x.device) if ids is None else ids
     gates = torch.empty(N, k, dtype=torch.float32, device=x.device) if gates is None else gates
     _n(1)
-    check(_lib.lib().vmm_route_lookahead(ptr(x), ptr(router), layer, L_, N, H, E, k, ptr(ids), ptr(gates),
-                                         ptr(counts), ptr(la_counts), stream_ptr(stream)))
+    check(_lib.lib().vmm_route_lookahead_ex(ptr(x), ptr(router), layer, L_, N, H, E, k, ptr(ids), ptr(gates),
+                                            ptr(counts), ptr(la_counts), max(N, batch_rows or 0),
+                                            stream_ptr(stream)))
     return ids, gates
 
 
@@ -233,6 +239,19 @@ def permute_rows(x, src_row, n_rows: int, stream=None, out=None):
     _n(1)
     check(_lib.lib().vmm_permute_rows(ptr(x), ptr(src_row), n_rows, H, ptr(out), stream_ptr(stream)))
     return out
+
+
+class keep_h1:
+    """Context: the fused FFN keeps its H1 scratch (by default the CTA-pair path
+    drops consumed H1 rows from L2 without a write-back, so H1 is undefined
+    after the call -- vmm_ffn_keep_h1)."""
+
+    def __enter__(self):
+        check(_lib.lib().vmm_ffn_keep_h1(1))
+        return self
+
+    def __exit__(self, *exc):
+        check(_lib.lib().vmm_ffn_keep_h1(0))
 
 
 def grouped_swiglu(xp, offsets, arena, slot_of, inter: int, stream=None, h1=None, y=None, simt: bool = False,

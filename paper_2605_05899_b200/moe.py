@@ -541,7 +541,7 @@ class MoEStack:
                     rows_c = torch.arange(r0, r1, dtype=torch.int32, device=dev) if c.routing == "trace" else None
                     out_c, _, _ = self._native_layers(None, x[r0:r1], n, 0, lpe, 0, -1, rows=rows_c, counts=counts_c,
                                                       trace=trace, record_into=routes_c,
-                                                      region=(base[lane], caps[lane], lane))
+                                                      region=(base[lane], caps[lane], lane), batch_rows=T)
                     cur_full[r0:r1].copy_(out_c)
                     if c.predictor == "gate" and not skip_last:  # boot emission context (layer lp-1 input)
                         xn_full[r0:r1].copy_(bufs["xn"][base[lane]:base[lane] + n])
@@ -617,12 +617,14 @@ class MoEStack:
 
 
     def _native_layers(self, eng, x, n_rows, l0, l1, phase, step, rows=None, counts=None, oracle_table=None,
-                       trace=None, record=False, record_into=None, region=None, mlp_ids=None):
+                       trace=None, record=False, record_into=None, region=None, mlp_ids=None, batch_rows=0):
         """Run layers [l0, l1) through the native executor (csrc/stack.cpp).
         eng=None: pinned-prefix mode (no decisions / copies / host syncs).
         region=(row_base, cap, lane): run in rows [row_base, row_base+cap) of the
         scratch buffers with lane's own small buffers (two pinned-prefix chunks
-        on two streams at once; enqueued on the current stream)."""
+        on two streams at once; enqueued on the current stream).
+        batch_rows: the rows are a chunk of a batch of that many rows (the router's
+        numerics follow the batch: chunked prefixes route like one launch)."""
         c = self.cfg
         L, E, k = c.layers, c.experts, c.k
         bufs = self._buffers(n_rows)
@@ -665,7 +667,7 @@ class MoEStack:
             shared_src=at("shared_src", max(S, 1) * 4), shared_off=bufs[b_soff].data_ptr(),
             xs=at("xs", max(S, 1) * H * 2), h1s=at("h1s", max(S, 1) * I * 2), ys=at("ys", max(S, 1) * H * 2),
             need_host=self.need_host.data_ptr(), need_dev=self.need_dev.data_ptr(),
-            ffn_done=bufs[b_done].data_ptr())
+            ffn_done=bufs[b_done].data_ptr(), route_batch_rows=int(batch_rows))
         mp = self._mlp
         if pred == 4 and eng is not None:
             ids_t = mp["ids"] if mlp_ids is None else mlp_ids

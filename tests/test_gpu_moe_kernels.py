@@ -153,6 +153,40 @@ def test_split_k_router_exact_on_integer_inputs(N, E, k):
         assert torch.equal(c2.cpu().long(), torch.bincount(rid1.reshape(-1).long(), minlength=E))
 
 
+@pytest.mark.parametrize("N,chunks", [(9728, (1216,)), (18944, (9472,)), (2432, (1216,)), (40, (12,)),
+                                      (75776 * 2, (75776,))])
+def test_router_chunks_bit_identical_to_one_launch(N, chunks):
+    """Batch invariance of the chunked router (vmm_route_topk_ex): the executor
+    routes a layer's first chunk early (decisions) and the two-stream prefix
+    routes request-aligned halves; with the batch's row count as the split hint
+    each chunk's ids/gates/counts equal one launch over the whole batch, bit for
+    bit, on N(0,1) inputs (real-valued logits, so a different K-split order would
+    show in the gates).  Chunk sizes are the R=8 headline layer (1216 of 9728),
+    the R=8 prefix halves, R=2, a chunk below the decode-sized kernel's 16 rows
+    and the R=64 prefix halves."""
+    g = torch.Generator(device="cuda").manual_seed(N)
+    L, H, E, k = 3, 2048, 128, 8
+    x = torch.randn(N, H, device="cuda", generator=g).to(torch.bfloat16)
+    router = (torch.randn(L, E, H, device="cuda", generator=g) / 45).to(torch.bfloat16)
+    bounds = [0, *chunks, N]
+    c_one = torch.zeros(E, dtype=torch.int32, device="cuda")
+    ids1, g1, _ = kernels.route_topk(x, router[0], k, counts=c_one)
+    ids2 = torch.empty_like(ids1)
+    g2 = torch.empty_like(g1)
+    c_ch = torch.zeros(E, dtype=torch.int32, device="cuda")
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        kernels.route_topk(x[a:b], router[0], k, counts=c_ch, ids=ids2[a:b], gates=g2[a:b], batch_rows=N)
+    assert torch.equal(ids1, ids2) and torch.equal(g1, g2) and torch.equal(c_one, c_ch)
+    c1, la1 = (torch.zeros(E, dtype=torch.int32, device="cuda") for _ in range(2))
+    ids3, g3 = kernels.route_lookahead(x, router, 0, k, c1, la1)
+    assert torch.equal(ids3, ids1) and torch.equal(g3, g1)  # the fused lookahead's router columns too
+    c2, la2 = (torch.zeros(E, dtype=torch.int32, device="cuda") for _ in range(2))
+    ids4, g4 = torch.empty_like(ids1), torch.empty_like(g1)
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        kernels.route_lookahead(x[a:b], router, 0, k, c2, la2, ids=ids4[a:b], gates=g4[a:b], batch_rows=N)
+    assert torch.equal(ids4, ids1) and torch.equal(g4, g1) and torch.equal(la1, la2) and torch.equal(c1, c2)
+
+
 @pytest.mark.parametrize("N", [1, 5, 32])
 def test_skinny_router_decode_sizes_exact(N):
     g = torch.Generator().manual_seed(N)
@@ -260,14 +294,18 @@ def test_fused_ffn_bit_identical_to_two_launches(shape):
     xp = kernels.permute_rows(x.cuda(), src, N * k)
     arena, slot_of = arena.cuda(), slot_of.cuda()
     h1a, ya = kernels.grouped_swiglu(xp, off, arena, slot_of, I, fused=False)
-    h1b, yb = kernels.grouped_swiglu(xp, off, arena, slot_of, I, fused=True)
-    # A rows gathered from the token rows by TMA gather4 (no permuted copy)
-    h1c, yc = kernels.grouped_swiglu(N * k, off, arena, slot_of, I, x_rows=x.cuda(), src_row=src)
+    with kernels.keep_h1():  # H1 is scratch: kept here so the GEMM1 tiles are compared too
+        h1b, yb = kernels.grouped_swiglu(xp, off, arena, slot_of, I, fused=True)
+        # A rows gathered from the token rows by TMA gather4 (no permuted copy)
+        h1c, yc = kernels.grouped_swiglu(N * k, off, arena, slot_of, I, x_rows=x.cuda(), src_row=src)
+    # the product path: consumed H1 rows dropped from L2 without write-back (CTA-pair tiles)
+    _, yd = kernels.grouped_swiglu(xp, off, arena, slot_of, I, fused=True)
     torch.cuda.synchronize()
     assert torch.equal(h1a, h1b)
     assert torch.equal(ya, yb)
     assert torch.equal(h1a, h1c)
     assert torch.equal(ya, yc)
+    assert torch.equal(ya, yd)
 
 
 @pytest.mark.parametrize("N", [1, 2, 1216, 5000])
@@ -300,6 +338,7 @@ def test_fused_ffn_waits_for_copy_stream_fills(N):
         y = torch.empty(N * k, H, dtype=torch.bfloat16, device="cuda")
         done = torch.empty(N * k // 128 + E + 1, dtype=torch.int32, device="cuda")
         w2 = dev_arena.data_ptr() + 2 * I * H * 2
+        _lib.check(L.vmm_ffn_keep_h1(int(N <= 1216)))  # N=5000 (CTA pairs) runs the product's H1 discard
         _lib.check(L.vmm_grouped_swiglu_fused(xp.data_ptr(), off.data_ptr(), E, N * k, H, I, dev_arena.data_ptr(),
                                               w2, 3 * I * H, E, slot_of.cuda().data_ptr(), need.data_ptr(), ready, 0,
                                               done.data_ptr(), None, None, 0, h1.data_ptr(), y.data_ptr(),
@@ -313,9 +352,11 @@ def test_fused_ffn_waits_for_copy_stream_fills(N):
         h1r, yr = kernels.grouped_swiglu(xp, off, dev_arena, slot_of.cuda(), I, fused=False)
         torch.cuda.synchronize()
         assert torch.equal(dev_arena.cpu(), arena)
-        assert torch.equal(h1, h1r)
+        if N <= 1216:
+            assert torch.equal(h1, h1r)
         assert torch.equal(y, yr)
     finally:
+        L.vmm_ffn_keep_h1(0)
         L.vmm_xfer_destroy(xf)
 
 
