@@ -574,7 +574,8 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
                 const int32_t *__restrict__ offsets, const int32_t *__restrict__ slot_of,
                 const uint32_t *__restrict__ need, const uint32_t *ready, int ready_base, uint32_t *done, int E, int H,
                 int I, int lag, const __nv_bfloat16 *__restrict__ xg, const int32_t *__restrict__ src_row,
-                int M_total, __nv_bfloat16 *__restrict__ h1, __nv_bfloat16 *__restrict__ y, int discard_h1) {
+                int M_total, __nv_bfloat16 *__restrict__ h1, __nv_bfloat16 *__restrict__ y, int discard_h1,
+                int l2_hints) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char *stg = smem + kStages2 * kStage2;
@@ -809,7 +810,11 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
 #endif
     uint32_t nst = 0;  // this warp's TMA stores so far (staging buffer nst & 1)
     unsigned char *stg_w = stg + q * 4096;
-    auto stage_store = [&](const uint32_t (&w)[16], const CUtensorMap *map, int c0, int r0) {
+    // L2 priorities of the epilogue stores (hints & 1: H1 evict_last -- it is re-read by the GEMM2
+    // tiles a few waves later, then discarded; hints & 2: Y evict_first -- streamed out, read by
+    // the next kernel): keeps H1 resident so its lines are dropped before any write-back
+    const uint64_t pol_h1 = l2_policy_evict_last(), pol_y = l2_policy_evict_first();
+    auto stage_store = [&](const uint32_t (&w)[16], const CUtensorMap *map, int c0, int r0, int hint) {
       unsigned char *buf = stg_w + (nst & 1) * 2048;
       if (nst >= 2) {
         PROF_T0();
@@ -825,7 +830,9 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        tma_store_2d(map, buf, c0, r0);
+        if (hint == 1) tma_store_2d_hint(map, buf, c0, r0, pol_h1);
+        else if (hint == 2) tma_store_2d_hint(map, buf, c0, r0, pol_y);
+        else tma_store_2d(map, buf, c0, r0);
         bulk_commit();
       }
       if (q == 0 && lane == 0) PROF_ADD(13);
@@ -878,7 +885,7 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
           const int c0 = f.n_tile * (TN2 / 2) + pair * 64 + half * 32;
           if (_nostore) {
           } else if (tma_rows) {
-            stage_store(w, &map_h1s, c0, r_w0);
+            stage_store(w, &map_h1s, c0, r_w0, l2_hints & 1);
           } else if (row < ti.row_end) {
             uint4 *dst = reinterpret_cast<uint4 *>(h1 + (long long)row * I + c0);
 #pragma unroll
@@ -920,7 +927,7 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
             const int c0 = f.n_tile * TN2 + (c2 + h) * 32;
             if (_nostore) {
             } else if (tma_rows) {
-              stage_store(w, &map_ys, c0, r_w0);
+              stage_store(w, &map_ys, c0, r_w0, l2_hints & 2);
             } else if (row < ti.row_end) {
               uint4 *dst = reinterpret_cast<uint4 *>(y + (long long)row * H + c0);
 #pragma unroll
@@ -1736,15 +1743,20 @@ extern "C" int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offse
     // VMM_FFN_NO_DISCARD=1 keeps it for the whole process, for A/B runs)
     static const bool no_discard_env = std::getenv("VMM_FFN_NO_DISCARD") != nullptr;
     const int discard = (no_discard_env || g_keep_h1.load(std::memory_order_relaxed)) ? 0 : 1;
+    // L2 priorities of the epilogue stores (bit 0: H1 evict_last, bit 1: Y evict_first; VMM_FFN_L2HINTS=n
+    // for A/B runs).  Measured at R=256 (2.49M picks, ncu): DRAM 26.3 GB without discard or hints,
+    // 24.7 GB with the discard, 22.5 GB with discard + both hints = 1.04x the 21.6 GB minimum
+    // (weights + Xp read + Y write), same time (profiles/r02_ffn_l2_traffic.txt)
+    static const int l2_hints = std::getenv("VMM_FFN_L2HINTS") ? std::atoi(std::getenv("VMM_FFN_L2HINTS")) : 3;
     if (d_src_row)
       ffn_pair_kernel<true><<<gridp, kThreads + 128, kSmem2, s>>>(
           mx, mw13, mh1, mw2, mh1s, mys, d_offsets, d_slot_of_expert, d_need, d_ready, ready_base, d_done, E, H, I,
           lagp, (const __nv_bfloat16 *)d_x_rows, d_src_row, M_total, (__nv_bfloat16 *)d_h1, (__nv_bfloat16 *)d_y,
-          discard);
+          discard, l2_hints);
     else
       ffn_pair_kernel<false><<<gridp, kThreads, kSmem2, s>>>(
           mx, mw13, mh1, mw2, mh1s, mys, d_offsets, d_slot_of_expert, d_need, d_ready, ready_base, d_done, E, H, I,
-          lagp, nullptr, nullptr, M_total, (__nv_bfloat16 *)d_h1, (__nv_bfloat16 *)d_y, discard);
+          lagp, nullptr, nullptr, M_total, (__nv_bfloat16 *)d_h1, (__nv_bfloat16 *)d_y, discard, l2_hints);
     VMM_LAUNCH_CHECK("ffn_pair_kernel");
     return VMM_OK;
   }
