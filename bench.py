@@ -605,8 +605,9 @@ def main():
         f1.record()
         f1.synchronize()
         durs.append(f0.elapsed_time(f1))
-    # weights of the demanded experts + permuted rows (read) + H1 write/read + Y write
-    nbytes = [ne * cfg.slot_bytes + M * w.hidden * 2 * 2 + M * w.inter * 2 * 2]
+    # algorithmic bytes: weights of the demanded experts + permuted rows (read) + Y (write); H1 never
+    # has to leave the chip (the CTA-pair kernel drops consumed H1 rows from L2 without write-back)
+    nbytes = [ne * cfg.slot_bytes + M * w.hidden * 2 * 2]
     nflops = [6.0 * M * w.hidden * w.inter]
     durs = [float(np.mean(durs))]
     peaks = {}

@@ -715,7 +715,7 @@ class MoEStack:
             M = n_rows * k
             for i in range(nl):
                 ne = c.experts if eng is None else int(n_dem[i])  # pinned prefix: every expert resident
-                nbytes = ne * c.slot_bytes + M * c.hidden * 2 * 2 + M * c.inter * 2 * 2
+                nbytes = ne * c.slot_bytes + M * c.hidden * 2 * 2  # weights + Xp read + Y write (H1 on chip)
                 self.profile.append((evs[i], evs[nl + i], nbytes, 6.0 * M * c.hidden * c.inter, eng is None))
         res = bufs["out"] if out.x_out == at("out", H * 2) else bufs["out2"]
         self.last_host_us = list(out.host_us)
