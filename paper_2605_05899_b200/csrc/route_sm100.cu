@@ -227,7 +227,11 @@ __device__ unsigned long long g_route_ts[8];
 template <int EG, int NG>
 struct SplitCfg {
   static constexpr int N = EG * NG;
-  static constexpr int kThreads = 64 + 128 * NG;
+  // warps 0 (TMA) and 1 (MMA), 4 * NG spill warps; all 16 warps share the reduce + top-k,
+  // one (row, gate) item per warp at a time: the item's DSMEM loads and REDUX rounds are
+  // latency chains, so more warps in flight is what shortens that phase
+  static constexpr int kSpillWarps = 4 * NG;
+  static constexpr int kThreads = 512;
   static constexpr uint32_t kA = BM * BK * 2;
   static constexpr uint32_t kB = N * BK * 2;
   static constexpr uint32_t kStage = kA + kB;
@@ -309,7 +313,7 @@ route_splitk_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_cons
       umma_commit(tmem_full);  // every MMA (and its smem reads) done: the ring may be overwritten
     }
     __syncwarp();
-  } else {
+  } else if (warp < 2 + Cfg::kSpillWarps) {
     // spill this CTA's partial: thread owns TMEM lane (= tile row) 32*(w%4)+lane, gate (w-2)/4
     const int q = warp & 3;
     const int gate = (warp - 2) >> 2;
