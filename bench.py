@@ -692,7 +692,7 @@ def main():
             "config": {"workload": w.name, "tokens": T, "layers": w.layers, "hidden": w.hidden, "experts": w.experts,
                        "top_k": w.k, "moe_inter": w.inter, "l_pinned": w.l_pinned, "num_slabs": w.num_slabs,
                        "routing": a.routing, "predictor": f"{predictor} B={w.budget} W={w.window}",
-                       "miss_source": a.source,
+                       "miss_source": a.source, "host_pool": store.host_pool_kind,
                        "parallelism": f"dp{world} (requests)", "requests_per_gpu_step": R,
                        "l2": "flushed (256 MB write) between timed steps"},
             "hit_rate": hit_rate, "hits": int(hits), "misses": int(misses), "evictions": int(evictions),

@@ -392,6 +392,12 @@ int vmm_xfer_reset_stats(vmm_xfer *x);
 /* per-(layer, expert) source pointers [L*E] (sharded mode: local or IPC-mapped
  * peer HBM home copies).  vmm_xfer_issue_engine with h_pool == NULL uses them. */
 int vmm_xfer_set_sources(vmm_xfer *x, const void *const *h_table, long long n);
+/* data-parallel host pool (SURVEY 8(e) mode DP): the ranks of a node map ONE
+ * shared-memory expert pool and each page-locks it for its own context
+ * (cudaHostRegisterPortable), so every rank's copy engine DMAs from the same
+ * host pages -- one copy of the experts per node instead of one per GPU. */
+int vmm_host_register(void *h_ptr, size_t bytes);
+int vmm_host_unregister(void *h_ptr);
 /* sharded expert cache plumbing: export / map a device allocation across
  * processes (64-byte handle) and enable peer access over NVLink */
 int vmm_ipc_get(const void *d_ptr, void *h_handle64);

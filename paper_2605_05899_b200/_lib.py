@@ -152,6 +152,8 @@ _SIGS = {
     "vmm_shared_plan": (I32, [I32, I32, P, P, P]),
     "vmm_combine_norm": (I32, [P, P, P, P, I32, I32, I32, P, I32, C.c_float, P, P, P]),
     "vmm_xfer_set_sources": (I32, [P, P, I64]),
+    "vmm_host_register": (I32, [P, SZ]),
+    "vmm_host_unregister": (I32, [P]),
     "vmm_ipc_get": (I32, [P, P]),
     "vmm_ipc_open": (I32, [P, C.POINTER(P)]),
     "vmm_ipc_offset": (I32, [P, C.POINTER(I64)]),

@@ -38,6 +38,19 @@ int vmm_device_check(int dev) {
   return VMM_OK;
 }
 
+// ---- data-parallel host pool: one shared-memory pool per node, page-locked in every rank ----
+int vmm_host_register(void *h_ptr, size_t bytes) {
+  cudaError_t e = cudaHostRegister(h_ptr, bytes, cudaHostRegisterPortable);
+  if (e != cudaSuccess) return vmm::fail(VMM_ECUDA, std::string("cudaHostRegister: ") + cudaGetErrorString(e));
+  return VMM_OK;
+}
+
+int vmm_host_unregister(void *h_ptr) {
+  cudaError_t e = cudaHostUnregister(h_ptr);
+  if (e != cudaSuccess) return vmm::fail(VMM_ECUDA, std::string("cudaHostUnregister: ") + cudaGetErrorString(e));
+  return VMM_OK;
+}
+
 // ---- sharded expert cache plumbing: IPC-mapped peer HBM + peer access ----
 int vmm_ipc_get(const void *d_ptr, void *h_handle64) {
   cudaIpcMemHandle_t h;

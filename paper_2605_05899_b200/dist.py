@@ -57,3 +57,81 @@ def sum_over_ranks(values, device=None) -> list[float]:
 def barrier():
     if dist.is_initialized() and dist.get_world_size() > 1:
         dist.barrier()
+
+
+class SharedHostPool:
+    """The node's expert pool in POSIX shared memory, page-locked in every rank
+    (SURVEY 8(e) mode DP: "each GPU runs its own policy and slab cache, against
+    one portable pinned pool").  Local rank 0 creates and sizes the segment
+    (posix_fallocate, so a full /dev/shm fails here rather than at a page
+    fault), every local rank maps it MAP_SHARED and registers it with
+    cudaHostRegisterPortable (vmm_host_register) for its own context, and the
+    name is unlinked once all ranks hold a mapping: one copy of the experts per
+    node, and nothing left behind if a rank dies.  `filler` is True on the one
+    rank that must write the weights; the others wait in `ready()`.
+    `create()` returns None when the segment cannot be made on any rank (the
+    caller then pins a pool per rank); all ranks agree on the outcome."""
+
+    def __init__(self, mm, nbytes, addr, filler):
+        self.mm, self.nbytes, self.addr, self.filler = mm, nbytes, addr, filler
+        self._registered = False
+
+    @staticmethod
+    def create(nbytes: int, tag: str, device=None):
+        import ctypes as C
+        import mmap
+
+        from . import _lib
+
+        rank, world, _ = env_rank_world()
+        if world == 1 or not dist.is_initialized():
+            return None
+        # ranks spawned without torchrun (tests) carry no LOCAL_RANK: one node, local = global rank
+        local = int(os.environ["LOCAL_RANK"]) if "LOCAL_RANK" in os.environ else rank
+        path = f"/dev/shm/vmm_pool_{tag}"
+        ok, fd = 1, -1
+        if local == 0:
+            try:
+                try:
+                    os.unlink(path)  # a stale segment of an earlier job with the same tag
+                except FileNotFoundError:
+                    pass
+                fd = os.open(path, os.O_CREAT | os.O_EXCL | os.O_RDWR, 0o600)
+                os.posix_fallocate(fd, 0, nbytes)
+            except OSError:
+                ok = 0
+        ok = int(-max_over_ranks(-ok, device))  # min over ranks: every rank takes the same branch
+        if not ok:
+            if fd >= 0:
+                os.close(fd)
+                os.unlink(path)
+            return None
+        barrier()
+        if local != 0:
+            fd = os.open(path, os.O_RDWR)
+        try:
+            mm = mmap.mmap(fd, nbytes, mmap.MAP_SHARED, mmap.PROT_READ | mmap.PROT_WRITE)
+        finally:
+            os.close(fd)
+        addr = C.addressof(C.c_char.from_buffer(mm))
+        _lib.check(_lib.lib().vmm_host_register(addr, nbytes))
+        barrier()  # every rank holds a mapping: the name can go
+        if local == 0:
+            os.unlink(path)
+        pool = SharedHostPool(mm, nbytes, addr, filler=local == 0)
+        pool._registered = True
+        return pool
+
+    def ready(self):
+        """Fence after the filler wrote the weights."""
+        barrier()
+
+    def close(self):
+        if self._registered:
+            try:
+                from . import _lib
+
+                _lib.lib().vmm_host_unregister(self.addr)
+            except Exception:  # noqa: BLE001  (interpreter teardown: the context may be gone)
+                pass
+            self._registered = False

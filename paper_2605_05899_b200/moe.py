@@ -107,9 +107,14 @@ class StackConfig:
 
 
 class ExpertStore:
-    """Expert weights: pinned host pool + HBM slot arena + router weights."""
+    """Expert weights: pinned host pool + HBM slot arena + router weights.
 
-    def __init__(self, cfg: StackConfig, seed: int = 0, device=None):
+    Under a multi-rank process group the host pool is ONE shared-memory
+    segment per node, page-locked in every rank (dist.SharedHostPool,
+    SURVEY 8(e) mode DP); alone, or when /dev/shm cannot hold it, each rank
+    pins its own (`self.host_pool_kind` says which)."""
+
+    def __init__(self, cfg: StackConfig, seed: int = 0, device=None, share_host_pool: bool = True):
         self.cfg = cfg
         dev = device or torch.device("cuda", torch.cuda.current_device())
         self.device = dev
@@ -117,14 +122,31 @@ class ExpertStore:
         self.host_layers = max(1, min(cfg.host_layers, L))
         n_host = self.host_layers * E
         g = torch.Generator(device=dev).manual_seed(seed)
-        self.pool = torch.empty((n_host, cfg.slot_elems), dtype=torch.bfloat16, pin_memory=True)
+        self._shared = None
+        if share_host_pool:
+            from . import dist as vdist
+
+            tag = f"{os.environ.get('MASTER_PORT', '0')}_{os.getppid()}_{seed}_{n_host}_{cfg.slot_bytes}"
+            self._shared = vdist.SharedHostPool.create(n_host * cfg.slot_bytes, tag, dev)
+        if self._shared is not None:
+            self.pool = torch.frombuffer(self._shared.mm, dtype=torch.bfloat16).view(n_host, cfg.slot_elems)
+            self.host_pool_kind = "shared (one page-locked shm pool per node)"
+            fill = self._shared.filler
+        else:
+            self.pool = torch.empty((n_host, cfg.slot_elems), dtype=torch.bfloat16, pin_memory=True)
+            self.host_pool_kind = "pinned per rank"
+            fill = True
         chunk = max(1, (512 << 20) // (cfg.slot_bytes))
         for s0 in range(0, n_host, chunk):
             s1 = min(n_host, s0 + chunk)
             w = torch.randn((s1 - s0, cfg.slot_elems), generator=g, device=dev, dtype=torch.float32)
             w[:, : 2 * I * H] *= 1.0 / math.sqrt(H)
             w[:, 2 * I * H:] *= 1.0 / math.sqrt(I)
-            self.pool[s0:s1].copy_(w.to(torch.bfloat16))
+            if fill:
+                self.pool[s0:s1].copy_(w.to(torch.bfloat16))
+        if self._shared is not None:
+            torch.cuda.synchronize(dev)
+            self._shared.ready()  # the filler's weights are in the segment before any rank reads it
         self.n_pinned_slots = cfg.l_pinned * E
         S = cfg.shared_experts
         # arena: [pinned prefix experts | cache slabs | always-resident shared experts (L*S)]

@@ -160,3 +160,55 @@ def test_sharded_cache_world2_peer_pulls_bit_identical():
     for p in procs:
         p.join(timeout=60)
     assert [o[1] for o in outs] == [True, True], outs
+
+
+def _pool_worker(rank, world, port, q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        from paper_2605_05899_b200.moe import ExpertStore
+
+        cfg = _cfg()
+        store = ExpertStore(cfg, seed=11)
+        # every rank reads the segment the filler (local rank 0) wrote, through its own page-locked mapping:
+        # a copy-engine H2D of the whole pool and a host-side checksum
+        dev_copy = torch.empty(store.pool.shape, dtype=store.pool.dtype, device="cuda")
+        dev_copy.copy_(store.pool, non_blocking=True)
+        torch.cuda.synchronize()
+        ck = float(dev_copy.float().abs().sum().item())
+        same = bool(torch.equal(dev_copy.cpu(), store.pool))
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, store.host_pool_kind, ck, same, float(store.router.float().abs().sum().item())))
+    except Exception as exc:  # noqa: BLE001
+        q.put((rank, f"error: {exc!r}", 0.0, False, 0.0))
+
+
+def test_dp_ranks_share_one_page_locked_host_pool():
+    """SURVEY 8(e) mode DP: the ranks of a node share ONE expert pool (a /dev/shm
+    segment page-locked in every rank); every rank's copy engine reads the
+    weights the filler wrote, identical to a single-process store of the same
+    seed (same generator stream: the router weights after the pool agree too)."""
+    import torch.multiprocessing as mp
+
+    from paper_2605_05899_b200.moe import ExpertStore
+
+    ref = ExpertStore(_cfg(), seed=11)
+    ref_ck = float(ref.pool.float().abs().sum().item())
+    ref_router = float(ref.router.float().abs().sum().item())
+    assert ref.host_pool_kind == "pinned per rank"  # alone: no process group, own pinned pool
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pool_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = sorted(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    for rank, kind, ck, same, router_ck in outs:
+        assert kind.startswith("shared"), outs
+        assert same and ck == ref_ck and router_ck == ref_router, outs
