@@ -1,9 +1,11 @@
 """Host->device link probe: what limits the pinned-pool expert copies?
 
-Two ranks sharing one GPU measured 43 GB/s EACH concurrently (87 GB/s total,
-gpurun_out/r2j) while one stream of 9.44 MB copies tops out near 53-56 GB/s,
-so a single copy stream is not the link's limit.  This probe measures, in one
-process:
+An early two-process run suggested 43 GB/s EACH (87 GB/s total); that was an
+artefact of unsynchronised timing windows -- with a synchronised start two
+processes get 27.7 GB/s each, 55.4 GB/s together, and a second CUDA context
+in one process adds nothing either (tools/probes/h2d_contexts.py,
+profiles/r02_h2d_contexts.json): ~55.5 GB/s is the link.  This probe measures,
+in one process:
   A  one 1 GiB copy                                        (copy engine, 1 stream)
   B  1 GiB split over N streams, N = 2/4/8                (several copy engines)
   C  N streams from N SEPARATELY pinned buffers            (host memory placement)
