@@ -249,6 +249,17 @@ int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offsets, int E, 
                              const uint32_t *d_ready, int ready_base, uint32_t *d_done,
                              const void *d_x_rows, const int32_t *d_src_row, int n_x_rows, void *d_h1, void *d_y,
                              void *stream);
+/* Same, walking the experts in d_order (nullable, a device permutation of
+ * [0, E)) instead of id order on the CTA-pair path: the executor puts a layer's
+ * resident experts first and its misses in copy-issue order, largest first, so
+ * the kernel's tail after the last copy lands is the smallest expert's tiles.
+ * Bit-identical to any other order (each output row depends on its own expert). */
+int vmm_grouped_swiglu_fused_ex(const void *d_xp, const int32_t *d_offsets, int E, int M_total, int H, int I,
+                                const void *d_w13_arena, const void *d_w2_arena, long long slot_stride,
+                                long long n_slots, const int32_t *d_slot_of_expert, const uint32_t *d_need,
+                                const uint32_t *d_ready, int ready_base, uint32_t *d_done, const void *d_x_rows,
+                                const int32_t *d_src_row, int n_x_rows, void *d_h1, void *d_y,
+                                const int32_t *d_order, void *stream);
 /* H1 is scratch.  On the CTA-pair path (tensor-bound batches) the last GEMM2 tile
  * that consumes an H1 block drops it from L2 without a write-back
  * (discard.global.L2), so d_h1's contents after the call are undefined; keep != 0
@@ -414,6 +425,15 @@ int vmm_copy_async(void *d_dst, const void *src, size_t bytes, void *stream);
  * expert) into arena slot (slab_offset + slab) */
 int vmm_xfer_issue_engine(vmm_xfer *x, vmm_engine *e, const void *h_pool, int host_layers, int experts,
                           void *d_arena, long long slab_offset, size_t slot_bytes, int *n_issued);
+/* Same, with the physical issue order of layer `layer_now`'s copies set by
+ * h_rank[expert] (lowest first; the other layers' copies follow in decided
+ * order; the decided order is kept whenever two copies target one slab).  The
+ * decisions, slabs and logical clock are the engine's -- only the order in
+ * which the copy engine moves them changes.  h_issued_experts (nullable, [E])
+ * receives layer_now's experts in issue order. */
+int vmm_xfer_issue_engine_ordered(vmm_xfer *x, vmm_engine *e, const void *h_pool, int host_layers, int experts,
+                                  void *d_arena, long long slab_offset, size_t slot_bytes, int layer_now,
+                                  const int32_t *h_rank, int32_t *h_issued_experts, int *n_issued);
 int vmm_xfer_sync(vmm_xfer *x);
 /* make compute_stream wait for every copy issued so far */
 int vmm_xfer_join(vmm_xfer *x, void *compute_stream);
@@ -500,6 +520,8 @@ typedef struct {
   double *mlp_hist;                     /* d [E] scratch: the history feature of the context layer */
   int route_batch_rows;                 /* rows of the logical batch these rows belong to (0: n_rows); the
                                            router's split count follows it (vmm_route_topk_ex) */
+  int32_t *order_host;                  /* nullable h pinned [L][E]: per-layer expert walk / copy order */
+  int32_t *order_dev;                   /* nullable d [L][E] (with order_host: largest experts first) */
 } vmm_stack_desc;
 
 typedef struct {

@@ -62,7 +62,7 @@ class StackDesc(C.Structure):
         ("mlp_emb", P), ("mlp_drift", P), ("mlp_hv", P), ("mlp_ids", P),
         ("mlp_dim", I32), ("mlp_n_ids", I32), ("mlp_hidden", I32), ("mlp_bottleneck", I32),
         ("mlp_w1", P), ("mlp_b1", P), ("mlp_w2", P), ("mlp_b2", P), ("mlp_wo", P), ("mlp_bo", P),
-        ("mlp_hist", P), ("route_batch_rows", I32),
+        ("mlp_hist", P), ("route_batch_rows", I32), ("order_host", P), ("order_dev", P),
     ]
 
 
@@ -104,6 +104,8 @@ _SIGS = {
     "vmm_decode_glue": (I32, [P, P, P, P, I32, I32, I32, P, P, P, P, P, I32, P, P, P, P, P, P, P]),
     "vmm_grouped_swiglu": (I32, [P, P, I32, I32, I32, I32, P, P, I64, I64, P, P, P, P]),
     "vmm_grouped_swiglu_fused": (I32, [P, P, I32, I32, I32, I32, P, P, I64, I64, P, P, P, I32, P, P, P, I32, P, P, P]),
+    "vmm_grouped_swiglu_fused_ex": (I32, [P, P, I32, I32, I32, I32, P, P, I64, I64, P, P, P, I32, P, P, P, I32, P, P, P,
+                                          P]),
     "vmm_grouped_swiglu_simt": (I32, [P, P, I32, I32, I32, I32, P, P, I64, P, P, P, P]),
     "vmm_engine_create": (I32, [C.POINTER(EngineConfig), C.POINTER(P)]),
     "vmm_engine_destroy": (None, [P]),
@@ -148,6 +150,7 @@ _SIGS = {
     "vmm_xfer_reset_stats": (I32, [P]),
     "vmm_xfer_stream": (P, [P]),
     "vmm_xfer_issue_engine": (I32, [P, P, P, I32, I32, P, I64, SZ, PI32]),
+    "vmm_xfer_issue_engine_ordered": (I32, [P, P, P, I32, I32, P, I64, SZ, I32, P, P, PI32]),
     "vmm_combine_shared": (I32, [P, P, P, P, I32, I32, I32, P, I32, P, P]),
     "vmm_shared_plan": (I32, [I32, I32, P, P, P]),
     "vmm_combine_norm": (I32, [P, P, P, P, I32, I32, I32, P, I32, C.c_float, P, P, P]),

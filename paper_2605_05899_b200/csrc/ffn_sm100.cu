@@ -541,8 +541,9 @@ constexpr size_t kSmem2 = (size_t)kStages2 * kStage2 + kStg2 + 1024 + 256;
 // group.  With the rotation every cluster cycles through all N-tiles.
 __device__ __forceinline__ int pair_sched(int w, int cid, int ncl) { return w * ncl + (cid + w) % ncl; }
 
+// tile_base[i] = first m-tile of the i-th expert in walk order (order[i]; identity by default)
 __device__ __forceinline__ TileInfo pair_tile_info(int m_tile, const int *tile_base, const int *offs, const int *slots,
-                                                   int E) {
+                                                   const int *order, int E) {
   TileInfo ti;
   int lo = 0, hi = E - 1;
   while (lo < hi) {
@@ -550,10 +551,11 @@ __device__ __forceinline__ TileInfo pair_tile_info(int m_tile, const int *tile_b
     if (tile_base[mid] <= m_tile) lo = mid; else hi = mid - 1;
   }
   while (lo + 1 < E && tile_base[lo + 1] <= m_tile) ++lo;
-  ti.expert = lo;
-  ti.row0 = offs[lo] + (m_tile - tile_base[lo]) * BM2;
-  ti.row_end = offs[lo + 1];
-  ti.slot = slots[lo];
+  const int e = order[lo];
+  ti.expert = e;
+  ti.row0 = offs[e] + (m_tile - tile_base[lo]) * BM2;
+  ti.row_end = offs[e + 1];
+  ti.slot = slots[e];
   ti.n_tile = 0;
   return ti;
 }
@@ -575,7 +577,7 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
                 const uint32_t *__restrict__ need, const uint32_t *ready, int ready_base, uint32_t *done, int E, int H,
                 int I, int lag, const __nv_bfloat16 *__restrict__ xg, const int32_t *__restrict__ src_row,
                 int M_total, __nv_bfloat16 *__restrict__ h1, __nv_bfloat16 *__restrict__ y, int discard_h1,
-                int l2_hints) {
+                int l2_hints, const int32_t *__restrict__ walk_order) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char *stg = smem + kStages2 * kStage2;
@@ -585,6 +587,7 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
   uint64_t *tmem_empty = tmem_full + 2;    // [2] (the leader's counts 8 epilogue warps of the pair)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 2);
   __shared__ int s_offs[VMM_MAX_EXPERTS + 1], s_tile_base[VMM_MAX_EXPERTS + 1], s_slots[VMM_MAX_EXPERTS];
+  __shared__ int s_order[VMM_MAX_EXPERTS];
   __shared__ uint32_t s_need[VMM_MAX_EXPERTS];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -594,12 +597,14 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     s_slots[e] = slot_of[e];
     s_need[e] = need ? need[e] : 0u;
+    s_order[e] = walk_order ? walk_order[e] : e;  // expert walk order (a permutation of [0, E))
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     int acc = 0;
-    for (int e = 0; e < E; ++e) {
-      s_tile_base[e] = acc;
+    for (int i = 0; i < E; ++i) {
+      const int e = s_order[i];
+      s_tile_base[i] = acc;
       acc += (s_offs[e + 1] - s_offs[e] + BM2 - 1) / BM2;
     }
     s_tile_base[E] = acc;
@@ -642,7 +647,7 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
         if (t >= total) continue;
         const FusedTile f = fused_tile(t, n1, n2, MT, lag);
         if (!f.valid) continue;
-        const TileInfo ti = pair_tile_info(f.m_tile, s_tile_base, s_offs, s_slots, E);
+        const TileInfo ti = pair_tile_info(f.m_tile, s_tile_base, s_offs, s_slots, s_order, E);
         const uint32_t nd = s_need[ti.expert];
         {
           PROF_T0();
@@ -766,7 +771,7 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
         }
         continue;
       }
-      const TileInfo ti = pair_tile_info(f.m_tile, s_tile_base, s_offs, s_slots, E);
+      const TileInfo ti = pair_tile_info(f.m_tile, s_tile_base, s_offs, s_slots, s_order, E);
       // warp gw4 owns local rows [32 gw4, +32); each cp.async instruction covers 4 rows x 128 B
       // (8 lanes per row: coalesced 128-byte pieces, 4 L1 wavefronts instead of 32)
       const int gw4 = t >> 5;
@@ -843,7 +848,7 @@ ffn_pair_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant
       if (t >= total) continue;
       const FusedTile f = fused_tile(t, n1, n2, MT, lag);
       if (!f.valid) continue;
-      const TileInfo ti = pair_tile_info(f.m_tile, s_tile_base, s_offs, s_slots, E);
+      const TileInfo ti = pair_tile_info(f.m_tile, s_tile_base, s_offs, s_slots, s_order, E);
       const int b = local & 1, use = local >> 1;
       ++local;
       const int r_w0 = ti.row0 + 128 * (int)rank + q * 32;
@@ -1620,12 +1625,32 @@ extern "C" int vmm_ffn_keep_h1(int keep) {
   return VMM_OK;
 }
 
+extern "C" int vmm_grouped_swiglu_fused_ex(const void *d_xp, const int32_t *d_offsets, int E, int M_total, int H,
+                                           int I, const void *d_w13_arena, const void *d_w2_arena,
+                                           long long slot_stride, long long n_slots, const int32_t *d_slot_of_expert,
+                                           const uint32_t *d_need, const uint32_t *d_ready, int ready_base,
+                                           uint32_t *d_done, const void *d_x_rows, const int32_t *d_src_row,
+                                           int n_x_rows, void *d_h1, void *d_y, const int32_t *d_order,
+                                           void *stream);
+
 extern "C" int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offsets, int E, int M_total, int H, int I,
                                         const void *d_w13_arena, const void *d_w2_arena, long long slot_stride,
                                         long long n_slots, const int32_t *d_slot_of_expert, const uint32_t *d_need,
                                         const uint32_t *d_ready, int ready_base, uint32_t *d_done,
                                         const void *d_x_rows, const int32_t *d_src_row, int n_x_rows, void *d_h1,
                                         void *d_y, void *stream) {
+  return vmm_grouped_swiglu_fused_ex(d_xp, d_offsets, E, M_total, H, I, d_w13_arena, d_w2_arena, slot_stride, n_slots,
+                                     d_slot_of_expert, d_need, d_ready, ready_base, d_done, d_x_rows, d_src_row,
+                                     n_x_rows, d_h1, d_y, nullptr, stream);
+}
+
+extern "C" int vmm_grouped_swiglu_fused_ex(const void *d_xp, const int32_t *d_offsets, int E, int M_total, int H,
+                                           int I, const void *d_w13_arena, const void *d_w2_arena,
+                                           long long slot_stride, long long n_slots, const int32_t *d_slot_of_expert,
+                                           const uint32_t *d_need, const uint32_t *d_ready, int ready_base,
+                                           uint32_t *d_done, const void *d_x_rows, const int32_t *d_src_row,
+                                           int n_x_rows, void *d_h1, void *d_y, const int32_t *d_order,
+                                           void *stream) {
   if (M_total <= 0) return VMM_OK;
   if (M_total <= kSkinnyRows) {  // decode-sized: persistent weight-streaming kernel (waits on flags too)
     if (d_src_row) return vmm::fail(VMM_ECONTRACT, "row gather needs the tensor-core path (M > 16)");
@@ -1752,11 +1777,11 @@ extern "C" int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offse
       ffn_pair_kernel<true><<<gridp, kThreads + 128, kSmem2, s>>>(
           mx, mw13, mh1, mw2, mh1s, mys, d_offsets, d_slot_of_expert, d_need, d_ready, ready_base, d_done, E, H, I,
           lagp, (const __nv_bfloat16 *)d_x_rows, d_src_row, M_total, (__nv_bfloat16 *)d_h1, (__nv_bfloat16 *)d_y,
-          discard, l2_hints);
+          discard, l2_hints, d_order);
     else
       ffn_pair_kernel<false><<<gridp, kThreads, kSmem2, s>>>(
           mx, mw13, mh1, mw2, mh1s, mys, d_offsets, d_slot_of_expert, d_need, d_ready, ready_base, d_done, E, H, I,
-          lagp, nullptr, nullptr, M_total, (__nv_bfloat16 *)d_h1, (__nv_bfloat16 *)d_y, discard, l2_hints);
+          lagp, nullptr, nullptr, M_total, (__nv_bfloat16 *)d_h1, (__nv_bfloat16 *)d_y, discard, l2_hints, d_order);
     VMM_LAUNCH_CHECK("ffn_pair_kernel");
     return VMM_OK;
   }

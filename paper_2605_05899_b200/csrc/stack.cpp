@@ -50,6 +50,9 @@ int vmm_engine_slots(const vmm_engine *e, int layer, const int32_t *h_demand, in
 int vmm_engine_emit(vmm_engine *e, int layer, const double *h_y);
 int vmm_xfer_issue_engine(vmm_xfer *x, vmm_engine *e, const void *h_pool, int host_layers, int experts,
                           void *d_arena, long long slab_offset, size_t slot_bytes, int *n_issued);
+int vmm_xfer_issue_engine_ordered(vmm_xfer *x, vmm_engine *e, const void *h_pool, int host_layers, int experts,
+                                  void *d_arena, long long slab_offset, size_t slot_bytes, int layer_now,
+                                  const int32_t *h_rank, int32_t *h_issued_experts, int *n_issued);
 int vmm_gather_i32(const int32_t *d_src, const int32_t *d_rows, int n, int width, int32_t *d_dst, void *stream);
 int vmm_gather_f32(const float *d_src, const int32_t *d_rows, int n, int width, float *d_dst, void *stream);
 const uint32_t *vmm_xfer_ready(vmm_xfer *x);
@@ -149,6 +152,10 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
   int ping = 0, copies = 0;
   std::vector<int32_t> demand, slabs;
   std::vector<uint32_t> need;
+  // expert walk / copy order (largest first) for the CTA-pair FFN; VMM_NO_WALK_ORDER=1: id order
+  static const bool no_walk = std::getenv("VMM_NO_WALK_ORDER") != nullptr;
+  std::vector<int32_t> by_size(E), rank_of(E), issued(E);
+  std::vector<char> is_miss(E);
   const uint32_t *ready = vmm_xfer_ready(xf);
   // tensor-core FFN with per-expert ready flags: the layer's FFN starts while its misses still stream in
   // (VMM_FFN_FENCE=1: whole-layer event fence instead, e.g. under a serialising profiler)
@@ -314,6 +321,7 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
     }
     auto c1 = clk::now(), c2 = c1;
     int n = 0;
+    const int32_t *order_of = nullptr;  // FFN expert walk order (nullptr: id order)
     demand.clear();
     if (!pinned_only) {
       bool known = false;
@@ -345,7 +353,37 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
       VMM_TRY(vmm_engine_layer(eng, l, demand.data(), (int)demand.size(), phase, step, nullptr));
       if (out && out->copy_marks)
         VMM_TRY(vmm_xfer_mark(xf, out->copy_marks[3 * (l - l0)]));
-      VMM_TRY(vmm_xfer_issue_engine(xf, eng, d.pool, d.host_layers, E, d.arena, d.n_pinned_slots, d.slot_bytes, &n));
+      // the CTA-pair FFN (every expert >= 256 rows on average) with per-expert ready flags
+      const bool walk = !no_walk && flagged && d.order_host && d.order_dev && l >= lp &&
+                        (long long)n_rows * k >= 256LL * E;
+      if (walk) {
+        // largest experts first (the counts on the host: the first chunk's at prefill sizes): the
+        // layer's misses cross PCIe in that order, and the FFN walks its resident experts first,
+        // then the misses in landing order -- so the work left when the last copy lands is the
+        // smallest expert's.  Issue order only: decisions and slabs are the engine's.
+        for (int e = 0; e < E; ++e) by_size[e] = e;
+        std::stable_sort(by_size.begin(), by_size.end(), [&](int a, int b) { return ch[a] > ch[b]; });
+        for (int i = 0; i < E; ++i) rank_of[by_size[i]] = i;
+        std::fill(issued.begin(), issued.end(), -1);
+        VMM_TRY(vmm_xfer_issue_engine_ordered(xf, eng, d.pool, d.host_layers, E, d.arena, d.n_pinned_slots,
+                                              d.slot_bytes, l, rank_of.data(), issued.data(), &n));
+        // issued[]: this layer's copied experts in issue order, then -1
+        std::fill(is_miss.begin(), is_miss.end(), 0);
+        int n_miss = 0;
+        while (n_miss < E && issued[n_miss] >= 0 && issued[n_miss] < E && !is_miss[issued[n_miss]])
+          is_miss[issued[n_miss++]] = 1;
+        int32_t *orow = d.order_host + (size_t)l * E;
+        int w = 0;
+        for (int i = 0; i < E; ++i)
+          if (!is_miss[by_size[i]]) orow[w++] = by_size[i];  // resident (or not demanded) experts first
+        for (int i = 0; i < n_miss; ++i) orow[w++] = issued[i];
+        int32_t *odev = d.order_dev + (size_t)l * E;
+        VMM_CUDA(cudaMemcpyAsync(odev, orow, sizeof(int32_t) * E, cudaMemcpyHostToDevice, st), "order H2D");
+        order_of = odev;
+      } else {
+        VMM_TRY(vmm_xfer_issue_engine(xf, eng, d.pool, d.host_layers, E, d.arena, d.n_pinned_slots, d.slot_bytes,
+                                      &n));
+      }
       copies += n;
       if (out && out->copy_marks)
         VMM_TRY(vmm_xfer_mark(xf, out->copy_marks[3 * (l - l0) + 1]));
@@ -392,10 +430,11 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
     }
     if (out && out->ffn_start)
       VMM_CUDA(cudaEventRecord((cudaEvent_t)out->ffn_start[l - l0], st), "ffn start event");
-    VMM_TRY(vmm_grouped_swiglu_fused(d.xp, d.off, E, M, H, I, d.arena, (const char *)d.arena + (size_t)2 * I * H * 2,
-                                     (long long)3 * I * H, d.n_slots, slot_of, need_of, ready,
-                                     (int)d.n_pinned_slots, d.ffn_done, gather ? xn : nullptr,
-                                     gather ? d.src : nullptr, n_rows, d.h1, d.y, stream));
+    VMM_TRY(vmm_grouped_swiglu_fused_ex(d.xp, d.off, E, M, H, I, d.arena,
+                                        (const char *)d.arena + (size_t)2 * I * H * 2, (long long)3 * I * H, d.n_slots,
+                                        slot_of, need_of, ready, (int)d.n_pinned_slots, d.ffn_done,
+                                        gather ? xn : nullptr, gather ? d.src : nullptr, n_rows, d.h1, d.y, order_of,
+                                        stream));
     if (out && out->ffn_end) VMM_CUDA(cudaEventRecord((cudaEvent_t)out->ffn_end[l - l0], st), "ffn end event");
     void *dst = ping ? d.out1 : d.out0;
     const int S = d.shared;

@@ -20,6 +20,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -289,25 +290,59 @@ int vmm_xfer_set_sources(vmm_xfer *x, const void *const *h_table, long long n) {
 
 int vmm_engine_copies(vmm_engine *e, int32_t *out, int cap);
 
-int vmm_xfer_issue_engine(vmm_xfer *x, vmm_engine *e, const void *h_pool, int host_layers, int experts,
-                          void *d_arena, long long slab_offset, size_t slot_bytes, int *n_issued) {
+int vmm_xfer_issue_engine_ordered(vmm_xfer *x, vmm_engine *e, const void *h_pool, int host_layers, int experts,
+                                  void *d_arena, long long slab_offset, size_t slot_bytes, int layer_now,
+                                  const int32_t *h_rank, int32_t *h_issued_experts, int *n_issued) {
+  // every decided copy, in the engine's order
+  std::vector<int32_t> all;
   int32_t buf[3 * 256];
-  int total = 0;
   for (;;) {
     int n = vmm_engine_copies(e, buf, 256);
     if (n <= 0) break;
-    for (int i = 0; i < n; ++i) {
-      int layer = buf[3 * i], expert = buf[3 * i + 1], slab = buf[3 * i + 2];
-      const char *src = h_pool ? (const char *)h_pool + ((size_t)(layer % host_layers) * experts + expert) * slot_bytes
-                               : (const char *)x->sources.at((size_t)layer * experts + expert);
-      char *dst = (char *)d_arena + (size_t)(slab_offset + slab) * slot_bytes;
-      int st = vmm_xfer_copy(x, slab, src, dst, slot_bytes, 0);
-      if (st) return st;
-    }
-    total += n;
+    all.insert(all.end(), buf, buf + 3 * n);
   }
-  if (n_issued) *n_issued = total;
+  const int n = (int)all.size() / 3;
+  std::vector<int> idx(n);
+  for (int i = 0; i < n; ++i) idx[i] = i;
+  if (h_rank && n > 1) {
+    // Physical issue order only (the decisions, slabs and logical clock are the engine's): this
+    // layer's copies by h_rank (lowest first), then the rest in decided order.  Kept as decided
+    // when two copies target one slab, so a slab's fills land in decided order.
+    const int nslabs = (int)x->slab_fill_seq.size();
+    std::vector<char> seen((size_t)nslabs, 0);
+    bool distinct = true;
+    for (int i = 0; i < n && distinct; ++i) {
+      const int slab = all[3 * i + 2];
+      if (slab < 0 || slab >= nslabs || seen[slab]) distinct = false;
+      else seen[slab] = 1;
+    }
+    if (distinct)
+      std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {
+        const bool ca = all[3 * a] == layer_now, cb = all[3 * b] == layer_now;
+        if (ca != cb) return ca;
+        if (!ca) return false;
+        return h_rank[all[3 * a + 1]] < h_rank[all[3 * b + 1]];
+      });
+  }
+  int n_now = 0;
+  for (int j = 0; j < n; ++j) {
+    const int i = idx[j];
+    int layer = all[3 * i], expert = all[3 * i + 1], slab = all[3 * i + 2];
+    const char *src = h_pool ? (const char *)h_pool + ((size_t)(layer % host_layers) * experts + expert) * slot_bytes
+                             : (const char *)x->sources.at((size_t)layer * experts + expert);
+    char *dst = (char *)d_arena + (size_t)(slab_offset + slab) * slot_bytes;
+    int st = vmm_xfer_copy(x, slab, src, dst, slot_bytes, 0);
+    if (st) return st;
+    if (h_issued_experts && layer == layer_now && n_now < experts) h_issued_experts[n_now++] = expert;
+  }
+  if (n_issued) *n_issued = n;
   return VMM_OK;
+}
+
+int vmm_xfer_issue_engine(vmm_xfer *x, vmm_engine *e, const void *h_pool, int host_layers, int experts,
+                          void *d_arena, long long slab_offset, size_t slot_bytes, int *n_issued) {
+  return vmm_xfer_issue_engine_ordered(x, e, h_pool, host_layers, experts, d_arena, slab_offset, slot_bytes, -1,
+                                       nullptr, nullptr, n_issued);
 }
 
 }  // extern "C"

@@ -255,7 +255,8 @@ class keep_h1:
 
 
 def grouped_swiglu(xp, offsets, arena, slot_of, inter: int, stream=None, h1=None, y=None, simt: bool = False,
-                   fused: bool = True, need=None, ready=None, ready_base: int = 0, x_rows=None, src_row=None):
+                   fused: bool = True, need=None, ready=None, ready_base: int = 0, x_rows=None, src_row=None,
+                   order=None):
     """Grouped SwiGLU over expert-contiguous rows of xp.
 
     Default: the fused persistent tcgen05 kernel (GEMM1+GEMM2 in one launch);
@@ -263,7 +264,8 @@ def grouped_swiglu(xp, offsets, arena, slot_of, inter: int, stream=None, h1=None
     need/ready: optional per-expert fill sequence numbers / device flags
     (vmm_grouped_swiglu_fused's copy overlap).  x_rows/src_row: gather the
     GEMM1 rows from the token rows (TMA gather4) -- xp may then be None and
-    only its row count matters (pass an int).
+    only its row count matters (pass an int).  order: optional i32 [E] device
+    permutation, the fused CTA-pair kernel's expert walk order.
     arena: bf16 [n_slots, 3*I*H] -- per slot W13 ([2I,H], interleaved) then W2 ([H,I])."""
     if src_row is not None:
         M, H = int(xp), int(x_rows.shape[1])
@@ -286,10 +288,10 @@ def grouped_swiglu(xp, offsets, arena, slot_of, inter: int, stream=None, h1=None
     elif fused:
         _n(1)
         done = torch.empty(M // 128 + E + 1, dtype=torch.int32, device=dev)
-        check(L.vmm_grouped_swiglu_fused(ptr(xp), ptr(offsets), E, M, H, inter, ptr(arena), w2_base, stride,
-                                         n_slots, ptr(slot_of), ptr(need), ready, ready_base, ptr(done),
-                                         ptr(x_rows), ptr(src_row), 0 if x_rows is None else int(x_rows.shape[0]),
-                                         ptr(h1), ptr(y), stream_ptr(stream)))
+        check(L.vmm_grouped_swiglu_fused_ex(ptr(xp), ptr(offsets), E, M, H, inter, ptr(arena), w2_base, stride,
+                                            n_slots, ptr(slot_of), ptr(need), ready, ready_base, ptr(done),
+                                            ptr(x_rows), ptr(src_row), 0 if x_rows is None else int(x_rows.shape[0]),
+                                            ptr(h1), ptr(y), ptr(order), stream_ptr(stream)))
     else:
         _n(1 if M <= 16 else 2)
         check(L.vmm_grouped_swiglu(ptr(xp), ptr(offsets), E, M, H, inter, ptr(arena), w2_base, stride, n_slots,

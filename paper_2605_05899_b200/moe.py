@@ -323,6 +323,9 @@ class MoEStack:
         self.need_host = torch.zeros((L, E), dtype=torch.int32, pin_memory=True)
         self.need_dev = torch.zeros((L, E), dtype=torch.int32, device=self.device)
         self.counts_host = torch.zeros((L, E), dtype=torch.int32, pin_memory=True)
+        # per-layer expert walk / copy order of the CTA-pair FFN (largest experts first)
+        self.order_host = torch.zeros((L, E), dtype=torch.int32, pin_memory=True)
+        self.order_dev = torch.zeros((L, E), dtype=torch.int32, device=self.device)
         self.y_host = torch.zeros((L + 1, E), dtype=torch.float64, pin_memory=True)
         self.pow = torch.tensor(pow_table(cfg.history_decay, L), dtype=torch.float64, device=self.device)
         self.layer_ids = torch.arange(L, dtype=torch.int32, device=self.device)
@@ -689,7 +692,8 @@ class MoEStack:
             shared_src=at("shared_src", max(S, 1) * 4), shared_off=bufs[b_soff].data_ptr(),
             xs=at("xs", max(S, 1) * H * 2), h1s=at("h1s", max(S, 1) * I * 2), ys=at("ys", max(S, 1) * H * 2),
             need_host=self.need_host.data_ptr(), need_dev=self.need_dev.data_ptr(),
-            ffn_done=bufs[b_done].data_ptr(), route_batch_rows=int(batch_rows))
+            ffn_done=bufs[b_done].data_ptr(), route_batch_rows=int(batch_rows),
+            order_host=self.order_host.data_ptr(), order_dev=self.order_dev.data_ptr())
         mp = self._mlp
         if pred == 4 and eng is not None:
             ids_t = mp["ids"] if mlp_ids is None else mlp_ids

@@ -300,7 +300,11 @@ def test_fused_ffn_bit_identical_to_two_launches(shape):
         h1c, yc = kernels.grouped_swiglu(N * k, off, arena, slot_of, I, x_rows=x.cuda(), src_row=src)
     # the product path: consumed H1 rows dropped from L2 without write-back (CTA-pair tiles)
     _, yd = kernels.grouped_swiglu(xp, off, arena, slot_of, I, fused=True)
+    # any expert walk order (the executor's largest-first order on the CTA-pair path)
+    perm = torch.randperm(E, generator=torch.Generator().manual_seed(N)).int().cuda()
+    _, ye = kernels.grouped_swiglu(xp, off, arena, slot_of, I, fused=True, order=perm)
     torch.cuda.synchronize()
+    assert torch.equal(ya, ye)
     assert torch.equal(h1a, h1b)
     assert torch.equal(ya, yb)
     assert torch.equal(h1a, h1c)
