@@ -123,7 +123,59 @@ route_kernel(const __nv_bfloat16 *__restrict__ x, const __nv_bfloat16 *__restric
 // ---- skinny path (decode-sized N): spread the gate rows over many CTAs ----
 constexpr int kSkinnyMaxN = 32;
 
-// logits[n][g] = x[n] . W[g] for g in [0, G): one warp per gate row, all N tokens
+// logits[n][g] = x[n] . W[g] for g in [0, G): one warp per gate row, all N tokens.
+// The warp's whole gate row (CPL 16-byte chunks per lane) is loaded up front, so a
+// launch is one DRAM round trip for W plus the token rows from L2 -- not CPL of
+// them in sequence.  Lane sums run over its chunks c = lane + 32 j in j order,
+// then an xor tree: the same arithmetic as the generic loop below.
+template <int CPL>
+__global__ void __launch_bounds__(64) skinny_logits_reg_kernel(const __nv_bfloat16 *__restrict__ x,
+                                                               const __nv_bfloat16 *__restrict__ w, int N, int H,
+                                                               int G, float *__restrict__ logits) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= G) return;
+  const uint4 *wr = reinterpret_cast<const uint4 *>(w + (long long)warp * H);
+  const int nv = H / 8;
+  uint4 wv[CPL];
+#pragma unroll
+  for (int j = 0; j < CPL; ++j) {
+    const int c = lane + 32 * j;
+    wv[j] = c < nv ? __ldg(wr + c) : make_uint4(0u, 0u, 0u, 0u);
+  }
+  for (int n0 = 0; n0 < N; n0 += 2) {
+    float acc[2] = {0.f, 0.f};
+    uint4 xv[2][CPL];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {
+        const int c = lane + 32 * j;
+        xv[r][j] = (n0 + r < N && c < nv) ? __ldg(reinterpret_cast<const uint4 *>(x + (long long)(n0 + r) * H) + c)
+                                          : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {
+        if (lane + 32 * j < nv) {
+          const __nv_bfloat16 *wh = reinterpret_cast<const __nv_bfloat16 *>(&wv[j]);
+          const __nv_bfloat16 *xh = reinterpret_cast<const __nv_bfloat16 *>(&xv[r][j]);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc[r] = fmaf(__bfloat162float(xh[q]), __bfloat162float(wh[q]), acc[r]);
+        }
+      }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      float v = acc[r];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0 && n0 + r < N) logits[(long long)(n0 + r) * G + warp] = v;
+    }
+  }
+}
+
+// generic H (more than 16 chunks per lane): the same sums, one chunk at a time
 __global__ void skinny_logits_kernel(const __nv_bfloat16 *__restrict__ x, const __nv_bfloat16 *__restrict__ w,
                                      int N, int H, int G, float *__restrict__ logits) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -161,7 +213,9 @@ __global__ void skinny_logits_kernel(const __nv_bfloat16 *__restrict__ x, const 
   }
 }
 
-// per (token, gate group): top-k by (logit desc, id asc) with a warp argmax per pick
+// per (token, gate group): top-k by (logit desc, id asc; NaN ranks last) -- order-preserving
+// u32 keys, one warp max + one warp min (the lowest id among the equal keys) per pick (REDUX);
+// taken / padding columns carry key 0, below every real key (-inf maps to 0x007fffff)
 __global__ void skinny_topk_kernel(const float *__restrict__ logits, int N, int E, int NG, int k,
                                    int32_t *__restrict__ ids, float *__restrict__ gates,
                                    float *__restrict__ logits_out, uint32_t *__restrict__ counts,
@@ -171,38 +225,35 @@ __global__ void skinny_topk_kernel(const float *__restrict__ logits, int N, int 
   const int lane = threadIdx.x & 31;
   if (t >= N || g >= NG) return;
   const float *row = logits + (long long)t * NG * E + (long long)g * E;
-  float v[kMaxE / 32];
+  uint32_t key[kMaxE / 32];
 #pragma unroll
   for (int j = 0; j < kMaxE / 32; ++j) {
-    int e = lane + 32 * j;
+    const int e = lane + 32 * j;
     float f = e < E ? row[e] : -INFINITY;
     if (f != f) f = -INFINITY;
-    v[j] = f;
     if (g == 0 && logits_out && e < E) logits_out[(long long)t * E + e] = f;
+    const uint32_t u = __float_as_uint(f);
+    key[j] = e < E ? ((u & 0x80000000u) ? ~u : (u | 0x80000000u)) : 0u;
   }
-  unsigned taken[kMaxE / 32];
-#pragma unroll
-  for (int j = 0; j < kMaxE / 32; ++j) taken[j] = 0;
   float vals[kMaxK];
   int sel[kMaxK];
   for (int s = 0; s < k; ++s) {
-    float best = -INFINITY;
-    int bi = 0x7fffffff;
+    uint32_t bk = 0u;
+    int bj = 0;
 #pragma unroll
-    for (int j = 0; j < kMaxE / 32; ++j) {
-      int e = lane + 32 * j;
-      if (e < E && !((taken[j] >> lane) & 1u) && (bi == 0x7fffffff || v[j] > best)) { best = v[j]; bi = e; }
-    }
+    for (int j = 0; j < kMaxE / 32; ++j)
+      if (key[j] > bk) { bk = key[j]; bj = j; }  // strict: the lower column wins in-lane ties
+    const uint32_t m = __reduce_max_sync(0xffffffffu, bk);
+    const uint32_t cand = (bk == m) ? (uint32_t)(lane + 32 * bj) : 0xffffffffu;
+    int e = (int)__reduce_min_sync(0xffffffffu, cand);
+    if (e >= E) e = 0;  // unreachable for k <= E; keeps indices in range
+    sel[s] = e;
+    vals[s] = __uint_as_float((m & 0x80000000u) ? (m & 0x7fffffffu) : ~m);
+    if ((e & 31) == lane) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      float ov = __shfl_xor_sync(0xffffffffu, best, o);
-      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (oi != 0x7fffffff && (bi == 0x7fffffff || ov > best || (ov == best && oi < bi))) { best = ov; bi = oi; }
+      for (int j = 0; j < kMaxE / 32; ++j)
+        if (j == (e >> 5)) key[j] = 0u;
     }
-    if (bi == 0x7fffffff) bi = 0;
-    vals[s] = best;
-    sel[s] = bi;
-    if ((bi & 31) == lane) taken[bi >> 5] |= 1u << lane;
   }
   if (lane == 0) {
     if (g == 0) {
@@ -227,8 +278,17 @@ int route_skinny(const void *x, const void *w, int N, int H, int E, int NG, int 
     if (e != cudaSuccess) return vmm::cuda_status(e, "skinny scratch");
   }
   const int G = NG * E;
-  skinny_logits_kernel<<<(G * 32 + 255) / 256, 256, 0, s>>>((const __nv_bfloat16 *)x, (const __nv_bfloat16 *)w, N,
-                                                            H, G, scratch);
+  const int cpl = (H / 8 + 31) / 32;  // 16-byte chunks of a gate row per lane
+  const __nv_bfloat16 *xb = (const __nv_bfloat16 *)x, *wb = (const __nv_bfloat16 *)w;
+  const int grid2 = (G + 1) / 2;       // two warps (gate rows) per CTA: G/2 SMs stream W at once
+  switch (cpl) {
+#define VMM_CPL(C) \
+  case C: skinny_logits_reg_kernel<C><<<grid2, 64, 0, s>>>(xb, wb, N, H, G, scratch); break;
+    VMM_CPL(1) VMM_CPL(2) VMM_CPL(3) VMM_CPL(4) VMM_CPL(5) VMM_CPL(6) VMM_CPL(7) VMM_CPL(8)
+    VMM_CPL(9) VMM_CPL(10) VMM_CPL(11) VMM_CPL(12) VMM_CPL(13) VMM_CPL(14) VMM_CPL(15) VMM_CPL(16)
+#undef VMM_CPL
+    default: skinny_logits_kernel<<<(G * 32 + 255) / 256, 256, 0, s>>>(xb, wb, N, H, G, scratch);
+  }
   VMM_LAUNCH_CHECK("skinny_logits_kernel");
   skinny_topk_kernel<<<N, 32 * NG, 0, s>>>(scratch, N, E, NG, k, ids, gates, logits_out, counts, la_counts);
   VMM_LAUNCH_CHECK("skinny_topk_kernel");
