@@ -722,6 +722,9 @@ def main():
                          "bytes_per_launch": float(np.mean(nbytes)), "flops_per_launch": float(np.mean(nflops)),
                          "hbm_frac": (sum(nbytes) / t_act / 1e9) / hbm_peak,
                          "tensor_frac": (sum(nflops) / t_act / 1e12) / tc_peak,
+                         # the replay runs right after the long timed steps, in the power-capped regime the
+                         # in-step FFN runs in: its fraction of the SUSTAINED tensor peak beside the burst one
+                         "tensor_frac_of_sustained": (sum(nflops) / t_act / 1e12) / tc_sus,
                          "peak_source": peak_src,
                          "step": step_rl},
             "clocks": clk.summary(local),
