@@ -125,3 +125,89 @@ def test_headline_shape_live_gate_decisions_and_hidden_states(R):
             _, y = moe_ref.expert_ffn(xl[t:t + 1], wg, wu, wd)
             acc[t] += gates[t, j] * y[0].float()
     torch.testing.assert_close(res.hidden.cpu()[rows].float(), acc[rows], rtol=3e-2, atol=3e-2)
+
+
+@pytest.mark.parametrize("name,R", [("c2_phi2", 1), ("c4_dsvl2s", 1), ("c4_dsvl2s", 4)])
+def test_named_shapes_live_decisions_and_hidden_states(name, R):
+    """BASELINE configs[1] and [3] at their real geometry, as `bench.py --workload`
+    runs them: live routing with the workload's predictor (history), MoE-LLaVA-
+    Phi2 (H 2560, 4 experts top-2, I 10240: 157 MB experts, 128x256 FFN tiles) and
+    DeepSeek-VL2-Small (64 routed top-6 + 2 always-resident shared experts, I
+    1408, full last pinned layer).  Decisions replay exactly through the oracle
+    engine on the run's own routes and scores; hidden states equal a resident-
+    expert walk (routed + shared experts) bit for bit."""
+    w = WORKLOADS[name]
+    cfg = StackConfig.from_workload(w, routing="live", predictor=w.predictor, host_layers=8,
+                                    transfer_ms=w.expert_bytes / 55.6e9 * 1e3, gpu_ms=0.01)
+    store = ExpertStore(cfg, seed=2000)
+    stack = MoEStack(cfg, store=store)
+    trs = [generate_trace(w.trace_config(seed=s)) for s in range(R)]
+    T1 = trs[0].num_tokens
+    T = T1 * R
+    offs = [r * T1 for r in range(R + 1)]
+    g = torch.Generator(device="cuda").manual_seed(91 + R)
+    x = torch.randn((T, w.hidden), generator=g, device="cuda").to(torch.bfloat16)
+    sal = torch.from_numpy(np.concatenate([t.saliency for t in trs])).cuda()
+    mod = torch.from_numpy(np.concatenate([t.device_modality() for t in trs])).cuda()
+    res = stack.forward(x, sal, mod, record=True, req_off=offs)
+    torch.cuda.synchronize()
+    L, E, k, lp, S = cfg.layers, cfg.experts, cfg.k, cfg.l_pinned, cfg.shared_experts
+
+    # --- decisions
+    re = np.zeros((L, T, k), dtype=np.int64)
+    re[:] = np.arange(k)
+    re[:lp] = res.prefix_routes.cpu().numpy()
+    for i, l in enumerate(range(lp, L)):
+        re[l, res.retained] = res.routes[i].cpu().numpy()
+    exp_ret = []
+    for r, tr in enumerate(trs):
+        o = compress_ref.compress(tr.saliency, tr.modality, [], re[:, offs[r]:offs[r + 1]], E, cfg.alpha, cfg.beta,
+                                  cfg.lam, list(range(lp)))
+        exp_ret.append(np.asarray(o["retained"]) + offs[r])
+    exp_ret = np.concatenate(exp_ret)
+    assert res.retained.tolist() == exp_ret.tolist()
+    merged = RoutingTrace(L, E, k, re, np.full(re.shape, 1.0 / k), np.concatenate([t.saliency for t in trs]),
+                          np.concatenate([t.modality for t in trs]), np.concatenate([t.embedding for t in trs]))
+    s = cfg.sim_config()
+    sd = dict(bandwidth_mb_per_ms=s.bandwidth_mb_per_ms, expert_size_mb=s.expert_size_mb,
+              gpu_ms_per_expert=s.gpu_ms_per_expert, num_slabs=s.num_slabs, victim_policy=s.victim_policy,
+              speculative_grace=s.speculative_grace, l_pinned=lp, shared_experts=S,
+              compress_latency_ms=s.compress_latency_ms, predictor_bootstrap_ms=s.predictor_bootstrap_ms,
+              predictor=dict(kind="history", budget=cfg.budget, window=cfg.window, gamma=cfg.gamma,
+                             history_decay=cfg.history_decay))
+    comp = dict(alpha=cfg.alpha, beta=cfg.beta, lam=cfg.lam, prefix=list(range(lp)))
+    exp = harness.simulate(merged, sd, comp, False, y_override=lambda ctx, ids: res.scores[ctx], retained=exp_ret)
+    got = res.report.to_dict()
+    for key in _F:
+        assert got[key] == exp[key], key
+    assert got["per_layer"] == exp["per_layer"]
+
+    # --- data path: every routed expert resident (pool layer l % 8) + the shared experts' slots
+    hl = store.host_layers
+    full = torch.cat([store.pool[(l % hl) * E:(l % hl + 1) * E] for l in range(L)]).cuda()
+    arena = torch.cat([full, store.arena[store.shared_slot_of[0, 0]:]]) if S else full
+    shared0 = L * E
+    cur = x
+    for l in range(L):
+        if l == lp:
+            cur = kernels.gather_rows(cur, torch.from_numpy(res.retained.astype(np.int32)).cuda())
+        N = int(cur.shape[0])
+        xn = kernels.rmsnorm(cur)
+        ids, gates, _ = kernels.route_topk(xn, store.router[l], k)
+        slots = torch.arange(l * E, (l + 1) * E, dtype=torch.int32, device="cuda")
+        if S == 0:
+            cur = moe_layer_forward(cur, ids, gates, arena, slots, cfg.inter, E, xn=xn)
+            continue
+        off, src, pos = kernels.permute_plan(ids, E)
+        xp = kernels.permute_rows(xn, src, N * k)
+        _, y = kernels.grouped_swiglu(xp, off, arena, slots, cfg.inter)
+        ssrc = torch.arange(N, dtype=torch.int32, device="cuda").repeat(S)
+        soff = torch.tensor([j * N for j in range(S + 1)], dtype=torch.int32, device="cuda")
+        xs = kernels.permute_rows(xn, ssrc, N * S)
+        _, ys = kernels.grouped_swiglu(xs, soff, arena, torch.arange(shared0 + l * S, shared0 + (l + 1) * S,
+                                                                     dtype=torch.int32, device="cuda"), cfg.inter)
+        cur = kernels.combine_shared(y, pos, gates, cur, ys, S)
+    torch.cuda.synchronize()
+    assert torch.equal(res.hidden, cur)
+    del stack, store, full, arena
+    torch.cuda.empty_cache()
