@@ -502,9 +502,10 @@ def main():
     side = torch.cuda.Stream(device=dev)
     n_chunks = 8 if (R >= 8 and a.source != "ep") else 1
     bounds = [req_off[(R * (c + 1)) // n_chunks] for c in range(n_chunks)]
-    x_dev = torch.empty_like(x)  # device landing buffer (allocation is not a transfer)
+    x_dev = torch.empty_like(x)  # device landing buffers (allocation is not a transfer)
+    x_dev2 = torch.empty_like(x) if a.source != "ep" else None
 
-    def step(e2e=False):
+    def step(e2e=False, read_back=True):
         x_ready = None
         if e2e:
             sd = sal_h.to(dev, non_blocking=True)
@@ -531,7 +532,7 @@ def main():
                 torch.cuda.current_stream().wait_event(x_ready[-1][1])
                 x_ready = None
             res = stack.forward(xd, sd, md, trace=dtr, req_off=req_off, x_ready=x_ready)
-        if e2e:
+        if e2e and read_back:
             n = int(res.hidden.shape[0])
             if out_h[0] is None or out_h[0].shape[0] < n:  # pinned result buffer, allocated once
                 out_h[0] = torch.empty((max(n, T), w.hidden), dtype=res.hidden.dtype, pin_memory=True)
@@ -557,6 +558,75 @@ def main():
             stack.profile = None
         return times, results
 
+    def timed_e2e_streamed(n):
+        """End to end as a serving loop runs it, one timed region over the n steps: every
+        step's inputs cross PCIe (pinned host -> HBM) and its result is read back (HBM ->
+        pinned host).  The link is idle during a step's pinned prefix once that step's own
+        inputs have landed, so step i+1's inputs are copied then, into the other half of a
+        double-buffered landing area (the first step's inputs are copied inside the region in
+        request-aligned chunks the prefix starts on as they land); step i's result is staged
+        on the device and read back on its own stream beside step i+1's prefix.  Returns ms
+        per step."""
+        if a.source == "ep":  # the EP stack has no chunked-input path: the serial figure stands
+            return float(np.mean(e2e_times))
+        d2h = torch.cuda.Stream(device=dev)
+        n0 = int(res0_rows[0])
+        stage = [torch.empty((n0, w.hidden), dtype=torch.bfloat16, device=dev) for _ in range(2)]
+        outs = [torch.empty((n0, w.hidden), dtype=torch.bfloat16, pin_memory=True) for _ in range(2)]
+        xb = [x_dev, x_dev2]
+        sb = [torch.empty_like(sal) for _ in range(2)]
+        mb = [torch.empty_like(mod) for _ in range(2)]
+        ev_d2h = [None, None]
+
+        def enqueue_inputs(b):  # on the side stream, behind whatever it already holds
+            evs, r0 = [], 0
+            with torch.cuda.stream(side):
+                sb[b].copy_(sal_h, non_blocking=True)
+                mb[b].copy_(mod_h, non_blocking=True)
+                for r1 in bounds:
+                    xb[b][r0:r1].copy_(x_h[r0:r1], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(side)
+                    evs.append((r1, ev))
+                    r0 = r1
+            return evs
+
+        barrier()
+        main = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(main)
+        side.wait_stream(main)
+        pending = enqueue_inputs(0)
+        for i in range(n):
+            b = i & 1
+            evs = pending
+            if i + 1 < n:
+                side.wait_stream(main)  # buffer b^1 was last read by step i-1's prefix (already queued)
+                pending = enqueue_inputs(b ^ 1)
+            if i == 0 and n_chunks > 1:
+                res = stack.forward(xb[b], sb[b], mb[b], trace=dtr, req_off=req_off, x_ready=evs)
+            else:
+                main.wait_event(evs[-1][1])
+                res = stack.forward(xb[b], sb[b], mb[b], trace=dtr, req_off=req_off)
+            nr = int(res.hidden.shape[0])
+            if nr > n0:
+                raise SystemExit("retained rows grew between steps")
+            if ev_d2h[b] is not None:
+                main.wait_event(ev_d2h[b])  # staging buffer b's previous read-back is done
+            stage[b][:nr].copy_(res.hidden)
+            ev = torch.cuda.Event()
+            ev.record(main)
+            d2h.wait_event(ev)
+            with torch.cuda.stream(d2h):
+                outs[b][:nr].copy_(stage[b][:nr], non_blocking=True)
+            ev_d2h[b] = torch.cuda.Event()
+            ev_d2h[b].record(d2h)
+        main.wait_stream(d2h)
+        main.wait_stream(side)
+        e1.record(main)
+        e1.synchronize()
+        return e0.elapsed_time(e1) / n
+
     # warm-up
     timed(a.warmup)
     barrier()
@@ -568,13 +638,17 @@ def main():
         times, results = timed(a.steps, prof=True)
     launches = (vlib.load().vmm_launch_count() - launches0) // max(a.steps, 1)
     timed(1, e2e=True)  # warm the e2e path (pinned result buffer) outside the timed steps
-    e2e_times, e2e_results = timed(a.steps, e2e=True)
+    e2e_times, e2e_results = timed(a.steps, e2e=True)  # serial: each step's read-back inside its own step
+    res0_rows = [int(results[-1][0].hidden.shape[0])]
+    timed_e2e_streamed(1)  # warm the streamed path's buffers
+    ms_e2e_streamed = timed_e2e_streamed(a.steps)
 
     def max_over_ranks(v):
         return vdist.max_over_ranks(v, dev)
 
     ms = max_over_ranks(float(np.mean(times)))
-    ms_e2e = max_over_ranks(float(np.mean(e2e_times)))
+    ms_e2e_serial = max_over_ranks(float(np.mean(e2e_times)))
+    ms_e2e = max_over_ranks(float(ms_e2e_streamed))
     value = world * T / (ms * 1e-3)
     e2e_value = world * T / (ms_e2e * 1e-3)
 
@@ -730,7 +804,12 @@ def main():
             "clocks": clk.summary(local),
             "gpu_launches": int(launches),
             "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": int(T * w.hidden * 2 + T * 9),
-                    "d2h_bytes_per_step": int(res0.hidden.numel() * 2), "ms_per_step": ms_e2e},
+                    "d2h_bytes_per_step": int(res0.hidden.numel() * 2), "ms_per_step": ms_e2e,
+                    "mode": "streamed: one timed region over the steps, every step's inputs H2D and result D2H "
+                            "inside it; step i+1's inputs cross PCIe during step i's prefix (link idle), step i's "
+                            "read-back runs beside step i+1's prefix",
+                    "serial": {"value": world * T / (ms_e2e_serial * 1e-3), "ms_per_step": ms_e2e_serial,
+                               "mode": "each step's H2D and D2H inside its own timed step"}},
             "cpu_baseline": cpu,
             "config_clock": {"transfer_ms": cfg.transfer_ms, "gpu_ms": cfg.gpu_ms,
                              "basis": "transfer = expert slot / measured link peak; gpu = roofline time of the "
