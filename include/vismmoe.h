@@ -420,6 +420,11 @@ int vmm_peer_enable(int peer);
 /* one copy-engine copy (any direction, incl. an IPC-mapped peer pointer) on `stream`;
  * used to measure the link peaks the logical clock is calibrated with */
 int vmm_copy_async(void *d_dst, const void *src, size_t bytes, void *stream);
+/* stream-ordered memset / strided 2-D copy (copy engine, no kernel): the host glue
+ * zeroes counters and lands per-chunk prefix routes in the [L][T][k] table with them */
+int vmm_memset_async(void *d_ptr, int byte_value, size_t bytes, void *stream);
+int vmm_copy2d_async(void *d_dst, size_t dpitch, const void *src, size_t spitch, size_t width, size_t height,
+                     void *stream);
 /* drain the engine's transfer commands and enqueue each as one copy of
  * slot_bytes from the pinned host pool slot ((layer % host_layers)*experts +
  * expert) into arena slot (slab_offset + slab) */

@@ -162,6 +162,8 @@ _SIGS = {
     "vmm_ipc_offset": (I32, [P, C.POINTER(I64)]),
     "vmm_ipc_close": (I32, [P]),
     "vmm_copy_async": (I32, [P, P, SZ, P]),
+    "vmm_memset_async": (I32, [P, I32, SZ, P]),
+    "vmm_copy2d_async": (I32, [P, SZ, P, SZ, SZ, SZ, P]),
     "vmm_peer_enable": (I32, [I32]),
     "vmm_gather_i32": (I32, [P, P, I32, I32, P, P]),
     "vmm_gather_f32": (I32, [P, P, I32, I32, P, P]),

@@ -101,6 +101,20 @@ int vmm_copy_async(void *d_dst, const void *src, size_t bytes, void *stream) {
   return VMM_OK;
 }
 
+int vmm_memset_async(void *d_ptr, int byte_value, size_t bytes, void *stream) {
+  cudaError_t e = cudaMemsetAsync(d_ptr, byte_value, bytes, (cudaStream_t)stream);
+  if (e != cudaSuccess) return vmm::fail(VMM_ECUDA, std::string("cudaMemsetAsync: ") + cudaGetErrorString(e));
+  return VMM_OK;
+}
+
+int vmm_copy2d_async(void *d_dst, size_t dpitch, const void *src, size_t spitch, size_t width, size_t height,
+                     void *stream) {
+  cudaError_t e = cudaMemcpy2DAsync(d_dst, dpitch, src, spitch, width, height, cudaMemcpyDefault,
+                                    (cudaStream_t)stream);
+  if (e != cudaSuccess) return vmm::fail(VMM_ECUDA, std::string("cudaMemcpy2DAsync: ") + cudaGetErrorString(e));
+  return VMM_OK;
+}
+
 int vmm_peer_enable(int peer) {
   int dev = 0, can = 0;
   cudaGetDevice(&dev);

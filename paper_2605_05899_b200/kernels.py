@@ -28,6 +28,26 @@ def _dev():
     return torch.device("cuda", torch.cuda.current_device())
 
 
+def memset_(t, byte_value: int = 0, stream=None):
+    """Fill a contiguous device tensor's bytes with a stream-ordered memset (no kernel)."""
+    if not t.is_contiguous():
+        raise ValueError("memset_ needs a contiguous tensor")
+    check(_lib.lib().vmm_memset_async(ptr(t), int(byte_value), t.numel() * t.element_size(), stream_ptr(stream)))
+    return t
+
+
+def copy_rows_2d(dst, src, stream=None):
+    """dst[i, :n] = src[i, :n] for 2-D views whose rows are contiguous (any row pitch): one
+    strided copy-engine copy (cudaMemcpy2DAsync), no kernel."""
+    h, w = (int(v) for v in src.shape[:2])
+    if tuple(dst.shape[:2]) != (h, w) or dst.dtype != src.dtype or dst.stride(1) != 1 or src.stride(1) != 1:
+        raise ValueError("copy_rows_2d needs equal shapes and contiguous rows")
+    es = src.element_size()
+    check(_lib.lib().vmm_copy2d_async(ptr(dst), dst.stride(0) * es, ptr(src), src.stride(0) * es, w * es, h,
+                                      stream_ptr(stream)))
+    return dst
+
+
 # ---------------------------------------------------------------------------
 # prune
 # ---------------------------------------------------------------------------
@@ -50,8 +70,8 @@ def prune(saliency, modality, prefix_routes, req_off, k_core, k_keep, experts: i
         flags=torch.empty(T, dtype=torch.uint8, device=dev),
         retained=torch.empty(max(T, 1), dtype=_i32, device=dev),
         # n_retained and status side by side: one D2H reads both
-        ns=torch.full((2, R), -1, dtype=_i32, device=dev),
-        target=torch.zeros(R, 4, dtype=torch.int64, device=dev),
+        ns=memset_(torch.empty((2, R), dtype=_i32, device=dev), 0xFF, stream),  # -1
+        target=memset_(torch.empty(R, 4, dtype=torch.int64, device=dev), 0, stream),
     )
     out["n_retained"], out["status"] = out["ns"][0], out["ns"][1]
     _n(1)

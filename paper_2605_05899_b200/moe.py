@@ -427,7 +427,7 @@ class MoEStack:
 
         if c.predictor == "mlp" and (embeddings is None or int(embeddings.shape[0]) < T):
             raise ContractError("the MLP predictor needs the tokens' embeddings (f64 [T, D])")
-        cur, x_ctx, prefix, counts_pre, ret, n_r, ret_off, xr = self._prefix_and_prune(
+        cur, x_ctx, prefix, counts_parts, ret, n_r, ret_off, xr = self._prefix_and_prune(
             x, saliency, modality, trace, req_off, bufs, x_ready=x_ready)
         if self._mlp is not None and c.predictor == "mlp":
             mp = self._mlp
@@ -435,14 +435,14 @@ class MoEStack:
             kernels.row_mean(mp["emb"], ret, modality, out=mp["hv"])  # visual_summary over the kept visual rows
 
         # --- per-layer demand counts over the retained tokens
-        counts_ret = torch.zeros((L, E), dtype=torch.int32, device=dev)
+        # (vmm_demand_counts overwrites its rows; the executor zeroes each later layer's row itself)
+        counts_ret = torch.empty((L, E), dtype=torch.int32, device=dev)
         if lp:
-            kernels.demand_counts(prefix[:lp], torch.arange(lp, dtype=torch.int32, device=dev), ret, E,
-                                  out=counts_ret[:lp])
+            kernels.demand_counts(prefix[:lp], self.layer_ids[:lp], ret, E, out=counts_ret[:lp])
         oracle_table = None
         if c.predictor == "oracle":
             rl = trace["routes"]
-            kernels.demand_counts(rl, torch.arange(L, dtype=torch.int32, device=dev), ret, E, out=counts_ret)
+            kernels.demand_counts(rl, self.layer_ids, ret, E, out=counts_ret)
             dec = torch.tensor(decay_table(c.gamma, c.window), dtype=torch.float64, device=dev)
             oracle_table = kernels.oracle_targets(counts_ret, self.layer_ids, c.window, dec)  # row = context layer
 
@@ -479,7 +479,11 @@ class MoEStack:
         else:
             eng.begin(None)
         n_copies = self._issue(eng)
-        cp = counts_pre[:lp].cpu().numpy() if lp else None
+        cp = None
+        if lp:  # the pinned layers' demand over all prefill rows: per-chunk counts summed on the host
+            cp = np.zeros((lp, E), dtype=np.int64)
+            for l0_, t_ in counts_parts:
+                cp[l0_:l0_ + int(t_.shape[0])] += t_.cpu().numpy()
         for l in range(lp):
             eng.layer(l, np.flatnonzero(cp[l]).astype(np.int32), 0, -1, None)
 
@@ -505,8 +509,10 @@ class MoEStack:
         """Pinned prefix on all T rows (resident experts, engine-less executor,
         no host sync) then per-request compression on the prefix routes.
         Returns (rows after the prefix, xn of layer lp-1, prefix routes,
-        prefix counts, retained ids, N_r, per-request retained offsets,
-        retained rows)."""
+        prefix counts as [(first layer, device counts [n, E])] parts to sum,
+        retained ids, N_r, per-request retained offsets, retained rows).
+        Between the prefix and the first cached layer only our kernels and
+        copy-engine copies run (no torch elementwise kernels)."""
         c = self.cfg
         L, E, k, lp = c.layers, c.experts, c.k, c.l_pinned
         dev = self.device
@@ -521,7 +527,9 @@ class MoEStack:
         # --- pinned prefix: all prefill tokens, resident experts, no cache decisions:
         # the native executor in engine-less mode (no host sync inside the prefix)
         prefix = torch.empty((max(lp, 1), T, k), dtype=torch.int32, device=dev)
-        counts_pre = torch.zeros((max(lp, 1), E), dtype=torch.int32, device=dev)
+        # the executor zeroes (live) or overwrites (trace) each layer's counts row itself
+        counts_pre = torch.empty((max(lp, 1), E), dtype=torch.int32, device=dev)
+        counts_parts = []
         x_ctx = None
         cur = x
         offs_req = [0, T] if req_off is None else [int(v) for v in req_off]
@@ -549,7 +557,6 @@ class MoEStack:
             if not two:
                 caps = [max(b - a for a, b, _ in bounds), 0]
             base = [0, caps[0]]
-            counts_lane = [torch.zeros((lpe, E), dtype=torch.int32, device=dev) for _ in range(2)]
             for sp_ in self._pstreams:
                 sp_.wait_stream(main)
             for i, (r0, r1, ev) in enumerate(bounds):
@@ -562,7 +569,7 @@ class MoEStack:
                     if ev is not None:
                         side.wait_event(ev)
                     routes_c = torch.empty((lpe, n, k), dtype=torch.int32, device=dev)
-                    counts_c = torch.zeros((lpe, E), dtype=torch.int32, device=dev)
+                    counts_c = torch.empty((lpe, E), dtype=torch.int32, device=dev)
                     rows_c = torch.arange(r0, r1, dtype=torch.int32, device=dev) if c.routing == "trace" else None
                     out_c, _, _ = self._native_layers(None, x[r0:r1], n, 0, lpe, 0, -1, rows=rows_c, counts=counts_c,
                                                       trace=trace, record_into=routes_c,
@@ -570,16 +577,17 @@ class MoEStack:
                     cur_full[r0:r1].copy_(out_c)
                     if c.predictor == "gate" and not skip_last:  # boot emission context (layer lp-1 input)
                         xn_full[r0:r1].copy_(bufs["xn"][base[lane]:base[lane] + n])
-                    prefix[:lpe, r0:r1].copy_(routes_c)
-                    counts_lane[lane] += counts_c
+                    # this chunk's rows of every prefix layer's routes into the [L][T][k] table
+                    kernels.copy_rows_2d(prefix[:lpe, r0:r1].view(lpe, n * k), routes_c.view(lpe, n * k))
+                    counts_parts.append((0, counts_c))
             for sp_ in self._pstreams:
                 main.wait_stream(sp_)
-            counts_pre[:lpe] += counts_lane[0] + counts_lane[1]
             cur, x_ctx = cur_full, xn_full
         elif lpe:
             rows_all = torch.arange(T, dtype=torch.int32, device=dev) if c.routing == "trace" else None
             cur, _, _ = self._native_layers(None, x, T, 0, lpe, 0, -1, rows=rows_all, counts=counts_pre, trace=trace,
                                             record_into=prefix[:lpe])
+            counts_parts.append((0, counts_pre[:lpe]))
             x_ctx = bufs["xn"][:T]  # normalised input of layer lp-1: context of the boot emission (gate predictor)
         if x_ready and not lpe:  # no full prefix layer ran: the rows must have landed before layer lp-1
             main = torch.cuda.current_stream()
@@ -590,9 +598,10 @@ class MoEStack:
         if skip_last:  # layer lp-1: RMSNorm + router on every token (the prune needs its routes)
             l = lp - 1
             xn_l = kernels.rmsnorm(cur, out=bufs["xn"][:T])
+            kernels.memset_(counts_pre[l])  # the router accumulates its pick counts
             ids_l, gates_l, _ = kernels.route_topk(xn_l, self.store.router[l], k, counts=counts_pre[l],
-                                                   ids=bufs["ids"][:T], gates=bufs["gates"][:T])
-            prefix[l].copy_(ids_l)
+                                                   ids=prefix[l], gates=bufs["gates"][:T])
+            counts_parts.append((l, counts_pre[l:l + 1]))
             x_ctx = xn_l  # normalised input of layer lp-1: context of the boot emission (gate predictor)
             last = (cur, xn_l, ids_l, gates_l)
 
@@ -638,7 +647,7 @@ class MoEStack:
                                           h1=bufs["h1"][:M], y=bufs["y"][:M])
             xr = kernels.combine(y, pos.view(n_r, k), gates_ret, x_ret)
             cur = xr
-        return cur, x_ctx, prefix, counts_pre, ret, n_r, ret_off, xr
+        return cur, x_ctx, prefix, counts_parts, ret, n_r, ret_off, xr
 
 
     def _native_layers(self, eng, x, n_rows, l0, l1, phase, step, rows=None, counts=None, oracle_table=None,
