@@ -384,6 +384,7 @@ class MoEStack:
                 h1s=torch.empty(max(n_tok * c.shared_experts, 1), c.inter, dtype=torch.bfloat16, device=dev),
                 ys=torch.empty(max(n_tok * c.shared_experts, 1), c.hidden, dtype=torch.bfloat16, device=dev),
                 ffn_done=torch.empty(M // 128 + c.experts + 1, dtype=torch.int32, device=dev),
+                iota=torch.arange(n_tok, dtype=torch.int32, device=dev),  # row ids (trace routing), made once
             )
         return self._bufs
 
@@ -570,7 +571,7 @@ class MoEStack:
                         side.wait_event(ev)
                     routes_c = torch.empty((lpe, n, k), dtype=torch.int32, device=dev)
                     counts_c = torch.empty((lpe, E), dtype=torch.int32, device=dev)
-                    rows_c = torch.arange(r0, r1, dtype=torch.int32, device=dev) if c.routing == "trace" else None
+                    rows_c = bufs["iota"][r0:r1] if c.routing == "trace" else None
                     out_c, _, _ = self._native_layers(None, x[r0:r1], n, 0, lpe, 0, -1, rows=rows_c, counts=counts_c,
                                                       trace=trace, record_into=routes_c,
                                                       region=(base[lane], caps[lane], lane), batch_rows=T)
@@ -584,7 +585,7 @@ class MoEStack:
                 main.wait_stream(sp_)
             cur, x_ctx = cur_full, xn_full
         elif lpe:
-            rows_all = torch.arange(T, dtype=torch.int32, device=dev) if c.routing == "trace" else None
+            rows_all = bufs["iota"][:T] if c.routing == "trace" else None
             cur, _, _ = self._native_layers(None, x, T, 0, lpe, 0, -1, rows=rows_all, counts=counts_pre, trace=trace,
                                             record_into=prefix[:lpe])
             counts_parts.append((0, counts_pre[:lpe]))
