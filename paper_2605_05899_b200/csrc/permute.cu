@@ -652,60 +652,74 @@ decode_glue_kernel(const uint4 *__restrict__ y, const int32_t *pos_prev, const f
                    const float *tg_l, const int32_t *__restrict__ rows, int E, int32_t *ids, float *gates,
                    int32_t *offsets, int32_t *src_row, int32_t *pos, uint4 *xp, float eps) {
   __shared__ uint4 s_xn[kGlueMaxRows][kMaxRowVec];
-  __shared__ int s_src[kGlueMaxPicks];
+  __shared__ int s_src[kGlueMaxPicks], s_ids[kGlueMaxPicks];
+  __shared__ float s_gts[kGlueMaxPicks];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int M = n * k;
+  // B, part 1: the last warp stages this layer's trace ids/gates (consumed after the barrier)
+  if (warp == (int)(blockDim.x >> 5) - 1 && lane < M) {
+    const int t = lane / k, j = lane - t * k;
+    const long long src = (long long)rows[t] * k + j;
+    s_ids[lane] = tr_l[src];
+    s_gts[lane] = tg_l[src];
+  }
+  // A, part 1: every thread combines (row, 16-byte chunk) items -- the whole block gathers the
+  // k expert rows at once (one warp per row left this latency-bound) -- into out and s_xn
+  for (int it = threadIdx.x; it < n * row_vec; it += blockDim.x) {
+    const int t = it / row_vec, c = it - t * row_vec;
+    uint4 v;
+    if (y == nullptr) {
+      v = resid[(long long)t * row_vec + c];
+    } else {
+      float acc[8];
+      combine_chunk(y, pos_prev, gates_prev, t, k, row_vec, c, nullptr, 0, n, acc);
+      const uint4 rv = resid[(long long)t * row_vec + c];
+      const __nv_bfloat16 *rh = reinterpret_cast<const __nv_bfloat16 *>(&rv);
+      __nv_bfloat16 *oh = reinterpret_cast<__nv_bfloat16 *>(&v);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) oh[q] = __float2bfloat16(__bfloat162float(rh[q]) + acc[q]);
+      out[(long long)t * row_vec + c] = v;
+    }
+    s_xn[t][c] = v;
+  }
+  __syncthreads();  // phase A has read pos/gates of the previous layer before B overwrites them
+  // A, part 2: warp t normalises row t from shared memory with the warp-per-row kernel's exact
+  // arithmetic (lane L: chunks L + 32 i in i order, then the xor tree), in place
   if (warp < n) {
     const int t = warp;
     uint4 v[CH];
 #pragma unroll
     for (int i = 0; i < CH; ++i) {
       const int c = lane + 32 * i;
-      if (c >= row_vec) continue;
-      if (y == nullptr) {
-        v[i] = resid[(long long)t * row_vec + c];
-      } else {
-        float acc[8];
-        combine_chunk(y, pos_prev, gates_prev, t, k, row_vec, c, nullptr, 0, n, acc);
-        const uint4 rv = resid[(long long)t * row_vec + c];
-        const __nv_bfloat16 *rh = reinterpret_cast<const __nv_bfloat16 *>(&rv);
-        __nv_bfloat16 *oh = reinterpret_cast<__nv_bfloat16 *>(&v[i]);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) oh[q] = __float2bfloat16(__bfloat162float(rh[q]) + acc[q]);
-        out[(long long)t * row_vec + c] = v[i];
-      }
+      if (c < row_vec) v[i] = s_xn[t][c];
     }
     const float inv = rsqrtf(warp_row_ss<CH>(v, row_vec) / (float)(row_vec * 8) + eps);
+    __syncwarp();
     warp_row_norm_store<CH>(v, row_vec, inv, nullptr, s_xn[t]);
     __syncwarp();
     for (int c = lane; c < row_vec; c += 32) xn[(long long)t * row_vec + c] = s_xn[t][c];
   }
-  __syncthreads();  // phase A has read pos/gates of the previous layer before B overwrites them
-  const int M = n * k;
-  if (threadIdx.x == 0) {
-    int cnt[VMM_MAX_EXPERTS];
-    for (int e = 0; e < E; ++e) cnt[e] = 0;
-    for (int i = 0; i < M; ++i) {
-      const int t = i / k, j = i - t * k;
-      const int e = tr_l[(long long)rows[t] * k + j];
-      ids[i] = e;
-      gates[i] = tg_l[(long long)rows[t] * k + j];
-      cnt[e] += 1;
-    }
-    int run = 0;
-    for (int e = 0; e < E; ++e) {
-      offsets[e] = run;
-      const int c = cnt[e];
-      cnt[e] = run;
-      run += c;
-    }
-    offsets[E] = run;
-    for (int i = 0; i < M; ++i) {
-      const int e = ids[i];
-      const int p = cnt[e]++;
-      pos[i] = p;
-      src_row[p] = i / k;
-      s_src[p] = i / k;
-    }
+  // B, part 2 in parallel (it was one thread: ~20 us of dependent loads and local-memory counts
+  // per decode layer): lane i of warp 0 owns pick i; the stable (expert, pick) order of the plan
+  // is offsets[e] = #picks with a smaller expert, plus the pick's rank among the earlier picks
+  // of its expert (__match_any_sync)
+  for (int e = threadIdx.x; e <= E; e += blockDim.x) {
+    int below = 0;
+    for (int i = 0; i < M; ++i) below += s_ids[i] < e;
+    offsets[e] = below;
+  }
+  if (warp == 0 && lane < M) {
+    const unsigned act = M >= 32 ? 0xffffffffu : ((1u << M) - 1u);
+    const int e = s_ids[lane];
+    ids[lane] = e;
+    gates[lane] = s_gts[lane];
+    const unsigned peers = __match_any_sync(act, e);
+    int below = 0;
+    for (int i = 0; i < M; ++i) below += s_ids[i] < e;
+    const int p = below + __popc(peers & ((1u << lane) - 1u));
+    pos[lane] = p;
+    src_row[p] = lane / k;
+    s_src[p] = lane / k;
   }
   __syncthreads();
   for (int p = warp; p < M; p += 8) {
