@@ -769,8 +769,9 @@ def main():
                        "miss_source": a.source, "host_pool": store.host_pool_kind,
                        "parallelism": f"dp{world} (requests)", "requests_per_gpu_step": R,
                        "l2": "flushed (256 MB write) between the timed device-resident steps; the streamed e2e "
-                             "loop runs without a flush on inputs larger than L2 (hidden states "
-                             f"{T * w.hidden * 2 / 1e9:.2f} GB per step)"},
+                             "loop runs without a flush on "
+                             + ("inputs larger than L2" if T * w.hidden * 2 > (126 << 20) else "inputs smaller than L2")
+                             + f" (hidden states {T * w.hidden * 2 / 1e9:.3f} GB per step)"},
             "hit_rate": hit_rate, "hits": int(hits), "misses": int(misses), "evictions": int(evictions),
             "retained_tokens": int(retained),
             "h2d": {"gbs": h2d_gbs, "bytes_per_step": h2d_bytes, "copies_per_step": int(copies),
