@@ -1063,7 +1063,8 @@ skinny_ffn_kernel(const __nv_bfloat16 *__restrict__ xp, const int32_t *__restric
                   const __nv_bfloat16 *__restrict__ w2, long long stride, int H, int I, const uint32_t *need,
                   const uint32_t *ready, int ready_base, unsigned int *grid_bar, unsigned int bar_target,
                   __nv_bfloat16 *h1, __nv_bfloat16 *__restrict__ y) {
-  __shared__ int s_act[kSkinnyRows], s_r0[kSkinnyRows], s_r1[kSkinnyRows];
+  __shared__ int s_act[kSkinnyRows], s_r0[kSkinnyRows], s_r1[kSkinnyRows], s_slot[kSkinnyRows];
+  __shared__ uint32_t s_need[kSkinnyRows];
   __shared__ int s_nact;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef VMM_FFN_PROF
@@ -1086,6 +1087,14 @@ skinny_ffn_kernel(const __nv_bfloat16 *__restrict__ xp, const int32_t *__restric
       seen += __popc(bal);
     }
     if (lane == 0) s_nact = seen < kSkinnyRows ? seen : kSkinnyRows;
+    __syncwarp();
+    // the active experts' slots and fill sequences, read once per CTA (slot_of / need may be
+    // pinned host rows mapped into the device address space: the decode executor passes them
+    // without a per-layer upload)
+    if (lane < (seen < kSkinnyRows ? seen : kSkinnyRows)) {
+      s_slot[lane] = slot_of[s_act[lane]];
+      s_need[lane] = need ? need[s_act[lane]] : 0u;
+    }
   }
   __syncthreads();
   const int nact = s_nact;
@@ -1094,10 +1103,9 @@ skinny_ffn_kernel(const __nv_bfloat16 *__restrict__ xp, const int32_t *__restric
   const int rv1 = H / 8;
   for (int it = gw; it < nact * I; it += nwarps) {
     const int j = it / I, f = it - j * I;
-    const int e = s_act[j];
-    if (need && need[e] && lane == 0) wait_at_least(ready + (slot_of[e] - ready_base), need[e], 128);
+    if (s_need[j] && lane == 0) wait_at_least(ready + (s_slot[j] - ready_base), s_need[j], 128);
     __syncwarp();
-    const __nv_bfloat16 *w = w13 + (long long)slot_of[e] * stride;
+    const __nv_bfloat16 *w = w13 + (long long)s_slot[j] * stride;
     const int grow = (f >> 6) * 128 + (f & 63);  // interleaved 64|64 gate/up blocks
     const uint4 *rows[2] = {reinterpret_cast<const uint4 *>(w + (long long)grow * H),
                             reinterpret_cast<const uint4 *>(w + (long long)(grow + 64) * H)};
@@ -1130,8 +1138,7 @@ skinny_ffn_kernel(const __nv_bfloat16 *__restrict__ xp, const int32_t *__restric
   const int ncol4 = H / 4;
   for (int it = gw; it < nact * ncol4; it += nwarps) {
     const int j = it / ncol4, n = 4 * (it - j * ncol4);
-    const int e = s_act[j];
-    const __nv_bfloat16 *w = w2 + (long long)slot_of[e] * stride;
+    const __nv_bfloat16 *w = w2 + (long long)s_slot[j] * stride;
     const uint4 *rows[4] = {reinterpret_cast<const uint4 *>(w + (long long)(n + 0) * I),
                             reinterpret_cast<const uint4 *>(w + (long long)(n + 1) * I),
                             reinterpret_cast<const uint4 *>(w + (long long)(n + 2) * I),
