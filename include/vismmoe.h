@@ -260,6 +260,13 @@ int vmm_grouped_swiglu_fused_ex(const void *d_xp, const int32_t *d_offsets, int 
                                 const uint32_t *d_ready, int ready_base, uint32_t *d_done, const void *d_x_rows,
                                 const int32_t *d_src_row, int n_x_rows, void *d_h1, void *d_y,
                                 const int32_t *d_order, void *stream);
+/* Decode-sized layer (M_total <= 16 rows): the skinny weight-streaming FFN with the slot
+ * table and the fill sequences given as HOST rows [E] -- they travel in the kernel's
+ * parameter block, so a decode layer needs no per-layer upload in the compute stream. */
+int vmm_grouped_swiglu_decode(const void *d_xp, const int32_t *d_offsets, int E, int M_total, int H, int I,
+                              const void *d_w13_arena, const void *d_w2_arena, long long slot_stride,
+                              const int32_t *h_slot_of_expert, const uint32_t *h_need, const uint32_t *d_ready,
+                              int ready_base, void *d_h1, void *d_y, void *stream);
 /* H1 is scratch.  On the CTA-pair path (tensor-bound batches) the last GEMM2 tile
  * that consumes an H1 block drops it from L2 without a write-back
  * (discard.global.L2), so d_h1's contents after the call are undefined; keep != 0

@@ -82,6 +82,7 @@ _SIGS = {
     "vmm_route_topk": (I32, [P, P, I32, I32, I32, I32, P, P, P, P, P]),
     "vmm_route_lookahead": (I32, [P, P, I32, I32, I32, I32, I32, I32, P, P, P, P, P]),
     "vmm_ffn_keep_h1": (I32, [I32]),
+    "vmm_grouped_swiglu_decode": (I32, [P, P, I32, I32, I32, I32, P, P, I64, P, P, P, I32, P, P, P]),
     "vmm_route_topk_ex": (I32, [P, P, I32, I32, I32, I32, P, P, P, P, I32, P]),
     "vmm_route_lookahead_ex": (I32, [P, P, I32, I32, I32, I32, I32, I32, P, P, P, P, I32, P]),
     "vmm_normalize_counts": (I32, [P, I32, F64, P, P]),

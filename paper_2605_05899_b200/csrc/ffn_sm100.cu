@@ -1057,12 +1057,20 @@ __device__ __forceinline__ void warp_dot(const uint4 *const (&w)[NW], int row_ve
 
 constexpr int kSkinnyThreads = 512;
 
+// A decode layer's slot table and fill sequences passed BY VALUE (2 KB of kernel parameters,
+// captured at launch): no per-layer upload in the compute stream
+struct SkinnyRows {
+  int32_t slot[VMM_MAX_EXPERTS];
+  uint32_t need[VMM_MAX_EXPERTS];
+  int by_value, has_need;
+};
+
 __global__ void __launch_bounds__(kSkinnyThreads, 1)
 skinny_ffn_kernel(const __nv_bfloat16 *__restrict__ xp, const int32_t *__restrict__ offsets, int E,
                   const int32_t *__restrict__ slot_of, const __nv_bfloat16 *__restrict__ w13,
                   const __nv_bfloat16 *__restrict__ w2, long long stride, int H, int I, const uint32_t *need,
                   const uint32_t *ready, int ready_base, unsigned int *grid_bar, unsigned int bar_target,
-                  __nv_bfloat16 *h1, __nv_bfloat16 *__restrict__ y) {
+                  __nv_bfloat16 *h1, __nv_bfloat16 *__restrict__ y, const __grid_constant__ SkinnyRows rows) {
   __shared__ int s_act[kSkinnyRows], s_r0[kSkinnyRows], s_r1[kSkinnyRows], s_slot[kSkinnyRows];
   __shared__ uint32_t s_need[kSkinnyRows];
   __shared__ int s_nact;
@@ -1088,12 +1096,12 @@ skinny_ffn_kernel(const __nv_bfloat16 *__restrict__ xp, const int32_t *__restric
     }
     if (lane == 0) s_nact = seen < kSkinnyRows ? seen : kSkinnyRows;
     __syncwarp();
-    // the active experts' slots and fill sequences, read once per CTA (slot_of / need may be
-    // pinned host rows mapped into the device address space: the decode executor passes them
-    // without a per-layer upload)
+    // the active experts' slots and fill sequences, read once per CTA (from the by-value
+    // parameter block when the executor passes the host rows, else from device rows)
     if (lane < (seen < kSkinnyRows ? seen : kSkinnyRows)) {
-      s_slot[lane] = slot_of[s_act[lane]];
-      s_need[lane] = need ? need[s_act[lane]] : 0u;
+      const int e = s_act[lane];
+      s_slot[lane] = rows.by_value ? rows.slot[e] : slot_of[e];
+      s_need[lane] = rows.by_value ? (rows.has_need ? rows.need[e] : 0u) : (need ? need[e] : 0u);
     }
   }
   __syncthreads();
@@ -1462,7 +1470,7 @@ extern "C" int vmm_ffn_prof_read(unsigned long long *out, int reset) {
 static int skinny_launch(const void *d_xp, const int32_t *d_offsets, int E, int M_total, int H, int I,
                          const void *d_w13, const void *d_w2, long long stride, const int32_t *d_slot_of,
                          const uint32_t *d_need, const uint32_t *d_ready, int ready_base, void *d_h1, void *d_y,
-                         void *stream) {
+                         void *stream, const int32_t *h_slot_of = nullptr, const uint32_t *h_need = nullptr) {
   if (H % 8 || I % 8 || H % 4) return vmm::fail(VMM_EVALIDATION, "decode FFN: hidden/inter must be multiples of 8");
   constexpr int kBarRing = 64;
   static unsigned int *bar[64] = {nullptr};
@@ -1488,9 +1496,18 @@ static int skinny_launch(const void *d_xp, const int32_t *d_offsets, int E, int 
                       *w2 = (const __nv_bfloat16 *)d_w2;
   __nv_bfloat16 *h1 = (__nv_bfloat16 *)d_h1, *y = (__nv_bfloat16 *)d_y;
   unsigned int target = (unsigned int)grid;
+  SkinnyRows rows;
+  rows.by_value = h_slot_of != nullptr;
+  rows.has_need = h_need != nullptr;
+  if (rows.by_value) {
+    for (int e = 0; e < E; ++e) {
+      rows.slot[e] = h_slot_of[e];
+      rows.need[e] = h_need ? h_need[e] : 0u;
+    }
+  }
   void *args[] = {(void *)&xp, (void *)&d_offsets, (void *)&E, (void *)&d_slot_of, (void *)&w13, (void *)&w2,
                   (void *)&stride, (void *)&H, (void *)&I, (void *)&d_need, (void *)&d_ready, (void *)&ready_base,
-                  (void *)&counter, (void *)&target, (void *)&h1, (void *)&y};
+                  (void *)&counter, (void *)&target, (void *)&h1, (void *)&y, (void *)&rows};
   e = cudaLaunchCooperativeKernel((const void *)skinny_ffn_kernel, dim3(grid), dim3(kSkinnyThreads), args, 0,
                                   (cudaStream_t)stream);
   if (e != cudaSuccess) return vmm::cuda_status(e, "skinny_ffn_kernel (cooperative launch)");
@@ -1639,6 +1656,22 @@ extern "C" int vmm_grouped_swiglu_fused_ex(const void *d_xp, const int32_t *d_of
                                            uint32_t *d_done, const void *d_x_rows, const int32_t *d_src_row,
                                            int n_x_rows, void *d_h1, void *d_y, const int32_t *d_order,
                                            void *stream);
+
+// decode-sized layer (M_total <= 16) with the slot table and fill sequences given as HOST rows:
+// they travel as kernel parameters, so the layer needs no upload in the compute stream
+extern "C" int vmm_grouped_swiglu_decode(const void *d_xp, const int32_t *d_offsets, int E, int M_total, int H, int I,
+                                         const void *d_w13_arena, const void *d_w2_arena, long long slot_stride,
+                                         const int32_t *h_slot_of_expert, const uint32_t *h_need,
+                                         const uint32_t *d_ready, int ready_base, void *d_h1, void *d_y,
+                                         void *stream) {
+  if (M_total <= 0) return VMM_OK;
+  if (M_total > kSkinnyRows) return vmm::fail(VMM_ECONTRACT, "decode FFN: at most 16 rows");
+  if (E < 1 || E > VMM_MAX_EXPERTS) return vmm::fail(VMM_EVALIDATION, "experts must lie in [1, 256]");
+  if (!h_slot_of_expert) return vmm::fail(VMM_ECONTRACT, "decode FFN: host slot rows required");
+  if (h_need && !d_ready) return vmm::fail(VMM_ECONTRACT, "need[] without ready flags");
+  return skinny_launch(d_xp, d_offsets, E, M_total, H, I, d_w13_arena, d_w2_arena, slot_stride, nullptr, nullptr,
+                       d_ready, ready_base, d_h1, d_y, stream, h_slot_of_expert, h_need);
+}
 
 extern "C" int vmm_grouped_swiglu_fused(const void *d_xp, const int32_t *d_offsets, int E, int M_total, int H, int I,
                                         const void *d_w13_arena, const void *d_w2_arena, long long slot_stride,

@@ -53,6 +53,10 @@ int vmm_xfer_issue_engine(vmm_xfer *x, vmm_engine *e, const void *h_pool, int ho
 int vmm_xfer_issue_engine_ordered(vmm_xfer *x, vmm_engine *e, const void *h_pool, int host_layers, int experts,
                                   void *d_arena, long long slab_offset, size_t slot_bytes, int layer_now,
                                   const int32_t *h_rank, int32_t *h_issued_experts, int *n_issued);
+int vmm_grouped_swiglu_decode(const void *d_xp, const int32_t *d_offsets, int E, int M_total, int H, int I,
+                              const void *d_w13_arena, const void *d_w2_arena, long long slot_stride,
+                              const int32_t *h_slot_of_expert, const uint32_t *h_need, const uint32_t *d_ready,
+                              int ready_base, void *d_h1, void *d_y, void *stream);
 int vmm_gather_i32(const int32_t *d_src, const int32_t *d_rows, int n, int width, int32_t *d_dst, void *stream);
 int vmm_gather_f32(const float *d_src, const int32_t *d_rows, int n, int width, float *d_dst, void *stream);
 const uint32_t *vmm_xfer_ready(vmm_xfer *x);
@@ -154,6 +158,10 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
   std::vector<uint32_t> need;
   // expert walk / copy order (largest first) for the CTA-pair FFN; VMM_NO_WALK_ORDER=1: id order
   static const bool no_walk = std::getenv("VMM_NO_WALK_ORDER") != nullptr;
+  // decode-sized layers: slot / need rows as kernel parameters (VMM_DECODE_UPLOAD_ROWS=1: upload them;
+  // the opt-in tensor-core decode FFN, VMM_DECODE_TC=1, reads device rows)
+  static const bool by_value_rows =
+      std::getenv("VMM_DECODE_UPLOAD_ROWS") == nullptr && std::getenv("VMM_DECODE_TC") == nullptr;
   std::vector<int32_t> by_size(E), rank_of(E), issued(E);
   std::vector<char> is_miss(E);
   const uint32_t *ready = vmm_xfer_ready(xf);
@@ -390,6 +398,9 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
     }
     const int32_t *slot_of;
     const uint32_t *need_of = nullptr;
+    bool host_rows = false;  // decode-sized layer: slot / need rows passed by value (see below)
+    const int32_t *h_slot_row = nullptr;
+    const uint32_t *h_need_row = nullptr;
     if (l < lp) {
       slot_of = d.pinned_slot_of + (size_t)l * E;
     } else {
@@ -399,7 +410,11 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
       std::memset(row, 0, sizeof(int32_t) * E);
       for (size_t i = 0; i < demand.size(); ++i) row[demand[i]] = slabs[i] + (int32_t)d.n_pinned_slots;
       int32_t *drow = d.slot_dev + (size_t)l * E;
-      VMM_CUDA(cudaMemcpyAsync(drow, row, sizeof(int32_t) * E, cudaMemcpyHostToDevice, st), "slot table H2D");
+      // decode-sized layers hand the rows to the skinny FFN as kernel parameters
+      // (vmm_grouped_swiglu_decode): no per-layer uploads in the compute stream
+      host_rows = by_value_rows && (long long)n_rows * k <= 16 && flagged && d.shared == 0;
+      if (!host_rows)
+        VMM_CUDA(cudaMemcpyAsync(drow, row, sizeof(int32_t) * E, cudaMemcpyHostToDevice, st), "slot table H2D");
       if (flagged) {
         need.resize(demand.size());
         VMM_TRY(vmm_xfer_need(xf, slabs.data(), (int)slabs.size(), need.data()));
@@ -407,12 +422,17 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
         std::memset(nrow, 0, sizeof(uint32_t) * E);
         for (size_t i = 0; i < demand.size(); ++i) nrow[demand[i]] = need[i];
         uint32_t *ndev = d.need_dev + (size_t)l * E;
-        VMM_CUDA(cudaMemcpyAsync(ndev, nrow, sizeof(uint32_t) * E, cudaMemcpyHostToDevice, st), "need H2D");
+        if (host_rows) {
+          h_need_row = nrow;
+        } else {
+          VMM_CUDA(cudaMemcpyAsync(ndev, nrow, sizeof(uint32_t) * E, cudaMemcpyHostToDevice, st), "need H2D");
+        }
         need_of = ndev;
       } else {
         VMM_TRY(vmm_xfer_fence(xf, slabs.data(), (int)slabs.size(), stream));
       }
       slot_of = drow;
+      h_slot_row = row;
     }
     auto c3 = clk::now();
     const int M = n_rows * k;
@@ -430,11 +450,16 @@ int vmm_stack_layers(vmm_stack *s, vmm_engine *eng, vmm_xfer *xf, const void *d_
     }
     if (out && out->ffn_start)
       VMM_CUDA(cudaEventRecord((cudaEvent_t)out->ffn_start[l - l0], st), "ffn start event");
-    VMM_TRY(vmm_grouped_swiglu_fused_ex(d.xp, d.off, E, M, H, I, d.arena,
-                                        (const char *)d.arena + (size_t)2 * I * H * 2, (long long)3 * I * H, d.n_slots,
-                                        slot_of, need_of, ready, (int)d.n_pinned_slots, d.ffn_done,
-                                        gather ? xn : nullptr, gather ? d.src : nullptr, n_rows, d.h1, d.y, order_of,
-                                        stream));
+    if (host_rows)
+      VMM_TRY(vmm_grouped_swiglu_decode(d.xp, d.off, E, M, H, I, d.arena,
+                                        (const char *)d.arena + (size_t)2 * I * H * 2, (long long)3 * I * H,
+                                        h_slot_row, h_need_row, ready, (int)d.n_pinned_slots, d.h1, d.y, stream));
+    else
+      VMM_TRY(vmm_grouped_swiglu_fused_ex(d.xp, d.off, E, M, H, I, d.arena,
+                                          (const char *)d.arena + (size_t)2 * I * H * 2, (long long)3 * I * H,
+                                          d.n_slots, slot_of, need_of, ready, (int)d.n_pinned_slots, d.ffn_done,
+                                          gather ? xn : nullptr, gather ? d.src : nullptr, n_rows, d.h1, d.y,
+                                          order_of, stream));
     if (out && out->ffn_end) VMM_CUDA(cudaEventRecord((cudaEvent_t)out->ffn_end[l - l0], st), "ffn end event");
     void *dst = ping ? d.out1 : d.out0;
     const int S = d.shared;
